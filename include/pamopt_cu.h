@@ -1,0 +1,153 @@
+/* pamopt_cu.h — C-ABI of the B200-native remesh hot path (UDF -> DMC -> QEM with
+ * self-intersection undo).  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * The reference (`/root/reference/proj`, namespace pamopt) is an in-process C++ library with
+ * no FFI; its hot-path modules exist only as SPEC operations (the .cpp files
+ * are listed at proj/CMakeLists.txt:19-23,26 but absent).  Each entry below replaces one
+ * reference operation; the C++ drop-in headers in include/pamopt/ wrap them under the
+ * reference names:
+ *
+ *   pamopt_cu_mesh_*            IndexedMesh (mesh.hpp:18-33): f64 AoS vertices, i32 faces
+ *   pamopt_cu_compute_udf       build_hierarchy + compute_udf
+ *   pamopt_cu_udf_to_sdf        udf_to_sdf
+ *   pamopt_cu_hierarchy_pairs   VoxelHierarchy level view, debug/parity
+ *   pamopt_cu_dmc_extract       dual_mc::extract
+ *   pamopt_cu_self_intersections  detect_self_intersections
+ *   pamopt_cu_tri_tri_pairs     classify_pair + intersect_3d/intersect_coplanar
+ *   pamopt_cu_simplify          simplify_to
+ *   pamopt_cu_remesh            run_pipeline stages 1-2 (stage 3 excluded)
+ *
+ * Conventions.  Every function returns PAMOPT_CU_OK (0) or a negative status; the message
+ * of the last failure on the calling thread is pamopt_cu_last_error().  The C++ wrappers map
+ * PAMOPT_CU_EINVAL to std::invalid_argument (mesh.cpp:186-187,302) and the others to
+ * std::runtime_error.  A context binds one device and one CUDA stream; handles created from a
+ * context run on its stream.  Calls on distinct contexts are thread-safe.  Variable-size
+ * results are count-then-fill (pass NULL to get the count), mirroring the 2-kernel gather.
+ */
+#ifndef PAMOPT_CU_H_
+#define PAMOPT_CU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PAMOPT_CU_OK 0
+#define PAMOPT_CU_EINVAL -1   /* invalid argument / invalid mesh / out-of-range parameter */
+#define PAMOPT_CU_ECUDA -2    /* CUDA runtime failure */
+#define PAMOPT_CU_ENOMEM -3   /* device allocation failure */
+#define PAMOPT_CU_ENUMERIC -4 /* NaN edge cost */
+#define PAMOPT_CU_ECAP -5     /* a fixed per-element capacity was exceeded (valence > 255) */
+
+typedef struct pamopt_cu_ctx_s* pamopt_cu_ctx;
+typedef struct pamopt_cu_mesh_s* pamopt_cu_mesh;
+typedef struct pamopt_cu_grid_s* pamopt_cu_grid;
+
+/* simplify parameters */
+typedef struct {
+  double w_e;             /* edge-length weight, default 1e-3 */
+  double w_s;             /* skinny-triangle weight, default 5e-3 */
+  int32_t tolerance;      /* invalid-flag retention, default 4 */
+  int32_t stall_iterations; /* stall rule, default 10 */
+} pamopt_cu_simplify_params;
+
+typedef struct {
+  int64_t iterations;
+  int64_t collapses;
+  int64_t undone;
+  int64_t link_failures;
+  int64_t max_undo_rounds;
+  int64_t undo_hist[8]; /* batches needing k undo rounds (index 7 = 7 or more) */
+} pamopt_cu_simplify_stats;
+
+typedef struct {
+  float udf_ms;      /* build_hierarchy + compute_udf + udf_to_sdf */
+  float dmc_ms;      /* extract */
+  float simplify_ms; /* simplify_to incl. undo loops */
+  float total_ms;
+  int64_t dmc_faces;
+  int64_t dmc_vertices;
+} pamopt_cu_stage_times;
+
+const char* pamopt_cu_last_error(void);
+const char* pamopt_cu_version(void);
+
+/* ---- context ---------------------------------------------------------------------- */
+int pamopt_cu_ctx_create(int32_t device, pamopt_cu_ctx* out);
+int pamopt_cu_ctx_destroy(pamopt_cu_ctx ctx);
+/* the cudaStream_t the context launches on (for event timing by the caller) */
+void* pamopt_cu_ctx_stream(pamopt_cu_ctx ctx);
+int pamopt_cu_ctx_synchronize(pamopt_cu_ctx ctx);
+/* number of kernels this context launched since creation (telemetry) */
+int64_t pamopt_cu_ctx_launches(pamopt_cu_ctx ctx);
+
+/* ---- meshes (IndexedMesh) ------------------------------------------------------------ */
+int pamopt_cu_mesh_upload(pamopt_cu_ctx ctx, const double* vertices, int64_t nv,
+                          const int32_t* faces, int64_t nf, pamopt_cu_mesh* out);
+/* same, from device pointers (copied device-to-device) */
+int pamopt_cu_mesh_from_device(pamopt_cu_ctx ctx, const double* d_vertices, int64_t nv,
+                               const int32_t* d_faces, int64_t nf, pamopt_cu_mesh* out);
+int pamopt_cu_mesh_size(pamopt_cu_mesh mesh, int64_t* nv, int64_t* nf);
+int pamopt_cu_mesh_download(pamopt_cu_mesh mesh, double* vertices, int32_t* faces);
+int pamopt_cu_mesh_free(pamopt_cu_mesh mesh);
+
+/* ---- stage 1a: voxel_field --------------------------------------------------------- */
+/* R: power of two >= 8.  Returns the UDF lattice ((R+1)^3 f32, x-fastest, +INF sentinel). */
+int pamopt_cu_compute_udf(pamopt_cu_ctx ctx, pamopt_cu_mesh mesh, int32_t R, pamopt_cu_grid* out);
+/* in place; PAMOPT_CU_EINVAL unless sqrt(3)/(2R) <= eps <= 3/R - sqrt(3)/(2R) */
+int pamopt_cu_udf_to_sdf(pamopt_cu_grid grid, double eps);
+/* fused compute_udf + udf_to_sdf (the pipeline path) */
+int pamopt_cu_compute_sdf(pamopt_cu_ctx ctx, pamopt_cu_mesh mesh, int32_t R, double eps,
+                          pamopt_cu_grid* out);
+int pamopt_cu_grid_upload(pamopt_cu_ctx ctx, int32_t R, const float* samples, pamopt_cu_grid* out);
+int pamopt_cu_grid_resolution(pamopt_cu_grid grid, int32_t* R);
+int pamopt_cu_grid_download(pamopt_cu_grid grid, float* samples);
+int pamopt_cu_grid_free(pamopt_cu_grid grid);
+/* surviving (cell, triangle) pairs of hierarchy level r (8 <= r <= R), sorted by (cell, tri);
+ * pairs = int64[2*n] or NULL (count only).  Debug/parity view of build_hierarchy. */
+int pamopt_cu_hierarchy_pairs(pamopt_cu_ctx ctx, pamopt_cu_mesh mesh, int32_t R, int32_t r,
+                              int64_t* pairs, int64_t cap, int64_t* n);
+
+/* ---- stage 1b: dual_mc -------------------------------------------------------------- */
+int pamopt_cu_dmc_extract(pamopt_cu_grid sdf, double beta, pamopt_cu_mesh* out);
+/* active cells of the last extract on this grid: linear cell index, case, flip mask */
+int pamopt_cu_dmc_active_cells(pamopt_cu_grid sdf, int64_t* cells, uint8_t* cases,
+                               uint8_t* flips, int64_t cap, int64_t* n);
+/* the 256-entry patch table: per case {n, mask0..3, doubly-covered faces} (int32[256*6]) */
+int pamopt_cu_dmc_table(int32_t* out);
+
+/* ---- tri_isect ------------------------------------------------------------------------ */
+/* all intersecting face pairs (f1<f2), sorted; pairs = int32[2*n] or NULL */
+int pamopt_cu_self_intersections(pamopt_cu_mesh mesh, int32_t* pairs, int64_t cap, int64_t* n);
+/* narrow-phase verdict for explicit face pairs (host arrays) */
+int pamopt_cu_tri_tri_pairs(pamopt_cu_mesh mesh, const int32_t* pairs, int64_t n, int32_t* out);
+
+/* ---- stage 2: simplify ---------------------------------------------------------------- */
+/* in place; on success the mesh is compacted (mesh.cpp:278-292).  PAMOPT_CU_EINVAL for a
+ * non-manifold input.  per_iter_collapses may be NULL. */
+int pamopt_cu_simplify(pamopt_cu_mesh mesh, int64_t target_faces,
+                       const pamopt_cu_simplify_params* params, pamopt_cu_simplify_stats* stats,
+                       int64_t* per_iter_collapses, int64_t per_iter_cap);
+
+/* ---- pipeline: UDF -> SDF -> DMC -> QEM ------------------------------------------------ */
+int pamopt_cu_remesh(pamopt_cu_ctx ctx, pamopt_cu_mesh input, int32_t R, double eps, double beta,
+                     int64_t target_faces, const pamopt_cu_simplify_params* params,
+                     pamopt_cu_mesh* out, pamopt_cu_simplify_stats* stats,
+                     pamopt_cu_stage_times* times);
+/* same, host buffers in and out (the end-to-end entry the reference's caller would bind);
+ * out_vertices/out_faces must hold the returned sizes: call with NULL outputs first is NOT
+ * supported — the result is retained in the context until the next call and fetched with
+ * pamopt_cu_remesh_fetch. */
+int pamopt_cu_remesh_host(pamopt_cu_ctx ctx, const double* vertices, int64_t nv,
+                          const int32_t* faces, int64_t nf, int32_t R, double eps, double beta,
+                          int64_t target_faces, const pamopt_cu_simplify_params* params,
+                          int64_t* out_nv, int64_t* out_nf, pamopt_cu_simplify_stats* stats,
+                          pamopt_cu_stage_times* times);
+int pamopt_cu_remesh_fetch(pamopt_cu_ctx ctx, double* vertices, int32_t* faces);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PAMOPT_CU_H_ */

@@ -1,0 +1,119 @@
+"""ctypes binding of libpamopt_cu.so (the C-ABI in include/pamopt_cu.h).
+
+There is no fallback: if the shared library is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpamopt_cu.so")
+
+OK, EINVAL, ECUDA, ENOMEM, ENUMERIC, ECAP = 0, -1, -2, -3, -4, -5
+
+
+class SimplifyParams(C.Structure):
+    _fields_ = [("w_e", C.c_double), ("w_s", C.c_double), ("tolerance", C.c_int32),
+                ("stall_iterations", C.c_int32)]
+
+
+class SimplifyStats(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("collapses", C.c_int64), ("undone", C.c_int64),
+                ("link_failures", C.c_int64), ("max_undo_rounds", C.c_int64), ("undo_hist", C.c_int64 * 8)]
+
+    def as_dict(self) -> dict:
+        return {"iterations": self.iterations, "collapses": self.collapses, "undone": self.undone,
+                "link_failures": self.link_failures, "max_undo_rounds": self.max_undo_rounds,
+                "undo_hist": list(self.undo_hist)}
+
+
+class StageTimes(C.Structure):
+    _fields_ = [("udf_ms", C.c_float), ("dmc_ms", C.c_float), ("simplify_ms", C.c_float), ("total_ms", C.c_float),
+                ("dmc_faces", C.c_int64), ("dmc_vertices", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class PamoptError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class PamoptInvalidArgument(PamoptError, ValueError):
+    """Maps PAMOPT_CU_EINVAL (the reference's std::invalid_argument, mesh.cpp:186-187,302)."""
+
+
+_L = None
+
+vp = C.c_void_p
+i64 = C.c_int64
+i32 = C.c_int32
+dbl = C.c_double
+P = C.POINTER
+
+_SIGS = {
+    "pamopt_cu_last_error": (C.c_char_p, []),
+    "pamopt_cu_version": (C.c_char_p, []),
+    "pamopt_cu_ctx_create": (C.c_int, [i32, P(vp)]),
+    "pamopt_cu_ctx_destroy": (C.c_int, [vp]),
+    "pamopt_cu_ctx_stream": (vp, [vp]),
+    "pamopt_cu_ctx_synchronize": (C.c_int, [vp]),
+    "pamopt_cu_ctx_launches": (i64, [vp]),
+    "pamopt_cu_mesh_upload": (C.c_int, [vp, vp, i64, vp, i64, P(vp)]),
+    "pamopt_cu_mesh_from_device": (C.c_int, [vp, vp, i64, vp, i64, P(vp)]),
+    "pamopt_cu_mesh_size": (C.c_int, [vp, P(i64), P(i64)]),
+    "pamopt_cu_mesh_download": (C.c_int, [vp, vp, vp]),
+    "pamopt_cu_mesh_free": (C.c_int, [vp]),
+    "pamopt_cu_compute_udf": (C.c_int, [vp, vp, i32, P(vp)]),
+    "pamopt_cu_udf_to_sdf": (C.c_int, [vp, dbl]),
+    "pamopt_cu_compute_sdf": (C.c_int, [vp, vp, i32, dbl, P(vp)]),
+    "pamopt_cu_grid_upload": (C.c_int, [vp, i32, vp, P(vp)]),
+    "pamopt_cu_grid_resolution": (C.c_int, [vp, P(i32)]),
+    "pamopt_cu_grid_download": (C.c_int, [vp, vp]),
+    "pamopt_cu_grid_free": (C.c_int, [vp]),
+    "pamopt_cu_hierarchy_pairs": (C.c_int, [vp, vp, i32, i32, vp, i64, P(i64)]),
+    "pamopt_cu_dmc_extract": (C.c_int, [vp, dbl, P(vp)]),
+    "pamopt_cu_dmc_active_cells": (C.c_int, [vp, vp, vp, vp, i64, P(i64)]),
+    "pamopt_cu_dmc_table": (C.c_int, [vp]),
+    "pamopt_cu_self_intersections": (C.c_int, [vp, vp, i64, P(i64)]),
+    "pamopt_cu_tri_tri_pairs": (C.c_int, [vp, vp, i64, vp]),
+    "pamopt_cu_simplify": (C.c_int, [vp, i64, P(SimplifyParams), P(SimplifyStats), vp, i64]),
+    "pamopt_cu_remesh": (C.c_int, [vp, vp, i32, dbl, dbl, i64, P(SimplifyParams), P(vp), P(SimplifyStats),
+                                   P(StageTimes)]),
+    "pamopt_cu_remesh_host": (C.c_int, [vp, vp, i64, vp, i64, i32, dbl, dbl, i64, P(SimplifyParams), P(i64),
+                                        P(i64), P(SimplifyStats), P(StageTimes)]),
+    "pamopt_cu_remesh_fetch": (C.c_int, [vp, vp, vp]),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def lib():
+    global _L
+    if _L is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _L = L
+    return _L
+
+
+def check(rc: int) -> None:
+    if rc != OK:
+        msg = lib().pamopt_cu_last_error().decode()
+        if rc == EINVAL:
+            raise PamoptInvalidArgument(rc, msg)
+        raise PamoptError(rc, msg)
+
+
+def ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)

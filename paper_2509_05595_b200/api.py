@@ -1,0 +1,291 @@
+"""Python host mirror of the reference's SPEC operations over the C-ABI (libpamopt_cu.so).
+
+Names follow the reference (SPEC.md `[OP]`s / proj/include/pamopt): `compute_udf`,
+`udf_to_sdf`, `build_hierarchy` (debug view), `extract`, `detect_self_intersections`,
+`simplify_to`, `run_pipeline`.  Everything runs on the GPU; errors surface as
+`PamoptInvalidArgument` (std::invalid_argument in the reference) or `PamoptError`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib, ptr
+
+DEFAULT_BETA = 5.0
+DEFAULT_WE = 1e-3
+DEFAULT_WS = 5e-3
+DEFAULT_TOL = 4
+
+
+def default_eps(R: int) -> float:
+    return 0.9 / R
+
+
+class Context:
+    """One device + one CUDA stream (pamopt_cu_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().pamopt_cu_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    @property
+    def stream(self) -> int:
+        return int(lib().pamopt_cu_ctx_stream(self.h) or 0)
+
+    def synchronize(self) -> None:
+        check(lib().pamopt_cu_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().pamopt_cu_ctx_launches(self.h))
+
+    def close(self) -> None:
+        if self.h:
+            lib().pamopt_cu_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class DeviceMesh:
+    """Device-resident IndexedMesh (mesh.hpp:18-33)."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    @classmethod
+    def upload(cls, vertices, faces, ctx: Context | None = None) -> "DeviceMesh":
+        ctx = ctx or default_context()
+        v = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+        f = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
+        h = C.c_void_p()
+        check(lib().pamopt_cu_mesh_upload(ctx.h, ptr(v), len(v), ptr(f), len(f), C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def from_device(cls, vptr: int, nv: int, fptr: int, nf: int, ctx: Context | None = None) -> "DeviceMesh":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib().pamopt_cu_mesh_from_device(ctx.h, C.c_void_p(vptr), nv, C.c_void_p(fptr), nf, C.byref(h)))
+        return cls(h, ctx)
+
+    def size(self):
+        nv, nf = C.c_int64(), C.c_int64()
+        check(lib().pamopt_cu_mesh_size(self.h, C.byref(nv), C.byref(nf)))
+        return nv.value, nf.value
+
+    def download(self):
+        nv, nf = self.size()
+        v = np.empty((nv, 3), np.float64)
+        f = np.empty((nf, 3), np.int32)
+        check(lib().pamopt_cu_mesh_download(self.h, ptr(v), ptr(f)))
+        return v, f
+
+    def free(self):
+        if self.h:
+            lib().pamopt_cu_mesh_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class DeviceGrid:
+    """Device-resident ScalarGrid ((R+1)^3 f32, x-fastest)."""
+
+    def __init__(self, handle, ctx: Context, R: int):
+        self.h = handle
+        self.ctx = ctx
+        self.R = R
+
+    @classmethod
+    def upload(cls, samples, R: int, ctx: Context | None = None) -> "DeviceGrid":
+        ctx = ctx or default_context()
+        s = np.ascontiguousarray(samples, np.float32).ravel()
+        assert s.size == (R + 1) ** 3
+        h = C.c_void_p()
+        check(lib().pamopt_cu_grid_upload(ctx.h, R, ptr(s), C.byref(h)))
+        return cls(h, ctx, R)
+
+    def download(self) -> np.ndarray:
+        out = np.empty((self.R + 1) ** 3, np.float32)
+        check(lib().pamopt_cu_grid_download(self.h, ptr(out)))
+        return out
+
+    def free(self):
+        if self.h:
+            lib().pamopt_cu_grid_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _mesh(m, ctx=None) -> DeviceMesh:
+    if isinstance(m, DeviceMesh):
+        return m
+    v, f = m
+    return DeviceMesh.upload(v, f, ctx)
+
+
+# ------------------------------------------------------------------ voxel_field (stage 1a)
+def compute_udf(mesh, R: int, ctx: Context | None = None) -> DeviceGrid:
+    """build_hierarchy + compute_udf."""
+    m = _mesh(mesh, ctx)
+    h = C.c_void_p()
+    check(lib().pamopt_cu_compute_udf(m.ctx.h, m.h, int(R), C.byref(h)))
+    return DeviceGrid(h, m.ctx, R)
+
+
+def udf_to_sdf(grid: DeviceGrid, eps: float | None = None) -> DeviceGrid:
+    """In place."""
+    check(lib().pamopt_cu_udf_to_sdf(grid.h, default_eps(grid.R) if eps is None else float(eps)))
+    return grid
+
+
+def compute_sdf(mesh, R: int, eps: float | None = None, ctx: Context | None = None) -> DeviceGrid:
+    m = _mesh(mesh, ctx)
+    h = C.c_void_p()
+    check(lib().pamopt_cu_compute_sdf(m.ctx.h, m.h, int(R), default_eps(R) if eps is None else float(eps),
+                                      C.byref(h)))
+    return DeviceGrid(h, m.ctx, R)
+
+
+def build_hierarchy_pairs(mesh, R: int, r: int, ctx: Context | None = None) -> np.ndarray:
+    """Surviving (cell, tri) pairs of level r, sorted (VoxelHierarchy view)."""
+    m = _mesh(mesh, ctx)
+    n = C.c_int64()
+    check(lib().pamopt_cu_hierarchy_pairs(m.ctx.h, m.h, int(R), int(r), None, 0, C.byref(n)))
+    out = np.empty((n.value, 2), np.int64)
+    check(lib().pamopt_cu_hierarchy_pairs(m.ctx.h, m.h, int(R), int(r), ptr(out), n.value, C.byref(n)))
+    return out
+
+
+# ------------------------------------------------------------------ dual_mc (stage 1b)
+def extract(grid: DeviceGrid, beta: float = DEFAULT_BETA) -> DeviceMesh:
+    """dual_mc::extract."""
+    h = C.c_void_p()
+    check(lib().pamopt_cu_dmc_extract(grid.h, float(beta), C.byref(h)))
+    return DeviceMesh(h, grid.ctx)
+
+
+def dmc_active_cells(grid: DeviceGrid):
+    n = C.c_int64()
+    check(lib().pamopt_cu_dmc_active_cells(grid.h, None, None, None, 0, C.byref(n)))
+    cells = np.empty(n.value, np.int64)
+    cases = np.empty(n.value, np.uint8)
+    flips = np.empty(n.value, np.uint8)
+    check(lib().pamopt_cu_dmc_active_cells(grid.h, ptr(cells), ptr(cases), ptr(flips), n.value, C.byref(n)))
+    return cells, cases, flips
+
+
+def dmc_table() -> np.ndarray:
+    out = np.empty(256 * 6, np.int32)
+    check(lib().pamopt_cu_dmc_table(ptr(out)))
+    return out.reshape(256, 6)
+
+
+# ------------------------------------------------------------------ tri_isect
+def detect_self_intersections(mesh, ctx: Context | None = None) -> np.ndarray:
+    """Sorted (f1<f2) intersecting face pairs."""
+    m = _mesh(mesh, ctx)
+    n = C.c_int64()
+    check(lib().pamopt_cu_self_intersections(m.h, None, 0, C.byref(n)))
+    out = np.empty((n.value, 2), np.int32)
+    check(lib().pamopt_cu_self_intersections(m.h, ptr(out), n.value, C.byref(n)))
+    return out
+
+
+def tri_tri_pairs(mesh, pairs, ctx: Context | None = None) -> np.ndarray:
+    m = _mesh(mesh, ctx)
+    p = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    out = np.empty(len(p), np.int32)
+    check(lib().pamopt_cu_tri_tri_pairs(m.h, ptr(p), len(p), ptr(out)))
+    return out
+
+
+# ------------------------------------------------------------------ simplify (stage 2)
+def _params(we, ws, tolerance, stall=10) -> _lib.SimplifyParams:
+    return _lib.SimplifyParams(float(we), float(ws), int(tolerance), int(stall))
+
+
+def simplify_to(mesh, target_faces: int, we: float = DEFAULT_WE, ws: float = DEFAULT_WS,
+                tolerance: int = DEFAULT_TOL, ctx: Context | None = None, per_iter_cap: int = 100000):
+    """simplify_to.  Simplifies a DeviceMesh in place; returns (mesh, stats)."""
+    m = _mesh(mesh, ctx)
+    st = _lib.SimplifyStats()
+    per = np.zeros(per_iter_cap, np.int64)
+    p = _params(we, ws, tolerance)
+    check(lib().pamopt_cu_simplify(m.h, int(target_faces), C.byref(p), C.byref(st), ptr(per), per_iter_cap))
+    stats = st.as_dict()
+    stats["per_iter_collapses"] = per[: stats["iterations"]].copy()
+    return m, stats
+
+
+# ------------------------------------------------------------------ pipeline (stages 1-2)
+@dataclass
+class RemeshResult:
+    vertices: np.ndarray
+    faces: np.ndarray
+    stats: dict = field(default_factory=dict)
+    times: dict = field(default_factory=dict)
+
+
+def run_pipeline(vertices, faces, R: int, target_faces: int, eps: float | None = None,
+                 beta: float = DEFAULT_BETA, we: float = DEFAULT_WE, ws: float = DEFAULT_WS,
+                 tolerance: int = DEFAULT_TOL, ctx: Context | None = None) -> RemeshResult:
+    """UDF -> SDF -> DMC -> QEM (run_pipeline stages 1-2) through the host
+    C-ABI entry (pamopt_cu_remesh_host): host arrays in, host arrays out."""
+    ctx = ctx or default_context()
+    v = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+    f = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
+    nv, nf = C.c_int64(), C.c_int64()
+    st = _lib.SimplifyStats()
+    tm = _lib.StageTimes()
+    p = _params(we, ws, tolerance)
+    check(lib().pamopt_cu_remesh_host(ctx.h, ptr(v), len(v), ptr(f), len(f), int(R),
+                                      default_eps(R) if eps is None else float(eps), float(beta), int(target_faces),
+                                      C.byref(p), C.byref(nv), C.byref(nf), C.byref(st), C.byref(tm)))
+    vo = np.empty((nv.value, 3), np.float64)
+    fo = np.empty((nf.value, 3), np.int32)
+    check(lib().pamopt_cu_remesh_fetch(ctx.h, ptr(vo), ptr(fo)))
+    return RemeshResult(vo, fo, st.as_dict(), tm.as_dict())
+
+
+def remesh_device(mesh: DeviceMesh, R: int, target_faces: int, eps: float | None = None, beta: float = DEFAULT_BETA,
+                  we: float = DEFAULT_WE, ws: float = DEFAULT_WS, tolerance: int = DEFAULT_TOL):
+    """Device-resident pipeline (pamopt_cu_remesh): returns (DeviceMesh, stats, times)."""
+    h = C.c_void_p()
+    st = _lib.SimplifyStats()
+    tm = _lib.StageTimes()
+    p = _params(we, ws, tolerance)
+    check(lib().pamopt_cu_remesh(mesh.ctx.h, mesh.h, int(R), default_eps(R) if eps is None else float(eps),
+                                 float(beta), int(target_faces), C.byref(p), C.byref(h), C.byref(st), C.byref(tm)))
+    return DeviceMesh(h, mesh.ctx), st.as_dict(), tm.as_dict()

@@ -1,0 +1,507 @@
+// capi.cu — the extern "C" boundary (include/pamopt_cu.h).  Translates C++ exceptions into
+// status codes + a thread-local message, owns the device-resident handles, and hosts the
+// CUB-backed scan/sort helpers shared by the modules.
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+struct pamopt_cu_ctx_s {
+  pcu::Ctx ctx;
+};
+
+struct pamopt_cu_mesh_s {
+  pamopt_cu_ctx owner;
+  pcu::DevBuf<double> V;
+  pcu::DevBuf<int32_t> F;
+  int64_t nv = 0, nf = 0;
+};
+
+struct pamopt_cu_grid_s {
+  pamopt_cu_ctx owner;
+  int32_t R = 0;
+  pcu::DevBuf<float> g;
+  pcu::DmcResult last;  // debug view of the last extract
+};
+
+namespace pcu {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+template <class Fn>
+static int guarded(Fn&& fn) {
+  try {
+    fn();
+    return PAMOPT_CU_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return PAMOPT_CU_ECUDA;
+  }
+}
+
+// ------------------------------------------------------------------------- CUB helpers
+static void* tmp_storage(Ctx& ctx, size_t bytes) {
+  if (bytes > ctx.scratch_bytes) {
+    if (ctx.scratch) cudaFreeAsync(ctx.scratch, ctx.stream);
+    ctx.scratch_bytes = bytes + bytes / 2 + 4096;
+    PCU_CUDA(cudaMallocAsync(&ctx.scratch, ctx.scratch_bytes, ctx.stream));
+  }
+  return ctx.scratch;
+}
+
+void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n) {
+  if (n <= 0) return;
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, n, ctx.stream);
+  void* t = tmp_storage(ctx, need);
+  PCU_CUDA(cub::DeviceScan::ExclusiveSum(t, need, in, out, n, ctx.stream));
+  ++ctx.launches;
+}
+
+void exclusive_scan_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n) {
+  if (n <= 0) return;
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, n, ctx.stream);
+  void* t = tmp_storage(ctx, need);
+  PCU_CUDA(cub::DeviceScan::ExclusiveSum(t, need, in, out, n, ctx.stream));
+  ++ctx.launches;
+}
+
+void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit) {
+  if (n <= 1) return;
+  DevBuf<uint64_t> alt(n, ctx.stream);
+  cub::DoubleBuffer<uint64_t> db(keys, alt.get());
+  size_t need = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, need, db, static_cast<int>(n), 0, end_bit, ctx.stream);
+  void* t = tmp_storage(ctx, need);
+  PCU_CUDA(cub::DeviceRadixSort::SortKeys(t, need, db, static_cast<int>(n), 0, end_bit, ctx.stream));
+  ++ctx.launches;
+  if (db.Current() != keys)
+    PCU_CUDA(cudaMemcpyAsync(keys, db.Current(), n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
+}  // namespace pcu
+
+using pcu::guarded;
+
+static void check_ctx(pamopt_cu_ctx c) { PCU_REQUIRE(c != nullptr, PAMOPT_CU_EINVAL, "null context"); }
+
+extern "C" {
+
+const char* pamopt_cu_last_error(void) { return pcu::g_last_error.c_str(); }
+const char* pamopt_cu_version(void) { return "pamopt_cu 0.1 (sm_100a)"; }
+
+int pamopt_cu_ctx_create(int32_t device, pamopt_cu_ctx* out) {
+  return guarded([&] {
+    PCU_REQUIRE(out != nullptr, PAMOPT_CU_EINVAL, "null output");
+    int n = 0;
+    PCU_CUDA(cudaGetDeviceCount(&n));
+    PCU_REQUIRE(device >= 0 && device < n, PAMOPT_CU_EINVAL, "no such CUDA device");
+    auto* c = new pamopt_cu_ctx_s();
+    c->ctx.device = device;
+    pcu::DeviceGuard g(device);
+    PCU_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
+    PCU_CUDA(cudaDeviceGetAttribute(&c->ctx.num_sms, cudaDevAttrMultiProcessorCount, device));
+    cudaMemPool_t pool;
+    PCU_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~0ull;  // keep freed blocks cached in the pool
+    PCU_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = c;
+  });
+}
+
+int pamopt_cu_ctx_destroy(pamopt_cu_ctx c) {
+  return guarded([&] {
+    if (!c) return;
+    pcu::DeviceGuard g(c->ctx.device);
+    if (c->ctx.scratch) cudaFreeAsync(c->ctx.scratch, c->ctx.stream);
+    cudaStreamSynchronize(c->ctx.stream);
+    cudaStreamDestroy(c->ctx.stream);
+    delete c;
+  });
+}
+
+void* pamopt_cu_ctx_stream(pamopt_cu_ctx c) { return c ? static_cast<void*>(c->ctx.stream) : nullptr; }
+
+int pamopt_cu_ctx_synchronize(pamopt_cu_ctx c) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_CUDA(cudaStreamSynchronize(c->ctx.stream));
+  });
+}
+
+int64_t pamopt_cu_ctx_launches(pamopt_cu_ctx c) { return c ? c->ctx.launches : 0; }
+
+// ---------------------------------------------------------------------------- meshes
+static int mesh_create(pamopt_cu_ctx c, const double* v, int64_t nv, const int32_t* f, int64_t nf,
+                       cudaMemcpyKind kind, pamopt_cu_mesh* out) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(out && nv >= 0 && nf >= 0 && (nv == 0 || v) && (nf == 0 || f), PAMOPT_CU_EINVAL, "bad mesh arguments");
+    pcu::DeviceGuard g(c->ctx.device);
+    auto* m = new pamopt_cu_mesh_s();
+    m->owner = c;
+    m->nv = nv;
+    m->nf = nf;
+    m->V.alloc(3 * (nv ? nv : 1), c->ctx.stream);
+    m->F.alloc(3 * (nf ? nf : 1), c->ctx.stream);
+    if (nv) PCU_CUDA(cudaMemcpyAsync(m->V.get(), v, 3 * nv * sizeof(double), kind, c->ctx.stream));
+    if (nf) PCU_CUDA(cudaMemcpyAsync(m->F.get(), f, 3 * nf * sizeof(int32_t), kind, c->ctx.stream));
+    *out = m;
+  });
+}
+
+int pamopt_cu_mesh_upload(pamopt_cu_ctx c, const double* v, int64_t nv, const int32_t* f, int64_t nf,
+                          pamopt_cu_mesh* out) {
+  return mesh_create(c, v, nv, f, nf, cudaMemcpyHostToDevice, out);
+}
+
+int pamopt_cu_mesh_from_device(pamopt_cu_ctx c, const double* v, int64_t nv, const int32_t* f, int64_t nf,
+                               pamopt_cu_mesh* out) {
+  return mesh_create(c, v, nv, f, nf, cudaMemcpyDeviceToDevice, out);
+}
+
+int pamopt_cu_mesh_size(pamopt_cu_mesh m, int64_t* nv, int64_t* nf) {
+  return guarded([&] {
+    PCU_REQUIRE(m != nullptr, PAMOPT_CU_EINVAL, "null mesh");
+    if (nv) *nv = m->nv;
+    if (nf) *nf = m->nf;
+  });
+}
+
+int pamopt_cu_mesh_download(pamopt_cu_mesh m, double* v, int32_t* f) {
+  return guarded([&] {
+    PCU_REQUIRE(m != nullptr, PAMOPT_CU_EINVAL, "null mesh");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    if (v && m->nv) PCU_CUDA(cudaMemcpyAsync(v, m->V.get(), 3 * m->nv * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    if (f && m->nf) PCU_CUDA(cudaMemcpyAsync(f, m->F.get(), 3 * m->nf * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+int pamopt_cu_mesh_free(pamopt_cu_mesh m) {
+  return guarded([&] {
+    if (!m) return;
+    pcu::DeviceGuard g(m->owner->ctx.device);
+    delete m;
+  });
+}
+
+// ---------------------------------------------------------------------------- stage 1a
+static void check_R(int32_t R) {
+  PCU_REQUIRE(R >= 8 && R <= 2048 && (R & (R - 1)) == 0, PAMOPT_CU_EINVAL, "R must be a power of two in [8, 2048]");
+}
+
+static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, double eps, pamopt_cu_grid* out) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(m && out, PAMOPT_CU_EINVAL, "null argument");
+    check_R(R);
+    if (mode == 1) {
+      const double lo = 0.8660254037844386 / R, hi = 3.0 / R - 0.8660254037844386 / R;
+      PCU_REQUIRE(eps >= lo && eps <= hi, PAMOPT_CU_EINVAL, "udf_to_sdf: epsilon out of range");
+    }
+    pcu::DeviceGuard g(c->ctx.device);
+    auto* gr = new pamopt_cu_grid_s();
+    gr->owner = c;
+    gr->R = R;
+    const int64_t n1 = R + 1;
+    gr->g.alloc(n1 * n1 * n1, c->ctx.stream);
+    try {
+      pcu::udf_run(c->ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, mode, eps, gr->g.get());
+    } catch (...) {
+      delete gr;
+      throw;
+    }
+    *out = gr;
+  });
+}
+
+int pamopt_cu_compute_udf(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, pamopt_cu_grid* out) {
+  return make_grid(c, m, R, 0, 0.0, out);
+}
+
+int pamopt_cu_compute_sdf(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, double eps, pamopt_cu_grid* out) {
+  return make_grid(c, m, R, 1, eps, out);
+}
+
+int pamopt_cu_udf_to_sdf(pamopt_cu_grid gr, double eps) {
+  return guarded([&] {
+    PCU_REQUIRE(gr != nullptr, PAMOPT_CU_EINVAL, "null grid");
+    const int R = gr->R;
+    const double lo = 0.8660254037844386 / R, hi = 3.0 / R - 0.8660254037844386 / R;
+    PCU_REQUIRE(eps >= lo && eps <= hi, PAMOPT_CU_EINVAL, "udf_to_sdf: epsilon out of range");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    const int64_t n1 = R + 1;
+    pcu::udf_to_sdf_inplace(ctx, gr->g.get(), n1 * n1 * n1, eps);
+  });
+}
+
+int pamopt_cu_grid_upload(pamopt_cu_ctx c, int32_t R, const float* samples, pamopt_cu_grid* out) {
+  return guarded([&] {
+    check_ctx(c);
+    check_R(R);
+    PCU_REQUIRE(samples && out, PAMOPT_CU_EINVAL, "null argument");
+    pcu::DeviceGuard g(c->ctx.device);
+    auto* gr = new pamopt_cu_grid_s();
+    gr->owner = c;
+    gr->R = R;
+    const int64_t n1 = R + 1;
+    gr->g.alloc(n1 * n1 * n1, c->ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(gr->g.get(), samples, n1 * n1 * n1 * sizeof(float), cudaMemcpyHostToDevice, c->ctx.stream));
+    *out = gr;
+  });
+}
+
+int pamopt_cu_grid_resolution(pamopt_cu_grid gr, int32_t* R) {
+  return guarded([&] {
+    PCU_REQUIRE(gr && R, PAMOPT_CU_EINVAL, "null argument");
+    *R = gr->R;
+  });
+}
+
+int pamopt_cu_grid_download(pamopt_cu_grid gr, float* samples) {
+  return guarded([&] {
+    PCU_REQUIRE(gr && samples, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    const int64_t n1 = gr->R + 1;
+    PCU_CUDA(cudaMemcpyAsync(samples, gr->g.get(), n1 * n1 * n1 * sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+int pamopt_cu_grid_free(pamopt_cu_grid gr) {
+  return guarded([&] {
+    if (!gr) return;
+    pcu::DeviceGuard g(gr->owner->ctx.device);
+    delete gr;
+  });
+}
+
+int pamopt_cu_hierarchy_pairs(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int32_t r, int64_t* pairs, int64_t cap,
+                              int64_t* n) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(m && n, PAMOPT_CU_EINVAL, "null argument");
+    pcu::DeviceGuard g(c->ctx.device);
+    const std::vector<int64_t> h = pcu::hierarchy_pairs(c->ctx, m->V.get(), m->F.get(), m->nf, R, r);
+    *n = static_cast<int64_t>(h.size() / 2);
+    if (pairs) std::memcpy(pairs, h.data(), std::min<int64_t>(cap, *n) * 2 * sizeof(int64_t));
+  });
+}
+
+// ---------------------------------------------------------------------------- stage 1b
+int pamopt_cu_dmc_extract(pamopt_cu_grid gr, double beta, pamopt_cu_mesh* out) {
+  return guarded([&] {
+    PCU_REQUIRE(gr && out, PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(beta > 0.0, PAMOPT_CU_EINVAL, "beta must be positive");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    gr->last = pcu::DmcResult();
+    pcu::dmc_extract(ctx, gr->g.get(), gr->R, beta, gr->last);
+    auto* m = new pamopt_cu_mesh_s();
+    m->owner = gr->owner;
+    m->nv = static_cast<int64_t>(gr->last.nv);
+    m->nf = static_cast<int64_t>(gr->last.nf);
+    m->V = std::move(gr->last.V);
+    m->F = std::move(gr->last.F);
+    *out = m;
+  });
+}
+
+int pamopt_cu_dmc_active_cells(pamopt_cu_grid gr, int64_t* cells, uint8_t* cases, uint8_t* flips, int64_t cap,
+                               int64_t* n) {
+  return guarded([&] {
+    PCU_REQUIRE(gr && n, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    const int64_t na = gr->last.n_active;
+    *n = na;
+    const int64_t k = std::min(cap, na);
+    if (k <= 0) return;
+    std::vector<uint32_t> c32(k);
+    PCU_CUDA(cudaMemcpyAsync(c32.data(), gr->last.cells.get(), k * 4, cudaMemcpyDeviceToHost, ctx.stream));
+    if (cases) PCU_CUDA(cudaMemcpyAsync(cases, gr->last.cases.get(), k, cudaMemcpyDeviceToHost, ctx.stream));
+    if (flips) PCU_CUDA(cudaMemcpyAsync(flips, gr->last.flips.get(), k, cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (cells)
+      for (int64_t i = 0; i < k; ++i) cells[i] = c32[i];
+  });
+}
+
+int pamopt_cu_dmc_table(int32_t* out) {
+  return guarded([&] {
+    PCU_REQUIRE(out != nullptr, PAMOPT_CU_EINVAL, "null argument");
+    pcu::dmc_table_host(out);
+  });
+}
+
+// -------------------------------------------------------------------------- tri_isect
+int pamopt_cu_self_intersections(pamopt_cu_mesh m, int32_t* pairs, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    PCU_REQUIRE(m && n, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    const std::vector<int32_t> h = pcu::self_intersections(ctx, m->V.get(), m->nv, m->F.get(), m->nf, nullptr, nullptr);
+    *n = static_cast<int64_t>(h.size() / 2);
+    if (pairs) std::memcpy(pairs, h.data(), std::min<int64_t>(cap, *n) * 2 * sizeof(int32_t));
+  });
+}
+
+int pamopt_cu_tri_tri_pairs(pamopt_cu_mesh m, const int32_t* pairs, int64_t n, int32_t* out) {
+  return guarded([&] {
+    PCU_REQUIRE(m && (n == 0 || (pairs && out)), PAMOPT_CU_EINVAL, "null argument");
+    if (n == 0) return;
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    for (int64_t i = 0; i < 2 * n; ++i)
+      PCU_REQUIRE(pairs[i] >= 0 && pairs[i] < m->nf, PAMOPT_CU_EINVAL, "face index out of range");
+    pcu::DevBuf<int32_t> dp(2 * n, ctx.stream), dout(n, ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(dp.get(), pairs, 2 * n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx.stream));
+    pcu::tri_tri_pairs(ctx, m->V.get(), m->F.get(), dp.get(), n, dout.get());
+    PCU_CUDA(cudaMemcpyAsync(out, dout.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+// ---------------------------------------------------------------------------- stage 2
+static pcu::SimplifyParams to_params(const pamopt_cu_simplify_params* p) {
+  pcu::SimplifyParams P;
+  if (p) {
+    P.we = p->w_e;
+    P.ws = p->w_s;
+    P.tolerance = p->tolerance;
+    P.stall = p->stall_iterations > 0 ? p->stall_iterations : 10;
+  }
+  PCU_REQUIRE(P.we >= 0 && P.ws >= 0 && P.tolerance >= 1, PAMOPT_CU_EINVAL, "bad simplify parameters");
+  return P;
+}
+
+static void to_stats(const pcu::SimplifyStats& S, pamopt_cu_simplify_stats* o) {
+  if (!o) return;
+  o->iterations = S.iterations;
+  o->collapses = S.collapses;
+  o->undone = S.undone;
+  o->link_failures = S.link_failures;
+  o->max_undo_rounds = S.max_undo_rounds;
+  for (int k = 0; k < 8; ++k) o->undo_hist[k] = S.undo_hist[k];
+}
+
+int pamopt_cu_simplify(pamopt_cu_mesh m, int64_t target, const pamopt_cu_simplify_params* params,
+                       pamopt_cu_simplify_stats* stats, int64_t* per_iter, int64_t per_iter_cap) {
+  return guarded([&] {
+    PCU_REQUIRE(m != nullptr, PAMOPT_CU_EINVAL, "null mesh");
+    const pcu::SimplifyParams P = to_params(params);
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    pcu::SimplifyStats S;
+    pcu::simplify_run(ctx, m->V, m->F, m->nv, m->nf, target, P, S);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    to_stats(S, stats);
+    if (per_iter)
+      for (int64_t i = 0; i < std::min<int64_t>(per_iter_cap, static_cast<int64_t>(S.per_iter.size())); ++i)
+        per_iter[i] = S.per_iter[i];
+  });
+}
+
+// ---------------------------------------------------------------------------- pipeline
+static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double eps, double beta, int64_t target,
+                        const pamopt_cu_simplify_params* params, pamopt_cu_mesh* out, pamopt_cu_simplify_stats* stats,
+                        pamopt_cu_stage_times* times) {
+  check_ctx(c);
+  PCU_REQUIRE(in && out, PAMOPT_CU_EINVAL, "null argument");
+  check_R(R);
+  const double lo = 0.8660254037844386 / R, hi = 3.0 / R - 0.8660254037844386 / R;
+  PCU_REQUIRE(eps >= lo && eps <= hi, PAMOPT_CU_EINVAL, "udf_to_sdf: epsilon out of range");
+  const pcu::SimplifyParams P = to_params(params);
+  pcu::Ctx& ctx = c->ctx;
+  pcu::DeviceGuard g(ctx.device);
+  cudaEvent_t ev[4];
+  for (auto& e : ev) PCU_CUDA(cudaEventCreate(&e));
+  PCU_CUDA(cudaEventRecord(ev[0], ctx.stream));
+  const int64_t n1 = R + 1;
+  pcu::DevBuf<float> sdf(n1 * n1 * n1, ctx.stream);
+  pcu::udf_run(ctx, in->V.get(), in->nv, in->F.get(), in->nf, R, 1, eps, sdf.get());
+  PCU_CUDA(cudaEventRecord(ev[1], ctx.stream));
+  pcu::DmcResult d;
+  pcu::dmc_extract(ctx, sdf.get(), R, beta, d);
+  sdf.release();
+  PCU_CUDA(cudaEventRecord(ev[2], ctx.stream));
+  auto* m = new pamopt_cu_mesh_s();
+  m->owner = c;
+  m->nv = static_cast<int64_t>(d.nv);
+  m->nf = static_cast<int64_t>(d.nf);
+  m->V = std::move(d.V);
+  m->F = std::move(d.F);
+  pcu::SimplifyStats S;
+  try {
+    pcu::simplify_run(ctx, m->V, m->F, m->nv, m->nf, target, P, S);
+  } catch (...) {
+    delete m;
+    throw;
+  }
+  PCU_CUDA(cudaEventRecord(ev[3], ctx.stream));
+  PCU_CUDA(cudaEventSynchronize(ev[3]));
+  if (times) {
+    PCU_CUDA(cudaEventElapsedTime(&times->udf_ms, ev[0], ev[1]));
+    PCU_CUDA(cudaEventElapsedTime(&times->dmc_ms, ev[1], ev[2]));
+    PCU_CUDA(cudaEventElapsedTime(&times->simplify_ms, ev[2], ev[3]));
+    PCU_CUDA(cudaEventElapsedTime(&times->total_ms, ev[0], ev[3]));
+    times->dmc_faces = static_cast<int64_t>(d.nf);
+    times->dmc_vertices = static_cast<int64_t>(d.nv);
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  to_stats(S, stats);
+  *out = m;
+}
+
+int pamopt_cu_remesh(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double eps, double beta, int64_t target,
+                     const pamopt_cu_simplify_params* params, pamopt_cu_mesh* out, pamopt_cu_simplify_stats* stats,
+                     pamopt_cu_stage_times* times) {
+  return guarded([&] { remesh_impl(c, in, R, eps, beta, target, params, out, stats, times); });
+}
+
+int pamopt_cu_remesh_host(pamopt_cu_ctx c, const double* v, int64_t nv, const int32_t* f, int64_t nf, int32_t R,
+                          double eps, double beta, int64_t target, const pamopt_cu_simplify_params* params,
+                          int64_t* out_nv, int64_t* out_nf, pamopt_cu_simplify_stats* stats,
+                          pamopt_cu_stage_times* times) {
+  pamopt_cu_mesh in = nullptr;
+  int rc = pamopt_cu_mesh_upload(c, v, nv, f, nf, &in);
+  if (rc) return rc;
+  rc = guarded([&] {
+    pamopt_cu_mesh out = nullptr;
+    remesh_impl(c, in, R, eps, beta, target, params, &out, stats, times);
+    pcu::Ctx& ctx = c->ctx;
+    ctx.host_v.resize(3 * out->nv);
+    ctx.host_f.resize(3 * out->nf);
+    if (out->nv) PCU_CUDA(cudaMemcpyAsync(ctx.host_v.data(), out->V.get(), 3 * out->nv * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (out->nf) PCU_CUDA(cudaMemcpyAsync(ctx.host_f.data(), out->F.get(), 3 * out->nf * 4, cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (out_nv) *out_nv = out->nv;
+    if (out_nf) *out_nf = out->nf;
+    delete out;
+  });
+  pamopt_cu_mesh_free(in);
+  return rc;
+}
+
+int pamopt_cu_remesh_fetch(pamopt_cu_ctx c, double* v, int32_t* f) {
+  return guarded([&] {
+    check_ctx(c);
+    if (v) std::memcpy(v, c->ctx.host_v.data(), c->ctx.host_v.size() * 8);
+    if (f) std::memcpy(f, c->ctx.host_f.data(), c->ctx.host_f.size() * 4);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,226 @@
+// common.cuh — shared runtime + device arithmetic of the B200 remesh path.
+//
+// Everything here compiles with `--fmad=false` (see build.py): every decision-bearing FP64
+// operation rounds exactly like the FP64 scalar code it mirrors, so integer outputs (candidate
+// lists, MC cases, DMC topology, collapse sets) are bit-identical to the checker.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pamopt_cu.h"
+
+namespace pcu {
+
+// ------------------------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PCU_CUDA(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      throw ::pcu::Error(_e == cudaErrorMemoryAllocation ? PAMOPT_CU_ENOMEM : PAMOPT_CU_ECUDA, \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e));            \
+  } while (0)
+
+#define PCU_REQUIRE(cond, code, msg) \
+  do {                               \
+    if (!(cond)) throw ::pcu::Error((code), (msg)); \
+  } while (0)
+
+void set_last_error(const std::string& m);
+
+// ------------------------------------------------------------------------------ context
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int num_sms = 148;
+  // scratch reused across calls
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  // last remesh_host result
+  std::vector<double> host_v;
+  std::vector<int32_t> host_f;
+};
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// stream-ordered device buffer
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) PCU_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+  }
+  // grow-only reallocation (contents not preserved)
+  void ensure(size_t count, cudaStream_t st) {
+    if (count > n || p == nullptr) alloc(count > 0 ? count : 1, st);
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  T* get() const { return p; }
+  void memset(int v, cudaStream_t st) {
+    if (n) PCU_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), st));
+  }
+};
+
+inline unsigned grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 0x7fffffff) g = 0x7fffffff;
+  return static_cast<unsigned>(g);
+}
+
+#define PCU_LAUNCH(ctx, kernel, grid, block, smem, ...)                       \
+  do {                                                                        \
+    kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);           \
+    ++(ctx).launches;                                                         \
+    PCU_CUDA(cudaGetLastError());                                             \
+  } while (0)
+
+// ------------------------------------------------------------------- CUB-backed helpers
+// exclusive scan of n elements (in -> out), returns nothing; out may alias in.
+void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n);
+void exclusive_scan_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n);
+void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit = 64);
+template <class T>
+T read_scalar(Ctx& ctx, const T* dptr) {
+  T h;
+  PCU_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
+  PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  return h;
+}
+
+// --------------------------------------------------------------------- device geometry
+struct D3 {
+  double x, y, z;
+};
+
+__host__ __device__ __forceinline__ D3 d3(double x, double y, double z) { return D3{x, y, z}; }
+__host__ __device__ __forceinline__ D3 sub(D3 a, D3 b) { return D3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+// (x0*y0 + x1*y1) + x2*y2 — the Eigen fixed-size redux order (oracle/eigen_shim)
+__host__ __device__ __forceinline__ double dot(D3 a, D3 b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; }
+__host__ __device__ __forceinline__ double sqn(D3 a) { return dot(a, a); }
+__host__ __device__ __forceinline__ D3 cross(D3 a, D3 b) {
+  return D3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__host__ __device__ __forceinline__ D3 axpy(D3 a, double t, D3 d) {  // a + t*d
+  return D3{a.x + t * d.x, a.y + t * d.y, a.z + t * d.z};
+}
+
+// point–segment squared distance (distance.cpp:10-21)
+__device__ __forceinline__ double pseg_sq(D3 p, D3 a, D3 b) {
+  const D3 ab = sub(b, a);
+  const double denom = sqn(ab);
+  double t = denom > 0.0 ? dot(sub(p, a), ab) / denom : 0.0;
+  t = t < 0.0 ? 0.0 : (1.0 < t ? 1.0 : t);
+  return sqn(sub(p, axpy(a, t, ab)));
+}
+
+// point–triangle squared distance (distance.cpp:26-79): face candidate then edges, strict '<'
+__device__ __forceinline__ double ptri_sq(D3 p, D3 a, D3 b, D3 c) {
+  const D3 n = cross(sub(b, a), sub(c, a));
+  const double nn = sqn(n);
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  if (nn > 0.0) {
+    const D3 ap = sub(p, a);
+    const double dist_n = dot(ap, n);
+    const double s = dist_n / nn;
+    const D3 proj = D3{p.x - s * n.x, p.y - s * n.y, p.z - s * n.z};
+    const D3 v0 = sub(b, a), v1 = sub(c, a), v2 = sub(proj, a);
+    const double d00 = sqn(v0), d01 = dot(v0, v1), d11 = sqn(v1);
+    const double d20 = dot(v2, v0), d21 = dot(v2, v1);
+    const double denom = d00 * d11 - d01 * d01;
+    if (denom > 0.0) {
+      const double v = (d11 * d20 - d01 * d21) / denom;
+      const double w = (d00 * d21 - d01 * d20) / denom;
+      if (v >= 0.0 && w >= 0.0 && v + w <= 1.0) best = dist_n * dist_n / nn;
+    }
+  }
+  const double e0 = pseg_sq(p, a, b);
+  if (e0 < best) best = e0;
+  const double e1 = pseg_sq(p, b, c);
+  if (e1 < best) best = e1;
+  const double e2 = pseg_sq(p, c, a);
+  if (e2 < best) best = e2;
+  return best;
+}
+
+// ------------------------------------------------------------- pinned exp and sigmoid
+// exp(x) = p(r) * 2^k, k = floor(x log2e + 1/2), r = (x - k ln2_hi) - k ln2_lo,
+// p = degree-13 Taylor polynomial (Horner), 2^k assembled from bits (two steps below
+// 2^-1022).  The DMC sigmoid t' = 1/(1+exp(-beta(t-1/2))) is evaluated with
+// this exact op sequence so patch vertices are reproducible bit for bit.
+__device__ __forceinline__ double pow2i(int k) {
+  return __longlong_as_double(static_cast<long long>(k + 1023) << 52);
+}
+__device__ __forceinline__ double det_exp(double x) {
+  if (x != x) return x;
+  if (x > 709.0) return __longlong_as_double(0x7ff0000000000000ll);
+  if (x < -745.0) return 0.0;
+  const double kd = floor(x * 1.4426950408889634 + 0.5);
+  const int k = static_cast<int>(kd);
+  const double r = (x - kd * 6.93147180369123816490e-01) - kd * 1.90821492927058770002e-10;
+  double p = 1.6059043836821613e-10;
+  p = p * r + 2.0876756987868100e-09;
+  p = p * r + 2.5052108385441720e-08;
+  p = p * r + 2.7557319223985888e-07;
+  p = p * r + 2.7557319223985893e-06;
+  p = p * r + 2.4801587301587302e-05;
+  p = p * r + 1.9841269841269841e-04;
+  p = p * r + 1.3888888888888889e-03;
+  p = p * r + 8.3333333333333332e-03;
+  p = p * r + 4.1666666666666664e-02;
+  p = p * r + 1.6666666666666666e-01;
+  p = p * r + 0.5;
+  p = p * r + 1.0;
+  p = p * r + 1.0;
+  if (k >= -1022) return p * pow2i(k);
+  return (p * pow2i(k + 600)) * pow2i(-600);
+}
+__device__ __forceinline__ double sigmoid_t(double t, double beta) {
+  return 1.0 / (1.0 + det_exp(-beta * (t - 0.5)));
+}
+
+}  // namespace pcu

@@ -1,0 +1,485 @@
+// dmc.cu — stage 1b: Dual Marching Cubes with the paper's intersection corrections
+// (PAPER.md:85-114,716-772), as count/write ("2-kernel gather") passes with
+// deterministic prefix sums so the output order never depends on scheduling.
+//
+//   classify   dense scan of the R^3 cells, 2048 cells per CTA: per-CTA active counts, an
+//              exclusive scan, then an ordered block-scan compaction -> active cells (x-fastest)
+//   patches    per active cell: case, the C16/C19 flip mask (neighbour rule),
+//              patch count -> scan -> patch vertices (sigmoid-smoothed crossings, centroid)
+//   quads      per active cell and axis: the interior valid edge at its corner 0 -> quad from
+//              the 4 cells' patches (dense cell -> active-id map), orientation, envelope
+//              concavity split decision -> (faces, extra vertices) counts -> scan -> write
+// The 256-entry patch table is generated on the host at load time (faces paired around
+// positive corners on ambiguous faces; cycles of the pairing graph are patches) and placed in
+// constant memory together with the doubly-covered-face masks and the flipped variants.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pcu {
+namespace {
+
+struct PatchSet {
+  uint8_t n;
+  uint8_t dc;
+  uint16_t mask[4];
+  int8_t edge_patch[12];
+};
+
+__constant__ PatchSet c_base[256];
+__constant__ PatchSet c_flip[256];  // resolution T on the (single) doubly-covered face
+
+// ----------------------------------------------------------------- host table generation
+// cube corner c = x | y<<1 | z<<2; edge e = 4*axis + sub (x: y+2z, y: x+2z, z: x+2y)
+int h_edge_id(int axis, int lower_corner) {
+  const int x = lower_corner & 1, y = (lower_corner >> 1) & 1, z = (lower_corner >> 2) & 1;
+  return axis == 0 ? y + 2 * z : (axis == 1 ? 4 + x + 2 * z : 8 + x + 2 * y);
+}
+
+struct HFace {
+  int corner[4];  // cyclic
+  int edge[4];    // edge[i] between corner[i] and corner[i+1]
+};
+
+HFace h_face(int f) {
+  const int axis = f >> 1, side = f & 1, b = (axis + 1) % 3, c = (axis + 2) % 3;
+  static const int cyc[4][2] = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+  HFace F;
+  for (int i = 0; i < 4; ++i) F.corner[i] = (side << axis) | (cyc[i][0] << b) | (cyc[i][1] << c);
+  for (int i = 0; i < 4; ++i) {
+    const int p = F.corner[i], q = F.corner[(i + 1) & 3], d = p ^ q;
+    F.edge[i] = h_edge_id(d == 1 ? 0 : (d == 2 ? 1 : 2), p & q);
+  }
+  return F;
+}
+
+PatchSet h_patches(int cs, int flip) {
+  int nb[12][2], deg[12] = {0};
+  auto join = [&](int a, int b) {
+    nb[a][deg[a]++] = b;
+    nb[b][deg[b]++] = a;
+  };
+  for (int f = 0; f < 6; ++f) {
+    const HFace F = h_face(f);
+    int sgn[4], crossing[4], nc = 0;
+    for (int i = 0; i < 4; ++i) sgn[i] = (cs >> F.corner[i]) & 1;
+    for (int i = 0; i < 4; ++i) nc += crossing[i] = sgn[i] != sgn[(i + 1) & 3];
+    if (nc == 2) {
+      int e[2], k = 0;
+      for (int i = 0; i < 4; ++i)
+        if (crossing[i]) e[k++] = F.edge[i];
+      join(e[0], e[1]);
+    } else if (nc == 4) {
+      // pair the two edges around every corner of the connected sign: positive (S) or negative (T)
+      const int around = (flip >> f) & 1;  // 1 -> around negative corners
+      for (int i = 0; i < 4; ++i)
+        if (sgn[i] == around) join(F.edge[(i + 3) & 3], F.edge[i]);
+    }
+  }
+  PatchSet P{};
+  for (int e = 0; e < 12; ++e) P.edge_patch[e] = -1;
+  for (int e0 = 0; e0 < 12; ++e0) {
+    if (!deg[e0] || P.edge_patch[e0] >= 0) continue;
+    int prev = -1, cur = e0;
+    uint16_t m = 0;
+    do {
+      m |= static_cast<uint16_t>(1u << cur);
+      P.edge_patch[cur] = static_cast<int8_t>(P.n);
+      const int nx = nb[cur][0] == prev ? nb[cur][1] : nb[cur][0];
+      prev = cur;
+      cur = nx;
+    } while (cur != e0);
+    P.mask[P.n++] = m;
+  }
+  return P;
+}
+
+int h_doubly_covered(int cs) {
+  const PatchSet P = h_patches(cs, 0);
+  int m = 0;
+  for (int f = 0; f < 6; ++f) {
+    const HFace F = h_face(f);
+    int s[4];
+    for (int i = 0; i < 4; ++i) s[i] = (cs >> F.corner[i]) & 1;
+    const bool amb = s[0] == s[2] && s[1] == s[3] && s[0] != s[1];
+    if (amb && P.edge_patch[F.edge[0]] == P.edge_patch[F.edge[1]] &&
+        P.edge_patch[F.edge[0]] == P.edge_patch[F.edge[2]] && P.edge_patch[F.edge[0]] == P.edge_patch[F.edge[3]])
+      m |= 1 << f;
+  }
+  return m;
+}
+
+struct HostTable {
+  PatchSet base[256], flip[256];
+  HostTable() {
+    for (int cs = 0; cs < 256; ++cs) {
+      base[cs] = h_patches(cs, 0);
+      base[cs].dc = static_cast<uint8_t>(h_doubly_covered(cs));
+      // every doubly-covered case has exactly one such face (checked at generation time)
+      if (__builtin_popcount(base[cs].dc) > 1) throw Error(PAMOPT_CU_ECUDA, "dmc table: >1 doubly covered face");
+      flip[cs] = base[cs].dc ? h_patches(cs, base[cs].dc) : base[cs];
+      flip[cs].dc = base[cs].dc;
+    }
+  }
+};
+
+const HostTable& host_table() {
+  static HostTable t;
+  return t;
+}
+
+void upload_table(int device) {
+  static std::mutex mu;
+  static uint64_t done_mask = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 64 && ((done_mask >> device) & 1)) return;
+  const HostTable& t = host_table();
+  PCU_CUDA(cudaMemcpyToSymbol(c_base, t.base, sizeof(t.base)));
+  PCU_CUDA(cudaMemcpyToSymbol(c_flip, t.flip, sizeof(t.flip)));
+  if (device < 64) done_mask |= 1ull << device;
+}
+
+// ------------------------------------------------------------------------- device side
+constexpr int kCellsPerBlock = 2048;
+
+struct GridView {
+  const float* s;
+  int R;
+  int64_t n1;
+  __device__ __forceinline__ float at(int64_t x, int64_t y, int64_t z) const { return s[x + n1 * (y + n1 * z)]; }
+  __device__ __forceinline__ int case_of(int64_t x, int64_t y, int64_t z) const {
+    int cs = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      cs |= (at(x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1)) < 0.0f) << c;
+    return cs;
+  }
+};
+
+__device__ __forceinline__ void cell_xyz(int64_t c, int R, int64_t& x, int64_t& y, int64_t& z) {
+  x = c % R;
+  y = (c / R) % R;
+  z = c / (static_cast<int64_t>(R) * R);
+}
+
+__global__ void __launch_bounds__(256) k_classify_count(GridView g, int64_t ncell, uint32_t* __restrict__ bcount) {
+  typedef cub::BlockReduce<uint32_t, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kCellsPerBlock;
+  uint32_t cnt = 0;
+  for (int k = 0; k < kCellsPerBlock / 256; ++k) {
+    const int64_t c = base + k * 256 + threadIdx.x;
+    if (c < ncell) {
+      int64_t x, y, z;
+      cell_xyz(c, g.R, x, y, z);
+      const int cs = g.case_of(x, y, z);
+      cnt += (cs != 0 && cs != 255);
+    }
+  }
+  const uint32_t tot = BR(tmp).Sum(cnt);
+  if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256) k_classify_write(GridView g, int64_t ncell, const uint32_t* __restrict__ boff,
+                                                        uint32_t* __restrict__ cells, uint8_t* __restrict__ cases) {
+  typedef cub::BlockScan<uint32_t, 256> BS;
+  __shared__ typename BS::TempStorage tmp;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kCellsPerBlock;
+  uint32_t run = boff[blockIdx.x];
+  for (int k = 0; k < kCellsPerBlock / 256; ++k) {
+    const int64_t c = base + k * 256 + threadIdx.x;
+    int cs = 0;
+    if (c < ncell) {
+      int64_t x, y, z;
+      cell_xyz(c, g.R, x, y, z);
+      cs = g.case_of(x, y, z);
+    }
+    const uint32_t flag = (c < ncell && cs != 0 && cs != 255) ? 1u : 0u;
+    uint32_t pos, tot;
+    BS(tmp).ExclusiveSum(flag, pos, tot);
+    if (flag) {
+      cells[run + pos] = static_cast<uint32_t>(c);
+      cases[run + pos] = static_cast<uint8_t>(cs);
+    }
+    run += tot;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ const PatchSet& patches_of(int cs, int flip) { return flip ? c_flip[cs] : c_base[cs]; }
+
+__global__ void k_patch_count(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
+                              int64_t na, uint8_t* __restrict__ flips, uint32_t* __restrict__ npatch,
+                              uint32_t* __restrict__ cellmap) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na) return;
+  const int cs = cases[i];
+  int flip = 0;
+  const int dc = c_base[cs].dc;
+  if (dc) {
+    int64_t xyz[3];
+    cell_xyz(cells[i], g.R, xyz[0], xyz[1], xyz[2]);
+    const int f = __ffs(dc) - 1, axis = f >> 1, side = f & 1;
+    int64_t n[3] = {xyz[0], xyz[1], xyz[2]};
+    n[axis] += side ? 1 : -1;
+    if (n[axis] >= 0 && n[axis] < g.R) {
+      const int ncs = g.case_of(n[0], n[1], n[2]);
+      if ((c_base[ncs].dc >> (2 * axis + (1 - side))) & 1) flip = dc;
+    }
+  }
+  flips[i] = static_cast<uint8_t>(flip);
+  npatch[i] = patches_of(cs, flip).n;
+  cellmap[cells[i]] = static_cast<uint32_t>(i);
+}
+
+__device__ __forceinline__ D3 gpoint(int64_t x, int64_t y, int64_t z, int R) {
+  return D3{static_cast<double>(x) / R, static_cast<double>(y) / R, static_cast<double>(z) / R};
+}
+
+__device__ __forceinline__ D3 crossing(D3 p0, D3 p1, float f0, float f1, double beta) {
+  const double t = -static_cast<double>(f0) / (static_cast<double>(f1) - static_cast<double>(f0));
+  const double ts = sigmoid_t(t, beta);
+  return D3{p0.x + ts * (p1.x - p0.x), p0.y + ts * (p1.y - p0.y), p0.z + ts * (p1.z - p0.z)};
+}
+
+// edge e of the cell: lower corner and axis
+__device__ __forceinline__ void edge_corners(int e, int& c0, int& axis) {
+  axis = e >> 2;
+  const int sub = e & 3, u = sub & 1, w = sub >> 1;
+  c0 = axis == 0 ? ((u << 1) | (w << 2)) : (axis == 1 ? (u | (w << 2)) : (u | (w << 1)));
+}
+
+__global__ void k_patch_vertices(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
+                                 const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase, int64_t na,
+                                 double beta, double* __restrict__ V) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na) return;
+  int64_t x, y, z;
+  cell_xyz(cells[i], g.R, x, y, z);
+  const PatchSet& P = patches_of(cases[i], flips[i]);
+  for (int p = 0; p < P.n; ++p) {
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    int cnt = 0;
+    for (int e = 0; e < 12; ++e) {
+      if (!((P.mask[p] >> e) & 1)) continue;
+      int c0, ax;
+      edge_corners(e, c0, ax);
+      const int c1 = c0 | (1 << ax);
+      const int64_t x0 = x + (c0 & 1), y0 = y + ((c0 >> 1) & 1), z0 = z + ((c0 >> 2) & 1);
+      const int64_t x1 = x + (c1 & 1), y1 = y + ((c1 >> 1) & 1), z1 = z + ((c1 >> 2) & 1);
+      const D3 q = crossing(gpoint(x0, y0, z0, g.R), gpoint(x1, y1, z1, g.R), g.at(x0, y0, z0), g.at(x1, y1, z1), beta);
+      sx = sx + q.x;
+      sy = sy + q.y;
+      sz = sz + q.z;
+      ++cnt;
+    }
+    const int64_t vi = vbase[i] + p;
+    V[3 * vi] = sx / cnt;
+    V[3 * vi + 1] = sy / cnt;
+    V[3 * vi + 2] = sz / cnt;
+  }
+}
+
+struct QuadGeo {
+  uint32_t q[4];
+  D3 plo, phi;
+  float f0, f1;
+};
+
+// Builds the quad of the axis-a valid edge at the corner 0 of active cell i (returns false if none)
+__device__ __forceinline__ bool make_quad(GridView g, int64_t x, int64_t y, int64_t z, int a,
+                                          const uint32_t* __restrict__ cellmap, const uint8_t* __restrict__ cases,
+                                          const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase,
+                                          QuadGeo& Q) {
+  const int64_t xyz[3] = {x, y, z};
+  const int b = (a + 1) % 3, c = (a + 2) % 3;
+  if (xyz[b] < 1 || xyz[c] < 1) return false;
+  int64_t up[3] = {x, y, z};
+  up[a] += 1;
+  Q.f0 = g.at(x, y, z);
+  Q.f1 = g.at(up[0], up[1], up[2]);
+  if ((Q.f0 < 0.0f) == (Q.f1 < 0.0f)) return false;
+  const int offs[4][2] = {{-1, -1}, {0, -1}, {0, 0}, {-1, 0}};
+  for (int k = 0; k < 4; ++k) {
+    int64_t cl[3] = {x, y, z};
+    cl[b] += offs[k][0];
+    cl[c] += offs[k][1];
+    int c0 = 0;
+    if (offs[k][0] == -1) c0 |= 1 << b;
+    if (offs[k][1] == -1) c0 |= 1 << c;
+    const int cx = c0 & 1, cy = (c0 >> 1) & 1, cz = (c0 >> 2) & 1;
+    const int e = a == 0 ? cy + 2 * cz : (a == 1 ? 4 + cx + 2 * cz : 8 + cx + 2 * cy);
+    const uint32_t j = cellmap[cl[0] + g.R * (cl[1] + static_cast<int64_t>(g.R) * cl[2])];
+    Q.q[k] = vbase[j] + patches_of(cases[j], flips[j]).edge_patch[e];
+  }
+  if (!(Q.f0 < 0.0f)) {  // lower endpoint positive: reverse so the normal points - -> +
+    const uint32_t t = Q.q[1];
+    Q.q[1] = Q.q[3];
+    Q.q[3] = t;
+  }
+  Q.plo = gpoint(x, y, z, g.R);
+  Q.phi = gpoint(up[0], up[1], up[2], g.R);
+  return true;
+}
+
+__device__ __forceinline__ D3 ld3(const double* V, uint32_t i) { return D3{V[3 * i], V[3 * i + 1], V[3 * i + 2]}; }
+
+// 1: diagonal 0-2, 2: diagonal 1-3, 3: four triangles around the edge crossing
+__device__ __forceinline__ int split_code(const QuadGeo& Q, const double* __restrict__ V) {
+  D3 P[4];
+  for (int k = 0; k < 4; ++k) P[k] = ld3(V, Q.q[k]);
+  const bool lower_neg = Q.f0 < 0.0f;
+  const D3 vp = lower_neg ? Q.phi : Q.plo, vn = lower_neg ? Q.plo : Q.phi;
+  bool conc[4];
+  for (int k = 0; k < 4; ++k) {
+    const D3 L = P[(k + 3) & 3], Rr = P[(k + 1) & 3];
+    const double t1 = dot(sub(P[k], vp), cross(sub(L, vp), sub(Rr, vp)));
+    const double t2 = dot(sub(P[k], vn), cross(sub(L, vn), sub(Rr, vn)));
+    conc[k] = t1 < 0.0 || t2 > 0.0;
+  }
+  const bool d02 = conc[0] || conc[2], d13 = conc[1] || conc[3];
+  if (d02 && !d13) return 1;
+  if (d13 && !d02) return 2;
+  if (d02 && d13) return 3;
+  auto maxcos = [&](int i0, int i1, int i2) {
+    const D3 T[3] = {P[i0], P[i1], P[i2]};
+    double m = -2.0;
+    for (int k = 0; k < 3; ++k) {
+      const D3 u = sub(T[(k + 1) % 3], T[k]), w = sub(T[(k + 2) % 3], T[k]);
+      const double cs = dot(u, w) / sqrt(sqn(u) * sqn(w));
+      if (cs > m) m = cs;
+    }
+    return m;
+  };
+  const double m02 = fmax(maxcos(0, 1, 2), maxcos(0, 2, 3));
+  const double m13 = fmax(maxcos(0, 1, 3), maxcos(1, 2, 3));
+  return m02 <= m13 ? 1 : 2;
+}
+
+__global__ void k_quad_count(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
+                             const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase,
+                             const uint32_t* __restrict__ cellmap, int64_t na, const double* __restrict__ V,
+                             uint64_t* __restrict__ counts, uint8_t* __restrict__ codes) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na) return;
+  int64_t x, y, z;
+  cell_xyz(cells[i], g.R, x, y, z);
+  uint32_t nfaces = 0, nextra = 0;
+  uint8_t code = 0;
+  for (int a = 0; a < 3; ++a) {
+    QuadGeo Q;
+    if (!make_quad(g, x, y, z, a, cellmap, cases, flips, vbase, Q)) continue;
+    const int sc = split_code(Q, V);
+    code |= static_cast<uint8_t>(sc << (2 * a));
+    nfaces += sc == 3 ? 4 : 2;
+    nextra += sc == 3;
+  }
+  codes[i] = code;
+  counts[i] = (static_cast<uint64_t>(nfaces) << 32) | nextra;
+}
+
+__global__ void k_quad_write(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
+                             const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase,
+                             const uint32_t* __restrict__ cellmap, int64_t na, const uint8_t* __restrict__ codes,
+                             const uint64_t* __restrict__ offs, uint64_t nv_patch, double beta,
+                             double* __restrict__ V, int32_t* __restrict__ Fo) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na || codes[i] == 0) return;
+  int64_t x, y, z;
+  cell_xyz(cells[i], g.R, x, y, z);
+  uint64_t fo = offs[i] >> 32, eo = offs[i] & 0xffffffffu;
+  for (int a = 0; a < 3; ++a) {
+    const int sc = (codes[i] >> (2 * a)) & 3;
+    if (!sc) continue;
+    QuadGeo Q;
+    make_quad(g, x, y, z, a, cellmap, cases, flips, vbase, Q);
+    const uint32_t* q = Q.q;
+    int32_t* o = Fo + 3 * fo;
+    if (sc == 1) {
+      const int32_t t[6] = {(int32_t)q[0], (int32_t)q[1], (int32_t)q[2], (int32_t)q[0], (int32_t)q[2], (int32_t)q[3]};
+      for (int k = 0; k < 6; ++k) o[k] = t[k];
+      fo += 2;
+    } else if (sc == 2) {
+      const int32_t t[6] = {(int32_t)q[0], (int32_t)q[1], (int32_t)q[3], (int32_t)q[1], (int32_t)q[2], (int32_t)q[3]};
+      for (int k = 0; k < 6; ++k) o[k] = t[k];
+      fo += 2;
+    } else {
+      const uint64_t ve = nv_patch + eo;
+      const D3 p = crossing(Q.plo, Q.phi, Q.f0, Q.f1, beta);
+      V[3 * ve] = p.x;
+      V[3 * ve + 1] = p.y;
+      V[3 * ve + 2] = p.z;
+      const int32_t e = static_cast<int32_t>(ve);
+      const int32_t t[12] = {(int32_t)q[0], (int32_t)q[1], e, (int32_t)q[1], (int32_t)q[2], e,
+                             (int32_t)q[2], (int32_t)q[3], e, (int32_t)q[3], (int32_t)q[0], e};
+      for (int k = 0; k < 12; ++k) o[k] = t[k];
+      fo += 4;
+      eo += 1;
+    }
+  }
+}
+
+}  // namespace
+
+void dmc_table_host(int32_t* out) {
+  const HostTable& t = host_table();
+  for (int cs = 0; cs < 256; ++cs) {
+    out[6 * cs] = t.base[cs].n;
+    for (int k = 0; k < 4; ++k) out[6 * cs + 1 + k] = t.base[cs].mask[k];
+    out[6 * cs + 5] = t.base[cs].dc;
+  }
+}
+
+void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res) {
+  upload_table(ctx.device);
+  GridView g{d_sdf, R, static_cast<int64_t>(R) + 1};
+  const int64_t ncell = static_cast<int64_t>(R) * R * R;
+  const int64_t nblk = (ncell + kCellsPerBlock - 1) / kCellsPerBlock;
+  DevBuf<uint32_t> bcount(nblk, ctx.stream), boff(nblk, ctx.stream);
+  PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, ncell, bcount.get());
+  exclusive_scan_u32(ctx, bcount.get(), boff.get(), nblk);
+  const uint32_t na = read_scalar(ctx, boff.get() + nblk - 1) + read_scalar(ctx, bcount.get() + nblk - 1);
+  res.cells.alloc(na ? na : 1, ctx.stream);
+  res.cases.alloc(na ? na : 1, ctx.stream);
+  res.flips.alloc(na ? na : 1, ctx.stream);
+  res.n_active = na;
+  PCU_LAUNCH(ctx, k_classify_write, static_cast<unsigned>(nblk), 256, 0, g, ncell, boff.get(), res.cells.get(),
+             res.cases.get());
+  if (na == 0) {
+    res.nv = res.nf = 0;
+    res.V.alloc(1, ctx.stream);
+    res.F.alloc(1, ctx.stream);
+    return;
+  }
+  DevBuf<uint32_t> npatch(na, ctx.stream), vbase(na, ctx.stream);
+  DevBuf<uint32_t> cellmap(ncell, ctx.stream);  // only active entries are written / read
+  PCU_LAUNCH(ctx, k_patch_count, grid_for(na, 256), 256, 0, g, res.cells.get(), res.cases.get(), na, res.flips.get(),
+             npatch.get(), cellmap.get());
+  exclusive_scan_u32(ctx, npatch.get(), vbase.get(), na);
+  const uint64_t nv_patch = static_cast<uint64_t>(read_scalar(ctx, vbase.get() + na - 1)) + read_scalar(ctx, npatch.get() + na - 1);
+  DevBuf<uint64_t> counts(na, ctx.stream), offs(na, ctx.stream);
+  DevBuf<uint8_t> codes(na, ctx.stream);
+  // patch vertices first (the quad pass reads them); extra vertices appended after
+  DevBuf<double> Vp(3 * nv_patch, ctx.stream);
+  PCU_LAUNCH(ctx, k_patch_vertices, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
+             vbase.get(), na, beta, Vp.get());
+  PCU_LAUNCH(ctx, k_quad_count, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
+             vbase.get(), cellmap.get(), na, Vp.get(), counts.get(), codes.get());
+  exclusive_scan_u64(ctx, counts.get(), offs.get(), na);
+  const uint64_t last = read_scalar(ctx, offs.get() + na - 1) + read_scalar(ctx, counts.get() + na - 1);
+  const uint64_t nf = last >> 32, nextra = last & 0xffffffffu;
+  res.nv = nv_patch + nextra;
+  res.nf = nf;
+  res.n_quads = 0;
+  res.V.alloc(3 * res.nv, ctx.stream);
+  res.F.alloc(3 * (nf ? nf : 1), ctx.stream);
+  PCU_CUDA(cudaMemcpyAsync(res.V.get(), Vp.get(), 3 * nv_patch * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+  PCU_LAUNCH(ctx, k_quad_write, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
+             vbase.get(), cellmap.get(), na, codes.get(), offs.get(), nv_patch, beta, res.V.get(), res.F.get());
+}
+
+}  // namespace pcu

@@ -1,0 +1,61 @@
+// kernels.cuh — host-side entry points of the device modules (udf.cu, dmc.cu, isect.cu,
+// simplify.cu), called by the C-ABI layer in capi.cu.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace pcu {
+
+// ---- stage 1a (udf.cu)
+// mode 0: UDF (+INF sentinel); mode 1: fused SDF (u - eps, sentinel +1.0)
+void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf, int R, int mode, double eps,
+             float* d_out);
+void udf_to_sdf_inplace(Ctx& ctx, float* g, int64_t n, double eps);
+std::vector<int64_t> hierarchy_pairs(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf, int R, int r);
+
+// ---- stage 1b (dmc.cu)
+struct DmcResult {
+  DevBuf<uint32_t> cells;
+  DevBuf<uint8_t> cases, flips;
+  uint32_t n_active = 0;
+  DevBuf<double> V;
+  DevBuf<int32_t> F;
+  uint64_t nv = 0, nf = 0, n_quads = 0;
+};
+void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res);
+void dmc_table_host(int32_t* out);
+
+// ---- tri_isect (isect.cu)
+// all intersecting pairs (i<j) among faces with alive[i] (alive may be null); if `query` is
+// non-null only pairs with at least one query face are reported.  Result sorted (host).
+std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf,
+                                        const uint8_t* d_alive, const uint8_t* d_query);
+void tri_tri_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int32_t* d_out);
+
+// Broad phase + narrow phase used inside the QEM undo loop: for every intersecting pair with
+// a query face, flag `hit[owner[f]]` for both faces' owners (owner -1 = none).  Returns the
+// number of intersecting pairs found (device counter read back).
+struct IsectScratch;
+int64_t undo_detect(Ctx& ctx, IsectScratch& scratch, const double* dV, const int32_t* dF, int64_t nf,
+                    const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query,
+                    const int32_t* d_owner, const uint8_t* d_applied, uint8_t* d_revert);
+IsectScratch* isect_scratch_create();
+void isect_scratch_destroy(IsectScratch* s);
+
+// ---- stage 2 (simplify.cu)
+struct SimplifyParams {
+  double we = 1e-3, ws = 5e-3;
+  int tolerance = 4, stall = 10;
+};
+struct SimplifyStats {
+  int64_t iterations = 0, collapses = 0, undone = 0, link_failures = 0, max_undo_rounds = 0;
+  int64_t undo_hist[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::vector<int64_t> per_iter;
+};
+// Simplifies in place.  On return dV/dF hold the compacted mesh (sizes updated).
+void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& F, int64_t& nv, int64_t& nf, int64_t target,
+                  const SimplifyParams& P, SimplifyStats& S);
+
+}  // namespace pcu

@@ -1,0 +1,788 @@
+// simplify.cu — stage 2: parallel intersection-free QEM simplification (Algorithm 1;
+// SPEC.md:473-574), device resident.  Per iteration (bulk synchronous,
+// SPEC.md:563):
+//
+//   incidence  vertex -> alive faces CSR by counting sort; every list sorted by face id
+//   edges      per vertex a: sorted unique neighbours b > a  -> lexicographic edge ids (P5)
+//   cost       Eq. 1 per valid edge (FP64, fmad off): merged quadric, adjugate placement with
+//              the 1-norm condition fallback to {mid, a, b}, edge length, skinny ring cost;
+//              key = f32 bits << 32 | id
+//   propagate  64-bit atomicMin edge keys -> vertices (REDG.MIN.64), face key = min of its
+//              vertices, then faces -> vertices; an edge is marked iff both endpoints' face
+//              minima equal its key (== every face of its 1-ring holds it; Gautron et al.)
+//   link       link condition (mesh.cpp:301-358) per marked edge on the pre-batch mesh
+//   trim       marked edges in key order; keep while the batch would not undershoot (P9)
+//   collapse   b -> a in b's faces, shared faces deleted, x placed, K_a += K_b (mesh.cpp:363-395)
+//   undo       grid broad phase over the faces owned by applied collapses, probed by every alive
+//              face, exact narrow phase; owners of intersecting faces revert from the pre-batch
+//              snapshot and are flagged invalid; repeat until clean
+//   flags      invalid list (sorted (a<<32|b) keys), kept one iteration, accumulated across
+//              zero-collapse iterations up to `tolerance`
+// The host reads a handful of counters per iteration (edge count, marked count, collapse and
+// undo results) to size the next launches and to drive the termination rule.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pcu {
+namespace {
+
+constexpr int kMaxDeg = 255;      // per-vertex incident-face capacity of the local buffers
+constexpr double k4Sqrt3 = 6.928203230275509;
+
+struct Counters {
+  unsigned long long edges, marked, link_fail, newinv, query, removed, applied, err, cap, undone;
+};
+
+__device__ __forceinline__ D3 P3(const double* X, int v) { return D3{X[3 * v], X[3 * v + 1], X[3 * v + 2]}; }
+__device__ __forceinline__ bool has(const int32_t* t, int v) { return t[0] == v || t[1] == v || t[2] == v; }
+
+// ------------------------------------------------------------------------- incidence
+__global__ void k_deg(const int32_t* __restrict__ F, const uint8_t* __restrict__ falive, int64_t nf,
+                      uint32_t* __restrict__ deg) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nf || !falive[f]) return;
+  atomicAdd(&deg[F[3 * f]], 1u);
+  atomicAdd(&deg[F[3 * f + 1]], 1u);
+  atomicAdd(&deg[F[3 * f + 2]], 1u);
+}
+
+__global__ void k_fill(const int32_t* __restrict__ F, const uint8_t* __restrict__ falive, int64_t nf,
+                       const uint32_t* __restrict__ off, uint32_t* __restrict__ cur, int32_t* __restrict__ inc) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nf || !falive[f]) return;
+  for (int k = 0; k < 3; ++k) {
+    const int v = F[3 * f + k];
+    inc[off[v] + atomicAdd(&cur[v], 1u)] = static_cast<int32_t>(f);
+  }
+}
+
+__global__ void k_sort_lists(const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg, int64_t nv,
+                             int32_t* __restrict__ inc) {
+  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (v >= nv) return;
+  int32_t* L = inc + off[v];
+  const int n = static_cast<int>(deg[v]);
+  for (int i = 1; i < n; ++i) {
+    const int32_t x = L[i];
+    int j = i - 1;
+    while (j >= 0 && L[j] > x) {
+      L[j + 1] = L[j];
+      --j;
+    }
+    L[j + 1] = x;
+  }
+}
+
+// quadrics gathered in ascending face id
+__device__ void face_quadric(const double* X, const int32_t* t, double* o) {
+  const D3 p0 = P3(X, t[0]), p1 = P3(X, t[1]), p2 = P3(X, t[2]);
+  const D3 n = cross(sub(p1, p0), sub(p2, p0));
+  const double len = sqrt(sqn(n));
+  if (!(len > 0.0)) {
+    for (int k = 0; k < 10; ++k) o[k] = 0.0;
+    return;
+  }
+  const double a = n.x / len, b = n.y / len, c = n.z / len;
+  const double d = -((a * p0.x + b * p0.y) + c * p0.z);
+  const double w = 0.5 * len;
+  o[0] = w * (a * a); o[1] = w * (a * b); o[2] = w * (a * c); o[3] = w * (a * d);
+  o[4] = w * (b * b); o[5] = w * (b * c); o[6] = w * (b * d);
+  o[7] = w * (c * c); o[8] = w * (c * d); o[9] = w * (d * d);
+}
+
+__global__ void k_quadrics(const double* __restrict__ X, const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
+                           const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int64_t nv,
+                           double* __restrict__ Q) {
+  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (v >= nv) return;
+  double q[10];
+  for (int k = 0; k < 10; ++k) q[k] = 0.0;
+  for (uint32_t i = 0; i < deg[v]; ++i) {
+    double fq[10];
+    face_quadric(X, F + 3 * inc[off[v] + i], fq);
+    for (int k = 0; k < 10; ++k) q[k] = q[k] + fq[k];
+  }
+  for (int k = 0; k < 10; ++k) Q[10 * v + k] = q[k];
+}
+
+// ----------------------------------------------------------------------------- edges
+// neighbours b > a of vertex a, sorted unique; returns count (or -1 on capacity overflow).
+// mult[i] = number of alive faces holding edge (a, nb[i]).
+__device__ int upper_neighbours(int a, const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
+                                const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int32_t* nb,
+                                uint8_t* mult) {
+  const int d = static_cast<int>(deg[a]);
+  if (d > kMaxDeg) return -1;
+  int n = 0;
+  for (int i = 0; i < d; ++i) {
+    const int32_t* t = F + 3 * inc[off[a] + i];
+    for (int k = 0; k < 3; ++k)
+      if (t[k] > a) nb[n++] = t[k];
+  }
+  for (int i = 1; i < n; ++i) {
+    const int32_t x = nb[i];
+    int j = i - 1;
+    while (j >= 0 && nb[j] > x) {
+      nb[j + 1] = nb[j];
+      --j;
+    }
+    nb[j + 1] = x;
+  }
+  int u = 0;
+  for (int i = 0; i < n;) {
+    int j = i;
+    while (j < n && nb[j] == nb[i]) ++j;
+    nb[u] = nb[i];
+    mult[u] = static_cast<uint8_t>(min(j - i, 255));
+    ++u;
+    i = j;
+  }
+  return u;
+}
+
+__global__ void k_edge_count(const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
+                             const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int64_t nv,
+                             uint32_t* __restrict__ ecount, Counters* cnt) {
+  const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (a >= nv) return;
+  int32_t nb[2 * kMaxDeg];
+  uint8_t mult[2 * kMaxDeg];
+  const int u = deg[a] ? upper_neighbours(static_cast<int>(a), F, off, deg, inc, nb, mult) : 0;
+  if (u < 0) {
+    atomicAdd(&cnt->cap, 1ull);
+    ecount[a] = 0;
+    return;
+  }
+  int bad = 0;
+  for (int i = 0; i < u; ++i) bad |= (mult[i] != 1 && mult[i] != 2);
+  if (bad) atomicAdd(&cnt->err, 1ull);  // non-manifold edge: input must come from stage 1
+  ecount[a] = static_cast<uint32_t>(u);
+}
+
+__global__ void k_edge_fill(const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
+                            const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int64_t nv,
+                            const uint32_t* __restrict__ eoff, int32_t* __restrict__ ea, int32_t* __restrict__ eb,
+                            uint8_t* __restrict__ enf) {
+  const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (a >= nv || !deg[a]) return;
+  int32_t nb[2 * kMaxDeg];
+  uint8_t mult[2 * kMaxDeg];
+  const int u = upper_neighbours(static_cast<int>(a), F, off, deg, inc, nb, mult);
+  for (int i = 0; i < u; ++i) {
+    ea[eoff[a] + i] = static_cast<int32_t>(a);
+    eb[eoff[a] + i] = nb[i];
+    enf[eoff[a] + i] = mult[i];
+  }
+}
+
+__global__ void k_mark_invalid(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb, int64_t ne,
+                               const uint64_t* __restrict__ inv, int64_t ninv, uint8_t* __restrict__ valid) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= ne) return;
+  const uint64_t key = (static_cast<uint64_t>(ea[e]) << 32) | static_cast<uint32_t>(eb[e]);
+  int64_t lo = 0, hi = ninv;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (inv[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  valid[e] = (lo < ninv && inv[lo] == key) ? 0 : 1;
+}
+
+// ------------------------------------------------------------------------------ cost
+__device__ double qeval(const double* q, D3 p) {
+  const double x = p.x, y = p.y, z = p.z;
+  double r = q[0] * x * x;
+  r = r + 2.0 * q[1] * x * y;
+  r = r + 2.0 * q[2] * x * z;
+  r = r + 2.0 * q[3] * x;
+  r = r + q[4] * y * y;
+  r = r + 2.0 * q[5] * y * z;
+  r = r + 2.0 * q[6] * y;
+  r = r + q[7] * z * z;
+  r = r + 2.0 * q[8] * z;
+  r = r + q[9];
+  return r < 0.0 ? 0.0 : r;
+}
+
+__device__ double ring_skinny(const double* X, const int32_t* F, const int32_t* ia, int na, const int32_t* ib, int nb,
+                              int a, int b, D3 x) {
+  int i = 0, j = 0;
+  double cs = 0.0;
+  while (i < na || j < nb) {
+    int f;
+    if (j == nb || (i < na && ia[i] < ib[j])) f = ia[i++];
+    else if (i == na || ib[j] < ia[i]) f = ib[j++];
+    else {
+      f = ia[i++];
+      ++j;
+    }
+    const int32_t* t = F + 3 * f;
+    if (has(t, a) && has(t, b)) continue;
+    D3 P[3];
+    for (int k = 0; k < 3; ++k) P[k] = (t[k] == a || t[k] == b) ? x : P3(X, t[k]);
+    const D3 n = cross(sub(P[1], P[0]), sub(P[2], P[0]));
+    const double area = 0.5 * sqrt(sqn(n));
+    const double l01 = sqn(sub(P[1], P[0])), l12 = sqn(sub(P[2], P[1])), l20 = sqn(sub(P[0], P[2]));
+    const double den = (l01 + l12) + l20;
+    const double c = den > 0.0 ? (k4Sqrt3 * area) / den : 0.0;
+    cs = cs + (1.0 - c);
+  }
+  return cs;
+}
+
+__global__ void k_cost(const double* __restrict__ X, const int32_t* __restrict__ F, const double* __restrict__ Q,
+                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
+                       const int32_t* __restrict__ inc, const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                       const uint8_t* __restrict__ valid, int64_t ne, double we, double ws,
+                       uint64_t* __restrict__ key, double* __restrict__ place, Counters* cnt) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= ne) return;
+  if (!valid[e]) {
+    key[e] = ~0ull;
+    return;
+  }
+  const int a = ea[e], b = eb[e];
+  double q[10];
+  for (int k = 0; k < 10; ++k) q[k] = Q[10 * a + k] + Q[10 * b + k];
+  const D3 pa = P3(X, a), pb = P3(X, b);
+  const double l = sqrt(sqn(sub(pa, pb)));
+  const double m00 = q[0], m01 = q[1], m02 = q[2], m10 = q[1], m11 = q[4], m12 = q[5], m20 = q[2], m21 = q[5],
+               m22 = q[7];
+  const double det = m00 * (m11 * m22 - m12 * m21) - m01 * (m10 * m22 - m12 * m20) + m02 * (m10 * m21 - m11 * m20);
+  bool ok = det != 0.0;
+  D3 x{0.0, 0.0, 0.0};
+  if (ok) {
+    const double i00 = (m11 * m22 - m12 * m21) / det, i01 = (m02 * m21 - m01 * m22) / det,
+                 i02 = (m01 * m12 - m02 * m11) / det, i10 = (m12 * m20 - m10 * m22) / det,
+                 i11 = (m00 * m22 - m02 * m20) / det, i12 = (m02 * m10 - m00 * m12) / det,
+                 i20 = (m10 * m21 - m11 * m20) / det, i21 = (m01 * m20 - m00 * m21) / det,
+                 i22 = (m00 * m11 - m01 * m10) / det;
+    const double nA = fmax(fmax((fabs(m00) + fabs(m10)) + fabs(m20), (fabs(m01) + fabs(m11)) + fabs(m21)),
+                           (fabs(m02) + fabs(m12)) + fabs(m22));
+    const double nI = fmax(fmax((fabs(i00) + fabs(i10)) + fabs(i20), (fabs(i01) + fabs(i11)) + fabs(i21)),
+                           (fabs(i02) + fabs(i12)) + fabs(i22));
+    const double cond = nA * nI;
+    if (!(cond <= 1e8)) {
+      ok = false;
+    } else {
+      const double b0 = q[3], b1 = q[6], b2 = q[8];
+      x = D3{-((i00 * b0 + i01 * b1) + i02 * b2), -((i10 * b0 + i11 * b1) + i12 * b2),
+             -((i20 * b0 + i21 * b1) + i22 * b2)};
+    }
+  }
+  const int32_t* ia = inc + off[a];
+  const int32_t* ib = inc + off[b];
+  const int na = static_cast<int>(deg[a]), nb = static_cast<int>(deg[b]);
+  double cost;
+  if (ok) {
+    cost = (qeval(q, x) + we * l) + ws * ring_skinny(X, F, ia, na, ib, nb, a, b, x);
+  } else {
+    const D3 c0 = D3{(pa.x + pb.x) * 0.5, (pa.y + pb.y) * 0.5, (pa.z + pb.z) * 0.5};
+    x = c0;
+    cost = (qeval(q, c0) + we * l) + ws * ring_skinny(X, F, ia, na, ib, nb, a, b, c0);
+    const double ca = (qeval(q, pa) + we * l) + ws * ring_skinny(X, F, ia, na, ib, nb, a, b, pa);
+    if (ca < cost) {
+      cost = ca;
+      x = pa;
+    }
+    const double cb = (qeval(q, pb) + we * l) + ws * ring_skinny(X, F, ia, na, ib, nb, a, b, pb);
+    if (cb < cost) {
+      cost = cb;
+      x = pb;
+    }
+  }
+  if (cost != cost) {
+    atomicAdd(&cnt->err, 1ull);
+    key[e] = ~0ull;
+    return;
+  }
+  const float cf = __double2float_rn(cost < 0.0 ? 0.0 : cost);
+  key[e] = (static_cast<uint64_t>(__float_as_uint(cf)) << 32) | static_cast<uint64_t>(e);
+  place[3 * e] = x.x;
+  place[3 * e + 1] = x.y;
+  place[3 * e + 2] = x.z;
+}
+
+// --------------------------------------------------------------------- propagation
+__global__ void k_prop_edges(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                             const uint64_t* __restrict__ key, const uint8_t* __restrict__ valid, int64_t ne,
+                             unsigned long long* __restrict__ vmin) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= ne || !valid[e]) return;
+  atomicMin(&vmin[ea[e]], static_cast<unsigned long long>(key[e]));
+  atomicMin(&vmin[eb[e]], static_cast<unsigned long long>(key[e]));
+}
+
+__global__ void k_prop_faces(const int32_t* __restrict__ F, const uint8_t* __restrict__ falive, int64_t nf,
+                             const unsigned long long* __restrict__ vmin, unsigned long long* __restrict__ vfmin) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nf || !falive[f]) return;
+  const int v0 = F[3 * f], v1 = F[3 * f + 1], v2 = F[3 * f + 2];
+  unsigned long long k = vmin[v0];
+  k = vmin[v1] < k ? vmin[v1] : k;
+  k = vmin[v2] < k ? vmin[v2] : k;
+  atomicMin(&vfmin[v0], k);
+  atomicMin(&vfmin[v1], k);
+  atomicMin(&vfmin[v2], k);
+}
+
+__global__ void k_mark(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb, const uint64_t* __restrict__ key,
+                       const uint8_t* __restrict__ valid, int64_t ne, const unsigned long long* __restrict__ vfmin,
+                       uint64_t* __restrict__ marked, Counters* cnt) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (e >= ne || !valid[e]) return;
+  const uint64_t k = key[e];
+  if (k == vfmin[ea[e]] && k == vfmin[eb[e]]) marked[atomicAdd(&cnt->marked, 1ull)] = k;
+}
+
+// ---------------------------------------------------------------------- link condition
+// restatement of mesh.cpp:301-358 on the CSR incidence (-2 = the virtual boundary vertex)
+__device__ bool is_boundary_vertex(int v, const int32_t* F, const uint32_t* off, const uint32_t* deg,
+                                   const int32_t* inc) {
+  const int d = static_cast<int>(deg[v]);
+  for (int i = 0; i < d; ++i) {
+    const int32_t* t = F + 3 * inc[off[v] + i];
+    for (int k = 0; k < 3; ++k) {
+      const int x = t[k];
+      if (x == v) continue;
+      int c = 0;
+      for (int j = 0; j < d && c < 2; ++j) c += has(F + 3 * inc[off[v] + j], x);
+      if (c == 1) return true;
+    }
+  }
+  return false;
+}
+
+__device__ int faces_of_edge(int a, int b, const int32_t* F, const uint32_t* off, const uint32_t* deg,
+                             const int32_t* inc) {
+  int c = 0;
+  for (uint32_t i = 0; i < deg[a]; ++i) c += has(F + 3 * inc[off[a] + i], b);
+  return c;
+}
+
+// sorted unique link vertex set of v (+ -2 if boundary); returns size
+__device__ int link_set(int v, const int32_t* F, const uint32_t* off, const uint32_t* deg, const int32_t* inc,
+                        int32_t* out) {
+  int n = 0;
+  const int d = min(static_cast<int>(deg[v]), kMaxDeg);
+  for (int i = 0; i < d; ++i) {
+    const int32_t* t = F + 3 * inc[off[v] + i];
+    for (int k = 0; k < 3; ++k)
+      if (t[k] != v) out[n++] = t[k];
+  }
+  if (is_boundary_vertex(v, F, off, deg, inc)) out[n++] = -2;
+  for (int i = 1; i < n; ++i) {
+    const int32_t x = out[i];
+    int j = i - 1;
+    while (j >= 0 && out[j] > x) {
+      out[j + 1] = out[j];
+      --j;
+    }
+    out[j + 1] = x;
+  }
+  int u = 0;
+  for (int i = 0; i < n; ++i)
+    if (u == 0 || out[u - 1] != out[i]) out[u++] = out[i];
+  return u;
+}
+
+__device__ bool link_condition(int a, int b, const int32_t* F, const uint32_t* off, const uint32_t* deg,
+                               const int32_t* inc) {
+  int32_t la[2 * kMaxDeg + 1], lb[2 * kMaxDeg + 1];
+  const int na = link_set(a, F, off, deg, inc, la);
+  const int nb = link_set(b, F, off, deg, inc, lb);
+  // common = la ∩ lb (sorted)
+  int32_t common[2 * kMaxDeg + 1];
+  int nc = 0;
+  for (int i = 0, j = 0; i < na && j < nb;) {
+    if (la[i] < lb[j]) ++i;
+    else if (lb[j] < la[i]) ++j;
+    else {
+      common[nc++] = la[i];
+      ++i;
+      ++j;
+    }
+  }
+  // link(ab): opposite vertices of faces(a,b) (+ -2 if boundary edge)
+  int32_t lab[8];
+  int nl = 0, nfe = 0;
+  for (uint32_t i = 0; i < deg[a]; ++i) {
+    const int32_t* t = F + 3 * inc[off[a] + i];
+    if (!has(t, b)) continue;
+    ++nfe;
+    for (int k = 0; k < 3; ++k)
+      if (t[k] != a && t[k] != b && nl < 7) lab[nl++] = t[k];
+  }
+  if (nfe == 1) lab[nl++] = -2;
+  for (int i = 1; i < nl; ++i) {
+    const int32_t x = lab[i];
+    int j = i - 1;
+    while (j >= 0 && lab[j] > x) {
+      lab[j + 1] = lab[j];
+      --j;
+    }
+    lab[j + 1] = x;
+  }
+  int ul = 0;
+  for (int i = 0; i < nl; ++i)
+    if (ul == 0 || lab[ul - 1] != lab[i]) lab[ul++] = lab[i];
+  if (ul != nc) return false;
+  for (int i = 0; i < nc; ++i)
+    if (lab[i] != common[i]) return false;
+  const bool has_vb = nc > 0 && common[0] == -2;
+  for (int i = 0; i < nc; ++i) {
+    const int x = common[i];
+    if (x == -2) continue;
+    for (int j = 0; j < nc; ++j) {
+      const int y = common[j];
+      if (y == -2 || y <= x) continue;
+      bool in_la = false, in_lb = false;
+      for (uint32_t k = 0; k < deg[x]; ++k) {
+        const int32_t* t = F + 3 * inc[off[x] + k];
+        if (!has(t, y)) continue;
+        if (has(t, a)) in_la = true;
+        if (has(t, b)) in_lb = true;
+      }
+      if (in_la && in_lb) return false;
+    }
+    if (has_vb && faces_of_edge(a, x, F, off, deg, inc) == 1 && faces_of_edge(b, x, F, off, deg, inc) == 1)
+      return false;
+  }
+  return true;
+}
+
+// marked[i] (sorted keys) -> pass flag, removal count; failures appended to the invalid list
+__global__ void k_link(const uint64_t* __restrict__ marked, int64_t nm, const int32_t* __restrict__ ea,
+                       const int32_t* __restrict__ eb, const uint8_t* __restrict__ enf, const int32_t* __restrict__ F,
+                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
+                       const int32_t* __restrict__ inc, uint32_t* __restrict__ rem, uint64_t* __restrict__ newinv,
+                       Counters* cnt) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nm) return;
+  const uint32_t e = static_cast<uint32_t>(marked[i]);
+  const int a = ea[e], b = eb[e];
+  if (link_condition(a, b, F, off, deg, inc)) {
+    rem[i] = enf[e];
+  } else {
+    rem[i] = 0;
+    atomicAdd(&cnt->link_fail, 1ull);
+    newinv[atomicAdd(&cnt->newinv, 1ull)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+  }
+}
+
+// ----------------------------------------------------------------------------- collapse
+struct Batch {
+  int32_t* ca;      // kept vertex
+  int32_t* cb;      // removed vertex
+  uint8_t* applied;
+  double* oldx;     // 3 per collapse
+  double* oldq;     // 10 per collapse
+  uint32_t* nrem;   // faces removed
+};
+
+__global__ void k_collapse(const uint64_t* __restrict__ marked, int64_t nm, const uint32_t* __restrict__ rem,
+                           const uint32_t* __restrict__ remoff, int64_t alive_faces, int64_t target,
+                           const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                           const double* __restrict__ place, const uint32_t* __restrict__ off,
+                           const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, double* __restrict__ X,
+                           int32_t* __restrict__ F, uint8_t* __restrict__ falive, uint8_t* __restrict__ valive,
+                           double* __restrict__ Q, int32_t* __restrict__ owner, int32_t* __restrict__ qfaces,
+                           Batch B, Counters* cnt) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nm) return;
+  B.applied[i] = 0;
+  if (rem[i] == 0) return;                                             // failed the link condition
+  if (!(alive_faces - static_cast<int64_t>(remoff[i]) > target)) return;  // overshoot trim (P9)
+  const uint32_t e = static_cast<uint32_t>(marked[i]);
+  const int a = ea[e], b = eb[e];
+  B.ca[i] = a;
+  B.cb[i] = b;
+  B.nrem[i] = rem[i];
+  for (int k = 0; k < 3; ++k) B.oldx[3 * i + k] = X[3 * a + k];
+  for (int k = 0; k < 10; ++k) B.oldq[10 * i + k] = Q[10 * a + k];
+  for (uint32_t j = 0; j < deg[b]; ++j) {
+    const int f = inc[off[b] + j];
+    int32_t* t = F + 3 * f;
+    if (has(t, a)) {
+      falive[f] = 0;
+    } else {
+      for (int k = 0; k < 3; ++k)
+        if (t[k] == b) t[k] = a;
+    }
+  }
+  for (int k = 0; k < 3; ++k) X[3 * a + k] = place[3 * e + k];
+  for (int k = 0; k < 10; ++k) Q[10 * a + k] = Q[10 * a + k] + Q[10 * b + k];
+  valive[b] = 0;
+  B.applied[i] = 1;
+  atomicAdd(&cnt->applied, 1ull);
+  atomicAdd(&cnt->removed, static_cast<unsigned long long>(rem[i]));
+  // owned faces: alive faces of a and of b after the collapse
+  for (uint32_t j = 0; j < deg[a]; ++j) {
+    const int f = inc[off[a] + j];
+    if (falive[f]) {
+      owner[f] = static_cast<int32_t>(i);
+      qfaces[atomicAdd(&cnt->query, 1ull)] = f;
+    }
+  }
+  for (uint32_t j = 0; j < deg[b]; ++j) {
+    const int f = inc[off[b] + j];
+    if (falive[f]) {
+      owner[f] = static_cast<int32_t>(i);
+      qfaces[atomicAdd(&cnt->query, 1ull)] = f;
+    }
+  }
+}
+
+// keep query faces whose owner is still applied
+__global__ void k_requery(const int32_t* __restrict__ qin, int64_t n, const int32_t* __restrict__ owner,
+                          const uint8_t* __restrict__ applied, int32_t* __restrict__ qout, Counters* cnt) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int f = qin[i];
+  const int o = owner[f];
+  if (o >= 0 && applied[o]) qout[atomicAdd(&cnt->query, 1ull)] = f;
+}
+
+__global__ void k_revert(int64_t nm, const uint8_t* __restrict__ revert, const uint32_t* __restrict__ off,
+                         const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc,
+                         const int32_t* __restrict__ Fprev, double* __restrict__ X, int32_t* __restrict__ F,
+                         uint8_t* __restrict__ falive, uint8_t* __restrict__ valive, double* __restrict__ Q,
+                         int32_t* __restrict__ owner, Batch B, uint64_t* __restrict__ newinv, Counters* cnt) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nm || !revert[i] || !B.applied[i]) return;
+  const int a = B.ca[i], b = B.cb[i];
+  for (uint32_t j = 0; j < deg[a]; ++j) {
+    const int f = inc[off[a] + j];
+    if (owner[f] == i) owner[f] = -1;
+  }
+  for (uint32_t j = 0; j < deg[b]; ++j) {
+    const int f = inc[off[b] + j];
+    if (owner[f] == i) owner[f] = -1;
+    falive[f] = 1;
+    for (int k = 0; k < 3; ++k) F[3 * f + k] = Fprev[3 * f + k];
+  }
+  for (int k = 0; k < 3; ++k) X[3 * a + k] = B.oldx[3 * i + k];
+  for (int k = 0; k < 10; ++k) Q[10 * a + k] = B.oldq[10 * i + k];
+  valive[b] = 1;
+  B.applied[i] = 0;
+  atomicAdd(&cnt->applied, ~0ull);  // -1
+  atomicAdd(&cnt->undone, 1ull);
+  atomicAdd(&cnt->removed, static_cast<unsigned long long>(-static_cast<long long>(B.nrem[i])));
+  newinv[atomicAdd(&cnt->newinv, 1ull)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+}
+
+// ------------------------------------------------------------------------------ compaction
+__global__ void k_used(const int32_t* __restrict__ F, const uint8_t* __restrict__ falive, int64_t nf,
+                       uint32_t* __restrict__ used) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nf || !falive[f]) return;
+  for (int k = 0; k < 3; ++k) used[F[3 * f + k]] = 1u;
+}
+__global__ void k_vkeep(const uint8_t* __restrict__ valive, int64_t nv, uint32_t* __restrict__ used) {
+  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (v < nv) used[v] = (used[v] && valive[v]) ? 1u : 0u;
+}
+__global__ void k_fkeep(const uint8_t* __restrict__ falive, int64_t nf, uint32_t* __restrict__ fk) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f < nf) fk[f] = falive[f] ? 1u : 0u;
+}
+__global__ void k_compact(const double* __restrict__ X, const int32_t* __restrict__ F, int64_t nv, int64_t nf,
+                          const uint32_t* __restrict__ vkeep, const uint32_t* __restrict__ vmap,
+                          const uint32_t* __restrict__ fkeep, const uint32_t* __restrict__ fmap,
+                          double* __restrict__ Xo, int32_t* __restrict__ Fo) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < nv && vkeep[i])
+    for (int k = 0; k < 3; ++k) Xo[3 * vmap[i] + k] = X[3 * i + k];
+  if (i < nf && fkeep[i])
+    for (int k = 0; k < 3; ++k) Fo[3 * fmap[i] + k] = static_cast<int32_t>(vmap[F[3 * i + k]]);
+}
+
+}  // namespace
+
+void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv, int64_t& nf, int64_t target,
+                  const SimplifyParams& P, SimplifyStats& S) {
+  cudaStream_t st = ctx.stream;
+  PCU_REQUIRE(target >= 0, PAMOPT_CU_EINVAL, "simplify_to: negative target");
+  if (nf <= target || nf == 0) return;
+  double* X = V.get();
+  int32_t* F = Fb.get();
+  DevBuf<uint8_t> falive(nf, st), valive(nv, st);
+  PCU_CUDA(cudaMemsetAsync(falive.get(), 1, nf, st));
+  PCU_CUDA(cudaMemsetAsync(valive.get(), 1, nv, st));
+  DevBuf<double> Q(10 * nv, st);
+  DevBuf<uint32_t> deg(nv, st), off(nv, st), cur(nv, st), ecount(nv, st), eoff(nv, st);
+  const int64_t ecap = 3 * nf + 16;
+  DevBuf<int32_t> inc(3 * nf, st), ea(ecap, st), eb(ecap, st), owner(nf, st), qf(3 * nf + 16, st),
+      qf2(3 * nf + 16, st), Fprev(3 * nf, st);
+  DevBuf<uint8_t> enf(ecap, st), valid(ecap, st), revert(ecap, st);
+  DevBuf<uint64_t> key(ecap, st), marked(ecap, st), marked_sorted(ecap, st);
+  DevBuf<double> place(3 * ecap, st);
+  DevBuf<unsigned long long> vmin(nv, st), vfmin(nv, st);
+  DevBuf<uint32_t> rem(ecap, st), remoff(ecap, st);
+  DevBuf<Counters> cnt(1, st);
+  DevBuf<uint64_t> inv(16, st), newinv(ecap, st), invtmp(16, st);
+  int64_t ninv = 0;
+  DevBuf<int32_t> bca(ecap, st), bcb(ecap, st);
+  DevBuf<uint8_t> bapplied(ecap, st);
+  DevBuf<double> boldx(3 * ecap, st), boldq(10 * ecap, st);
+  DevBuf<uint32_t> bnrem(ecap, st);
+  Batch B{bca.get(), bcb.get(), bapplied.get(), boldx.get(), boldq.get(), bnrem.get()};
+  IsectScratch* isc = isect_scratch_create();
+  struct ScratchGuard {
+    IsectScratch* s;
+    ~ScratchGuard() { isect_scratch_destroy(s); }
+  } guard{isc};
+  size_t sort_tmp_bytes = 0;
+  DevBuf<uint8_t> sort_tmp;
+
+  auto build_incidence = [&]() {
+    deg.memset(0, st);
+    PCU_LAUNCH(ctx, k_deg, grid_for(nf, 256), 256, 0, F, falive.get(), nf, deg.get());
+    exclusive_scan_u32(ctx, deg.get(), off.get(), nv);
+    cur.memset(0, st);
+    PCU_LAUNCH(ctx, k_fill, grid_for(nf, 256), 256, 0, F, falive.get(), nf, off.get(), cur.get(), inc.get());
+    PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
+  };
+
+  build_incidence();
+  PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, off.get(), deg.get(), inc.get(), nv, Q.get());
+
+  int64_t alive_faces = nf;
+  int retain = 0, zero_run = 0;
+  while (alive_faces > target && zero_run < P.stall) {
+    S.iterations++;
+    if (S.iterations > 1) build_incidence();
+    cnt.memset(0, st);
+    // edges
+    PCU_LAUNCH(ctx, k_edge_count, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, ecount.get(),
+               cnt.get());
+    exclusive_scan_u32(ctx, ecount.get(), eoff.get(), nv);
+    const int64_t ne = static_cast<int64_t>(read_scalar(ctx, eoff.get() + nv - 1)) + read_scalar(ctx, ecount.get() + nv - 1);
+    Counters h = read_scalar(ctx, cnt.get());
+    PCU_REQUIRE(h.cap == 0, PAMOPT_CU_ECAP, "simplify_to: vertex valence exceeds 255 incident faces");
+    if (S.iterations == 1)
+      PCU_REQUIRE(h.err == 0, PAMOPT_CU_EINVAL, "simplify_to: non-manifold input (an edge has >2 faces); run stage 1");
+    PCU_LAUNCH(ctx, k_edge_fill, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, eoff.get(), ea.get(),
+               eb.get(), enf.get());
+    PCU_LAUNCH(ctx, k_mark_invalid, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), ne, inv.get(), ninv, valid.get());
+    cnt.memset(0, st);
+    PCU_LAUNCH(ctx, k_cost, grid_for(ne, 128), 128, 0, X, F, Q.get(), off.get(), deg.get(), inc.get(), ea.get(), eb.get(),
+               valid.get(), ne, P.we, P.ws, key.get(), place.get(), cnt.get());
+    vmin.memset(0xFF, st);
+    vfmin.memset(0xFF, st);
+    PCU_LAUNCH(ctx, k_prop_edges, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), key.get(), valid.get(), ne, vmin.get());
+    PCU_LAUNCH(ctx, k_prop_faces, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vmin.get(), vfmin.get());
+    PCU_LAUNCH(ctx, k_mark, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), key.get(), valid.get(), ne, vfmin.get(),
+               marked.get(), cnt.get());
+    h = read_scalar(ctx, cnt.get());
+    PCU_REQUIRE(h.err == 0, PAMOPT_CU_ENUMERIC, "simplify_to: NaN edge cost");
+    const int64_t nm = static_cast<int64_t>(h.marked);
+    int64_t succ = 0;
+    int rounds = 0;
+    int64_t nnew = 0;
+    if (nm > 0) {
+      // marked keys in ascending order (deterministic collapse ids + the trim order)
+      size_t need = 0;
+      cub::DeviceRadixSort::SortKeys(nullptr, need, marked.get(), marked_sorted.get(), static_cast<int>(nm), 0, 64, st);
+      if (need > sort_tmp_bytes) {
+        sort_tmp.alloc(need, st);
+        sort_tmp_bytes = need;
+      }
+      cub::DeviceRadixSort::SortKeys(sort_tmp.get(), sort_tmp_bytes, marked.get(), marked_sorted.get(),
+                                     static_cast<int>(nm), 0, 64, st);
+      PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, marked_sorted.get(), nm, ea.get(), eb.get(), enf.get(), F,
+                 off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get());
+      exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
+      PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), st));
+      PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, marked_sorted.get(), nm, rem.get(), remoff.get(),
+                 alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
+                 falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
+      h = read_scalar(ctx, cnt.get());
+      int64_t nq = static_cast<int64_t>(h.query);
+      int32_t* qa = qf.get();
+      int32_t* qb = qf2.get();
+      while (nq > 0) {
+        revert.memset(0, st);
+        const int64_t found =
+            undo_detect(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get());
+        if (found == 0) break;
+        ++rounds;
+        PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
+                   Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get());
+        // rebuild the query list from still-applied collapses
+        PCU_CUDA(cudaMemsetAsync(&cnt.get()->query, 0, 8, st));
+        PCU_LAUNCH(ctx, k_requery, grid_for(nq, 256), 256, 0, qa, nq, owner.get(), B.applied, qb, cnt.get());
+        h = read_scalar(ctx, cnt.get());
+        nq = static_cast<int64_t>(h.query);
+        std::swap(qa, qb);
+      }
+      h = read_scalar(ctx, cnt.get());
+      succ = static_cast<int64_t>(h.applied);
+      alive_faces -= static_cast<int64_t>(h.removed);
+      nnew = static_cast<int64_t>(h.newinv);
+      S.link_failures += static_cast<int64_t>(h.link_fail);
+      S.undone += static_cast<int64_t>(h.undone);
+    }
+    S.undo_hist[std::min(rounds, 7)]++;
+    S.max_undo_rounds = std::max<int64_t>(S.max_undo_rounds, rounds);
+    S.collapses += succ;
+    S.per_iter.push_back(succ);
+    // invalid-flag update
+    bool keep_old;
+    if (succ > 0) {
+      keep_old = false;
+      retain = 0;
+      zero_run = 0;
+    } else {
+      ++zero_run;
+      ++retain;
+      keep_old = retain < P.tolerance;
+      if (!keep_old) retain = 0;
+    }
+    const int64_t nall = (keep_old ? ninv : 0) + nnew;
+    DevBuf<uint64_t> merged(nall ? nall : 1, st);
+    if (keep_old && ninv)
+      PCU_CUDA(cudaMemcpyAsync(merged.get(), inv.get(), ninv * 8, cudaMemcpyDeviceToDevice, st));
+    if (nnew)
+      PCU_CUDA(cudaMemcpyAsync(merged.get() + (keep_old ? ninv : 0), newinv.get(), nnew * 8, cudaMemcpyDeviceToDevice, st));
+    inv.alloc(nall ? nall : 1, st);
+    if (nall) {
+      sort_pairs_u64(ctx, merged.get(), nall);
+      // unique
+      DevBuf<int> nsel(1, st);
+      size_t need = 0;
+      cub::DeviceSelect::Unique(nullptr, need, merged.get(), inv.get(), nsel.get(), static_cast<int>(nall), st);
+      DevBuf<uint8_t> tmp(need ? need : 1, st);
+      cub::DeviceSelect::Unique(tmp.get(), need, merged.get(), inv.get(), nsel.get(), static_cast<int>(nall), st);
+      ninv = read_scalar(ctx, nsel.get());
+    } else {
+      ninv = 0;
+    }
+  }
+  // compaction (mesh.cpp:278-292): alive vertices used by alive faces, order preserving
+  DevBuf<uint32_t> vk(nv, st), vmap(nv, st), fk(nf, st), fmap(nf, st);
+  vk.memset(0, st);
+  PCU_LAUNCH(ctx, k_used, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vk.get());
+  PCU_LAUNCH(ctx, k_vkeep, grid_for(nv, 256), 256, 0, valive.get(), nv, vk.get());
+  PCU_LAUNCH(ctx, k_fkeep, grid_for(nf, 256), 256, 0, falive.get(), nf, fk.get());
+  exclusive_scan_u32(ctx, vk.get(), vmap.get(), nv);
+  exclusive_scan_u32(ctx, fk.get(), fmap.get(), nf);
+  const int64_t nv2 = static_cast<int64_t>(read_scalar(ctx, vmap.get() + nv - 1)) + read_scalar(ctx, vk.get() + nv - 1);
+  const int64_t nf2 = static_cast<int64_t>(read_scalar(ctx, fmap.get() + nf - 1)) + read_scalar(ctx, fk.get() + nf - 1);
+  DevBuf<double> Vo(3 * (nv2 ? nv2 : 1), st);
+  DevBuf<int32_t> Fo(3 * (nf2 ? nf2 : 1), st);
+  PCU_LAUNCH(ctx, k_compact, grid_for(std::max(nv, nf), 256), 256, 0, X, F, nv, nf, vk.get(), vmap.get(), fk.get(),
+             fmap.get(), Vo.get(), Fo.get());
+  V = std::move(Vo);
+  Fb = std::move(Fo);
+  nv = nv2;
+  nf = nf2;
+}
+
+}  // namespace pcu

@@ -1,0 +1,472 @@
+// udf.cu — stage 1a: narrow-band UDF over the voxel-grid hierarchy (SPEC.md:157-236,
+// PAPER.md:55-74) and the fused UDF->SDF band subtraction.
+//
+// Device pipeline (all on the context stream, inputs resident in HBM):
+//   1. prep      per triangle: vertices + AABB into a 128 B record (one coalesced load later)
+//   2. level 0   per triangle: the r=8 cells of its conservative index box that pass the
+//                pinned predicate -> (cell, tri) pairs, warp-aggregated append
+//   3. refine    per surviving pair x 8 children, levels 16 .. r_b (r_b = max(8, R/8), the
+//                "brick" level: one brick = bs^3 finest cells, bs = R/r_b <= 8)
+//   4. bin       counting sort of brick-level pairs by brick; work items of <= 128 triangles
+//   5. brick     one CTA per work item: every warp takes a triangle, descends the last
+//                log2(bs) levels inside the brick with ballots (8 -> 64 -> 512 cell masks in
+//                shared memory), dilates the finest mask to the (bs+1)^3 brick vertices and
+//                evaluates each needed vertex ONCE per triangle; per-vertex minima live in
+//                shared memory (64-bit atomicMin on the f64 bit pattern, order independent),
+//                then merge into the per-brick global block
+//   6. finalize  per lattice vertex: min over the <=8 bricks that hold it, sqrt, f32, and the
+//                band subtraction s = (float)((double)u - eps); no candidate -> +INF / +1.0
+// The pinned predicate: box_d2(c, aabb) <= (thr+1e-9)^2 && sqrt(ptri_sq(c,t))
+// <= thr, thr = 3/R + 0.8660254037844386/r — FP64, no FMA contraction.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pcu {
+namespace {
+
+constexpr double kHalfSqrt3 = 0.8660254037844386;
+constexpr int kChunk = 128;  // triangles per brick work item
+
+struct __align__(16) TriD {
+  double a[3], b[3], c[3], lo[3], hi[3], pad;
+};
+
+__device__ __forceinline__ bool survives(const TriD& t, double cx, double cy, double cz, double thr) {
+  const double tb = thr + 1e-9;
+  const double dx = fmax(fmax(t.lo[0] - cx, cx - t.hi[0]), 0.0);
+  const double dy = fmax(fmax(t.lo[1] - cy, cy - t.hi[1]), 0.0);
+  const double dz = fmax(fmax(t.lo[2] - cz, cz - t.hi[2]), 0.0);
+  if ((dx * dx + dy * dy) + dz * dz > tb * tb) return false;
+  const double d2 = ptri_sq(D3{cx, cy, cz}, D3{t.a[0], t.a[1], t.a[2]}, D3{t.b[0], t.b[1], t.b[2]},
+                            D3{t.c[0], t.c[1], t.c[2]});
+  return sqrt(d2) <= thr;
+}
+
+__device__ __forceinline__ double level_thr(int R, int r) {
+  return 3.0 / static_cast<double>(R) + kHalfSqrt3 / static_cast<double>(r);
+}
+
+__global__ void k_prep(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t nf,
+                       TriD* __restrict__ T) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nf) return;
+  const int i0 = F[3 * i], i1 = F[3 * i + 1], i2 = F[3 * i + 2];
+  TriD t;
+  for (int k = 0; k < 3; ++k) {
+    t.a[k] = V[3 * i0 + k];
+    t.b[k] = V[3 * i1 + k];
+    t.c[k] = V[3 * i2 + k];
+    t.lo[k] = fmin(fmin(t.a[k], t.b[k]), t.c[k]);
+    t.hi[k] = fmax(fmax(t.a[k], t.b[k]), t.c[k]);
+  }
+  t.pad = 0.0;
+  T[i] = t;
+}
+
+// warp-aggregated append of one 64-bit value per active lane with `keep`
+__device__ __forceinline__ void append(bool keep, uint64_t val, uint64_t* out, unsigned long long* cnt,
+                                       uint64_t cap) {
+  const unsigned m = __ballot_sync(__activemask(), keep);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(cnt, static_cast<unsigned long long>(__popc(m)));
+  base = __shfl_sync(__activemask(), base, leader);
+  if (keep) {
+    const uint64_t pos = base + __popc(m & ((1u << lane) - 1u));
+    if (pos < cap) out[pos] = val;
+  }
+}
+
+__global__ void k_level0(const TriD* __restrict__ T, int64_t nf, int R, uint64_t* out,
+                         unsigned long long* cnt, uint64_t cap) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool active = i < nf;
+  TriD t;
+  int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+  const int r = 8;
+  const double thr = level_thr(R, r);
+  if (active) {
+    t = T[i];
+    const double tb = thr + 1e-9;
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = max(0, static_cast<int>(floor((t.lo[k] - tb) * r - 0.5)) - 1);
+      hi[k] = min(r - 1, static_cast<int>(ceil((t.hi[k] + tb) * r - 0.5)) + 1);
+    }
+  }
+  const int nx = hi[0] - lo[0] + 1, ny = hi[1] - lo[1] + 1, nz = hi[2] - lo[2] + 1;
+  const int n = active ? nx * ny * nz : 0;
+  // every lane walks its own box; ballots need convergence -> loop to the warp max
+  int nmax = n;
+  for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+  for (int j = 0; j < nmax; ++j) {
+    bool keep = false;
+    uint64_t val = 0;
+    if (j < n) {
+      const int x = lo[0] + j % nx, y = lo[1] + (j / nx) % ny, z = lo[2] + j / (nx * ny);
+      keep = survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, thr);
+      val = (static_cast<uint64_t>(x + r * (y + r * z)) << 32) | static_cast<uint64_t>(i);
+    }
+    append(keep, val, out, cnt, cap);
+  }
+}
+
+__global__ void k_refine(const uint64_t* __restrict__ in, uint64_t n_in, const TriD* __restrict__ T,
+                         int R, int r, uint64_t* out, unsigned long long* cnt, uint64_t cap) {
+  const uint64_t gid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  bool keep = false;
+  uint64_t val = 0;
+  if (gid < n_in * 8) {
+    const uint64_t pr = in[gid >> 3];
+    const int ch = static_cast<int>(gid & 7);
+    const uint32_t pc = static_cast<uint32_t>(pr >> 32), tri = static_cast<uint32_t>(pr);
+    const int rp = r >> 1;
+    const int px = pc % rp, py = (pc / rp) % rp, pz = pc / (rp * rp);
+    const int x = 2 * px + (ch & 1), y = 2 * py + ((ch >> 1) & 1), z = 2 * pz + ((ch >> 2) & 1);
+    const TriD t = T[tri];
+    keep = survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, level_thr(R, r));
+    val = (static_cast<uint64_t>(x + r * (y + r * z)) << 32) | tri;
+  }
+  append(keep, val, out, cnt, cap);
+}
+
+__global__ void k_brick_count(const uint64_t* __restrict__ pairs, uint64_t n, uint32_t* __restrict__ cnt) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[pairs[i] >> 32], 1u);
+}
+
+__global__ void k_brick_scatter(const uint64_t* __restrict__ pairs, uint64_t n, const uint32_t* __restrict__ off,
+                                uint32_t* __restrict__ cursor, uint32_t* __restrict__ tris) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t b = static_cast<uint32_t>(pairs[i] >> 32);
+  const uint32_t pos = atomicAdd(&cursor[b], 1u);
+  tris[off[b] + pos] = static_cast<uint32_t>(pairs[i]);
+}
+
+// per brick: compact id (or -1) and number of work items
+__global__ void k_brick_items(const uint32_t* __restrict__ cnt, int64_t nb, uint32_t* __restrict__ nitems,
+                              uint32_t* __restrict__ isactive) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nb) return;
+  nitems[i] = (cnt[i] + kChunk - 1) / kChunk;
+  isactive[i] = cnt[i] > 0 ? 1u : 0u;
+}
+
+struct Item {
+  uint32_t brick;    // dense brick index
+  uint32_t compact;  // active brick id
+  uint32_t begin, end;
+};
+
+__global__ void k_make_items(const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                             const uint32_t* __restrict__ item_off, const uint32_t* __restrict__ act_off,
+                             int64_t nb, Item* __restrict__ items, int32_t* __restrict__ bmap) {
+  const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (b >= nb) return;
+  const uint32_t c = cnt[b];
+  bmap[b] = c ? static_cast<int32_t>(act_off[b]) : -1;
+  if (!c) return;
+  uint32_t k = item_off[b];
+  for (uint32_t s = 0; s < c; s += kChunk, ++k)
+    items[k] = Item{static_cast<uint32_t>(b), act_off[b], off[b] + s, off[b] + min(c, s + kChunk)};
+}
+
+// One CTA (8 warps) per work item.  bs = cells per brick edge (1..8), J = log2(bs).
+__global__ void __launch_bounds__(256) k_brick(const Item* __restrict__ items, const uint32_t* __restrict__ tris,
+                                               const TriD* __restrict__ T, int R, int rb, int bs, int J,
+                                               unsigned long long* __restrict__ blocks) {
+  __shared__ unsigned long long vmin[729];
+  __shared__ uint32_t masks[8][2][16];  // per warp, ping-pong level masks (<= 512 bits)
+  __shared__ TriD tsh[8];
+  const Item it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv1 = bs + 1, nvb = nv1 * nv1 * nv1;
+  for (int v = threadIdx.x; v < nvb; v += blockDim.x) vmin[v] = ~0ull;
+  __syncthreads();
+  const int bx = it.brick % rb, by = (it.brick / rb) % rb, bz = it.brick / (rb * rb);
+  for (uint32_t k = it.begin + warp; k < it.end; k += 8) {
+    if (lane == 0) tsh[warp] = T[tris[k]];
+    __syncwarp();
+    const TriD& t = tsh[warp];
+    // level 0 inside the brick: the brick itself survived (the pair exists)
+    int cur = 0;
+    masks[warp][0][0] = 1u;
+    for (int j = 1; j <= J; ++j) {
+      const int side = 1 << j, n = side * side * side, pside = side >> 1;
+      const int r = rb << j;
+      const double thr = level_thr(R, r);
+      const int nxt = cur ^ 1;
+      for (int base = 0; base < n; base += 32) {
+        const int c = base + lane;
+        bool keep = false;
+        if (c < n) {
+          const int x = c % side, y = (c / side) % side, z = c / (side * side);
+          const int pc = (x >> 1) + pside * ((y >> 1) + pside * (z >> 1));
+          if ((masks[warp][cur][pc >> 5] >> (pc & 31)) & 1u) {
+            const int gx = bx * side + x, gy = by * side + y, gz = bz * side + z;
+            keep = survives(t, (gx + 0.5) / r, (gy + 0.5) / r, (gz + 0.5) / r, thr);
+          }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) masks[warp][nxt][base >> 5] = m;
+      }
+      __syncwarp();
+      cur = nxt;
+    }
+    // dilate the finest mask to vertices and evaluate
+    const uint32_t* fm = masks[warp][cur];
+    for (int v = lane; v < nvb; v += 32) {
+      const int vx = v % nv1, vy = (v / nv1) % nv1, vz = v / (nv1 * nv1);
+      bool need = false;
+      for (int d = 0; d < 8 && !need; ++d) {
+        const int cx = vx - (d & 1), cy = vy - ((d >> 1) & 1), cz = vz - ((d >> 2) & 1);
+        if (cx < 0 || cy < 0 || cz < 0 || cx >= bs || cy >= bs || cz >= bs) continue;
+        const int c = cx + bs * (cy + bs * cz);
+        need = (fm[c >> 5] >> (c & 31)) & 1u;
+      }
+      if (!need) continue;
+      const int gx = bx * bs + vx, gy = by * bs + vy, gz = bz * bs + vz;
+      const D3 p{static_cast<double>(gx) / R, static_cast<double>(gy) / R, static_cast<double>(gz) / R};
+      const double d2 = ptri_sq(p, D3{t.a[0], t.a[1], t.a[2]}, D3{t.b[0], t.b[1], t.b[2]},
+                                D3{t.c[0], t.c[1], t.c[2]});
+      atomicMin(&vmin[v], static_cast<unsigned long long>(__double_as_longlong(d2)));
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  unsigned long long* blk = blocks + static_cast<uint64_t>(it.compact) * nvb;
+  for (int v = threadIdx.x; v < nvb; v += blockDim.x)
+    if (vmin[v] != ~0ull) atomicMin(&blk[v], vmin[v]);
+}
+
+// mode 0: UDF (+INF sentinel); mode 1: SDF (u - eps, sentinel +1.0)
+__global__ void k_finalize(const unsigned long long* __restrict__ blocks, const int32_t* __restrict__ bmap, int R,
+                           int rb, int bs, int mode, double eps, float* __restrict__ out) {
+  const int64_t n1 = R + 1;
+  const int64_t total = n1 * n1 * n1;
+  const int nv1 = bs + 1;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int x = static_cast<int>(i % n1), y = static_cast<int>((i / n1) % n1), z = static_cast<int>(i / (n1 * n1));
+    int bxs[2], bys[2], bzs[2], nbx = 0, nby = 0, nbz = 0;
+    if (x / bs < rb) bxs[nbx++] = x / bs;
+    if (x % bs == 0 && x > 0) bxs[nbx++] = x / bs - 1;
+    if (y / bs < rb) bys[nby++] = y / bs;
+    if (y % bs == 0 && y > 0) bys[nby++] = y / bs - 1;
+    if (z / bs < rb) bzs[nbz++] = z / bs;
+    if (z % bs == 0 && z > 0) bzs[nbz++] = z / bs - 1;
+    unsigned long long best = ~0ull;
+    if (!bmap) nbz = 0;
+    for (int a = 0; a < nbz; ++a)
+      for (int b = 0; b < nby; ++b)
+        for (int c = 0; c < nbx; ++c) {
+          const int cid = bmap[bxs[c] + rb * (bys[b] + rb * bzs[a])];
+          if (cid < 0) continue;
+          const int lx = x - bxs[c] * bs, ly = y - bys[b] * bs, lz = z - bzs[a] * bs;
+          const unsigned long long val = blocks[static_cast<uint64_t>(cid) * nv1 * nv1 * nv1 + lx + nv1 * (ly + nv1 * lz)];
+          best = val < best ? val : best;
+        }
+    float res;
+    if (best == ~0ull) {
+      res = mode ? 1.0f : __int_as_float(0x7f800000);
+    } else {
+      const float u = static_cast<float>(sqrt(__longlong_as_double(static_cast<long long>(best))));
+      res = mode ? static_cast<float>(static_cast<double>(u) - eps) : u;
+    }
+    out[i] = res;
+  }
+}
+
+__global__ void k_udf_to_sdf(float* g, int64_t n, double eps) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float u = g[i];
+    g[i] = isinf(u) ? 1.0f : static_cast<float>(static_cast<double>(u) - eps);
+  }
+}
+
+// debug: descend inside the brick to level jt and emit (cell at that level, tri)
+__global__ void k_debug_pairs(const uint64_t* __restrict__ bpairs, uint64_t n, const TriD* __restrict__ T, int R,
+                              int rb, int jt, uint64_t* out, unsigned long long* cnt, uint64_t cap) {
+  const uint64_t gid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const int side = 1 << jt;
+  const uint64_t per = static_cast<uint64_t>(side) * side * side;
+  bool keep = false;
+  uint64_t val = 0;
+  if (gid < n * per) {
+    const uint64_t pr = bpairs[gid / per];
+    const int c = static_cast<int>(gid % per);
+    const uint32_t b = static_cast<uint32_t>(pr >> 32), tri = static_cast<uint32_t>(pr);
+    const int bx = b % rb, by = (b / rb) % rb, bz = b / (rb * rb);
+    const int x = c % side, y = (c / side) % side, z = c / (side * side);
+    const TriD t = T[tri];
+    keep = true;
+    for (int j = 1; j <= jt && keep; ++j) {
+      const int sh = jt - j, r = rb << j;
+      const int gx = bx * (1 << j) + (x >> sh), gy = by * (1 << j) + (y >> sh), gz = bz * (1 << j) + (z >> sh);
+      keep = survives(t, (gx + 0.5) / r, (gy + 0.5) / r, (gz + 0.5) / r, level_thr(R, r));
+    }
+    const int r = rb << jt;
+    const uint64_t gx = bx * side + x, gy = by * side + y, gz = bz * side + z;
+    val = ((gx + static_cast<uint64_t>(r) * (gy + static_cast<uint64_t>(r) * gz)) << 32) | tri;
+  }
+  append(keep, val, out, cnt, cap);
+}
+
+int ilog2(int x) {
+  int l = 0;
+  while ((1 << l) < x) ++l;
+  return l;
+}
+
+}  // namespace
+
+// Runs levels 8..r_b; returns the brick-level pairs (and the pairs of `keep_level` if >= 0).
+static DevBuf<uint64_t> hierarchy_to_bricks(Ctx& ctx, const TriD* T, int64_t nf, int R, int rb,
+                                            uint64_t& n_out, int keep_r, DevBuf<uint64_t>* kept,
+                                            uint64_t* kept_n) {
+  DevBuf<unsigned long long> cnt(1, ctx.stream);
+  uint64_t cap = static_cast<uint64_t>(nf) * 16 + (1 << 16);
+  DevBuf<uint64_t> cur;
+  uint64_t n = 0;
+  for (int r = 8; r <= rb; r <<= 1) {
+    while (true) {
+      DevBuf<uint64_t> out(cap, ctx.stream);
+      cnt.memset(0, ctx.stream);
+      if (r == 8) {
+        PCU_LAUNCH(ctx, k_level0, grid_for(nf, 128), 128, 0, T, nf, R, out.get(), cnt.get(), cap);
+      } else {
+        PCU_LAUNCH(ctx, k_refine, grid_for(static_cast<int64_t>(n * 8), 256), 256, 0, cur.get(), n, T, R, r,
+                   out.get(), cnt.get(), cap);
+      }
+      const uint64_t got = read_scalar(ctx, cnt.get());
+      if (got > cap) {
+        cap = got + got / 4 + 1024;
+        continue;
+      }
+      cur = std::move(out);
+      n = got;
+      break;
+    }
+    if (r == keep_r && kept) {
+      kept->alloc(n ? n : 1, ctx.stream);
+      if (n) PCU_CUDA(cudaMemcpyAsync(kept->get(), cur.get(), n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+      *kept_n = n;
+    }
+    cap = n * 8 + (1 << 16);
+  }
+  n_out = n;
+  return cur;
+}
+
+void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf, int R, int mode, double eps,
+             float* d_out) {
+  (void)nv;
+  PCU_REQUIRE(R >= 8 && (R & (R - 1)) == 0 && R <= 2048, PAMOPT_CU_EINVAL, "compute_udf: R must be a power of two in [8, 2048]");
+  const int rb = R >= 64 ? R / 8 : 8;
+  const int bs = R / rb, J = ilog2(bs);
+  const int64_t n1 = R + 1;
+  const int64_t nvert = n1 * n1 * n1;
+  if (nf == 0) {
+    PCU_LAUNCH(ctx, k_finalize, static_cast<unsigned>(ctx.num_sms * 8), 256, 0, nullptr, nullptr, R, rb, bs, mode, eps, d_out);
+    return;
+  }
+  DevBuf<TriD> T(nf, ctx.stream);
+  PCU_LAUNCH(ctx, k_prep, grid_for(nf, 256), 256, 0, dV, dF, nf, T.get());
+  uint64_t npairs = 0;
+  DevBuf<uint64_t> bp = hierarchy_to_bricks(ctx, T.get(), nf, R, rb, npairs, -1, nullptr, nullptr);
+  const int64_t nb = static_cast<int64_t>(rb) * rb * rb;
+  DevBuf<uint32_t> bcnt(nb, ctx.stream), boff(nb, ctx.stream), bcur(nb, ctx.stream);
+  DevBuf<uint32_t> nitems(nb, ctx.stream), item_off(nb, ctx.stream), isact(nb, ctx.stream), act_off(nb, ctx.stream);
+  bcnt.memset(0, ctx.stream);
+  bcur.memset(0, ctx.stream);
+  DevBuf<uint32_t> tris(npairs ? npairs : 1, ctx.stream);
+  if (npairs) {
+    PCU_LAUNCH(ctx, k_brick_count, grid_for(static_cast<int64_t>(npairs), 256), 256, 0, bp.get(), npairs, bcnt.get());
+  }
+  exclusive_scan_u32(ctx, bcnt.get(), boff.get(), nb);
+  if (npairs) {
+    PCU_LAUNCH(ctx, k_brick_scatter, grid_for(static_cast<int64_t>(npairs), 256), 256, 0, bp.get(), npairs, boff.get(),
+               bcur.get(), tris.get());
+  }
+  PCU_LAUNCH(ctx, k_brick_items, grid_for(nb, 256), 256, 0, bcnt.get(), nb, nitems.get(), isact.get());
+  // totals: last offset + last count
+  exclusive_scan_u32(ctx, nitems.get(), item_off.get(), nb);
+  exclusive_scan_u32(ctx, isact.get(), act_off.get(), nb);
+  uint32_t last_item_off = read_scalar(ctx, item_off.get() + nb - 1), last_nitems = read_scalar(ctx, nitems.get() + nb - 1);
+  uint32_t last_act_off = read_scalar(ctx, act_off.get() + nb - 1), last_isact = read_scalar(ctx, isact.get() + nb - 1);
+  const uint32_t n_items = last_item_off + last_nitems, n_active = last_act_off + last_isact;
+  DevBuf<Item> items(n_items ? n_items : 1, ctx.stream);
+  DevBuf<int32_t> bmap(nb, ctx.stream);
+  PCU_LAUNCH(ctx, k_make_items, grid_for(nb, 256), 256, 0, bcnt.get(), boff.get(), item_off.get(), act_off.get(), nb,
+             items.get(), bmap.get());
+  const int nvb = (bs + 1) * (bs + 1) * (bs + 1);
+  DevBuf<unsigned long long> blocks(static_cast<size_t>(n_active ? n_active : 1) * nvb, ctx.stream);
+  blocks.memset(0xFF, ctx.stream);
+  if (n_items) {
+    PCU_LAUNCH(ctx, k_brick, n_items, 256, 0, items.get(), tris.get(), T.get(), R, rb, bs, J, blocks.get());
+  }
+  PCU_LAUNCH(ctx, k_finalize, static_cast<unsigned>(ctx.num_sms * 16), 256, 0, blocks.get(), bmap.get(), R, rb, bs,
+             mode, eps, d_out);
+  (void)nvert;
+}
+
+void udf_to_sdf_inplace(Ctx& ctx, float* g, int64_t n, double eps) {
+  PCU_LAUNCH(ctx, k_udf_to_sdf, static_cast<unsigned>(ctx.num_sms * 16), 256, 0, g, n, eps);
+}
+
+std::vector<int64_t> hierarchy_pairs(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf, int R, int r) {
+  PCU_REQUIRE(R >= 8 && (R & (R - 1)) == 0, PAMOPT_CU_EINVAL, "hierarchy_pairs: bad R");
+  PCU_REQUIRE(r >= 8 && r <= R && (r & (r - 1)) == 0, PAMOPT_CU_EINVAL, "hierarchy_pairs: bad level");
+  std::vector<int64_t> host;
+  if (nf == 0) return host;
+  const int rb = R >= 64 ? R / 8 : 8;
+  DevBuf<TriD> T(nf, ctx.stream);
+  PCU_LAUNCH(ctx, k_prep, grid_for(nf, 256), 256, 0, dV, dF, nf, T.get());
+  uint64_t npairs = 0, nk = 0;
+  DevBuf<uint64_t> kept;
+  DevBuf<uint64_t> bp = hierarchy_to_bricks(ctx, T.get(), nf, R, rb, npairs, r <= rb ? r : -1, &kept, &nk);
+  DevBuf<uint64_t> res;
+  uint64_t nres = 0;
+  if (r <= rb) {
+    res = std::move(kept);
+    nres = nk;
+  } else {
+    const int jt = ilog2(r / rb);
+    const uint64_t per = 1ull << (3 * jt);
+    DevBuf<unsigned long long> cnt(1, ctx.stream);
+    uint64_t cap = npairs * per / 4 + 1024;
+    while (true) {
+      DevBuf<uint64_t> out(cap, ctx.stream);
+      cnt.memset(0, ctx.stream);
+      PCU_LAUNCH(ctx, k_debug_pairs, grid_for(static_cast<int64_t>(npairs * per), 256), 256, 0, bp.get(), npairs,
+                 T.get(), R, rb, jt, out.get(), cnt.get(), cap);
+      const uint64_t got = read_scalar(ctx, cnt.get());
+      if (got > cap) {
+        cap = got + 1024;
+        continue;
+      }
+      res = std::move(out);
+      nres = got;
+      break;
+    }
+  }
+  std::vector<uint64_t> raw(nres);
+  if (nres) PCU_CUDA(cudaMemcpyAsync(raw.data(), res.get(), nres * 8, cudaMemcpyDeviceToHost, ctx.stream));
+  PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  std::sort(raw.begin(), raw.end());
+  host.resize(2 * nres);
+  for (uint64_t i = 0; i < nres; ++i) {
+    host[2 * i] = static_cast<int64_t>(raw[i] >> 32);
+    host[2 * i + 1] = static_cast<int64_t>(raw[i] & 0xffffffffu);
+  }
+  return host;
+}
+
+}  // namespace pcu

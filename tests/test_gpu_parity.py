@@ -1,0 +1,132 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the oracle on identical inputs.
+
+Bar: integer/index outputs bit-exact; because every FP decision is pinned
+(FP64, no FMA, identical op order) the FP outputs are bit-exact as well, which the tests
+assert (a stricter bar than the FP32 tolerance the north star allows).
+"""
+import numpy as np
+import pytest
+
+from paper_2509_05595_b200 import fixtures as FX
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def test_udf_c1_bitexact(api, c1):
+    g = api.compute_udf((c1["v"], c1["f"]), c1["R"])
+    udf = g.download()
+    assert np.array_equal(bits(udf), bits(c1["udf"]))
+    api.udf_to_sdf(g)
+    assert np.array_equal(bits(g.download()), bits(c1["sdf"]))
+    g2 = api.compute_sdf((c1["v"], c1["f"]), c1["R"])
+    assert np.array_equal(bits(g2.download()), bits(c1["sdf"]))
+
+
+@pytest.mark.parametrize("R", [8, 16, 32, 64])
+def test_hierarchy_levels_bitexact(api, oracle, R):
+    rng = FX.Rng(11)
+    n = 300
+    a = 0.15 + 0.7 * rng.uniform(3 * n).reshape(n, 3)
+    tri = a[:, None, :] + 0.08 * (rng.uniform(6 * n).reshape(n, 2, 3) - 0.5)
+    v = np.concatenate([a[:, None, :], tri], 1).reshape(-1, 3)
+    f = np.arange(3 * n, dtype=np.int32).reshape(n, 3)
+    r = 8
+    while r <= R:
+        got = api.build_hierarchy_pairs((v, f), R, r)
+        ref = oracle.hierarchy_pairs(v, f, R, r)
+        assert np.array_equal(got, ref), (R, r, len(got), len(ref))
+        r *= 2
+    u_gpu = api.compute_udf((v, f), R).download()
+    u_ref, _ = oracle.compute_udf_sdf(v, f, R)
+    assert np.array_equal(bits(u_gpu), bits(u_ref))
+
+
+def test_udf_in_band_equals_brute_force(api, oracle):
+    """in-band values equal the brute-force all-triangle minima."""
+    rng = FX.Rng(5)
+    n = 200
+    a = 0.2 + 0.6 * rng.uniform(3 * n).reshape(n, 3)
+    v = (a[:, None, :] + 0.1 * (rng.uniform(9 * n).reshape(n, 3, 3) - 0.5)).reshape(-1, 3)
+    f = np.arange(3 * n, dtype=np.int32).reshape(n, 3)
+    R = 32
+    u = api.compute_udf((v, f), R).download()
+    b = oracle.brute_udf(v, f, R)
+    band = b <= 3.0 / R
+    assert band.any()
+    assert np.array_equal(bits(u[band]), bits(b[band]))
+
+
+def test_dmc_c1_bitexact(api, c1):
+    g = api.DeviceGrid.upload(c1["sdf"], c1["R"])
+    m = api.extract(g)
+    v, f = m.download()
+    ref = c1["dmc"]
+    cells, cases, flips = api.dmc_active_cells(g)
+    assert np.array_equal(cells, ref["cells"])
+    assert np.array_equal(cases, ref["cases"])
+    assert np.array_equal(flips, ref["flips"])
+    assert np.array_equal(f, ref["faces"])
+    assert np.array_equal(bits(v), bits(ref["vertices"]))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_dmc_random_grid_bitexact(api, oracle, seed):
+    R = 32
+    g = np.random.default_rng(seed).uniform(-1, 1, (R + 1) ** 3).astype(np.float32)
+    ref = oracle.dmc_extract(g, R)
+    m = api.extract(api.DeviceGrid.upload(g, R))
+    v, f = m.download()
+    assert np.array_equal(f, ref["faces"])
+    assert np.array_equal(bits(v), bits(ref["vertices"]))
+    assert ref["flips"].any()  # the C16/C19 rule is exercised
+
+
+def test_dmc_table_matches_oracle(api, oracle):
+    assert np.array_equal(api.dmc_table(), oracle.dmc_table())
+
+
+def test_self_intersections_match_oracle(api, oracle, c1):
+    dv, df = c1["dmc"]["vertices"], c1["dmc"]["faces"]
+    assert len(api.detect_self_intersections((dv, df))) == 0
+    # perturb: push a vertex set outward to create intersections
+    v = dv.copy()
+    rng = np.random.default_rng(3)
+    idx = rng.choice(len(v), 200, replace=False)
+    v[idx] += rng.normal(0, 0.02, (200, 3))
+    got = api.detect_self_intersections((v, df))
+    ref = oracle.self_intersections(v, df)
+    assert len(ref) > 0
+    assert np.array_equal(got, ref)
+
+
+def test_tri_tri_verdicts_match_oracle(api, oracle):
+    from tests.tri_corpus import corpus
+    v, f, pairs = corpus(4000, seed=7)
+    got = api.tri_tri_pairs((v, f), pairs)
+    ref = oracle.tri_tri_pairs(v, f, pairs)
+    assert np.array_equal(got, ref)
+
+
+def test_simplify_c1_bitexact(api, oracle, c1):
+    dv, df = c1["dmc"]["vertices"], c1["dmc"]["faces"]
+    vo, fo, st = oracle.simplify(dv, df, c1["target"])
+    m, gst = api.simplify_to((dv, df), c1["target"])
+    v, f = m.download()
+    assert gst["iterations"] == st["iterations"]
+    assert np.array_equal(gst["per_iter_collapses"], st["per_iter_collapses"])
+    assert np.array_equal(f, fo)
+    assert np.array_equal(bits(v), bits(vo))
+    assert len(f) <= c1["target"]
+
+
+def test_pipeline_c1(api, oracle, c1):
+    res = api.run_pipeline(c1["v"], c1["f"], c1["R"], c1["target"])
+    vo, fo, st = oracle.simplify(c1["dmc"]["vertices"], c1["dmc"]["faces"], c1["target"])
+    assert np.array_equal(res.faces, fo)
+    assert np.array_equal(bits(res.vertices), bits(vo))
+    assert res.times["total_ms"] > 0
