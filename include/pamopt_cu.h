@@ -59,6 +59,8 @@ typedef struct {
   int64_t link_failures;
   int64_t max_undo_rounds;
   int64_t undo_hist[8]; /* batches needing k undo rounds (index 7 = 7 or more) */
+  int64_t face_iterations; /* sum over iterations of the alive face count (work units) */
+  int64_t alg_bytes;       /* SURVEY §8(d) QEM algorithmic bytes: sum 28 F_i + 92 V_i + 8 E_i */
 } pamopt_cu_simplify_stats;
 
 typedef struct {

@@ -210,12 +210,13 @@ STAT_KEYS = ["iterations", "collapses", "undone", "link_failures", "max_undo_rou
 
 def simplify(v, f, target: int, we: float = 1e-3, ws: float = 5e-3, tolerance: int = 4):
     v, f = _vf(v, f)
-    st = np.zeros(16, np.int64)
+    st = np.zeros(17, np.int64)
     rc = lib().orc_simplify(v.ravel(), len(v), f.ravel(), len(f), int(target), we, ws, tolerance, st)
     if rc != 0:
         raise ValueError("oracle simplify: NaN edge cost")
     stats = {k: int(st[i]) for i, k in enumerate(STAT_KEYS)}
     stats["undo_hist"] = [int(x) for x in st[8:16]]
+    stats["face_iterations"] = int(st[16])
     nv, nf = stats["nv_out"], stats["nf_out"]
     vo = np.empty((nv, 3), np.float64)
     fo = np.empty((nf, 3), np.int32)

@@ -29,7 +29,6 @@
 namespace orc {
 namespace isect {
 
-static int sgn(int x) { return (x > 0) - (x < 0); }
 
 // ---- non-coplanar, no shared vertex: Guigue & Devillers (2003), closed, exact -------
 static int o3(V3 a, V3 b, V3 c, V3 d) { return orient3d(a, b, c, d); }
@@ -198,8 +197,11 @@ bool tri_tri_verdict(const int32_t* t1, const int32_t* t2, const double* v) {
   const V3 a = P(t1[0]), b = P(t1[1]), c = P(t1[2]);
   const V3 d = P(t2[0]), e = P(t2[1]), f = P(t2[2]);
   if (degenerate(a, b, c) || degenerate(d, e, f)) return true;
-  const int od = orient3d(d, a, b, c), oe = orient3d(e, a, b, c), of = orient3d(f, a, b, c);
-  const bool coplanar = od == 0 && oe == 0 && of == 0;
+  // shared vertices lie on T1's plane by definition: only the unshared ones are tested
+  const V3 T2v[3] = {d, e, f};
+  bool coplanar = true;
+  for (int j = 0; j < 3 && coplanar; ++j)
+    if (s2[j] < 0 && orient3d(T2v[j], a, b, c) != 0) coplanar = false;
   if (!coplanar) {
     if (shared == 2) return false;
     if (shared == 0) return noncoplanar_disjoint_vertices(a, b, c, d, e, f);

@@ -290,6 +290,7 @@ struct Stats {
   int64_t link_failures = 0;
   int64_t undo_hist[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // batches needing k undo rounds (7 = >=7)
   int64_t max_undo_rounds = 0;
+  int64_t face_iterations = 0;
   int error = 0;
 };
 
@@ -311,6 +312,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
   int retain = 0, zero_run = 0;
   while (m.alive_faces > target && zero_run < P.stall) {
     S.iterations++;
+    S.face_iterations += m.alive_faces;
     const Incidence I = build_incidence(m);
     // edges in lexicographic order
     std::vector<std::pair<int32_t, int32_t>> edges;
@@ -514,9 +516,9 @@ std::vector<int64_t> g_iters;
 
 extern "C" {
 
-// simplify_to.  stats_out (int64[16]):
+// simplify_to.  stats_out (int64[17]):
 //  [iterations, collapses, undone, link_failures, max_undo_rounds, error, nv_out, nf_out,
-//   undo_hist[0..7]]
+//   undo_hist[0..7], face_iterations]
 int orc_simplify(const double* v, int64_t nv, const int32_t* f, int64_t nf, int64_t target,
                  double we, double ws, int tolerance, int64_t* stats_out) {
   Mesh m;
@@ -556,6 +558,7 @@ int orc_simplify(const double* v, int64_t nv, const int32_t* f, int64_t nf, int6
   stats_out[6] = static_cast<int64_t>(g_v.size() / 3);
   stats_out[7] = static_cast<int64_t>(g_f.size() / 3);
   for (int k = 0; k < 8; ++k) stats_out[8 + k] = S.undo_hist[k];
+  stats_out[16] = S.face_iterations;
   return S.error ? -1 : 0;
 }
 

@@ -22,12 +22,14 @@ class SimplifyParams(C.Structure):
 
 class SimplifyStats(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("collapses", C.c_int64), ("undone", C.c_int64),
-                ("link_failures", C.c_int64), ("max_undo_rounds", C.c_int64), ("undo_hist", C.c_int64 * 8)]
+                ("link_failures", C.c_int64), ("max_undo_rounds", C.c_int64), ("undo_hist", C.c_int64 * 8),
+                ("face_iterations", C.c_int64), ("alg_bytes", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {"iterations": self.iterations, "collapses": self.collapses, "undone": self.undone,
                 "link_failures": self.link_failures, "max_undo_rounds": self.max_undo_rounds,
-                "undo_hist": list(self.undo_hist)}
+                "undo_hist": list(self.undo_hist), "face_iterations": self.face_iterations,
+                "alg_bytes": self.alg_bytes}
 
 
 class StageTimes(C.Structure):

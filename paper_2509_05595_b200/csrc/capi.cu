@@ -107,6 +107,8 @@ int pamopt_cu_ctx_create(int32_t device, pamopt_cu_ctx* out) {
     PCU_REQUIRE(device >= 0 && device < n, PAMOPT_CU_EINVAL, "no such CUDA device");
     auto* c = new pamopt_cu_ctx_s();
     c->ctx.device = device;
+    const char* pe = std::getenv("PAMOPT_PROFILE");
+    c->ctx.prof.on = pe && pe[0] == '1';
     pcu::DeviceGuard g(device);
     PCU_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
     PCU_CUDA(cudaDeviceGetAttribute(&c->ctx.num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -396,6 +398,8 @@ static void to_stats(const pcu::SimplifyStats& S, pamopt_cu_simplify_stats* o) {
   o->link_failures = S.link_failures;
   o->max_undo_rounds = S.max_undo_rounds;
   for (int k = 0; k < 8; ++k) o->undo_hist[k] = S.undo_hist[k];
+  o->face_iterations = S.face_iterations;
+  o->alg_bytes = S.alg_bytes;
 }
 
 int pamopt_cu_simplify(pamopt_cu_mesh m, int64_t target, const pamopt_cu_simplify_params* params,

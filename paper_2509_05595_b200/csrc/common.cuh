@@ -8,6 +8,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -37,8 +41,42 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& m);
 
+// ------------------------------------------------------------------------------ profiler
+// PAMOPT_PROFILE=1: synchronise at phase marks and accumulate host wall time per phase
+// (diagnostics only; never enabled in timed runs).
+struct Prof {
+  bool on = false;
+  std::map<std::string, double> ms;
+  std::map<std::string, int64_t> n;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(cudaStream_t s, const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    ms[name] += std::chrono::duration<double, std::milli>(now - t).count();
+    n[name] += 1;
+    t = now;
+  }
+  void reset(cudaStream_t s) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    t = std::chrono::steady_clock::now();
+  }
+  void dump(const char* title) {
+    if (!on) return;
+    double tot = 0;
+    for (auto& kv : ms) tot += kv.second;
+    std::fprintf(stderr, "[pamopt profile] %s total %.2f ms\n", title, tot);
+    for (auto& kv : ms)
+      std::fprintf(stderr, "  %-22s %10.2f ms  %8lld calls\n", kv.first.c_str(), kv.second, (long long)n[kv.first]);
+    ms.clear();
+    n.clear();
+  }
+};
+
 // ------------------------------------------------------------------------------ context
 struct Ctx {
+  Prof prof;
   int device = 0;
   cudaStream_t stream = nullptr;
   int64_t launches = 0;

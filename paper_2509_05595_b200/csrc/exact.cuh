@@ -140,6 +140,9 @@ __device__ __forceinline__ int orient3d(D3 a, D3 b, D3 c, D3 d) {
   const double bound = (7.0 + 56.0 * 1.1102230246251565e-16) * 1.1102230246251565e-16 * perm;
   if (det > bound) return 1;
   if (-det > bound) return -1;
+  // coincident points give an exact zero without the expansion arithmetic
+  auto same = [](D3 p, D3 q) { return p.x == q.x && p.y == q.y && p.z == q.z; };
+  if (same(a, b) || same(a, c) || same(a, d) || same(b, c) || same(b, d) || same(c, d)) return 0;
   return orient3d_exact(a, b, c, d);
 }
 

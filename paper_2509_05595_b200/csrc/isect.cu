@@ -32,7 +32,8 @@ struct IsectScratch {
   DevBuf<int32_t> big;
   DevBuf<unsigned long long> counters;  // [0] entries, [1] big, [2] pairs
   DevBuf<double> ext_sum;
-  DevBuf<uint8_t> reduce_tmp;
+  DevBuf<uint8_t> in_build;
+  DevBuf<uint64_t> cand;
 };
 
 IsectScratch* isect_scratch_create() { return new IsectScratch(); }
@@ -192,7 +193,17 @@ __device__ bool ray_in(P2 A, P2 P, P2 Q, P2 U) {
   return true;
 }
 
+// degenerate <=> the exact normal is zero (all three projected orientations are zero).  The
+// filtered determinants certify most faces non-degenerate without any exact evaluation.
+__device__ __forceinline__ bool certainly_nonzero2(double ax, double ay, double bx, double by, double cx, double cy) {
+  const double l = (ax - cx) * (by - cy), r = (ay - cy) * (bx - cx);
+  const double det = l - r;
+  return fabs(det) > (3.0 + 16.0 * 1.1102230246251565e-16) * 1.1102230246251565e-16 * (fabs(l) + fabs(r));
+}
 __device__ bool degenerate(D3 a, D3 b, D3 c) {
+  if (certainly_nonzero2(a.x, a.y, b.x, b.y, c.x, c.y) || certainly_nonzero2(a.y, a.z, b.y, b.z, c.y, c.z) ||
+      certainly_nonzero2(a.z, a.x, b.z, b.x, c.z, c.x))
+    return false;
   return orient2d(a.y, a.z, b.y, b.z, c.y, c.z) == 0 && orient2d(a.z, a.x, b.z, b.x, c.z, c.x) == 0 &&
          orient2d(a.x, a.y, b.x, b.y, c.x, c.y) == 0;
 }
@@ -210,8 +221,10 @@ __device__ bool verdict(const double* __restrict__ V, const int32_t* t1, const i
   const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
   const D3 T2[3] = {vtx(V, t2[0]), vtx(V, t2[1]), vtx(V, t2[2])};
   if (degenerate(T1[0], T1[1], T1[2]) || degenerate(T2[0], T2[1], T2[2])) return true;
-  const bool coplanar = orient3d(T2[0], T1[0], T1[1], T1[2]) == 0 && orient3d(T2[1], T1[0], T1[1], T1[2]) == 0 &&
-                        orient3d(T2[2], T1[0], T1[1], T1[2]) == 0;
+  // coplanar <=> every vertex of T2 lies on T1's plane (shared vertices trivially do)
+  bool coplanar = true;
+  for (int j = 0; j < 3 && coplanar; ++j)
+    if (s2[j] < 0 && orient3d(T2[j], T1[0], T1[1], T1[2]) != 0) coplanar = false;
   if (!coplanar) {
     if (shared == 2) return false;
     if (shared == 0) return gd_disjoint(T1[0], T1[1], T1[2], T2[0], T2[1], T2[2]);
@@ -314,60 +327,39 @@ __global__ void k_bin(const double* __restrict__ V, const int32_t* __restrict__ 
       }
 }
 
-struct ProbeOut {
-  // mode 0: append pairs (a<b) to `pairs`; mode 1: flag owners in `revert`
-  int mode;
-  int32_t* pairs;
-  uint64_t cap;
-  unsigned long long* npairs;
-  const int32_t* owner;
-  const uint8_t* applied;
-  uint8_t* revert;
-  const uint8_t* is_build;  // mode 0 symmetric dedup: probe==build set
-};
-
-__device__ __forceinline__ void report(const ProbeOut& o, int32_t p, int32_t a) {
-  if (o.mode == 0) {
-    const unsigned long long k = atomicAdd(o.npairs, 1ull);
-    if (k < o.cap) {
-      o.pairs[2 * k] = min(p, a);
-      o.pairs[2 * k + 1] = max(p, a);
-    }
-  } else {
-    atomicAdd(o.npairs, 1ull);
-    const int32_t oa = o.owner[a], op = o.owner[p];
-    if (oa >= 0 && o.applied[oa]) o.revert[oa] = 1;
-    if (op >= 0 && o.applied[op]) o.revert[op] = 1;
-  }
-}
-
-// probe faces (all alive faces when ids == null) against the build grid
-__global__ void k_probe(const double* __restrict__ V, const int32_t* __restrict__ F, const int32_t* __restrict__ ids,
-                        int64_t n, const uint8_t* __restrict__ alive, double inv_h, uint32_t mask,
-                        const uint32_t* __restrict__ bcount, const uint32_t* __restrict__ boff,
-                        const int32_t* __restrict__ entries, const int32_t* __restrict__ big, int64_t nbig,
-                        int symmetric, ProbeOut o) {
+// Broad phase: every probe face p walks the cells its box covers and emits candidate pairs
+// (p, a) with a in the build grid and closed inflated-box overlap (the reference's candidate
+// set).  `sym` = probe set == build set (each unordered pair once); otherwise a pair of two
+// build faces is emitted only from its smaller probe.
+__global__ void __launch_bounds__(128) k_probe(const double* __restrict__ V, const int32_t* __restrict__ F,
+                                               int64_t n, const uint8_t* __restrict__ alive, double inv_h,
+                                               uint32_t mask, const uint32_t* __restrict__ bcount,
+                                               const uint32_t* __restrict__ boff, const int32_t* __restrict__ entries,
+                                               const int32_t* __restrict__ big, int64_t nbig, int sym,
+                                               const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
+                                               uint64_t cap, unsigned long long* __restrict__ ncand) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= n) return;
-  const int32_t p = ids ? ids[k] : static_cast<int32_t>(k);
+  const int32_t p = static_cast<int32_t>(k);
   if (alive && !alive[p]) return;
-  const int32_t* tp = F + 3 * p;
-  const Box bp = face_box(V, tp);
+  const bool p_build = sym || (in_build && in_build[p]);
+  const Box bp = face_box(V, F + 3 * p);
   const CellRange cp = cells_of(bp, inv_h);
   auto consider = [&](int32_t a) {
     if (a == p) return;
-    if (symmetric && a < p) return;  // each unordered pair once (probe set == build set)
+    if (p_build && a < p) return;  // the pair is emitted from probe a instead
     const Box ba = face_box(V, F + 3 * a);
     if (!overlap(bp, ba)) return;
-    if (verdict(V, tp, F + 3 * a)) report(o, p, a);
+    const unsigned long long slot = atomicAdd(ncand, 1ull);
+    if (slot < cap) cand[slot] = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
   };
   if (cp.count() > kMaxCells) {
-    // huge probe: scan the whole build set (grid entries deduplicated by their own first cell)
+    // huge probe: scan the whole build set, each entry once (in the bucket of its first cell)
     for (uint32_t h = 0; h <= mask; ++h)
       for (uint32_t e = boff[h]; e < boff[h] + bcount[h]; ++e) {
         const int32_t a = entries[e];
         const CellRange ca = cells_of(face_box(V, F + 3 * a), inv_h);
-        if (cell_hash(ca.lo[0], ca.lo[1], ca.lo[2], mask) != h) continue;  // its first cell only
+        if (cell_hash(ca.lo[0], ca.lo[1], ca.lo[2], mask) != h) continue;
         consider(a);
       }
   } else {
@@ -378,7 +370,7 @@ __global__ void k_probe(const double* __restrict__ V, const int32_t* __restrict_
           for (uint32_t e = boff[h]; e < boff[h] + bcount[h]; ++e) {
             const int32_t a = entries[e];
             const CellRange ca = cells_of(face_box(V, F + 3 * a), inv_h);
-            // entry really covers (x,y,z) and this is the first common cell
+            // the entry really covers (x,y,z) and this is the first common cell of the two ranges
             if (x < ca.lo[0] || x > ca.hi[0] || y < ca.lo[1] || y > ca.hi[1] || z < ca.lo[2] || z > ca.hi[2]) continue;
             if (x != max(cp.lo[0], ca.lo[0]) || y != max(cp.lo[1], ca.lo[1]) || z != max(cp.lo[2], ca.lo[2])) continue;
             consider(a);
@@ -386,6 +378,37 @@ __global__ void k_probe(const double* __restrict__ V, const int32_t* __restrict_
         }
   }
   for (int64_t b = 0; b < nbig; ++b) consider(big[b]);
+}
+
+// Narrow phase over candidate pairs.  mode 0: append intersecting pairs (min, max);
+// mode 1: flag the applied owners of both faces for revert (QEM undo loop).
+__global__ void __launch_bounds__(128) k_narrow(const double* __restrict__ V, const int32_t* __restrict__ F,
+                                                const uint64_t* __restrict__ cand, int64_t n, int mode,
+                                                int32_t* __restrict__ pairs, uint64_t cap,
+                                                unsigned long long* __restrict__ npairs,
+                                                const int32_t* __restrict__ owner, const uint8_t* __restrict__ applied,
+                                                uint8_t* __restrict__ revert) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int32_t p = static_cast<int32_t>(cand[i] >> 32), a = static_cast<int32_t>(cand[i] & 0xffffffffu);
+  if (mode == 1) {
+    // only pairs whose owners can still be reverted matter
+    const int32_t op = owner[p], oa = owner[a];
+    const bool rp = op >= 0 && applied[op], ra = oa >= 0 && applied[oa];
+    if (!rp && !ra) return;
+    if (rp && ra && revert[op] && revert[oa]) return;  // both already flagged
+    if (!verdict(V, F + 3 * p, F + 3 * a)) return;
+    atomicAdd(npairs, 1ull);
+    if (rp) revert[op] = 1;
+    if (ra) revert[oa] = 1;
+  } else {
+    if (!verdict(V, F + 3 * p, F + 3 * a)) return;
+    const unsigned long long k = atomicAdd(npairs, 1ull);
+    if (k < cap) {
+      pairs[2 * k] = min(p, a);
+      pairs[2 * k + 1] = max(p, a);
+    }
+  }
 }
 
 __global__ void k_verdict_pairs(const double* __restrict__ V, const int32_t* __restrict__ F,
@@ -436,6 +459,26 @@ void build_grid(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, 
   nbig = static_cast<int64_t>(nb_big);
 }
 
+__global__ void k_flag_ids(const int32_t* __restrict__ ids, int64_t n, uint8_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) flag[ids[i]] = 1;
+}
+
+int64_t probe_candidates(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
+                         const uint8_t* d_alive, double inv_h, uint32_t mask, int64_t nbig, int sym,
+                         const uint8_t* in_build) {
+  uint64_t cap = std::max<uint64_t>(S.cand.n, static_cast<uint64_t>(nf) * 4 + 1024);
+  while (true) {
+    S.cand.ensure(cap, ctx.stream);
+    PCU_CUDA(cudaMemsetAsync(S.counters.get() + 3, 0, 8, ctx.stream));
+    PCU_LAUNCH(ctx, k_probe, grid_for(nf, 128), 128, 0, dV, dF, nf, d_alive, inv_h, mask, S.bcount.get(), S.boff.get(),
+               S.entries.get(), S.big.get(), nbig, sym, in_build, S.cand.get(), S.cand.n, S.counters.get() + 3);
+    const uint64_t got = read_scalar(ctx, S.counters.get() + 3);
+    if (got <= S.cand.n) return static_cast<int64_t>(got);
+    cap = got + got / 4 + 1024;
+  }
+}
+
 }  // namespace
 
 std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf,
@@ -449,13 +492,14 @@ std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, 
   uint32_t mask;
   int64_t nbig;
   build_grid(ctx, S, dV, dF, nullptr, nf, d_alive, inv_h, mask, nbig, nf);
-  uint64_t cap = static_cast<uint64_t>(nf) + 1024;
+  const int64_t ncand = probe_candidates(ctx, S, dV, dF, nf, d_alive, inv_h, mask, nbig, 1, nullptr);
+  uint64_t cap = 1024;
   while (true) {
     DevBuf<int32_t> pairs(2 * cap, ctx.stream);
-    S.counters.memset(0, ctx.stream);
-    ProbeOut o{0, pairs.get(), cap, S.counters.get() + 2, nullptr, nullptr, nullptr, nullptr};
-    PCU_LAUNCH(ctx, k_probe, grid_for(nf, 128), 128, 0, dV, dF, nullptr, nf, d_alive, inv_h, mask, S.bcount.get(),
-               S.boff.get(), S.entries.get(), S.big.get(), nbig, 1, o);
+    PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));
+    if (ncand)
+      PCU_LAUNCH(ctx, k_narrow, grid_for(ncand, 128), 128, 0, dV, dF, S.cand.get(), ncand, 0, pairs.get(), cap,
+                 S.counters.get() + 2, nullptr, nullptr, nullptr);
     const uint64_t got = read_scalar(ctx, S.counters.get() + 2);
     if (got > cap) {
       cap = got + 1024;
@@ -466,7 +510,6 @@ std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, 
     PCU_CUDA(cudaStreamSynchronize(ctx.stream));
     break;
   }
-  // sort pairs (host; output is small)
   std::vector<std::pair<int32_t, int32_t>> pv(out.size() / 2);
   for (size_t i = 0; i < pv.size(); ++i) pv[i] = {out[2 * i], out[2 * i + 1]};
   std::sort(pv.begin(), pv.end());
@@ -492,11 +535,18 @@ int64_t undo_detect(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* 
   uint32_t mask;
   int64_t nbig;
   // grid over the (few) query faces, probed by every alive face
+  ctx.prof.mark(ctx.stream, "undo_detect:pre");
   build_grid(ctx, S, dV, dF, d_query_faces, n_query, d_falive, inv_h, mask, nbig, n_query);
-  S.counters.memset(0, ctx.stream);
-  ProbeOut o{1, nullptr, 0, S.counters.get() + 2, d_owner, d_applied, d_revert, nullptr};
-  PCU_LAUNCH(ctx, k_probe, grid_for(nf, 128), 128, 0, dV, dF, nullptr, nf, d_falive, inv_h, mask, S.bcount.get(),
-             S.boff.get(), S.entries.get(), S.big.get(), nbig, 0, o);
+  S.in_build.ensure(nf, ctx.stream);
+  PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, ctx.stream));
+  PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_query, 256), 256, 0, d_query_faces, n_query, S.in_build.get());
+  ctx.prof.mark(ctx.stream, "undo_detect:grid");
+  const int64_t ncand = probe_candidates(ctx, S, dV, dF, nf, d_falive, inv_h, mask, nbig, 0, S.in_build.get());
+  ctx.prof.mark(ctx.stream, "undo_detect:broad");
+  if (ncand == 0) return 0;
+  PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));
+  PCU_LAUNCH(ctx, k_narrow, grid_for(ncand, 128), 128, 0, dV, dF, S.cand.get(), ncand, 1, nullptr, 0,
+             S.counters.get() + 2, d_owner, d_applied, d_revert);
   return static_cast<int64_t>(read_scalar(ctx, S.counters.get() + 2));
 }
 

@@ -52,6 +52,7 @@ struct SimplifyParams {
 struct SimplifyStats {
   int64_t iterations = 0, collapses = 0, undone = 0, link_failures = 0, max_undo_rounds = 0;
   int64_t undo_hist[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t face_iterations = 0, alg_bytes = 0;
   std::vector<int64_t> per_iter;
 };
 // Simplifies in place.  On return dV/dF hold the compacted mesh (sizes updated).

@@ -649,14 +649,17 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
   };
 
+  ctx.prof.reset(st);
   build_incidence();
   PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, off.get(), deg.get(), inc.get(), nv, Q.get());
 
-  int64_t alive_faces = nf;
+  int64_t alive_faces = nf, alive_verts = nv;
   int retain = 0, zero_run = 0;
   while (alive_faces > target && zero_run < P.stall) {
     S.iterations++;
+    ctx.prof.mark(st, "misc");
     if (S.iterations > 1) build_incidence();
+    ctx.prof.mark(st, "incidence");
     cnt.memset(0, st);
     // edges
     PCU_LAUNCH(ctx, k_edge_count, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, ecount.get(),
@@ -664,15 +667,19 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     exclusive_scan_u32(ctx, ecount.get(), eoff.get(), nv);
     const int64_t ne = static_cast<int64_t>(read_scalar(ctx, eoff.get() + nv - 1)) + read_scalar(ctx, ecount.get() + nv - 1);
     Counters h = read_scalar(ctx, cnt.get());
+    S.face_iterations += alive_faces;
+    S.alg_bytes += 28 * alive_faces + 92 * alive_verts + 8 * ne;
     PCU_REQUIRE(h.cap == 0, PAMOPT_CU_ECAP, "simplify_to: vertex valence exceeds 255 incident faces");
     if (S.iterations == 1)
       PCU_REQUIRE(h.err == 0, PAMOPT_CU_EINVAL, "simplify_to: non-manifold input (an edge has >2 faces); run stage 1");
     PCU_LAUNCH(ctx, k_edge_fill, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, eoff.get(), ea.get(),
                eb.get(), enf.get());
+    ctx.prof.mark(st, "edges");
     PCU_LAUNCH(ctx, k_mark_invalid, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), ne, inv.get(), ninv, valid.get());
     cnt.memset(0, st);
     PCU_LAUNCH(ctx, k_cost, grid_for(ne, 128), 128, 0, X, F, Q.get(), off.get(), deg.get(), inc.get(), ea.get(), eb.get(),
                valid.get(), ne, P.we, P.ws, key.get(), place.get(), cnt.get());
+    ctx.prof.mark(st, "cost");
     vmin.memset(0xFF, st);
     vfmin.memset(0xFF, st);
     PCU_LAUNCH(ctx, k_prop_edges, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), key.get(), valid.get(), ne, vmin.get());
@@ -680,6 +687,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     PCU_LAUNCH(ctx, k_mark, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), key.get(), valid.get(), ne, vfmin.get(),
                marked.get(), cnt.get());
     h = read_scalar(ctx, cnt.get());
+    ctx.prof.mark(st, "propagate+mark");
     PCU_REQUIRE(h.err == 0, PAMOPT_CU_ENUMERIC, "simplify_to: NaN edge cost");
     const int64_t nm = static_cast<int64_t>(h.marked);
     int64_t succ = 0;
@@ -698,12 +706,14 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
       PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, marked_sorted.get(), nm, ea.get(), eb.get(), enf.get(), F,
                  off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get());
       exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
+      ctx.prof.mark(st, "sort+link");
       PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
       PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), st));
       PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, marked_sorted.get(), nm, rem.get(), remoff.get(),
                  alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
                  falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
       h = read_scalar(ctx, cnt.get());
+      ctx.prof.mark(st, "collapse");
       int64_t nq = static_cast<int64_t>(h.query);
       int32_t* qa = qf.get();
       int32_t* qb = qf2.get();
@@ -711,6 +721,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
         revert.memset(0, st);
         const int64_t found =
             undo_detect(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get());
+        ctx.prof.mark(st, "undo_detect");
         if (found == 0) break;
         ++rounds;
         PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
@@ -721,6 +732,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
         h = read_scalar(ctx, cnt.get());
         nq = static_cast<int64_t>(h.query);
         std::swap(qa, qb);
+        ctx.prof.mark(st, "undo_revert");
       }
       h = read_scalar(ctx, cnt.get());
       succ = static_cast<int64_t>(h.applied);
@@ -732,6 +744,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     S.undo_hist[std::min(rounds, 7)]++;
     S.max_undo_rounds = std::max<int64_t>(S.max_undo_rounds, rounds);
     S.collapses += succ;
+    alive_verts -= succ;
     S.per_iter.push_back(succ);
     // invalid-flag update
     bool keep_old;
@@ -764,6 +777,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     } else {
       ninv = 0;
     }
+    ctx.prof.mark(st, "invalid_update");
   }
   // compaction (mesh.cpp:278-292): alive vertices used by alive faces, order preserving
   DevBuf<uint32_t> vk(nv, st), vmap(nv, st), fk(nf, st), fmap(nf, st);
@@ -783,6 +797,8 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
   Fb = std::move(Fo);
   nv = nv2;
   nf = nf2;
+  ctx.prof.mark(st, "compact");
+  ctx.prof.dump("simplify");
 }
 
 }  // namespace pcu
