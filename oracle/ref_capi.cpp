@@ -102,10 +102,14 @@ int ref_collapse_sequence(const double* v, int64_t nv, const int32_t* f, int64_t
     HalfEdgeAdjacency adj(m);
     std::vector<CollapseRecord> recs;
     for (int64_t i = 0; i < ne; ++i) {
-      auto r = adj.collapse_edge(edges[2 * i], edges[2 * i + 1],
-                                 Vec3d(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]));
-      ok[i] = r.has_value() ? 1 : 0;
-      if (r) recs.push_back(std::move(*r));
+      try {
+        auto r = adj.collapse_edge(edges[2 * i], edges[2 * i + 1],
+                                   Vec3d(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]));
+        ok[i] = r.has_value() ? 1 : 0;
+        if (r) recs.push_back(std::move(*r));
+      } catch (const std::invalid_argument&) {
+        ok[i] = -1;  // the edge no longer exists (mesh.cpp:302)
+      }
     }
     if (undo)
       for (auto it = recs.rbegin(); it != recs.rend(); ++it) adj.undo_collapse(*it);

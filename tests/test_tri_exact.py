@@ -1,0 +1,32 @@
+"""The oracle's narrow phase against an independent exact rational-arithmetic oracle
+(0% false negatives on a corpus covering coplanar, sharp, vertex-sharing and
+edge-sharing pairs).  Both are exact, so they must agree on every pair (FPR = FNR = 0)."""
+import numpy as np
+
+from tests.exact_tri import verdict_pairs
+from tests.tri_corpus import corpus
+
+
+def test_narrow_phase_exact_agreement(oracle):
+    v, f, pairs = corpus(1600, seed=3)
+    got = oracle.tri_tri_pairs(v, f, pairs)
+    ref = np.array(verdict_pairs(v.tolist(), f.tolist(), pairs.tolist()))
+    fn = int(((ref == 1) & (got == 0)).sum())
+    fp = int(((ref == 0) & (got == 1)).sum())
+    assert fn == 0 and fp == 0, (fn, fp)
+    # symmetry
+    got_sw = oracle.tri_tri_pairs(v, f, pairs[:, ::-1].copy())
+    assert np.array_equal(got, got_sw)
+    # both outcomes are represented in every case family (family 6 = non-coplanar shared edge,
+    # never an intersection by definition)
+    fam = got.reshape(-1, 8)
+    assert (fam.sum(0)[[0, 1, 2, 3, 4, 5, 7]] > 0).all() and fam[:, 6].sum() == 0
+    assert ((1 - fam).sum(0) > 0).all()
+
+
+def test_narrow_phase_rigid_invariance(oracle):
+    """translation + uniform power-of-two scaling keep every verdict."""
+    v, f, pairs = corpus(800, seed=5)
+    a = oracle.tri_tri_pairs(v, f, pairs)
+    b = oracle.tri_tri_pairs(v * 4.0 + 0.5, f, pairs)
+    assert np.array_equal(a, b)
