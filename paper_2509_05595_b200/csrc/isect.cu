@@ -34,6 +34,7 @@ struct IsectScratch {
   DevBuf<double> ext_sum;
   DevBuf<uint8_t> in_build;
   DevBuf<uint64_t> cand;
+  DevBuf<float> fbox;  // 6 floats per face
 };
 
 IsectScratch* isect_scratch_create() { return new IsectScratch(); }
@@ -66,6 +67,17 @@ __device__ __forceinline__ bool overlap(const Box& a, const Box& b) {
          a.hi[1] >= b.lo[1] && a.hi[2] >= b.lo[2];
 }
 
+// conservative float copy of the inflated box (lo rounded down, hi rounded up): the float
+// overlap test admits a superset of the double-box pairs; the exact test runs in k_narrow
+struct FBox {
+  float lo[3], hi[3];
+};
+
+__device__ __forceinline__ bool overlap(const FBox& a, const FBox& b) {
+  return a.lo[0] <= b.hi[0] && a.lo[1] <= b.hi[1] && a.lo[2] <= b.hi[2] && a.hi[0] >= b.lo[0] &&
+         a.hi[1] >= b.lo[1] && a.hi[2] >= b.lo[2];
+}
+
 struct CellRange {
   int64_t lo[3], hi[3];
   __device__ int64_t count() const { return (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1); }
@@ -76,6 +88,15 @@ __device__ __forceinline__ CellRange cells_of(const Box& b, double inv_h) {
   for (int k = 0; k < 3; ++k) {
     r.lo[k] = static_cast<int64_t>(floor(b.lo[k] * inv_h));
     r.hi[k] = static_cast<int64_t>(floor(b.hi[k] * inv_h));
+  }
+  return r;
+}
+
+__device__ __forceinline__ CellRange cells_of(const FBox& b, double inv_h) {
+  CellRange r;
+  for (int k = 0; k < 3; ++k) {
+    r.lo[k] = static_cast<int64_t>(floor(static_cast<double>(b.lo[k]) * inv_h));
+    r.hi[k] = static_cast<int64_t>(floor(static_cast<double>(b.hi[k]) * inv_h));
   }
   return r;
 }
@@ -287,8 +308,28 @@ __device__ bool verdict(const double* __restrict__ V, const int32_t* t1, const i
 }
 
 // ------------------------------------------------------------------------ grid kernels
-__global__ void k_ext_sum(const double* __restrict__ V, const int32_t* __restrict__ F, const int32_t* __restrict__ ids,
-                          int64_t n, const uint8_t* __restrict__ alive, double* __restrict__ out) {
+__global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t nf,
+                         const uint8_t* __restrict__ alive, FBox* __restrict__ out) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nf) return;
+  FBox fb;
+  if (alive && !alive[f]) {
+    for (int k = 0; k < 3; ++k) {
+      fb.lo[k] = __int_as_float(0x7f800000);
+      fb.hi[k] = __int_as_float(0xff800000);
+    }
+  } else {
+    const Box b = face_box(V, F + 3 * f);
+    for (int k = 0; k < 3; ++k) {
+      fb.lo[k] = __double2float_rd(b.lo[k]);
+      fb.hi[k] = __double2float_ru(b.hi[k]);
+    }
+  }
+  out[f] = fb;
+}
+
+__global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict__ ids, int64_t n,
+                          const uint8_t* __restrict__ alive, double* __restrict__ out) {
   typedef cub::BlockReduce<double, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   double s = 0.0;
@@ -296,7 +337,7 @@ __global__ void k_ext_sum(const double* __restrict__ V, const int32_t* __restric
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t f = ids ? ids[k] : k;
     if (alive && !alive[f]) continue;
-    const Box b = face_box(V, F + 3 * f);
+    const FBox& b = B[f];
     s += fmax(fmax(b.hi[0] - b.lo[0], b.hi[1] - b.lo[1]), b.hi[2] - b.lo[2]);
   }
   const double t = BR(tmp).Sum(s);
@@ -304,16 +345,15 @@ __global__ void k_ext_sum(const double* __restrict__ V, const int32_t* __restric
 }
 
 // pass 0: count bucket entries (or big); pass 1: fill
-__global__ void k_bin(const double* __restrict__ V, const int32_t* __restrict__ F, const int32_t* __restrict__ ids,
-                      int64_t n, const uint8_t* __restrict__ alive, double inv_h, uint32_t mask, int pass,
+__global__ void k_bin(const FBox* __restrict__ B, const int32_t* __restrict__ ids, int64_t n,
+                      const uint8_t* __restrict__ alive, double inv_h, uint32_t mask, int pass,
                       uint32_t* __restrict__ bcount, const uint32_t* __restrict__ boff, uint32_t* __restrict__ bcur,
                       int32_t* __restrict__ entries, int32_t* __restrict__ big, unsigned long long* counters) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= n) return;
   const int32_t f = ids ? ids[k] : static_cast<int32_t>(k);
   if (alive && !alive[f]) return;
-  const Box b = face_box(V, F + 3 * f);
-  const CellRange cr = cells_of(b, inv_h);
+  const CellRange cr = cells_of(B[f], inv_h);
   if (cr.count() > kMaxCells) {
     if (pass == 1) big[atomicAdd(&counters[1], 1ull)] = f;
     return;
@@ -328,12 +368,11 @@ __global__ void k_bin(const double* __restrict__ V, const int32_t* __restrict__ 
 }
 
 // Broad phase: every probe face p walks the cells its box covers and emits candidate pairs
-// (p, a) with a in the build grid and closed inflated-box overlap (the reference's candidate
-// set).  `sym` = probe set == build set (each unordered pair once); otherwise a pair of two
-// build faces is emitted only from its smaller probe.
-__global__ void __launch_bounds__(128) k_probe(const double* __restrict__ V, const int32_t* __restrict__ F,
-                                               int64_t n, const uint8_t* __restrict__ alive, double inv_h,
-                                               uint32_t mask, const uint32_t* __restrict__ bcount,
+// (p, a) with a in the build grid and overlapping (conservative float) boxes.  `sym` = probe
+// set == build set (each unordered pair once); otherwise a pair of two build faces is emitted
+// only from its smaller probe.
+__global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64_t n, const uint8_t* __restrict__ alive,
+                                               double inv_h, uint32_t mask, const uint32_t* __restrict__ bcount,
                                                const uint32_t* __restrict__ boff, const int32_t* __restrict__ entries,
                                                const int32_t* __restrict__ big, int64_t nbig, int sym,
                                                const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
@@ -343,12 +382,11 @@ __global__ void __launch_bounds__(128) k_probe(const double* __restrict__ V, con
   const int32_t p = static_cast<int32_t>(k);
   if (alive && !alive[p]) return;
   const bool p_build = sym || (in_build && in_build[p]);
-  const Box bp = face_box(V, F + 3 * p);
+  const FBox bp = B[p];
   const CellRange cp = cells_of(bp, inv_h);
-  auto consider = [&](int32_t a) {
+  auto consider = [&](int32_t a, const FBox& ba) {
     if (a == p) return;
     if (p_build && a < p) return;  // the pair is emitted from probe a instead
-    const Box ba = face_box(V, F + 3 * a);
     if (!overlap(bp, ba)) return;
     const unsigned long long slot = atomicAdd(ncand, 1ull);
     if (slot < cap) cand[slot] = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
@@ -358,26 +396,29 @@ __global__ void __launch_bounds__(128) k_probe(const double* __restrict__ V, con
     for (uint32_t h = 0; h <= mask; ++h)
       for (uint32_t e = boff[h]; e < boff[h] + bcount[h]; ++e) {
         const int32_t a = entries[e];
-        const CellRange ca = cells_of(face_box(V, F + 3 * a), inv_h);
+        const FBox ba = B[a];
+        const CellRange ca = cells_of(ba, inv_h);
         if (cell_hash(ca.lo[0], ca.lo[1], ca.lo[2], mask) != h) continue;
-        consider(a);
+        consider(a, ba);
       }
   } else {
     for (int64_t z = cp.lo[2]; z <= cp.hi[2]; ++z)
       for (int64_t y = cp.lo[1]; y <= cp.hi[1]; ++y)
         for (int64_t x = cp.lo[0]; x <= cp.hi[0]; ++x) {
           const uint32_t h = cell_hash(x, y, z, mask);
-          for (uint32_t e = boff[h]; e < boff[h] + bcount[h]; ++e) {
+          const uint32_t e1 = boff[h] + bcount[h];
+          for (uint32_t e = boff[h]; e < e1; ++e) {
             const int32_t a = entries[e];
-            const CellRange ca = cells_of(face_box(V, F + 3 * a), inv_h);
+            const FBox ba = B[a];
+            const CellRange ca = cells_of(ba, inv_h);
             // the entry really covers (x,y,z) and this is the first common cell of the two ranges
             if (x < ca.lo[0] || x > ca.hi[0] || y < ca.lo[1] || y > ca.hi[1] || z < ca.lo[2] || z > ca.hi[2]) continue;
             if (x != max(cp.lo[0], ca.lo[0]) || y != max(cp.lo[1], ca.lo[1]) || z != max(cp.lo[2], ca.lo[2])) continue;
-            consider(a);
+            consider(a, ba);
           }
         }
   }
-  for (int64_t b = 0; b < nbig; ++b) consider(big[b]);
+  for (int64_t b = 0; b < nbig; ++b) consider(big[b], B[big[b]]);
 }
 
 // Narrow phase over candidate pairs.  mode 0: append intersecting pairs (min, max);
@@ -391,6 +432,8 @@ __global__ void __launch_bounds__(128) k_narrow(const double* __restrict__ V, co
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const int32_t p = static_cast<int32_t>(cand[i] >> 32), a = static_cast<int32_t>(cand[i] & 0xffffffffu);
+  // the reference candidate set: closed overlap of the 1e-7-inflated double boxes
+  if (!overlap(face_box(V, F + 3 * p), face_box(V, F + 3 * a))) return;
   if (mode == 1) {
     // only pairs whose owners can still be reverted matter
     const int32_t op = owner[p], oa = owner[a];
@@ -424,13 +467,14 @@ uint32_t pow2_at_least(uint64_t x) {
   return p;
 }
 
-// Builds the grid over (ids or all alive faces) and returns (inv_h, mask, nbig).
-void build_grid(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, const int32_t* d_ids, int64_t n,
-                const uint8_t* d_alive, double& inv_h, uint32_t& mask, int64_t& nbig, int64_t n_alive_hint) {
+// Builds the grid over (ids or all alive faces) from the float boxes; returns (inv_h, mask, nbig).
+void build_grid(Ctx& ctx, IsectScratch& S, const int32_t* d_ids, int64_t n, const uint8_t* d_alive, double& inv_h,
+                uint32_t& mask, int64_t& nbig, int64_t n_alive_hint) {
+  const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
   S.ext_sum.ensure(1, ctx.stream);
   S.ext_sum.memset(0, ctx.stream);
-  PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n, 256), ctx.num_sms * 4)), 256, 0, dV,
-             dF, d_ids, n, d_alive, S.ext_sum.get());
+  PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n, 256), ctx.num_sms * 4)), 256, 0, B,
+             d_ids, n, d_alive, S.ext_sum.get());
   const double sum = read_scalar(ctx, S.ext_sum.get());
   const double mean = n_alive_hint > 0 ? sum / static_cast<double>(n_alive_hint) : 1.0;
   const double h = mean > 0.0 ? mean : 1e-3;
@@ -445,18 +489,23 @@ void build_grid(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, 
   PCU_CUDA(cudaMemsetAsync(S.bcur.get(), 0, nb * 4, ctx.stream));
   S.counters.memset(0, ctx.stream);
   S.big.ensure(1, ctx.stream);
-  PCU_LAUNCH(ctx, k_bin, grid_for(n, 256), 256, 0, dV, dF, d_ids, n, d_alive, inv_h, mask, 0, S.bcount.get(),
-             S.boff.get(), S.bcur.get(), nullptr, nullptr, S.counters.get());
+  PCU_LAUNCH(ctx, k_bin, grid_for(n, 256), 256, 0, B, d_ids, n, d_alive, inv_h, mask, 0, S.bcount.get(), S.boff.get(),
+             S.bcur.get(), nullptr, nullptr, S.counters.get());
   exclusive_scan_u32(ctx, S.bcount.get(), S.boff.get(), nb);
   const uint64_t total = static_cast<uint64_t>(read_scalar(ctx, S.boff.get() + nb - 1)) + read_scalar(ctx, S.bcount.get() + nb - 1);
   S.entries.ensure(total ? total : 1, ctx.stream);
   S.big.ensure(static_cast<size_t>(n > 0 ? n : 1), ctx.stream);
-  PCU_LAUNCH(ctx, k_bin, grid_for(n, 256), 256, 0, dV, dF, d_ids, n, d_alive, inv_h, mask, 1, S.bcount.get(),
-             S.boff.get(), S.bcur.get(), S.entries.get(), S.big.get(), S.counters.get());
+  PCU_LAUNCH(ctx, k_bin, grid_for(n, 256), 256, 0, B, d_ids, n, d_alive, inv_h, mask, 1, S.bcount.get(), S.boff.get(),
+             S.bcur.get(), S.entries.get(), S.big.get(), S.counters.get());
   unsigned long long nb_big = 0;
   PCU_CUDA(cudaMemcpyAsync(&nb_big, S.counters.get() + 1, 8, cudaMemcpyDeviceToHost, ctx.stream));
   PCU_CUDA(cudaStreamSynchronize(ctx.stream));
   nbig = static_cast<int64_t>(nb_big);
+}
+
+void make_fboxes(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive) {
+  S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), ctx.stream);
+  PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()));
 }
 
 __global__ void k_flag_ids(const int32_t* __restrict__ ids, int64_t n, uint8_t* __restrict__ flag) {
@@ -464,14 +513,14 @@ __global__ void k_flag_ids(const int32_t* __restrict__ ids, int64_t n, uint8_t* 
   if (i < n) flag[ids[i]] = 1;
 }
 
-int64_t probe_candidates(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
-                         const uint8_t* d_alive, double inv_h, uint32_t mask, int64_t nbig, int sym,
-                         const uint8_t* in_build) {
+int64_t probe_candidates(Ctx& ctx, IsectScratch& S, int64_t nf, const uint8_t* d_alive, double inv_h, uint32_t mask,
+                         int64_t nbig, int sym, const uint8_t* in_build) {
   uint64_t cap = std::max<uint64_t>(S.cand.n, static_cast<uint64_t>(nf) * 4 + 1024);
+  const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
   while (true) {
     S.cand.ensure(cap, ctx.stream);
     PCU_CUDA(cudaMemsetAsync(S.counters.get() + 3, 0, 8, ctx.stream));
-    PCU_LAUNCH(ctx, k_probe, grid_for(nf, 128), 128, 0, dV, dF, nf, d_alive, inv_h, mask, S.bcount.get(), S.boff.get(),
+    PCU_LAUNCH(ctx, k_probe, grid_for(nf, 128), 128, 0, B, nf, d_alive, inv_h, mask, S.bcount.get(), S.boff.get(),
                S.entries.get(), S.big.get(), nbig, sym, in_build, S.cand.get(), S.cand.n, S.counters.get() + 3);
     const uint64_t got = read_scalar(ctx, S.counters.get() + 3);
     if (got <= S.cand.n) return static_cast<int64_t>(got);
@@ -491,8 +540,9 @@ std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, 
   double inv_h;
   uint32_t mask;
   int64_t nbig;
-  build_grid(ctx, S, dV, dF, nullptr, nf, d_alive, inv_h, mask, nbig, nf);
-  const int64_t ncand = probe_candidates(ctx, S, dV, dF, nf, d_alive, inv_h, mask, nbig, 1, nullptr);
+  make_fboxes(ctx, S, dV, dF, nf, d_alive);
+  build_grid(ctx, S, nullptr, nf, d_alive, inv_h, mask, nbig, nf);
+  const int64_t ncand = probe_candidates(ctx, S, nf, d_alive, inv_h, mask, nbig, 1, nullptr);
   uint64_t cap = 1024;
   while (true) {
     DevBuf<int32_t> pairs(2 * cap, ctx.stream);
@@ -536,12 +586,13 @@ int64_t undo_detect(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* 
   int64_t nbig;
   // grid over the (few) query faces, probed by every alive face
   ctx.prof.mark(ctx.stream, "undo_detect:pre");
-  build_grid(ctx, S, dV, dF, d_query_faces, n_query, d_falive, inv_h, mask, nbig, n_query);
+  make_fboxes(ctx, S, dV, dF, nf, d_falive);
+  build_grid(ctx, S, d_query_faces, n_query, d_falive, inv_h, mask, nbig, n_query);
   S.in_build.ensure(nf, ctx.stream);
   PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, ctx.stream));
   PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_query, 256), 256, 0, d_query_faces, n_query, S.in_build.get());
   ctx.prof.mark(ctx.stream, "undo_detect:grid");
-  const int64_t ncand = probe_candidates(ctx, S, dV, dF, nf, d_falive, inv_h, mask, nbig, 0, S.in_build.get());
+  const int64_t ncand = probe_candidates(ctx, S, nf, d_falive, inv_h, mask, nbig, 0, S.in_build.get());
   ctx.prof.mark(ctx.stream, "undo_detect:broad");
   if (ncand == 0) return 0;
   PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));

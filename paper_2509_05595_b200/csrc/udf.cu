@@ -32,8 +32,47 @@ constexpr double kHalfSqrt3 = 0.8660254037844386;
 constexpr int kChunk = 128;  // triangles per brick work item
 
 struct __align__(16) TriD {
-  double a[3], b[3], c[3], lo[3], hi[3], pad;
+  double a[3], b[3], c[3], lo[3], hi[3];
+  float ab[3], ac[3];  // local frame (b-a, c-a computed in FP64, rounded to FP32)
+  float L2;            // max squared edge length
+  int wc;              // well conditioned: every corner angle has sin^2 >= 0.01
 };
+
+// FP32 point-triangle squared distance in the triangle's local frame (p relative to a).
+// Used only as a certified filter for well-conditioned triangles (see survives / k_brick):
+// its error is far below the 1e-4 * L^2 margin, so every decision it takes equals the FP64
+// decision; everything near a threshold is re-evaluated in FP64.
+__device__ __forceinline__ float fseg_sq(float px, float py, float pz, float ax, float ay, float az, float bx, float by,
+                                         float bz) {
+  const float ux = bx - ax, uy = by - ay, uz = bz - az;
+  const float den = ux * ux + uy * uy + uz * uz;
+  float t = den > 0.f ? ((px - ax) * ux + (py - ay) * uy + (pz - az) * uz) / den : 0.f;
+  t = fminf(fmaxf(t, 0.f), 1.f);
+  const float qx = px - (ax + t * ux), qy = py - (ay + t * uy), qz = pz - (az + t * uz);
+  return qx * qx + qy * qy + qz * qz;
+}
+__device__ __forceinline__ float fptri_sq(const TriD& t, float px, float py, float pz) {
+  const float bx = t.ab[0], by = t.ab[1], bz = t.ab[2], cx = t.ac[0], cy = t.ac[1], cz = t.ac[2];
+  const float nx = by * cz - bz * cy, ny = bz * cx - bx * cz, nz = bx * cy - by * cx;
+  const float nn = nx * nx + ny * ny + nz * nz;
+  float best = __int_as_float(0x7f800000);
+  if (nn > 0.f) {
+    const float dn = px * nx + py * ny + pz * nz;
+    const float s = dn / nn;
+    const float qx = px - s * nx, qy = py - s * ny, qz = pz - s * nz;
+    const float d00 = bx * bx + by * by + bz * bz, d01 = bx * cx + by * cy + bz * cz, d11 = cx * cx + cy * cy + cz * cz;
+    const float d20 = qx * bx + qy * by + qz * bz, d21 = qx * cx + qy * cy + qz * cz;
+    const float den = d00 * d11 - d01 * d01;
+    if (den > 0.f) {
+      const float v = (d11 * d20 - d01 * d21) / den, w = (d00 * d21 - d01 * d20) / den;
+      if (v >= 0.f && w >= 0.f && v + w <= 1.f) best = dn * s;
+    }
+  }
+  best = fminf(best, fseg_sq(px, py, pz, 0.f, 0.f, 0.f, bx, by, bz));
+  best = fminf(best, fseg_sq(px, py, pz, bx, by, bz, cx, cy, cz));
+  best = fminf(best, fseg_sq(px, py, pz, cx, cy, cz, 0.f, 0.f, 0.f));
+  return best;
+}
 
 __device__ __forceinline__ bool survives(const TriD& t, double cx, double cy, double cz, double thr) {
   const double tb = thr + 1e-9;
@@ -41,6 +80,16 @@ __device__ __forceinline__ bool survives(const TriD& t, double cx, double cy, do
   const double dy = fmax(fmax(t.lo[1] - cy, cy - t.hi[1]), 0.0);
   const double dz = fmax(fmax(t.lo[2] - cz, cz - t.hi[2]), 0.0);
   if ((dx * dx + dy * dy) + dz * dz > tb * tb) return false;
+  if (t.wc) {  // certified FP32 decision away from the threshold
+    const float px = static_cast<float>(cx - t.a[0]), py = static_cast<float>(cy - t.a[1]),
+                pz = static_cast<float>(cz - t.a[2]);
+    const float d2 = fptri_sq(t, px, py, pz);
+    const float L2 = fmaxf(t.L2, px * px + py * py + pz * pz);
+    const float th2 = static_cast<float>(thr * thr);
+    const float m = 1e-4f * L2 + 1e-3f * th2;
+    if (d2 < th2 - m) return true;
+    if (d2 > th2 + m) return false;
+  }
   const double d2 = ptri_sq(D3{cx, cy, cz}, D3{t.a[0], t.a[1], t.a[2]}, D3{t.b[0], t.b[1], t.b[2]},
                             D3{t.c[0], t.c[1], t.c[2]});
   return sqrt(d2) <= thr;
@@ -63,7 +112,19 @@ __global__ void k_prep(const double* __restrict__ V, const int32_t* __restrict__
     t.lo[k] = fmin(fmin(t.a[k], t.b[k]), t.c[k]);
     t.hi[k] = fmax(fmax(t.a[k], t.b[k]), t.c[k]);
   }
-  t.pad = 0.0;
+  const D3 A{t.a[0], t.a[1], t.a[2]}, B{t.b[0], t.b[1], t.b[2]}, C{t.c[0], t.c[1], t.c[2]};
+  const D3 ab = sub(B, A), ac = sub(C, A), bc = sub(C, B);
+  for (int k = 0; k < 3; ++k) {
+    t.ab[k] = static_cast<float>(k == 0 ? ab.x : (k == 1 ? ab.y : ab.z));
+    t.ac[k] = static_cast<float>(k == 0 ? ac.x : (k == 1 ? ac.y : ac.z));
+  }
+  const double lab = sqn(ab), lac = sqn(ac), lbc = sqn(bc);
+  t.L2 = static_cast<float>(fmax(fmax(lab, lac), lbc));
+  const double n2 = sqn(cross(ab, ac));
+  // sin^2 of the three corner angles: |n|^2 / (|e1|^2 |e2|^2)
+  const bool wc = lab > 0.0 && lac > 0.0 && lbc > 0.0 && n2 >= 0.01 * lab * lac && n2 >= 0.01 * lab * lbc &&
+                  n2 >= 0.01 * lac * lbc;
+  t.wc = wc ? 1 : 0;
   T[i] = t;
 }
 
@@ -178,11 +239,19 @@ __global__ void k_make_items(const uint32_t* __restrict__ cnt, const uint32_t* _
 }
 
 // One CTA (8 warps) per work item.  bs = cells per brick edge (1..8), J = log2(bs).
-__global__ void __launch_bounds__(256) k_brick(const Item* __restrict__ items, const uint32_t* __restrict__ tris,
-                                               const TriD* __restrict__ T, int R, int rb, int bs, int J,
-                                               unsigned long long* __restrict__ blocks) {
+// Divergence-free inner loops: every level first compacts its candidate cells (children of the
+// previous level's survivors) into a shared-memory list; the finest survivors are dilated to
+// brick vertices with bit-row operations (8-bit cell rows -> 9-bit vertex rows) and compacted,
+// so all 32 lanes evaluate distances on useful work.  Vertex distances: a certified FP32
+// evaluation first (well-conditioned triangles) skips every triangle that cannot lower the
+// vertex's running minimum; the rest are evaluated with the pinned FP64 routine.
+__global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items, const uint32_t* __restrict__ tris,
+                                                  const TriD* __restrict__ T, int R, int rb, int bs, int J,
+                                                  unsigned long long* __restrict__ blocks) {
   __shared__ unsigned long long vmin[729];
-  __shared__ uint32_t masks[8][2][16];  // per warp, ping-pong level masks (<= 512 bits)
+  __shared__ uint32_t rows[8][16];        // finest-level survivor bit rows: byte (y + bs z) holds x bits
+  __shared__ uint16_t list[8][2][512];    // ping-pong survivor lists (local cell index at level j)
+  __shared__ uint16_t vlist[8][729];      // needed vertices, packed x | y<<4 | z<<8
   __shared__ TriD tsh[8];
   const Item it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -190,51 +259,106 @@ __global__ void __launch_bounds__(256) k_brick(const Item* __restrict__ items, c
   for (int v = threadIdx.x; v < nvb; v += blockDim.x) vmin[v] = ~0ull;
   __syncthreads();
   const int bx = it.brick % rb, by = (it.brick / rb) % rb, bz = it.brick / (rb * rb);
+  const unsigned lt = (1u << lane) - 1u;
   for (uint32_t k = it.begin + warp; k < it.end; k += 8) {
     if (lane == 0) tsh[warp] = T[tris[k]];
     __syncwarp();
     const TriD& t = tsh[warp];
     // level 0 inside the brick: the brick itself survived (the pair exists)
-    int cur = 0;
-    masks[warp][0][0] = 1u;
+    int cur = 0, nsurv = 1;
+    if (lane == 0) list[warp][0][0] = 0;
+    __syncwarp();
     for (int j = 1; j <= J; ++j) {
-      const int side = 1 << j, n = side * side * side, pside = side >> 1;
+      const int lp = j - 1;  // log2 of the parent side
       const int r = rb << j;
       const double thr = level_thr(R, r);
-      const int nxt = cur ^ 1;
-      for (int base = 0; base < n; base += 32) {
+      const int ncand = nsurv * 8;
+      int nout = 0;
+      for (int base = 0; base < ncand; base += 32) {
         const int c = base + lane;
         bool keep = false;
-        if (c < n) {
-          const int x = c % side, y = (c / side) % side, z = c / (side * side);
-          const int pc = (x >> 1) + pside * ((y >> 1) + pside * (z >> 1));
-          if ((masks[warp][cur][pc >> 5] >> (pc & 31)) & 1u) {
-            const int gx = bx * side + x, gy = by * side + y, gz = bz * side + z;
-            keep = survives(t, (gx + 0.5) / r, (gy + 0.5) / r, (gz + 0.5) / r, thr);
-          }
+        int cell = 0;
+        if (c < ncand) {
+          const int pc = list[warp][cur][c >> 3], ch = c & 7;
+          const int px = pc & ((1 << lp) - 1), py = (pc >> lp) & ((1 << lp) - 1), pz = pc >> (2 * lp);
+          const int x = 2 * px + (ch & 1), y = 2 * py + ((ch >> 1) & 1), z = 2 * pz + ((ch >> 2) & 1);
+          cell = x | (y << j) | (z << (2 * j));
+          const int gx = (bx << j) + x, gy = (by << j) + y, gz = (bz << j) + z;
+          keep = survives(t, (gx + 0.5) / r, (gy + 0.5) / r, (gz + 0.5) / r, thr);
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) masks[warp][nxt][base >> 5] = m;
+        if (keep) list[warp][cur ^ 1][nout + __popc(m & lt)] = static_cast<uint16_t>(cell);
+        nout += __popc(m);
       }
       __syncwarp();
-      cur = nxt;
+      cur ^= 1;
+      nsurv = nout;
+      if (nsurv == 0) break;
     }
-    // dilate the finest mask to vertices and evaluate
-    const uint32_t* fm = masks[warp][cur];
-    for (int v = lane; v < nvb; v += 32) {
-      const int vx = v % nv1, vy = (v / nv1) % nv1, vz = v / (nv1 * nv1);
-      bool need = false;
-      for (int d = 0; d < 8 && !need; ++d) {
-        const int cx = vx - (d & 1), cy = vy - ((d >> 1) & 1), cz = vz - ((d >> 2) & 1);
-        if (cx < 0 || cy < 0 || cz < 0 || cx >= bs || cy >= bs || cz >= bs) continue;
-        const int c = cx + bs * (cy + bs * cz);
-        need = (fm[c >> 5] >> (c & 31)) & 1u;
+    if (nsurv == 0) {
+      __syncwarp();
+      continue;
+    }
+    // finest survivors -> 8-bit rows (row = y + bs*z) -> dilated 9-bit vertex rows -> list
+    if (lane < 16) rows[warp][lane] = 0u;
+    __syncwarp();
+    for (int i = lane; i < nsurv; i += 32) {
+      const int c = list[warp][cur][i];
+      const int x = c & (bs - 1), row = c >> J;
+      atomicOr(&rows[warp][row >> 2], (1u << x) << (8 * (row & 3)));
+    }
+    __syncwarp();
+    const uint8_t* rb8 = reinterpret_cast<const uint8_t*>(rows[warp]);
+    const int nrows = nv1 * nv1;
+    int nneed = 0;
+    for (int base = 0; base < nrows; base += 32) {
+      const int vr = base + lane;
+      uint32_t m = 0;
+      if (vr < nrows) {
+        const int vy = vr % nv1, vz = vr / nv1;
+        for (int dz = 0; dz < 2; ++dz)
+          for (int dy = 0; dy < 2; ++dy) {
+            const int cy = vy - dy, cz = vz - dz;
+            if (cy >= 0 && cz >= 0 && cy < bs && cz < bs) m |= rb8[cy + bs * cz];
+          }
+        m = m | (m << 1);
       }
-      if (!need) continue;
+      const int cnt = __popc(m);
+      int incl = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int pos = nneed + incl - cnt;
+      if (m) {
+        const int vy = vr % nv1, vz = vr / nv1;
+        while (m) {
+          const int x = __ffs(m) - 1;
+          m &= m - 1;
+          vlist[warp][pos++] = static_cast<uint16_t>(x | (vy << 4) | (vz << 8));
+        }
+      }
+      nneed += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    const D3 A{t.a[0], t.a[1], t.a[2]}, Bv{t.b[0], t.b[1], t.b[2]}, Cv{t.c[0], t.c[1], t.c[2]};
+    for (int i = lane; i < nneed; i += 32) {
+      const int pk = vlist[warp][i];
+      const int vx = pk & 15, vy = (pk >> 4) & 15, vz = pk >> 8;
+      const int v = vx + nv1 * (vy + nv1 * vz);
       const int gx = bx * bs + vx, gy = by * bs + vy, gz = bz * bs + vz;
       const D3 p{static_cast<double>(gx) / R, static_cast<double>(gy) / R, static_cast<double>(gz) / R};
-      const double d2 = ptri_sq(p, D3{t.a[0], t.a[1], t.a[2]}, D3{t.b[0], t.b[1], t.b[2]},
-                                D3{t.c[0], t.c[1], t.c[2]});
+      if (t.wc) {
+        // this triangle cannot lower the vertex's running minimum: skip the FP64 evaluation
+        // (the minimum is order independent, so skipping never changes the result)
+        const double curm = __longlong_as_double(static_cast<long long>(vmin[v]));  // NaN while unset
+        const float px = static_cast<float>(p.x - t.a[0]), py = static_cast<float>(p.y - t.a[1]),
+                    pz = static_cast<float>(p.z - t.a[2]);
+        const float d2f = fptri_sq(t, px, py, pz);
+        const float L2 = fmaxf(t.L2, px * px + py * py + pz * pz);
+        if (static_cast<double>(d2f) - 1e-4 * static_cast<double>(L2) > curm * (1.0 + 1e-3)) continue;
+      }
+      const double d2 = ptri_sq(p, A, Bv, Cv);
       atomicMin(&vmin[v], static_cast<unsigned long long>(__double_as_longlong(d2)));
     }
     __syncwarp();
