@@ -376,10 +376,11 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
                                                const uint32_t* __restrict__ boff, const int32_t* __restrict__ entries,
                                                const int32_t* __restrict__ big, int64_t nbig, int sym,
                                                const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
-                                               uint64_t cap, unsigned long long* __restrict__ ncand) {
+                                               uint64_t cap, unsigned long long* __restrict__ ncand,
+                                               const int32_t* __restrict__ probe_ids) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= n) return;
-  const int32_t p = static_cast<int32_t>(k);
+  const int32_t p = probe_ids ? probe_ids[k] : static_cast<int32_t>(k);
   if (alive && !alive[p]) return;
   const bool p_build = sym || (in_build && in_build[p]);
   const FBox bp = B[p];
@@ -514,14 +515,15 @@ __global__ void k_flag_ids(const int32_t* __restrict__ ids, int64_t n, uint8_t* 
 }
 
 int64_t probe_candidates(Ctx& ctx, IsectScratch& S, int64_t nf, const uint8_t* d_alive, double inv_h, uint32_t mask,
-                         int64_t nbig, int sym, const uint8_t* in_build) {
+                         int64_t nbig, int sym, const uint8_t* in_build, const int32_t* probe_ids = nullptr) {
   uint64_t cap = std::max<uint64_t>(S.cand.n, static_cast<uint64_t>(nf) * 4 + 1024);
   const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
   while (true) {
     S.cand.ensure(cap, ctx.stream);
     PCU_CUDA(cudaMemsetAsync(S.counters.get() + 3, 0, 8, ctx.stream));
     PCU_LAUNCH(ctx, k_probe, grid_for(nf, 128), 128, 0, B, nf, d_alive, inv_h, mask, S.bcount.get(), S.boff.get(),
-               S.entries.get(), S.big.get(), nbig, sym, in_build, S.cand.get(), S.cand.n, S.counters.get() + 3);
+               S.entries.get(), S.big.get(), nbig, sym, in_build, S.cand.get(), S.cand.n, S.counters.get() + 3,
+               probe_ids);
     const uint64_t got = read_scalar(ctx, S.counters.get() + 3);
     if (got <= S.cand.n) return static_cast<int64_t>(got);
     cap = got + got / 4 + 1024;
@@ -593,6 +595,29 @@ int64_t undo_detect(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* 
   PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_query, 256), 256, 0, d_query_faces, n_query, S.in_build.get());
   ctx.prof.mark(ctx.stream, "undo_detect:grid");
   const int64_t ncand = probe_candidates(ctx, S, nf, d_falive, inv_h, mask, nbig, 0, S.in_build.get());
+  ctx.prof.mark(ctx.stream, "undo_detect:broad");
+  if (ncand == 0) return 0;
+  PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));
+  PCU_LAUNCH(ctx, k_narrow, grid_for(ncand, 128), 128, 0, dV, dF, S.cand.get(), ncand, 1, nullptr, 0,
+             S.counters.get() + 2, d_owner, d_applied, d_revert);
+  return static_cast<int64_t>(read_scalar(ctx, S.counters.get() + 2));
+}
+
+// Later undo rounds: only pairs (restored face, face owned by an applied collapse) can be new —
+// every other pair is unchanged since the previous round's check.  Grid over the restored
+// faces, probed by the owned faces.
+int64_t undo_detect_restored(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
+                             const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
+                             const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
+                             const uint8_t* d_applied, uint8_t* d_revert) {
+  if (n_restored == 0 || n_owned == 0) return 0;
+  double inv_h;
+  uint32_t mask;
+  int64_t nbig;
+  make_fboxes(ctx, S, dV, dF, nf, d_falive);
+  build_grid(ctx, S, d_restored, n_restored, d_falive, inv_h, mask, nbig, n_restored);
+  ctx.prof.mark(ctx.stream, "undo_detect:grid");
+  const int64_t ncand = probe_candidates(ctx, S, n_owned, d_falive, inv_h, mask, nbig, 0, nullptr, d_owned);
   ctx.prof.mark(ctx.stream, "undo_detect:broad");
   if (ncand == 0) return 0;
   PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));

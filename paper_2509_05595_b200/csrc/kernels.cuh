@@ -41,6 +41,10 @@ struct IsectScratch;
 int64_t undo_detect(Ctx& ctx, IsectScratch& scratch, const double* dV, const int32_t* dF, int64_t nf,
                     const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query,
                     const int32_t* d_owner, const uint8_t* d_applied, uint8_t* d_revert);
+int64_t undo_detect_restored(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
+                             const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
+                             const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
+                             const uint8_t* d_applied, uint8_t* d_revert);
 IsectScratch* isect_scratch_create();
 void isect_scratch_destroy(IsectScratch* s);
 

@@ -34,7 +34,7 @@ constexpr int kMaxDeg = 255;      // per-vertex incident-face capacity of the lo
 constexpr double k4Sqrt3 = 6.928203230275509;
 
 struct Counters {
-  unsigned long long edges, marked, link_fail, newinv, query, removed, applied, err, cap, undone;
+  unsigned long long edges, marked, link_fail, newinv, query, removed, applied, err, cap, undone, restored;
 };
 
 __device__ __forceinline__ D3 P3(const double* X, int v) { return D3{X[3 * v], X[3 * v + 1], X[3 * v + 2]}; }
@@ -552,19 +552,23 @@ __global__ void k_revert(int64_t nm, const uint8_t* __restrict__ revert, const u
                          const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc,
                          const int32_t* __restrict__ Fprev, double* __restrict__ X, int32_t* __restrict__ F,
                          uint8_t* __restrict__ falive, uint8_t* __restrict__ valive, double* __restrict__ Q,
-                         int32_t* __restrict__ owner, Batch B, uint64_t* __restrict__ newinv, Counters* cnt) {
+                         int32_t* __restrict__ owner, Batch B, uint64_t* __restrict__ newinv, Counters* cnt,
+                         int32_t* __restrict__ restored) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= nm || !revert[i] || !B.applied[i]) return;
   const int a = B.ca[i], b = B.cb[i];
+  // restored faces = the pre-batch ring(a) ∪ ring(b) (listed for the next undo round)
   for (uint32_t j = 0; j < deg[a]; ++j) {
     const int f = inc[off[a] + j];
     if (owner[f] == i) owner[f] = -1;
+    if (!has(Fprev + 3 * f, b)) restored[atomicAdd(&cnt->restored, 1ull)] = f;
   }
   for (uint32_t j = 0; j < deg[b]; ++j) {
     const int f = inc[off[b] + j];
     if (owner[f] == i) owner[f] = -1;
     falive[f] = 1;
     for (int k = 0; k < 3; ++k) F[3 * f + k] = Fprev[3 * f + k];
+    restored[atomicAdd(&cnt->restored, 1ull)] = f;
   }
   for (int k = 0; k < 3; ++k) X[3 * a + k] = B.oldx[3 * i + k];
   for (int k = 0; k < 10; ++k) Q[10 * a + k] = B.oldq[10 * i + k];
@@ -617,6 +621,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
   DevBuf<double> Q(10 * nv, st);
   DevBuf<uint32_t> deg(nv, st), off(nv, st), cur(nv, st), ecount(nv, st), eoff(nv, st);
   const int64_t ecap = 3 * nf + 16;
+  DevBuf<int32_t> rlist(3 * nf + 16, st);
   DevBuf<int32_t> inc(3 * nf, st), ea(ecap, st), eb(ecap, st), owner(nf, st), qf(3 * nf + 16, st),
       qf2(3 * nf + 16, st), Fprev(3 * nf, st);
   DevBuf<uint8_t> enf(ecap, st), valid(ecap, st), revert(ecap, st);
@@ -717,20 +722,28 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
       int64_t nq = static_cast<int64_t>(h.query);
       int32_t* qa = qf.get();
       int32_t* qb = qf2.get();
+      bool first_round = true;
+      int64_t nrest = 0;
       while (nq > 0) {
         revert.memset(0, st);
         const int64_t found =
-            undo_detect(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get());
+            first_round ? undo_detect(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get())
+                        : undo_detect_restored(ctx, *isc, X, F, nf, falive.get(), rlist.get(), nrest, qa, nq,
+                                               owner.get(), B.applied, revert.get());
+        first_round = false;
         ctx.prof.mark(st, "undo_detect");
         if (found == 0) break;
         ++rounds;
+        PCU_CUDA(cudaMemsetAsync(&cnt.get()->restored, 0, 8, st));
         PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
-                   Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get());
+                   Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get(),
+                   rlist.get());
         // rebuild the query list from still-applied collapses
         PCU_CUDA(cudaMemsetAsync(&cnt.get()->query, 0, 8, st));
         PCU_LAUNCH(ctx, k_requery, grid_for(nq, 256), 256, 0, qa, nq, owner.get(), B.applied, qb, cnt.get());
         h = read_scalar(ctx, cnt.get());
         nq = static_cast<int64_t>(h.query);
+        nrest = static_cast<int64_t>(h.restored);
         std::swap(qa, qb);
         ctx.prof.mark(st, "undo_revert");
       }
