@@ -1,0 +1,81 @@
+// Drop-in smoke test: the reference's own C++ types and algorithms (IndexedMesh,
+// normalize_unit_cube, analyze_topology — compiled from /root/reference/proj/src) driving the
+// GPU path through include/pamopt/*.hpp, exactly as a reference caller would.
+// Built by tests/cpp/Makefile into tests/cpp/_bin/ (git-ignored, travels to the GPU box).
+#include <cmath>
+#include <cstdio>
+#include <map>
+
+#include "pamopt/dual_mc.hpp"
+#include "pamopt/mesh.hpp"
+#include "pamopt/mesh_io.hpp"
+#include "pamopt/pipeline.hpp"
+#include "pamopt/simplify.hpp"
+#include "pamopt/tri_isect.hpp"
+#include "pamopt/voxel_field.hpp"
+
+using namespace pamopt;
+
+static IndexedMesh icosphere(int sub) {
+  const double t = (1.0 + std::sqrt(5.0)) / 2.0;
+  IndexedMesh m;
+  const double v[12][3] = {{-1, t, 0}, {1, t, 0}, {-1, -t, 0}, {1, -t, 0}, {0, -1, t}, {0, 1, t},
+                           {0, -1, -t}, {0, 1, -t}, {t, 0, -1}, {t, 0, 1}, {-t, 0, -1}, {-t, 0, 1}};
+  for (auto& p : v) {
+    Vec3d q(p[0], p[1], p[2]);
+    m.vertices.push_back(q / q.norm());
+  }
+  const int f[20][3] = {{0, 11, 5}, {0, 5, 1}, {0, 1, 7}, {0, 7, 10}, {0, 10, 11}, {1, 5, 9}, {5, 11, 4},
+                        {11, 10, 2}, {10, 7, 6}, {7, 1, 8}, {3, 9, 4}, {3, 4, 2}, {3, 2, 6}, {3, 6, 8},
+                        {3, 8, 9}, {4, 9, 5}, {2, 4, 11}, {6, 2, 10}, {8, 6, 7}, {9, 8, 1}};
+  for (auto& q : f) m.faces.push_back(Vec3i(q[0], q[1], q[2]));
+  for (int s = 0; s < sub; ++s) {
+    std::map<std::pair<int, int>, int> mid;
+    auto midpoint = [&](int a, int b) {
+      auto key = std::make_pair(std::min(a, b), std::max(a, b));
+      auto it = mid.find(key);
+      if (it != mid.end()) return it->second;
+      Vec3d p = m.vertices[a] + m.vertices[b];
+      m.vertices.push_back(p / p.norm());
+      return mid[key] = m.vertex_count() - 1;
+    };
+    std::vector<Vec3i> nf;
+    for (const Vec3i& t3 : m.faces) {
+      const int a = midpoint(t3[0], t3[1]), b = midpoint(t3[1], t3[2]), c = midpoint(t3[2], t3[0]);
+      nf.push_back(Vec3i(t3[0], a, c));
+      nf.push_back(Vec3i(t3[1], b, a));
+      nf.push_back(Vec3i(t3[2], c, b));
+      nf.push_back(Vec3i(a, b, c));
+    }
+    m.faces = nf;
+  }
+  return m;
+}
+
+int main() {
+  const int R = 64;
+  IndexedMesh in = icosphere(4);
+  normalize_unit_cube(in, 6.0 / R);                  // reference mesh_io.cpp:393-408
+  ScalarGrid g = compute_udf(in, R);                 // GPU
+  udf_to_sdf(g, 0.9 / R);                            // GPU
+  IndexedMesh d = extract(g);                        // GPU
+  const TopologySummary td = analyze_topology(d);    // reference mesh.cpp:113-150
+  const auto pd = detect_self_intersections(d);      // GPU
+  SimplifyStats st;
+  IndexedMesh s = simplify_to(d, 1000, SimplifyParams{}, &st);  // GPU
+  const TopologySummary ts = analyze_topology(s);
+  const auto ps = detect_self_intersections(s);
+  StageTimings tm;
+  IndexedMesh e = remesh(in, R, 1000, SimplifyParams{}, 0.0, 5.0, nullptr, &tm);
+  const bool same = e.faces == s.faces && e.vertices == s.vertices;
+  std::printf("{\"dmc_faces\": %d, \"dmc_manifold\": %d, \"dmc_watertight\": %d, \"dmc_euler\": %d, "
+              "\"dmc_isect\": %zu, \"out_faces\": %d, \"out_manifold\": %d, \"out_euler\": %d, \"out_isect\": %zu, "
+              "\"iterations\": %lld, \"pipeline_equal\": %d, \"total_ms\": %.3f}\n",
+              d.face_count(), td.manifold, td.watertight, td.euler_characteristic, pd.size(), s.face_count(),
+              ts.manifold, ts.euler_characteristic, ps.size(), static_cast<long long>(st.iterations), same,
+              tm.total_ms);
+  const bool ok = td.manifold && td.watertight && pd.empty() && ts.manifold && ps.empty() && s.face_count() <= 1000 &&
+                  same;
+  std::fflush(stdout);
+  std::_Exit(ok ? 0 : 1);  // parallel.cpp pool: never run static destructors
+}

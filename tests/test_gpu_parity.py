@@ -4,6 +4,9 @@ Bar: integer/index outputs bit-exact; because every FP decision 
 (FP64, no FMA, identical op order) the FP outputs are bit-exact as well, which the tests
 assert (a stricter bar than the FP32 tolerance the north star allows).
 """
+import os
+import subprocess
+
 import numpy as np
 import pytest
 
@@ -130,3 +133,14 @@ def test_pipeline_c1(api, oracle, c1):
     assert np.array_equal(res.faces, fo)
     assert np.array_equal(bits(res.vertices), bits(vo))
     assert res.times["total_ms"] > 0
+
+
+def test_cpp_dropin_smoke():
+    """The reference's own C++ types/algorithms (IndexedMesh, normalize_unit_cube,
+    analyze_topology) drive the GPU path through include/pamopt/*.hpp."""
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "_bin", "dropin_smoke")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in smoke binary not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert '"pipeline_equal": 1' in r.stdout
