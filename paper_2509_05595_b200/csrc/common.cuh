@@ -5,6 +5,7 @@
 // lists, MC cases, DMC topology, collapse sets) are bit-identical to the checker.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -168,6 +169,35 @@ T read_scalar(Ctx& ctx, const T* dptr) {
   PCU_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
   PCU_CUDA(cudaStreamSynchronize(ctx.stream));
   return h;
+}
+
+// ------------------------------------------------------------ aggregated counter bumps
+// One atomic per group of converged lanes instead of one per lane: single-address counters
+// (list appends) otherwise serialise in the L2 atomic unit.
+__device__ __forceinline__ unsigned long long agg_inc(unsigned long long* ctr) {
+  namespace cg = cooperative_groups;
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(ctr, static_cast<unsigned long long>(g.size()));
+  return g.shfl(base, 0) + g.thread_rank();
+}
+__device__ __forceinline__ void agg_add(unsigned long long* ctr, unsigned long long v) {
+  namespace cg = cooperative_groups;
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long s = v;
+  for (unsigned o = 1; o < g.size(); o <<= 1) {
+    const unsigned long long t = g.shfl_down(s, o);
+    if (g.thread_rank() + o < g.size()) s += t;
+  }
+  if (g.thread_rank() == 0) atomicAdd(ctr, s);
+}
+// same, for lanes that may target different counters (grouped by label)
+__device__ __forceinline__ unsigned long long agg_inc_labeled(unsigned long long* ctr, unsigned label) {
+  namespace cg = cooperative_groups;
+  cg::coalesced_group g = cg::labeled_partition(cg::coalesced_threads(), label);
+  unsigned long long base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(ctr, static_cast<unsigned long long>(g.size()));
+  return g.shfl(base, 0) + g.thread_rank();
 }
 
 // --------------------------------------------------------------------- device geometry

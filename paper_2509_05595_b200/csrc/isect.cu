@@ -25,21 +25,6 @@
 
 namespace pcu {
 
-struct IsectScratch {
-  DevBuf<double> boxes;      // 6 per build entry
-  DevBuf<uint32_t> bcount, boff, bcur;
-  DevBuf<int32_t> entries;   // face ids by bucket
-  DevBuf<int32_t> big;
-  DevBuf<unsigned long long> counters;  // [0] entries, [1] big, [2] pairs
-  DevBuf<double> ext_sum;
-  DevBuf<uint8_t> in_build;
-  DevBuf<uint64_t> cand;
-  DevBuf<float> fbox;  // 6 floats per face
-};
-
-IsectScratch* isect_scratch_create() { return new IsectScratch(); }
-void isect_scratch_destroy(IsectScratch* s) { delete s; }
-
 namespace {
 
 constexpr int kMaxCells = 64;
@@ -111,9 +96,12 @@ __device__ __forceinline__ uint32_t cell_hash(int64_t x, int64_t y, int64_t z, u
 }
 
 // ------------------------------------------------------------------ narrow phase (device)
+// Out-of-line orientation: the narrow phase calls it ~20 times; inlining every copy blew the
+// instruction cache (ncu: `no_instruction` stalls) and the register budget.
+__device__ __noinline__ int o3(D3 a, D3 b, D3 c, D3 d) { return orient3d(a, b, c, d); }
 __device__ __forceinline__ bool check_min_max(D3 p1, D3 q1, D3 r1, D3 p2, D3 q2, D3 r2) {
-  if (orient3d(q2, p2, p1, q1) > 0) return false;
-  if (orient3d(r2, p2, r1, p1) > 0) return false;
+  if (o3(q2, p2, p1, q1) > 0) return false;
+  if (o3(r2, p2, r1, p1) > 0) return false;
   return true;
 }
 
@@ -141,43 +129,15 @@ __device__ bool gd_3d(D3 p1, D3 q1, D3 r1, D3 p2, D3 q2, D3 r2, int dp2, int dq2
   return true;
 }
 
-__device__ bool gd_disjoint(D3 p1, D3 q1, D3 r1, D3 p2, D3 q2, D3 r2) {
-  const int dp1 = orient3d(p1, p2, q2, r2), dq1 = orient3d(q1, p2, q2, r2), dr1 = orient3d(r1, p2, q2, r2);
-  if (dp1 * dq1 > 0 && dp1 * dr1 > 0) return false;
-  const int dp2 = orient3d(p2, p1, q1, r1), dq2 = orient3d(q2, p1, q1, r1), dr2 = orient3d(r2, p1, q1, r1);
-  if (dp2 * dq2 > 0 && dp2 * dr2 > 0) return false;
-  if (dp1 > 0) {
-    if (dq1 > 0) return gd_3d(r1, p1, q1, p2, r2, q2, dp2, dr2, dq2);
-    if (dr1 > 0) return gd_3d(q1, r1, p1, p2, r2, q2, dp2, dr2, dq2);
-    return gd_3d(p1, q1, r1, p2, q2, r2, dp2, dq2, dr2);
-  }
-  if (dp1 < 0) {
-    if (dq1 < 0) return gd_3d(r1, p1, q1, p2, q2, r2, dp2, dq2, dr2);
-    if (dr1 < 0) return gd_3d(q1, r1, p1, p2, q2, r2, dp2, dq2, dr2);
-    return gd_3d(p1, q1, r1, p2, r2, q2, dp2, dr2, dq2);
-  }
-  if (dq1 < 0) {
-    if (dr1 >= 0) return gd_3d(q1, r1, p1, p2, r2, q2, dp2, dr2, dq2);
-    return gd_3d(p1, q1, r1, p2, q2, r2, dp2, dq2, dr2);
-  }
-  if (dq1 > 0) {
-    if (dr1 > 0) return gd_3d(p1, q1, r1, p2, r2, q2, dp2, dr2, dq2);
-    return gd_3d(q1, r1, p1, p2, q2, r2, dp2, dq2, dr2);
-  }
-  if (dr1 > 0) return gd_3d(r1, p1, q1, p2, q2, r2, dp2, dq2, dr2);
-  if (dr1 < 0) return gd_3d(r1, p1, q1, p2, r2, q2, dp2, dr2, dq2);
-  return true;
-}
-
 // T1=(A,B,C), T2=(A,D,E) non-coplanar: intersection longer than the shared point?
 __device__ bool shared_vertex_3d(D3 A, D3 B, D3 C, D3 D, D3 E) {
-  if (orient3d(B, A, D, E) * orient3d(C, A, D, E) > 0) return false;
-  const int oD = orient3d(D, A, B, C), oE = orient3d(E, A, B, C);
+  if (o3(B, A, D, E) * o3(C, A, D, E) > 0) return false;
+  const int oD = o3(D, A, B, C), oE = o3(E, A, B, C);
   if (oD * oE > 0) return false;
   const D3 Z = oD != 0 ? D : E;   // a vertex of T2 off the plane of T1
   const D3 P = oD != 0 ? E : D;   // the side of the crossing point of DE with that plane
-  const int sP = orient3d(A, B, P, Z), sC = orient3d(A, B, C, Z);
-  const int tP = orient3d(A, C, P, Z), tB = orient3d(A, C, B, Z);
+  const int sP = o3(A, B, P, Z), sC = o3(A, B, C, Z);
+  const int tP = o3(A, C, P, Z), tB = o3(A, C, B, Z);
   return sP * sC >= 0 && tP * tB >= 0;
 }
 
@@ -229,87 +189,158 @@ __device__ bool degenerate(D3 a, D3 b, D3 c) {
          orient2d(a.x, a.y, b.x, b.y, c.x, c.y) == 0;
 }
 
-__device__ bool verdict(const double* __restrict__ V, const int32_t* t1, const int32_t* t2) {
-  int s1[3] = {-1, -1, -1}, s2[3] = {-1, -1, -1}, shared = 0;
+struct PairInfo {
+  int s1[3], s2[3];  // s1[k]: index in t2 of t1's vertex k (or -1); s2 likewise
+  int shared;
+};
+
+__device__ __forceinline__ PairInfo pair_info(const int32_t* t1, const int32_t* t2) {
+  PairInfo I{{-1, -1, -1}, {-1, -1, -1}, 0};
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j)
       if (t1[i] == t2[j]) {
-        s1[i] = j;
-        s2[j] = i;
-        ++shared;
+        I.s1[i] = j;
+        I.s2[j] = i;
+        ++I.shared;
       }
-  if (shared == 3) return true;
-  const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
-  const D3 T2[3] = {vtx(V, t2[0]), vtx(V, t2[1]), vtx(V, t2[2])};
-  if (degenerate(T1[0], T1[1], T1[2]) || degenerate(T2[0], T2[1], T2[2])) return true;
-  // coplanar <=> every vertex of T2 lies on T1's plane (shared vertices trivially do)
-  bool coplanar = true;
-  for (int j = 0; j < 3 && coplanar; ++j)
-    if (s2[j] < 0 && orient3d(T2[j], T1[0], T1[1], T1[2]) != 0) coplanar = false;
-  if (!coplanar) {
-    if (shared == 2) return false;
-    if (shared == 0) return gd_disjoint(T1[0], T1[1], T1[2], T2[0], T2[1], T2[2]);
-    int i1 = 0;
-    while (s1[i1] < 0) ++i1;
-    const int j1 = s1[i1];
-    return shared_vertex_3d(T1[i1], T1[(i1 + 1) % 3], T1[(i1 + 2) % 3], T2[(j1 + 1) % 3], T2[(j1 + 2) % 3]);
-  }
-  // projection: decreasing |n_i| of the double normal (ties -> lower axis), first with a
-  // nonzero exact 2D orientation of T1
+  return I;
+}
+
+// projection for coplanar pairs: decreasing |n_i| of T1's double normal (ties -> lower axis),
+// the first axis whose exact 2D orientation of T1 is nonzero
+__device__ int drop_axis(const D3* T1) {
   const D3 n = cross(sub(T1[1], T1[0]), sub(T1[2], T1[0]));
   const double an[3] = {fabs(n.x), fabs(n.y), fabs(n.z)};
   int ord[3] = {0, 1, 2};
-  for (int i = 1; i < 3; ++i)  // stable insertion sort, descending
+  for (int i = 1; i < 3; ++i)
     for (int j = i; j > 0 && an[ord[j]] > an[ord[j - 1]]; --j) {
       const int t = ord[j];
       ord[j] = ord[j - 1];
       ord[j - 1] = t;
     }
-  int drop = ord[0];
   for (int k = 0; k < 3; ++k)
-    if (o2(proj2(T1[0], ord[k]), proj2(T1[1], ord[k]), proj2(T1[2], ord[k])) != 0) {
-      drop = ord[k];
-      break;
+    if (o2(proj2(T1[0], ord[k]), proj2(T1[1], ord[k]), proj2(T1[2], ord[k])) != 0) return ord[k];
+  return ord[0];
+}
+
+// non-degenerate, 0 shared vertices
+__device__ __noinline__ bool verdict0(const double* __restrict__ V, const int32_t* t1, const int32_t* t2) {
+  const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
+  const D3 T2[3] = {vtx(V, t2[0]), vtx(V, t2[1]), vtx(V, t2[2])};
+  const int dp2 = o3(T2[0], T1[0], T1[1], T1[2]), dq2 = o3(T2[1], T1[0], T1[1], T1[2]),
+            dr2 = o3(T2[2], T1[0], T1[1], T1[2]);
+  if (dp2 != 0 || dq2 != 0 || dr2 != 0) {
+    if (dp2 * dq2 > 0 && dp2 * dr2 > 0) return false;
+    // Guigue-Devillers (closed), reusing the orientations of T2 w.r.t. T1
+    const D3 p1 = T1[0], q1 = T1[1], r1 = T1[2], p2 = T2[0], q2 = T2[1], r2 = T2[2];
+    const int dp1 = o3(p1, p2, q2, r2), dq1 = o3(q1, p2, q2, r2), dr1 = o3(r1, p2, q2, r2);
+    if (dp1 * dq1 > 0 && dp1 * dr1 > 0) return false;
+    if (dp1 > 0) {
+      if (dq1 > 0) return gd_3d(r1, p1, q1, p2, r2, q2, dp2, dr2, dq2);
+      if (dr1 > 0) return gd_3d(q1, r1, p1, p2, r2, q2, dp2, dr2, dq2);
+      return gd_3d(p1, q1, r1, p2, q2, r2, dp2, dq2, dr2);
     }
+    if (dp1 < 0) {
+      if (dq1 < 0) return gd_3d(r1, p1, q1, p2, q2, r2, dp2, dq2, dr2);
+      if (dr1 < 0) return gd_3d(q1, r1, p1, p2, q2, r2, dp2, dq2, dr2);
+      return gd_3d(p1, q1, r1, p2, r2, q2, dp2, dr2, dq2);
+    }
+    if (dq1 < 0) {
+      if (dr1 >= 0) return gd_3d(q1, r1, p1, p2, r2, q2, dp2, dr2, dq2);
+      return gd_3d(p1, q1, r1, p2, q2, r2, dp2, dq2, dr2);
+    }
+    if (dq1 > 0) {
+      if (dr1 > 0) return gd_3d(p1, q1, r1, p2, r2, q2, dp2, dr2, dq2);
+      return gd_3d(q1, r1, p1, p2, q2, r2, dp2, dq2, dr2);
+    }
+    if (dr1 > 0) return gd_3d(r1, p1, q1, p2, q2, r2, dp2, dq2, dr2);
+    if (dr1 < 0) return gd_3d(r1, p1, q1, p2, r2, q2, dp2, dr2, dq2);
+    return true;
+  }
+  const int drop = drop_axis(T1);
   P2 p1[3], p2[3];
   for (int k = 0; k < 3; ++k) {
     p1[k] = proj2(T1[k], drop);
     p2[k] = proj2(T2[k], drop);
   }
-  if (shared == 0) {
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j)
-        if (seg_seg2(p1[i], p1[(i + 1) % 3], p2[j], p2[(j + 1) % 3])) return true;
-    return inside2(p1[0], p2[0], p2[1], p2[2]) || inside2(p2[0], p1[0], p1[1], p1[2]);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (seg_seg2(p1[i], p1[(i + 1) % 3], p2[j], p2[(j + 1) % 3])) return true;
+  return inside2(p1[0], p2[0], p2[1], p2[2]) || inside2(p2[0], p1[0], p1[1], p1[2]);
+}
+
+// non-degenerate, exactly 1 shared vertex
+__device__ __noinline__ bool verdict1(const double* __restrict__ V, const int32_t* t1, const int32_t* t2,
+                                      const PairInfo& I) {
+  const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
+  const D3 T2[3] = {vtx(V, t2[0]), vtx(V, t2[1]), vtx(V, t2[2])};
+  int i1 = 0;
+  while (I.s1[i1] < 0) ++i1;
+  const int j1 = I.s1[i1];
+  bool coplanar = true;
+  for (int j = 0; j < 3 && coplanar; ++j)
+    if (I.s2[j] < 0 && o3(T2[j], T1[0], T1[1], T1[2]) != 0) coplanar = false;
+  if (!coplanar)
+    return shared_vertex_3d(T1[i1], T1[(i1 + 1) % 3], T1[(i1 + 2) % 3], T2[(j1 + 1) % 3], T2[(j1 + 2) % 3]);
+  const int drop = drop_axis(T1);
+  const P2 A = proj2(T1[i1], drop);
+  P2 B = proj2(T1[(i1 + 1) % 3], drop), C = proj2(T1[(i1 + 2) % 3], drop);
+  P2 D = proj2(T2[(j1 + 1) % 3], drop), E = proj2(T2[(j1 + 2) % 3], drop);
+  if (o2(A, B, C) < 0) {
+    const P2 t = B;
+    B = C;
+    C = t;
   }
-  if (shared == 1) {
-    int i1 = 0;
-    while (s1[i1] < 0) ++i1;
-    const int j1 = s1[i1];
-    const P2 A = p1[i1];
-    P2 B = p1[(i1 + 1) % 3], C = p1[(i1 + 2) % 3], D = p2[(j1 + 1) % 3], E = p2[(j1 + 2) % 3];
-    if (o2(A, B, C) < 0) {
-      const P2 t = B;
-      B = C;
-      C = t;
-    }
-    if (o2(A, D, E) < 0) {
-      const P2 t = D;
-      D = E;
-      E = t;
-    }
-    return ray_in(A, B, C, D) || ray_in(A, B, C, E) || ray_in(A, D, E, B) || ray_in(A, D, E, C);
+  if (o2(A, D, E) < 0) {
+    const P2 t = D;
+    D = E;
+    E = t;
   }
+  return ray_in(A, B, C, D) || ray_in(A, B, C, E) || ray_in(A, D, E, B) || ray_in(A, D, E, C);
+}
+
+// non-degenerate, exactly 2 shared vertices
+__device__ __noinline__ bool verdict2(const double* __restrict__ V, const int32_t* t1, const int32_t* t2,
+                                      const PairInfo& I) {
   int ia = 0, ja = 0;
-  while (s1[ia] >= 0) ++ia;
-  while (s2[ja] >= 0) ++ja;
-  const P2 A = p1[(ia + 1) % 3], B = p1[(ia + 2) % 3];
-  return o2(A, B, p1[ia]) * o2(A, B, p2[ja]) > 0;
+  while (I.s1[ia] >= 0) ++ia;
+  while (I.s2[ja] >= 0) ++ja;
+  const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
+  const D3 apex2 = vtx(V, t2[ja]);
+  if (o3(apex2, T1[0], T1[1], T1[2]) != 0) return false;  // non-coplanar edge neighbours never cross
+  const int drop = drop_axis(T1);
+  const P2 A = proj2(T1[(ia + 1) % 3], drop), B = proj2(T1[(ia + 2) % 3], drop);
+  return o2(A, B, proj2(T1[ia], drop)) * o2(A, B, proj2(apex2, drop)) > 0;
+}
+
+// full verdict (explicit pair API)
+__device__ bool verdict(const double* __restrict__ V, const int32_t* t1, const int32_t* t2) {
+  const PairInfo I = pair_info(t1, t2);
+  if (I.shared == 3) return true;
+  if (degenerate(vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])) || degenerate(vtx(V, t2[0]), vtx(V, t2[1]), vtx(V, t2[2])))
+    return true;
+  if (I.shared == 0) return verdict0(V, t1, t2);
+  if (I.shared == 1) return verdict1(V, t1, t2, I);
+  return verdict2(V, t1, t2, I);
 }
 
 // ------------------------------------------------------------------------ grid kernels
+// Device-side scalars of one detection round: the launches below read sizes and the cell size
+// from here, so a round issues no host synchronisation of its own.
+struct DetectScalars {
+  double ext_sum;
+  double inv_h;
+  unsigned long long nbig;
+  unsigned long long ncand;
+  unsigned long long found;
+  unsigned long long npairs;
+  unsigned long long ncls[3];
+  int redo;  // candidate buffer overflowed: the round's outputs are void, the caller repeats it
+  int pad;
+};
+
 __global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t nf,
-                         const uint8_t* __restrict__ alive, FBox* __restrict__ out) {
+                         const uint8_t* __restrict__ alive, FBox* __restrict__ out, uint8_t* __restrict__ degen) {
   const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (f >= nf) return;
   FBox fb;
@@ -324,12 +355,14 @@ __global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict
       fb.lo[k] = __double2float_rd(b.lo[k]);
       fb.hi[k] = __double2float_ru(b.hi[k]);
     }
+    const int32_t* t = F + 3 * f;
+    degen[f] = degenerate(vtx(V, t[0]), vtx(V, t[1]), vtx(V, t[2])) ? 1 : 0;
   }
   out[f] = fb;
 }
 
 __global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict__ ids, int64_t n,
-                          const uint8_t* __restrict__ alive, double* __restrict__ out) {
+                          const uint8_t* __restrict__ alive, DetectScalars* ds) {
   typedef cub::BlockReduce<double, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   double s = 0.0;
@@ -341,117 +374,204 @@ __global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict_
     s += fmax(fmax(b.hi[0] - b.lo[0], b.hi[1] - b.lo[1]), b.hi[2] - b.lo[2]);
   }
   const double t = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) atomicAdd(out, t);
+  if (threadIdx.x == 0) atomicAdd(&ds->ext_sum, t);
+}
+
+// cell size = mean box extent of the build set
+__global__ void k_set_invh(DetectScalars* ds, int64_t n) {
+  const double mean = n > 0 ? ds->ext_sum / static_cast<double>(n) : 1.0;
+  ds->inv_h = 1.0 / (mean > 0.0 ? mean : 1e-3);
 }
 
 // pass 0: count bucket entries (or big); pass 1: fill
 __global__ void k_bin(const FBox* __restrict__ B, const int32_t* __restrict__ ids, int64_t n,
-                      const uint8_t* __restrict__ alive, double inv_h, uint32_t mask, int pass,
+                      const uint8_t* __restrict__ alive, DetectScalars* __restrict__ ds, uint32_t mask, int pass,
                       uint32_t* __restrict__ bcount, const uint32_t* __restrict__ boff, uint32_t* __restrict__ bcur,
-                      int32_t* __restrict__ entries, int32_t* __restrict__ big, unsigned long long* counters) {
+                      int4* __restrict__ entries, int32_t* __restrict__ big, uint32_t* __restrict__ occ) {
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (k >= n) return;
   const int32_t f = ids ? ids[k] : static_cast<int32_t>(k);
   if (alive && !alive[f]) return;
-  const CellRange cr = cells_of(B[f], inv_h);
+  const CellRange cr = cells_of(B[f], ds->inv_h);
   if (cr.count() > kMaxCells) {
-    if (pass == 1) big[atomicAdd(&counters[1], 1ull)] = f;
+    if (pass == 1) big[agg_inc(&ds->nbig)] = f;
     return;
   }
   for (int64_t z = cr.lo[2]; z <= cr.hi[2]; ++z)
     for (int64_t y = cr.lo[1]; y <= cr.hi[1]; ++y)
       for (int64_t x = cr.lo[0]; x <= cr.hi[0]; ++x) {
         const uint32_t h = cell_hash(x, y, z, mask);
-        if (pass == 0) atomicAdd(&bcount[h], 1u);
-        else entries[boff[h] + atomicAdd(&bcur[h], 1u)] = f;
+        if (pass == 0) {
+          atomicAdd(&bcount[h], 1u);
+          atomicOr(&occ[h >> 5], 1u << (h & 31));
+        } else {
+          entries[boff[h] + atomicAdd(&bcur[h], 1u)] =
+              make_int4(f, static_cast<int>(cr.lo[0]), static_cast<int>(cr.lo[1]), static_cast<int>(cr.lo[2]));
+        }
       }
 }
 
 // Broad phase: every probe face p walks the cells its box covers and emits candidate pairs
-// (p, a) with a in the build grid and overlapping (conservative float) boxes.  `sym` = probe
-// set == build set (each unordered pair once); otherwise a pair of two build faces is emitted
-// only from its smaller probe.
+// (p, a) with a in the build grid and overlapping (conservative float) boxes, in the first
+// common cell of the two cell ranges only.  `sym` = probe set == build set (each unordered pair
+// once); otherwise a pair of two build faces is emitted only from its smaller probe.
 __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64_t n, const uint8_t* __restrict__ alive,
-                                               double inv_h, uint32_t mask, const uint32_t* __restrict__ bcount,
-                                               const uint32_t* __restrict__ boff, const int32_t* __restrict__ entries,
-                                               const int32_t* __restrict__ big, int64_t nbig, int sym,
+                                               const DetectScalars* __restrict__ ds, uint32_t mask,
+                                               const uint32_t* __restrict__ bcount, const uint32_t* __restrict__ boff,
+                                               const int4* __restrict__ entries, const int32_t* __restrict__ big,
+                                               const uint32_t* __restrict__ occ, int sym,
                                                const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
                                                uint64_t cap, unsigned long long* __restrict__ ncand,
                                                const int32_t* __restrict__ probe_ids) {
+  // candidates are staged in shared memory and flushed with one global atomic per block
+  // (a single-address counter bumped per candidate serialises in the L2 atomic unit)
+  constexpr int kBuf = 2048;
+  __shared__ uint64_t buf[kBuf];
+  __shared__ unsigned int nbuf;
+  __shared__ unsigned long long gbase;
+  if (threadIdx.x == 0) nbuf = 0;
+  __syncthreads();
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= n) return;
-  const int32_t p = probe_ids ? probe_ids[k] : static_cast<int32_t>(k);
-  if (alive && !alive[p]) return;
-  const bool p_build = sym || (in_build && in_build[p]);
-  const FBox bp = B[p];
-  const CellRange cp = cells_of(bp, inv_h);
-  auto consider = [&](int32_t a, const FBox& ba) {
-    if (a == p) return;
-    if (p_build && a < p) return;  // the pair is emitted from probe a instead
-    if (!overlap(bp, ba)) return;
-    const unsigned long long slot = atomicAdd(ncand, 1ull);
-    if (slot < cap) cand[slot] = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
-  };
-  if (cp.count() > kMaxCells) {
-    // huge probe: scan the whole build set, each entry once (in the bucket of its first cell)
-    for (uint32_t h = 0; h <= mask; ++h)
-      for (uint32_t e = boff[h]; e < boff[h] + bcount[h]; ++e) {
-        const int32_t a = entries[e];
-        const FBox ba = B[a];
-        const CellRange ca = cells_of(ba, inv_h);
-        if (cell_hash(ca.lo[0], ca.lo[1], ca.lo[2], mask) != h) continue;
-        consider(a, ba);
-      }
-  } else {
-    for (int64_t z = cp.lo[2]; z <= cp.hi[2]; ++z)
-      for (int64_t y = cp.lo[1]; y <= cp.hi[1]; ++y)
-        for (int64_t x = cp.lo[0]; x <= cp.hi[0]; ++x) {
-          const uint32_t h = cell_hash(x, y, z, mask);
-          const uint32_t e1 = boff[h] + bcount[h];
-          for (uint32_t e = boff[h]; e < e1; ++e) {
-            const int32_t a = entries[e];
-            const FBox ba = B[a];
-            const CellRange ca = cells_of(ba, inv_h);
-            // the entry really covers (x,y,z) and this is the first common cell of the two ranges
-            if (x < ca.lo[0] || x > ca.hi[0] || y < ca.lo[1] || y > ca.hi[1] || z < ca.lo[2] || z > ca.hi[2]) continue;
-            if (x != max(cp.lo[0], ca.lo[0]) || y != max(cp.lo[1], ca.lo[1]) || z != max(cp.lo[2], ca.lo[2])) continue;
-            consider(a, ba);
-          }
-        }
+  int32_t p = -1;
+  if (k < n) {
+    p = probe_ids ? probe_ids[k] : static_cast<int32_t>(k);
+    if (alive && !alive[p]) p = -1;
   }
-  for (int64_t b = 0; b < nbig; ++b) consider(big[b], B[big[b]]);
+  if (p >= 0) {
+    const double inv_h = ds->inv_h;
+    const int64_t nbig = static_cast<int64_t>(ds->nbig);
+    const bool p_build = sym || (in_build && in_build[p]);
+    const FBox bp = B[p];
+    const CellRange cp = cells_of(bp, inv_h);
+    auto consider = [&](int32_t a, const FBox& ba) {
+      if (a == p) return;
+      if (p_build && a < p) return;  // the pair is emitted from probe a instead
+      if (!overlap(bp, ba)) return;
+      const uint64_t v = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
+      const unsigned slot = atomicAdd(&nbuf, 1u);
+      if (slot < kBuf) {
+        buf[slot] = v;
+      } else {  // block buffer full: direct global append
+        const unsigned long long g = agg_inc(ncand);
+        if (g < cap) cand[g] = v;
+      }
+    };
+    if (cp.count() > kMaxCells) {
+      // huge probe: scan the whole build set, each entry once (in the bucket of its first cell)
+      for (uint32_t h = 0; h <= mask; ++h)
+        for (uint32_t e = boff[h]; e < boff[h] + bcount[h]; ++e) {
+          const int4 en = entries[e];
+          if (cell_hash(en.y, en.z, en.w, mask) != h) continue;
+          consider(en.x, B[en.x]);
+        }
+    } else {
+      for (int64_t z = cp.lo[2]; z <= cp.hi[2]; ++z)
+        for (int64_t y = cp.lo[1]; y <= cp.hi[1]; ++y)
+          for (int64_t x = cp.lo[0]; x <= cp.hi[0]; ++x) {
+            const uint32_t h = cell_hash(x, y, z, mask);
+            if (!((occ[h >> 5] >> (h & 31)) & 1u)) continue;  // empty bucket (L2-resident bitmap)
+            const uint32_t e0 = boff[h], e1 = e0 + bcount[h];
+            for (uint32_t e = e0; e < e1; ++e) {
+              const int4 en = entries[e];  // face id + its first cell: the dedup test needs no box load
+              // first common cell of the two ranges (a hash collision can at worst duplicate a pair)
+              if (x != max(cp.lo[0], static_cast<int64_t>(en.y)) || y != max(cp.lo[1], static_cast<int64_t>(en.z)) ||
+                  z != max(cp.lo[2], static_cast<int64_t>(en.w)))
+                continue;
+              consider(en.x, B[en.x]);
+            }
+          }
+    }
+    for (int64_t b = 0; b < nbig; ++b) consider(big[b], B[big[b]]);
+  }
+  __syncthreads();
+  const unsigned m = min(nbuf, static_cast<unsigned>(kBuf));
+  if (threadIdx.x == 0 && m) gbase = atomicAdd(ncand, static_cast<unsigned long long>(m));
+  __syncthreads();
+  for (unsigned i = threadIdx.x; i < m; i += blockDim.x)
+    if (gbase + i < cap) cand[gbase + i] = buf[i];
 }
 
-// Narrow phase over candidate pairs.  mode 0: append intersecting pairs (min, max);
-// mode 1: flag the applied owners of both faces for revert (QEM undo loop).
-__global__ void __launch_bounds__(128) k_narrow(const double* __restrict__ V, const int32_t* __restrict__ F,
-                                                const uint64_t* __restrict__ cand, int64_t n, int mode,
-                                                int32_t* __restrict__ pairs, uint64_t cap,
-                                                unsigned long long* __restrict__ npairs,
-                                                const int32_t* __restrict__ owner, const uint8_t* __restrict__ applied,
-                                                uint8_t* __restrict__ revert) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const int32_t p = static_cast<int32_t>(cand[i] >> 32), a = static_cast<int32_t>(cand[i] & 0xffffffffu);
-  // the reference candidate set: closed overlap of the 1e-7-inflated double boxes
-  if (!overlap(face_box(V, F + 3 * p), face_box(V, F + 3 * a))) return;
+__device__ __forceinline__ void report(DetectScalars* ds, int mode, int32_t p, int32_t a, int32_t* pairs,
+                                       uint64_t pair_cap, const int32_t* owner, const uint8_t* applied,
+                                       uint8_t* revert) {
   if (mode == 1) {
-    // only pairs whose owners can still be reverted matter
+    atomicAdd(&ds->found, 1ull);
     const int32_t op = owner[p], oa = owner[a];
-    const bool rp = op >= 0 && applied[op], ra = oa >= 0 && applied[oa];
-    if (!rp && !ra) return;
-    if (rp && ra && revert[op] && revert[oa]) return;  // both already flagged
-    if (!verdict(V, F + 3 * p, F + 3 * a)) return;
-    atomicAdd(npairs, 1ull);
-    if (rp) revert[op] = 1;
-    if (ra) revert[oa] = 1;
+    if (op >= 0 && applied[op]) revert[op] = 1;
+    if (oa >= 0 && applied[oa]) revert[oa] = 1;
   } else {
-    if (!verdict(V, F + 3 * p, F + 3 * a)) return;
-    const unsigned long long k = atomicAdd(npairs, 1ull);
-    if (k < cap) {
+    const unsigned long long k = atomicAdd(&ds->npairs, 1ull);
+    if (k < pair_cap) {
       pairs[2 * k] = min(p, a);
       pairs[2 * k + 1] = max(p, a);
     }
+  }
+}
+
+// Narrow phase, stage 1 (grid-stride over the device-side candidate count): the exact
+// inflated double-box test (the reference's candidate set), duplicates and degenerate faces
+// (always intersecting), then bucketing by shared-vertex count so stage 2 runs one uniform code
+// path per warp.  mode 1 (QEM undo) skips pairs none of whose owners can still be reverted.
+__global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, const int32_t* __restrict__ F,
+                                                  const uint8_t* __restrict__ degen, const uint64_t* __restrict__ cand,
+                                                  uint64_t cap, DetectScalars* __restrict__ ds, int mode,
+                                                  uint64_t* __restrict__ cls, int32_t* __restrict__ pairs,
+                                                  uint64_t pair_cap, const int32_t* __restrict__ owner,
+                                                  const uint8_t* __restrict__ applied, uint8_t* __restrict__ revert) {
+  const unsigned long long n = ds->ncand;
+  if (n > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ds->redo = 1;
+    return;
+  }
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int32_t p = static_cast<int32_t>(cand[i] >> 32), a = static_cast<int32_t>(cand[i] & 0xffffffffu);
+    if (mode == 1) {
+      const int32_t op = owner[p], oa = owner[a];
+      if (!(op >= 0 && applied[op]) && !(oa >= 0 && applied[oa])) continue;
+    }
+    const int32_t* tp = F + 3 * p;
+    const int32_t* ta = F + 3 * a;
+    if (!overlap(face_box(V, tp), face_box(V, ta))) continue;
+    int shared = 0;
+    for (int u = 0; u < 3; ++u)
+      for (int w = 0; w < 3; ++w) shared += tp[u] == ta[w];
+    if (shared == 3 || degen[p] || degen[a]) {
+      report(ds, mode, p, a, pairs, pair_cap, owner, applied, revert);
+      continue;
+    }
+    const unsigned long long slot = agg_inc_labeled(&ds->ncls[shared], static_cast<unsigned>(shared));
+    cls[shared * cap + slot] = cand[i];
+  }
+}
+
+template <int SHARED>
+__global__ void __launch_bounds__(128) k_narrow(const double* __restrict__ V, const int32_t* __restrict__ F,
+                                                const uint64_t* __restrict__ cls, uint64_t cap,
+                                                DetectScalars* __restrict__ ds, int mode, int32_t* __restrict__ pairs,
+                                                uint64_t pair_cap, const int32_t* __restrict__ owner,
+                                                const uint8_t* __restrict__ applied, uint8_t* __restrict__ revert) {
+  if (ds->redo) return;
+  const unsigned long long n = ds->ncls[SHARED];
+  const uint64_t* L = cls + SHARED * cap;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int32_t p = static_cast<int32_t>(L[i] >> 32), a = static_cast<int32_t>(L[i] & 0xffffffffu);
+    if (mode == 1) {
+      const int32_t op = owner[p], oa = owner[a];
+      const bool rp = op >= 0 && applied[op], ra = oa >= 0 && applied[oa];
+      if ((!rp || revert[op]) && (!ra || revert[oa])) continue;  // nothing left to flag
+    }
+    const int32_t* tp = F + 3 * p;
+    const int32_t* ta = F + 3 * a;
+    bool hit;
+    if (SHARED == 0) {
+      hit = verdict0(V, tp, ta);
+    } else {
+      const PairInfo I = pair_info(tp, ta);
+      hit = SHARED == 1 ? verdict1(V, tp, ta, I) : verdict2(V, tp, ta, I);
+    }
+    if (hit) report(ds, mode, p, a, pairs, pair_cap, owner, applied, revert);
   }
 }
 
@@ -462,72 +582,96 @@ __global__ void k_verdict_pairs(const double* __restrict__ V, const int32_t* __r
   out[i] = verdict(V, F + 3 * pairs[2 * i], F + 3 * pairs[2 * i + 1]) ? 1 : 0;
 }
 
+__global__ void k_flag_ids(const int32_t* __restrict__ ids, int64_t n, uint8_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) flag[ids[i]] = 1;
+}
+
 uint32_t pow2_at_least(uint64_t x) {
   uint32_t p = 1024;
   while (p < x && p < (1u << 30)) p <<= 1;
   return p;
 }
 
-// Builds the grid over (ids or all alive faces) from the float boxes; returns (inv_h, mask, nbig).
-void build_grid(Ctx& ctx, IsectScratch& S, const int32_t* d_ids, int64_t n, const uint8_t* d_alive, double& inv_h,
-                uint32_t& mask, int64_t& nbig, int64_t n_alive_hint) {
+}  // namespace
+
+struct IsectScratch {
+  DevBuf<uint32_t> bcount, boff, bcur;
+  DevBuf<int4> entries;      // (face id, first cell x, y, z) by bucket
+  DevBuf<uint32_t> occ;      // non-empty bucket bitmap
+  DevBuf<int32_t> big;
+  DevBuf<uint8_t> in_build;
+  DevBuf<uint64_t> cand;
+  DevBuf<float> fbox;        // 6 floats per face
+  DevBuf<uint8_t> degen;     // degenerate-face flags
+  DevBuf<uint64_t> cls;      // candidate pairs by shared-vertex count (3 x cap)
+  DevBuf<DetectScalars> ds;
+  uint64_t cand_cap = 0;
+};
+
+IsectScratch* isect_scratch_create() { return new IsectScratch(); }
+void isect_scratch_destroy(IsectScratch* s) { delete s; }
+
+namespace {
+
+// One detection round, entirely asynchronous (no host sync):
+//   boxes of all faces -> grid over `build` (ids, or every alive face) -> probe with `probe`
+//   (ids, or every alive face) -> narrow phase.  Results stay in S.ds (found / npairs / redo).
+void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive,
+                  const int32_t* build_ids, int64_t n_build, const int32_t* probe_ids, int64_t n_probe, int sym,
+                  int mode, int32_t* pairs, uint64_t pair_cap, const int32_t* owner, const uint8_t* applied,
+                  uint8_t* revert) {
+  cudaStream_t st = ctx.stream;
+  S.ds.ensure(1, st);
+  PCU_CUDA(cudaMemsetAsync(S.ds.get(), 0, sizeof(DetectScalars), st));
+  S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), st);
   const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
-  S.ext_sum.ensure(1, ctx.stream);
-  S.ext_sum.memset(0, ctx.stream);
-  PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n, 256), ctx.num_sms * 4)), 256, 0, B,
-             d_ids, n, d_alive, S.ext_sum.get());
-  const double sum = read_scalar(ctx, S.ext_sum.get());
-  const double mean = n_alive_hint > 0 ? sum / static_cast<double>(n_alive_hint) : 1.0;
-  const double h = mean > 0.0 ? mean : 1e-3;
-  inv_h = 1.0 / h;
-  const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_alive_hint) * 2 + 1);
-  mask = nb - 1;
-  S.bcount.ensure(nb, ctx.stream);
-  S.boff.ensure(nb, ctx.stream);
-  S.bcur.ensure(nb, ctx.stream);
-  S.counters.ensure(4, ctx.stream);
-  PCU_CUDA(cudaMemsetAsync(S.bcount.get(), 0, nb * 4, ctx.stream));
-  PCU_CUDA(cudaMemsetAsync(S.bcur.get(), 0, nb * 4, ctx.stream));
-  S.counters.memset(0, ctx.stream);
-  S.big.ensure(1, ctx.stream);
-  PCU_LAUNCH(ctx, k_bin, grid_for(n, 256), 256, 0, B, d_ids, n, d_alive, inv_h, mask, 0, S.bcount.get(), S.boff.get(),
-             S.bcur.get(), nullptr, nullptr, S.counters.get());
+  S.degen.ensure(static_cast<size_t>(nf > 0 ? nf : 1), st);
+  PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()),
+             S.degen.get());
+  PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n_build, 256), ctx.num_sms * 4)), 256, 0,
+             B, build_ids, n_build, d_alive, S.ds.get());
+  PCU_LAUNCH(ctx, k_set_invh, 1, 1, 0, S.ds.get(), n_build);
+  const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_build) * 2 + 1);
+  const uint32_t mask = nb - 1;
+  S.bcount.ensure(nb, st);
+  S.boff.ensure(nb, st);
+  S.bcur.ensure(nb, st);
+  PCU_CUDA(cudaMemsetAsync(S.bcount.get(), 0, nb * 4, st));
+  PCU_CUDA(cudaMemsetAsync(S.bcur.get(), 0, nb * 4, st));
+  S.occ.ensure(nb / 32 + 1, st);
+  PCU_CUDA(cudaMemsetAsync(S.occ.get(), 0, (nb / 32 + 1) * 4, st));
+  // hard capacity: a non-big face covers at most kMaxCells cells
+  S.entries.ensure(static_cast<size_t>(n_build) * kMaxCells + 16, st);
+  S.big.ensure(static_cast<size_t>(n_build) + 16, st);
+  PCU_LAUNCH(ctx, k_bin, grid_for(n_build, 256), 256, 0, B, build_ids, n_build, d_alive, S.ds.get(), mask, 0,
+             S.bcount.get(), S.boff.get(), S.bcur.get(), nullptr, nullptr, S.occ.get());
   exclusive_scan_u32(ctx, S.bcount.get(), S.boff.get(), nb);
-  const uint64_t total = static_cast<uint64_t>(read_scalar(ctx, S.boff.get() + nb - 1)) + read_scalar(ctx, S.bcount.get() + nb - 1);
-  S.entries.ensure(total ? total : 1, ctx.stream);
-  S.big.ensure(static_cast<size_t>(n > 0 ? n : 1), ctx.stream);
-  PCU_LAUNCH(ctx, k_bin, grid_for(n, 256), 256, 0, B, d_ids, n, d_alive, inv_h, mask, 1, S.bcount.get(), S.boff.get(),
-             S.bcur.get(), S.entries.get(), S.big.get(), S.counters.get());
-  unsigned long long nb_big = 0;
-  PCU_CUDA(cudaMemcpyAsync(&nb_big, S.counters.get() + 1, 8, cudaMemcpyDeviceToHost, ctx.stream));
-  PCU_CUDA(cudaStreamSynchronize(ctx.stream));
-  nbig = static_cast<int64_t>(nb_big);
-}
-
-void make_fboxes(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive) {
-  S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), ctx.stream);
-  PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()));
-}
-
-__global__ void k_flag_ids(const int32_t* __restrict__ ids, int64_t n, uint8_t* __restrict__ flag) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) flag[ids[i]] = 1;
-}
-
-int64_t probe_candidates(Ctx& ctx, IsectScratch& S, int64_t nf, const uint8_t* d_alive, double inv_h, uint32_t mask,
-                         int64_t nbig, int sym, const uint8_t* in_build, const int32_t* probe_ids = nullptr) {
-  uint64_t cap = std::max<uint64_t>(S.cand.n, static_cast<uint64_t>(nf) * 4 + 1024);
-  const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
-  while (true) {
-    S.cand.ensure(cap, ctx.stream);
-    PCU_CUDA(cudaMemsetAsync(S.counters.get() + 3, 0, 8, ctx.stream));
-    PCU_LAUNCH(ctx, k_probe, grid_for(nf, 128), 128, 0, B, nf, d_alive, inv_h, mask, S.bcount.get(), S.boff.get(),
-               S.entries.get(), S.big.get(), nbig, sym, in_build, S.cand.get(), S.cand.n, S.counters.get() + 3,
-               probe_ids);
-    const uint64_t got = read_scalar(ctx, S.counters.get() + 3);
-    if (got <= S.cand.n) return static_cast<int64_t>(got);
-    cap = got + got / 4 + 1024;
+  PCU_LAUNCH(ctx, k_bin, grid_for(n_build, 256), 256, 0, B, build_ids, n_build, d_alive, S.ds.get(), mask, 1,
+             S.bcount.get(), S.boff.get(), S.bcur.get(), S.entries.get(), S.big.get(), S.occ.get());
+  const uint8_t* in_build = nullptr;
+  if (!sym && mode == 1 && !probe_ids) {
+    S.in_build.ensure(nf, st);
+    PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, st));
+    PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_build, 256), 256, 0, build_ids, n_build, S.in_build.get());
+    in_build = S.in_build.get();
   }
+  if (S.cand_cap == 0) S.cand_cap = static_cast<uint64_t>(nf) * 4 + 4096;
+  S.cand.ensure(S.cand_cap, st);
+  PCU_LAUNCH(ctx, k_probe, grid_for(n_probe, 128), 128, 0, B, n_probe,
+             d_alive, S.ds.get(), mask, S.bcount.get(), S.boff.get(), S.entries.get(), S.big.get(), S.occ.get(), sym,
+             in_build,
+             S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids);
+  S.cls.ensure(3 * S.cand_cap, st);
+  const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
+  PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
+             S.cls.get(), pairs, pair_cap, owner, applied, revert);
+  PCU_LAUNCH(ctx, k_narrow<2>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
+             applied, revert);
+  PCU_LAUNCH(ctx, k_narrow<1>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
+             applied, revert);
+  PCU_LAUNCH(ctx, k_narrow<0>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
+             applied, revert);
 }
 
 }  // namespace
@@ -539,26 +683,24 @@ std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, 
   std::vector<int32_t> out;
   if (nf < 2) return out;
   IsectScratch S;
-  double inv_h;
-  uint32_t mask;
-  int64_t nbig;
-  make_fboxes(ctx, S, dV, dF, nf, d_alive);
-  build_grid(ctx, S, nullptr, nf, d_alive, inv_h, mask, nbig, nf);
-  const int64_t ncand = probe_candidates(ctx, S, nf, d_alive, inv_h, mask, nbig, 1, nullptr);
-  uint64_t cap = 1024;
+  uint64_t pair_cap = static_cast<uint64_t>(nf) + 1024;
+  DevBuf<int32_t> pairs(2 * pair_cap, ctx.stream);
   while (true) {
-    DevBuf<int32_t> pairs(2 * cap, ctx.stream);
-    PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));
-    if (ncand)
-      PCU_LAUNCH(ctx, k_narrow, grid_for(ncand, 128), 128, 0, dV, dF, S.cand.get(), ncand, 0, pairs.get(), cap,
-                 S.counters.get() + 2, nullptr, nullptr, nullptr);
-    const uint64_t got = read_scalar(ctx, S.counters.get() + 2);
-    if (got > cap) {
-      cap = got + 1024;
+    detect_round(ctx, S, dV, dF, nf, d_alive, nullptr, nf, nullptr, nf, 1, 0, pairs.get(), pair_cap, nullptr, nullptr,
+                 nullptr);
+    const DetectScalars ds = read_scalar(ctx, S.ds.get());
+    if (ds.redo) {
+      S.cand_cap = ds.ncand + ds.ncand / 4 + 4096;
       continue;
     }
-    out.resize(2 * got);
-    if (got) PCU_CUDA(cudaMemcpyAsync(out.data(), pairs.get(), got * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (ds.npairs > pair_cap) {
+      pair_cap = ds.npairs + 1024;
+      pairs.alloc(2 * pair_cap, ctx.stream);
+      continue;
+    }
+    out.resize(2 * ds.npairs);
+    if (ds.npairs)
+      PCU_CUDA(cudaMemcpyAsync(out.data(), pairs.get(), ds.npairs * 8, cudaMemcpyDeviceToHost, ctx.stream));
     PCU_CUDA(cudaStreamSynchronize(ctx.stream));
     break;
   }
@@ -579,51 +721,31 @@ void tri_tri_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t*
   PCU_LAUNCH(ctx, k_verdict_pairs, grid_for(n, 128), 128, 0, dV, dF, d_pairs, n, d_out);
 }
 
-int64_t undo_detect(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
-                    const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
-                    const uint8_t* d_applied, uint8_t* d_revert) {
-  if (n_query == 0) return 0;
-  double inv_h;
-  uint32_t mask;
-  int64_t nbig;
-  // grid over the (few) query faces, probed by every alive face
-  ctx.prof.mark(ctx.stream, "undo_detect:pre");
-  make_fboxes(ctx, S, dV, dF, nf, d_falive);
-  build_grid(ctx, S, d_query_faces, n_query, d_falive, inv_h, mask, nbig, n_query);
-  S.in_build.ensure(nf, ctx.stream);
-  PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, ctx.stream));
-  PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_query, 256), 256, 0, d_query_faces, n_query, S.in_build.get());
-  ctx.prof.mark(ctx.stream, "undo_detect:grid");
-  const int64_t ncand = probe_candidates(ctx, S, nf, d_falive, inv_h, mask, nbig, 0, S.in_build.get());
-  ctx.prof.mark(ctx.stream, "undo_detect:broad");
-  if (ncand == 0) return 0;
-  PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));
-  PCU_LAUNCH(ctx, k_narrow, grid_for(ncand, 128), 128, 0, dV, dF, S.cand.get(), ncand, 1, nullptr, 0,
-             S.counters.get() + 2, d_owner, d_applied, d_revert);
-  return static_cast<int64_t>(read_scalar(ctx, S.counters.get() + 2));
+void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
+                       const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
+                       const uint8_t* d_applied, uint8_t* d_revert) {
+  // round 1: grid over the faces owned by applied collapses, probed by every alive face
+  detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner, d_applied,
+               d_revert);
 }
 
-// Later undo rounds: only pairs (restored face, face owned by an applied collapse) can be new —
-// every other pair is unchanged since the previous round's check.  Grid over the restored
-// faces, probed by the owned faces.
-int64_t undo_detect_restored(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
-                             const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
-                             const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
-                             const uint8_t* d_applied, uint8_t* d_revert) {
-  if (n_restored == 0 || n_owned == 0) return 0;
-  double inv_h;
-  uint32_t mask;
-  int64_t nbig;
-  make_fboxes(ctx, S, dV, dF, nf, d_falive);
-  build_grid(ctx, S, d_restored, n_restored, d_falive, inv_h, mask, nbig, n_restored);
-  ctx.prof.mark(ctx.stream, "undo_detect:grid");
-  const int64_t ncand = probe_candidates(ctx, S, n_owned, d_falive, inv_h, mask, nbig, 0, nullptr, d_owned);
-  ctx.prof.mark(ctx.stream, "undo_detect:broad");
-  if (ncand == 0) return 0;
-  PCU_CUDA(cudaMemsetAsync(S.counters.get() + 2, 0, 8, ctx.stream));
-  PCU_LAUNCH(ctx, k_narrow, grid_for(ncand, 128), 128, 0, dV, dF, S.cand.get(), ncand, 1, nullptr, 0,
-             S.counters.get() + 2, d_owner, d_applied, d_revert);
-  return static_cast<int64_t>(read_scalar(ctx, S.counters.get() + 2));
+void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
+                                const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
+                                const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
+                                const uint8_t* d_applied, uint8_t* d_revert) {
+  // later rounds: only (restored face, applied-owned face) pairs can be new
+  detect_round(ctx, S, dV, dF, nf, d_falive, d_restored, n_restored, d_owned, n_owned, 0, 1, nullptr, 0, d_owner,
+               d_applied, d_revert);
+}
+
+const void* detect_scalars_ptr(IsectScratch& S) { return S.ds.get(); }
+size_t detect_scalars_size() { return sizeof(DetectScalars); }
+void detect_grow(IsectScratch& S, unsigned long long ncand) { S.cand_cap = ncand + ncand / 4 + 4096; }
+void detect_read(const void* host_copy, unsigned long long* found, int* redo, unsigned long long* ncand) {
+  const DetectScalars* d = static_cast<const DetectScalars*>(host_copy);
+  *found = d->found;
+  *redo = d->redo;
+  *ncand = d->ncand;
 }
 
 }  // namespace pcu

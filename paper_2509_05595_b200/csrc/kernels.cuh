@@ -34,17 +34,21 @@ std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, 
                                         const uint8_t* d_alive, const uint8_t* d_query);
 void tri_tri_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int32_t* d_out);
 
-// Broad phase + narrow phase used inside the QEM undo loop: for every intersecting pair with
-// a query face, flag `hit[owner[f]]` for both faces' owners (owner -1 = none).  Returns the
-// number of intersecting pairs found (device counter read back).
+// Broad phase + narrow phase of the QEM undo loop, asynchronous: results (found pairs, buffer
+// overflow) are left in device scalars; detect_scalars_ptr/size let the caller fetch them in
+// the same host synchronisation as its own counters.
 struct IsectScratch;
-int64_t undo_detect(Ctx& ctx, IsectScratch& scratch, const double* dV, const int32_t* dF, int64_t nf,
-                    const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query,
-                    const int32_t* d_owner, const uint8_t* d_applied, uint8_t* d_revert);
-int64_t undo_detect_restored(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
-                             const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
-                             const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
-                             const uint8_t* d_applied, uint8_t* d_revert);
+void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
+                       const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
+                       const uint8_t* d_applied, uint8_t* d_revert);
+void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
+                                const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
+                                const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
+                                const uint8_t* d_applied, uint8_t* d_revert);
+const void* detect_scalars_ptr(IsectScratch& S);
+size_t detect_scalars_size();
+void detect_grow(IsectScratch& S, unsigned long long ncand);
+void detect_read(const void* host_copy, unsigned long long* found, int* redo, unsigned long long* ncand);
 IsectScratch* isect_scratch_create();
 void isect_scratch_destroy(IsectScratch* s);
 

@@ -34,7 +34,7 @@ constexpr int kMaxDeg = 255;      // per-vertex incident-face capacity of the lo
 constexpr double k4Sqrt3 = 6.928203230275509;
 
 struct Counters {
-  unsigned long long edges, marked, link_fail, newinv, query, removed, applied, err, cap, undone, restored;
+  unsigned long long edges, marked, link_fail, newinv, query, removed, applied, err, cap, undone, restored, nan;
 };
 
 __device__ __forceinline__ D3 P3(const double* X, int v) { return D3{X[3 * v], X[3 * v + 1], X[3 * v + 2]}; }
@@ -179,10 +179,12 @@ __global__ void k_edge_fill(const int32_t* __restrict__ F, const uint32_t* __res
   }
 }
 
-__global__ void k_mark_invalid(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb, int64_t ne,
-                               const uint64_t* __restrict__ inv, int64_t ninv, uint8_t* __restrict__ valid) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= ne) return;
+__global__ void k_mark_invalid(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                               const unsigned long long* __restrict__ d_ne, const uint64_t* __restrict__ inv,
+                               int64_t ninv, uint8_t* __restrict__ valid) {
+  const int64_t ne = static_cast<int64_t>(*d_ne);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
   const uint64_t key = (static_cast<uint64_t>(ea[e]) << 32) | static_cast<uint32_t>(eb[e]);
   int64_t lo = 0, hi = ninv;
   while (lo < hi) {
@@ -191,6 +193,7 @@ __global__ void k_mark_invalid(const int32_t* __restrict__ ea, const int32_t* __
     else hi = mid;
   }
   valid[e] = (lo < ninv && inv[lo] == key) ? 0 : 1;
+  }
 }
 
 // ------------------------------------------------------------------------------ cost
@@ -238,13 +241,14 @@ __device__ double ring_skinny(const double* X, const int32_t* F, const int32_t* 
 __global__ void k_cost(const double* __restrict__ X, const int32_t* __restrict__ F, const double* __restrict__ Q,
                        const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
                        const int32_t* __restrict__ inc, const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
-                       const uint8_t* __restrict__ valid, int64_t ne, double we, double ws,
-                       uint64_t* __restrict__ key, double* __restrict__ place, Counters* cnt) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= ne) return;
+                       const uint8_t* __restrict__ valid, const unsigned long long* __restrict__ d_ne, double we,
+                       double ws, uint64_t* __restrict__ key, double* __restrict__ place, Counters* cnt) {
+  const int64_t ne = static_cast<int64_t>(*d_ne);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
   if (!valid[e]) {
     key[e] = ~0ull;
-    return;
+    continue;
   }
   const int a = ea[e], b = eb[e];
   double q[10];
@@ -297,25 +301,29 @@ __global__ void k_cost(const double* __restrict__ X, const int32_t* __restrict__
     }
   }
   if (cost != cost) {
-    atomicAdd(&cnt->err, 1ull);
+    atomicAdd(&cnt->nan, 1ull);
     key[e] = ~0ull;
-    return;
+    continue;
   }
   const float cf = __double2float_rn(cost < 0.0 ? 0.0 : cost);
   key[e] = (static_cast<uint64_t>(__float_as_uint(cf)) << 32) | static_cast<uint64_t>(e);
   place[3 * e] = x.x;
   place[3 * e + 1] = x.y;
   place[3 * e + 2] = x.z;
+  }
 }
 
 // --------------------------------------------------------------------- propagation
 __global__ void k_prop_edges(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
-                             const uint64_t* __restrict__ key, const uint8_t* __restrict__ valid, int64_t ne,
-                             unsigned long long* __restrict__ vmin) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= ne || !valid[e]) return;
-  atomicMin(&vmin[ea[e]], static_cast<unsigned long long>(key[e]));
-  atomicMin(&vmin[eb[e]], static_cast<unsigned long long>(key[e]));
+                             const uint64_t* __restrict__ key, const uint8_t* __restrict__ valid,
+                             const unsigned long long* __restrict__ d_ne, unsigned long long* __restrict__ vmin) {
+  const int64_t ne = static_cast<int64_t>(*d_ne);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!valid[e]) continue;
+    atomicMin(&vmin[ea[e]], static_cast<unsigned long long>(key[e]));
+    atomicMin(&vmin[eb[e]], static_cast<unsigned long long>(key[e]));
+  }
 }
 
 __global__ void k_prop_faces(const int32_t* __restrict__ F, const uint8_t* __restrict__ falive, int64_t nf,
@@ -332,12 +340,20 @@ __global__ void k_prop_faces(const int32_t* __restrict__ F, const uint8_t* __res
 }
 
 __global__ void k_mark(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb, const uint64_t* __restrict__ key,
-                       const uint8_t* __restrict__ valid, int64_t ne, const unsigned long long* __restrict__ vfmin,
-                       uint64_t* __restrict__ marked, Counters* cnt) {
-  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (e >= ne || !valid[e]) return;
-  const uint64_t k = key[e];
-  if (k == vfmin[ea[e]] && k == vfmin[eb[e]]) marked[atomicAdd(&cnt->marked, 1ull)] = k;
+                       const uint8_t* __restrict__ valid, const unsigned long long* __restrict__ d_ne,
+                       const unsigned long long* __restrict__ vfmin, uint64_t* __restrict__ marked, Counters* cnt) {
+  const int64_t ne = static_cast<int64_t>(*d_ne);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!valid[e]) continue;
+    const uint64_t k = key[e];
+    if (k == vfmin[ea[e]] && k == vfmin[eb[e]]) marked[agg_inc(&cnt->marked)] = k;
+  }
+}
+
+__global__ void k_total(const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, int64_t n,
+                        unsigned long long* __restrict__ out) {
+  *out = static_cast<unsigned long long>(off[n - 1]) + cnt[n - 1];
 }
 
 // ---------------------------------------------------------------------- link condition
@@ -471,7 +487,7 @@ __global__ void k_link(const uint64_t* __restrict__ marked, int64_t nm, const in
   } else {
     rem[i] = 0;
     atomicAdd(&cnt->link_fail, 1ull);
-    newinv[atomicAdd(&cnt->newinv, 1ull)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+    newinv[agg_inc(&cnt->newinv)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
   }
 }
 
@@ -519,21 +535,21 @@ __global__ void k_collapse(const uint64_t* __restrict__ marked, int64_t nm, cons
   for (int k = 0; k < 10; ++k) Q[10 * a + k] = Q[10 * a + k] + Q[10 * b + k];
   valive[b] = 0;
   B.applied[i] = 1;
-  atomicAdd(&cnt->applied, 1ull);
-  atomicAdd(&cnt->removed, static_cast<unsigned long long>(rem[i]));
+  agg_add(&cnt->applied, 1ull);
+  agg_add(&cnt->removed, static_cast<unsigned long long>(rem[i]));
   // owned faces: alive faces of a and of b after the collapse
   for (uint32_t j = 0; j < deg[a]; ++j) {
     const int f = inc[off[a] + j];
     if (falive[f]) {
       owner[f] = static_cast<int32_t>(i);
-      qfaces[atomicAdd(&cnt->query, 1ull)] = f;
+      qfaces[agg_inc(&cnt->query)] = f;
     }
   }
   for (uint32_t j = 0; j < deg[b]; ++j) {
     const int f = inc[off[b] + j];
     if (falive[f]) {
       owner[f] = static_cast<int32_t>(i);
-      qfaces[atomicAdd(&cnt->query, 1ull)] = f;
+      qfaces[agg_inc(&cnt->query)] = f;
     }
   }
 }
@@ -545,7 +561,7 @@ __global__ void k_requery(const int32_t* __restrict__ qin, int64_t n, const int3
   if (i >= n) return;
   const int f = qin[i];
   const int o = owner[f];
-  if (o >= 0 && applied[o]) qout[atomicAdd(&cnt->query, 1ull)] = f;
+  if (o >= 0 && applied[o]) qout[agg_inc(&cnt->query)] = f;
 }
 
 __global__ void k_revert(int64_t nm, const uint8_t* __restrict__ revert, const uint32_t* __restrict__ off,
@@ -561,14 +577,14 @@ __global__ void k_revert(int64_t nm, const uint8_t* __restrict__ revert, const u
   for (uint32_t j = 0; j < deg[a]; ++j) {
     const int f = inc[off[a] + j];
     if (owner[f] == i) owner[f] = -1;
-    if (!has(Fprev + 3 * f, b)) restored[atomicAdd(&cnt->restored, 1ull)] = f;
+    if (!has(Fprev + 3 * f, b)) restored[agg_inc(&cnt->restored)] = f;
   }
   for (uint32_t j = 0; j < deg[b]; ++j) {
     const int f = inc[off[b] + j];
     if (owner[f] == i) owner[f] = -1;
     falive[f] = 1;
     for (int k = 0; k < 3; ++k) F[3 * f + k] = Fprev[3 * f + k];
-    restored[atomicAdd(&cnt->restored, 1ull)] = f;
+    restored[agg_inc(&cnt->restored)] = f;
   }
   for (int k = 0; k < 3; ++k) X[3 * a + k] = B.oldx[3 * i + k];
   for (int k = 0; k < 10; ++k) Q[10 * a + k] = B.oldq[10 * i + k];
@@ -660,40 +676,55 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
 
   int64_t alive_faces = nf, alive_verts = nv;
   int retain = 0, zero_run = 0;
+  int64_t ne_hint = 3 * nf / 2 + 16;
+  unsigned long long* d_ne = &cnt.get()->edges;
+  std::vector<uint8_t> ds_host(detect_scalars_size());
+  // Host synchronisations per iteration: one after marking, one after the collapse batch, one
+  // per undo round (counters + detection scalars fetched together).
+  auto sync_counters = [&](bool with_detect) {
+    Counters h;
+    PCU_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    if (with_detect)
+      PCU_CUDA(cudaMemcpyAsync(ds_host.data(), detect_scalars_ptr(*isc), ds_host.size(), cudaMemcpyDeviceToHost, st));
+    PCU_CUDA(cudaStreamSynchronize(st));
+    return h;
+  };
+  const unsigned gs_grid = static_cast<unsigned>(ctx.num_sms * 16);
   while (alive_faces > target && zero_run < P.stall) {
     S.iterations++;
     ctx.prof.mark(st, "misc");
     if (S.iterations > 1) build_incidence();
     ctx.prof.mark(st, "incidence");
     cnt.memset(0, st);
-    // edges
+    // edges (device-side count; kernels below stride over it)
     PCU_LAUNCH(ctx, k_edge_count, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, ecount.get(),
                cnt.get());
     exclusive_scan_u32(ctx, ecount.get(), eoff.get(), nv);
-    const int64_t ne = static_cast<int64_t>(read_scalar(ctx, eoff.get() + nv - 1)) + read_scalar(ctx, ecount.get() + nv - 1);
-    Counters h = read_scalar(ctx, cnt.get());
+    PCU_LAUNCH(ctx, k_total, 1, 1, 0, eoff.get(), ecount.get(), nv, d_ne);
+    PCU_LAUNCH(ctx, k_edge_fill, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, eoff.get(), ea.get(),
+               eb.get(), enf.get());
+    ctx.prof.mark(st, "edges");
+    const unsigned eg = std::min<unsigned>(grid_for(ne_hint, 128), gs_grid);
+    PCU_LAUNCH(ctx, k_mark_invalid, eg, 128, 0, ea.get(), eb.get(), d_ne, inv.get(), ninv, valid.get());
+    PCU_LAUNCH(ctx, k_cost, eg, 128, 0, X, F, Q.get(), off.get(), deg.get(), inc.get(), ea.get(), eb.get(), valid.get(),
+               d_ne, P.we, P.ws, key.get(), place.get(), cnt.get());
+    ctx.prof.mark(st, "cost");
+    vmin.memset(0xFF, st);
+    vfmin.memset(0xFF, st);
+    PCU_LAUNCH(ctx, k_prop_edges, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vmin.get());
+    PCU_LAUNCH(ctx, k_prop_faces, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vmin.get(), vfmin.get());
+    PCU_LAUNCH(ctx, k_mark, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vfmin.get(), marked.get(),
+               cnt.get());
+    Counters h = sync_counters(false);  // ---- sync 1
+    const int64_t ne = static_cast<int64_t>(h.edges);
+    ne_hint = ne;
     S.face_iterations += alive_faces;
     S.alg_bytes += 28 * alive_faces + 92 * alive_verts + 8 * ne;
     PCU_REQUIRE(h.cap == 0, PAMOPT_CU_ECAP, "simplify_to: vertex valence exceeds 255 incident faces");
     if (S.iterations == 1)
       PCU_REQUIRE(h.err == 0, PAMOPT_CU_EINVAL, "simplify_to: non-manifold input (an edge has >2 faces); run stage 1");
-    PCU_LAUNCH(ctx, k_edge_fill, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, eoff.get(), ea.get(),
-               eb.get(), enf.get());
-    ctx.prof.mark(st, "edges");
-    PCU_LAUNCH(ctx, k_mark_invalid, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), ne, inv.get(), ninv, valid.get());
-    cnt.memset(0, st);
-    PCU_LAUNCH(ctx, k_cost, grid_for(ne, 128), 128, 0, X, F, Q.get(), off.get(), deg.get(), inc.get(), ea.get(), eb.get(),
-               valid.get(), ne, P.we, P.ws, key.get(), place.get(), cnt.get());
-    ctx.prof.mark(st, "cost");
-    vmin.memset(0xFF, st);
-    vfmin.memset(0xFF, st);
-    PCU_LAUNCH(ctx, k_prop_edges, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), key.get(), valid.get(), ne, vmin.get());
-    PCU_LAUNCH(ctx, k_prop_faces, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vmin.get(), vfmin.get());
-    PCU_LAUNCH(ctx, k_mark, grid_for(ne, 256), 256, 0, ea.get(), eb.get(), key.get(), valid.get(), ne, vfmin.get(),
-               marked.get(), cnt.get());
-    h = read_scalar(ctx, cnt.get());
+    PCU_REQUIRE(h.nan == 0, PAMOPT_CU_ENUMERIC, "simplify_to: NaN edge cost");
     ctx.prof.mark(st, "propagate+mark");
-    PCU_REQUIRE(h.err == 0, PAMOPT_CU_ENUMERIC, "simplify_to: NaN edge cost");
     const int64_t nm = static_cast<int64_t>(h.marked);
     int64_t succ = 0;
     int rounds = 0;
@@ -717,7 +748,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
       PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, marked_sorted.get(), nm, rem.get(), remoff.get(),
                  alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
                  falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
-      h = read_scalar(ctx, cnt.get());
+      h = sync_counters(false);  // ---- sync 2
       ctx.prof.mark(st, "collapse");
       int64_t nq = static_cast<int64_t>(h.query);
       int32_t* qa = qf.get();
@@ -726,28 +757,34 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
       int64_t nrest = 0;
       while (nq > 0) {
         revert.memset(0, st);
-        const int64_t found =
-            first_round ? undo_detect(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get())
-                        : undo_detect_restored(ctx, *isc, X, F, nf, falive.get(), rlist.get(), nrest, qa, nq,
-                                               owner.get(), B.applied, revert.get());
-        first_round = false;
-        ctx.prof.mark(st, "undo_detect");
-        if (found == 0) break;
-        ++rounds;
         PCU_CUDA(cudaMemsetAsync(&cnt.get()->restored, 0, 8, st));
+        if (first_round)
+          undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get());
+        else
+          undo_detect_restored_async(ctx, *isc, X, F, nf, falive.get(), rlist.get(), nrest, qa, nq, owner.get(),
+                                     B.applied, revert.get());
         PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
                    Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get(),
                    rlist.get());
         // rebuild the query list from still-applied collapses
         PCU_CUDA(cudaMemsetAsync(&cnt.get()->query, 0, 8, st));
         PCU_LAUNCH(ctx, k_requery, grid_for(nq, 256), 256, 0, qa, nq, owner.get(), B.applied, qb, cnt.get());
-        h = read_scalar(ctx, cnt.get());
+        h = sync_counters(true);  // ---- sync per round
+        unsigned long long found = 0, ncand = 0;
+        int redo = 0;
+        detect_read(ds_host.data(), &found, &redo, &ncand);
+        ctx.prof.mark(st, "undo_round");
+        if (redo) {  // candidate buffer overflow: nothing was flagged or reverted; grow and repeat
+          detect_grow(*isc, ncand);
+          continue;
+        }
+        if (found == 0) break;
+        ++rounds;
+        first_round = false;
         nq = static_cast<int64_t>(h.query);
         nrest = static_cast<int64_t>(h.restored);
         std::swap(qa, qb);
-        ctx.prof.mark(st, "undo_revert");
       }
-      h = read_scalar(ctx, cnt.get());
       succ = static_cast<int64_t>(h.applied);
       alive_faces -= static_cast<int64_t>(h.removed);
       nnew = static_cast<int64_t>(h.newinv);
@@ -759,7 +796,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     S.collapses += succ;
     alive_verts -= succ;
     S.per_iter.push_back(succ);
-    // invalid-flag update
+    // invalid-flag update (duplicates are harmless for the binary search)
     bool keep_old;
     if (succ > 0) {
       keep_old = false;
@@ -777,19 +814,9 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
       PCU_CUDA(cudaMemcpyAsync(merged.get(), inv.get(), ninv * 8, cudaMemcpyDeviceToDevice, st));
     if (nnew)
       PCU_CUDA(cudaMemcpyAsync(merged.get() + (keep_old ? ninv : 0), newinv.get(), nnew * 8, cudaMemcpyDeviceToDevice, st));
-    inv.alloc(nall ? nall : 1, st);
-    if (nall) {
-      sort_pairs_u64(ctx, merged.get(), nall);
-      // unique
-      DevBuf<int> nsel(1, st);
-      size_t need = 0;
-      cub::DeviceSelect::Unique(nullptr, need, merged.get(), inv.get(), nsel.get(), static_cast<int>(nall), st);
-      DevBuf<uint8_t> tmp(need ? need : 1, st);
-      cub::DeviceSelect::Unique(tmp.get(), need, merged.get(), inv.get(), nsel.get(), static_cast<int>(nall), st);
-      ninv = read_scalar(ctx, nsel.get());
-    } else {
-      ninv = 0;
-    }
+    if (nall) sort_pairs_u64(ctx, merged.get(), nall);
+    inv = std::move(merged);
+    ninv = nall;
     ctx.prof.mark(st, "invalid_update");
   }
   // compaction (mesh.cpp:278-292): alive vertices used by alive faces, order preserving
