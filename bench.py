@@ -332,6 +332,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    mesh.free()
     ctx.close()
     return 0
 

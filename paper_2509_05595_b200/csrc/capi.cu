@@ -10,9 +10,27 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <atomic>
+
+// Handles keep their context alive: pamopt_cu_ctx_destroy on a context that still owns meshes or
+// grids only marks it; the last handle freed releases it (no use-after-free at teardown).
 struct pamopt_cu_ctx_s {
   pcu::Ctx ctx;
+  std::atomic<int> refs{0};
+  std::atomic<bool> dead{false};
 };
+
+static void ctx_release(pamopt_cu_ctx c) {
+  pcu::DeviceGuard g(c->ctx.device);
+  if (c->ctx.scratch) cudaFreeAsync(c->ctx.scratch, c->ctx.stream);
+  cudaStreamSynchronize(c->ctx.stream);
+  cudaStreamDestroy(c->ctx.stream);
+  delete c;
+}
+
+static void ctx_unref(pamopt_cu_ctx c) {
+  if (--c->refs == 0 && c->dead) ctx_release(c);
+}
 
 struct pamopt_cu_mesh_s {
   pamopt_cu_ctx owner;
@@ -123,11 +141,8 @@ int pamopt_cu_ctx_create(int32_t device, pamopt_cu_ctx* out) {
 int pamopt_cu_ctx_destroy(pamopt_cu_ctx c) {
   return guarded([&] {
     if (!c) return;
-    pcu::DeviceGuard g(c->ctx.device);
-    if (c->ctx.scratch) cudaFreeAsync(c->ctx.scratch, c->ctx.stream);
-    cudaStreamSynchronize(c->ctx.stream);
-    cudaStreamDestroy(c->ctx.stream);
-    delete c;
+    c->dead = true;
+    if (c->refs == 0) ctx_release(c);
   });
 }
 
@@ -151,6 +166,7 @@ static int mesh_create(pamopt_cu_ctx c, const double* v, int64_t nv, const int32
     pcu::DeviceGuard g(c->ctx.device);
     auto* m = new pamopt_cu_mesh_s();
     m->owner = c;
+    ++c->refs;
     m->nv = nv;
     m->nf = nf;
     m->V.alloc(3 * (nv ? nv : 1), c->ctx.stream);
@@ -193,8 +209,12 @@ int pamopt_cu_mesh_download(pamopt_cu_mesh m, double* v, int32_t* f) {
 int pamopt_cu_mesh_free(pamopt_cu_mesh m) {
   return guarded([&] {
     if (!m) return;
-    pcu::DeviceGuard g(m->owner->ctx.device);
-    delete m;
+    pamopt_cu_ctx c = m->owner;
+    {
+      pcu::DeviceGuard g(c->ctx.device);
+      delete m;
+    }
+    ctx_unref(c);
   });
 }
 
@@ -215,6 +235,7 @@ static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, dou
     pcu::DeviceGuard g(c->ctx.device);
     auto* gr = new pamopt_cu_grid_s();
     gr->owner = c;
+    ++c->refs;
     gr->R = R;
     const int64_t n1 = R + 1;
     gr->g.alloc(n1 * n1 * n1, c->ctx.stream);
@@ -222,6 +243,7 @@ static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, dou
       pcu::udf_run(c->ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, mode, eps, gr->g.get());
     } catch (...) {
       delete gr;
+      ctx_unref(c);
       throw;
     }
     *out = gr;
@@ -257,6 +279,7 @@ int pamopt_cu_grid_upload(pamopt_cu_ctx c, int32_t R, const float* samples, pamo
     pcu::DeviceGuard g(c->ctx.device);
     auto* gr = new pamopt_cu_grid_s();
     gr->owner = c;
+    ++c->refs;
     gr->R = R;
     const int64_t n1 = R + 1;
     gr->g.alloc(n1 * n1 * n1, c->ctx.stream);
@@ -286,8 +309,12 @@ int pamopt_cu_grid_download(pamopt_cu_grid gr, float* samples) {
 int pamopt_cu_grid_free(pamopt_cu_grid gr) {
   return guarded([&] {
     if (!gr) return;
-    pcu::DeviceGuard g(gr->owner->ctx.device);
-    delete gr;
+    pamopt_cu_ctx c = gr->owner;
+    {
+      pcu::DeviceGuard g(c->ctx.device);
+      delete gr;
+    }
+    ctx_unref(c);
   });
 }
 
@@ -314,6 +341,7 @@ int pamopt_cu_dmc_extract(pamopt_cu_grid gr, double beta, pamopt_cu_mesh* out) {
     pcu::dmc_extract(ctx, gr->g.get(), gr->R, beta, gr->last);
     auto* m = new pamopt_cu_mesh_s();
     m->owner = gr->owner;
+    ++gr->owner->refs;
     m->nv = static_cast<int64_t>(gr->last.nv);
     m->nf = static_cast<int64_t>(gr->last.nf);
     m->V = std::move(gr->last.V);
@@ -444,6 +472,7 @@ static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double ep
   PCU_CUDA(cudaEventRecord(ev[2], ctx.stream));
   auto* m = new pamopt_cu_mesh_s();
   m->owner = c;
+  ++c->refs;
   m->nv = static_cast<int64_t>(d.nv);
   m->nf = static_cast<int64_t>(d.nf);
   m->V = std::move(d.V);
@@ -453,6 +482,7 @@ static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double ep
     pcu::simplify_run(ctx, m->V, m->F, m->nv, m->nf, target, P, S);
   } catch (...) {
     delete m;
+    ctx_unref(c);
     throw;
   }
   PCU_CUDA(cudaEventRecord(ev[3], ctx.stream));
@@ -494,7 +524,7 @@ int pamopt_cu_remesh_host(pamopt_cu_ctx c, const double* v, int64_t nv, const in
     PCU_CUDA(cudaStreamSynchronize(ctx.stream));
     if (out_nv) *out_nv = out->nv;
     if (out_nf) *out_nf = out->nf;
-    delete out;
+    pamopt_cu_mesh_free(out);
   });
   pamopt_cu_mesh_free(in);
   return rc;
