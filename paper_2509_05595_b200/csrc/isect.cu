@@ -339,10 +339,12 @@ struct DetectScalars {
   int pad;
 };
 
-__global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t nf,
-                         const uint8_t* __restrict__ alive, FBox* __restrict__ out, uint8_t* __restrict__ degen) {
-  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (f >= nf) return;
+__global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t n,
+                         const uint8_t* __restrict__ alive, FBox* __restrict__ out, uint8_t* __restrict__ degen,
+                         const int32_t* __restrict__ ids) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const int64_t f = ids ? ids[k] : k;
   FBox fb;
   if (alive && !alive[f]) {
     for (int k = 0; k < 3; ++k) {
@@ -512,7 +514,19 @@ __device__ __forceinline__ void report(DetectScalars* ds, int mode, int32_t p, i
 // inflated double-box test (the reference's candidate set), duplicates and degenerate faces
 // (always intersecting), then bucketing by shared-vertex count so stage 2 runs one uniform code
 // path per warp.  mode 1 (QEM undo) skips pairs none of whose owners can still be reverted.
+__device__ __forceinline__ bool deep_overlap(const FBox& a, const FBox& b) {
+  bool ok = true;
+  for (int k = 0; k < 3; ++k) {
+    // shrink each float box by 2 ulps (a superset of the 1-ulp outward rounding) before testing
+    const float alo = a.lo[k] + 2.5e-7f * fabsf(a.lo[k]) + 1e-30f, ahi = a.hi[k] - 2.5e-7f * fabsf(a.hi[k]) - 1e-30f;
+    const float blo = b.lo[k] + 2.5e-7f * fabsf(b.lo[k]) + 1e-30f, bhi = b.hi[k] - 2.5e-7f * fabsf(b.hi[k]) - 1e-30f;
+    ok = ok && alo <= bhi && ahi >= blo;
+  }
+  return ok;
+}
+
 __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, const int32_t* __restrict__ F,
+                                                  const FBox* __restrict__ B,
                                                   const uint8_t* __restrict__ degen, const uint64_t* __restrict__ cand,
                                                   uint64_t cap, DetectScalars* __restrict__ ds, int mode,
                                                   uint64_t* __restrict__ cls, int32_t* __restrict__ pairs,
@@ -532,7 +546,9 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
     }
     const int32_t* tp = F + 3 * p;
     const int32_t* ta = F + 3 * a;
-    if (!overlap(face_box(V, tp), face_box(V, ta))) continue;
+    // the float boxes enclose the double boxes within one f32 ulp per side: an overlap deeper
+    // than that margin in every axis certifies the double-box overlap without the vertex loads
+    if (!deep_overlap(B[p], B[a]) && !overlap(face_box(V, tp), face_box(V, ta))) continue;
     int shared = 0;
     for (int u = 0; u < 3; ++u)
       for (int w = 0; w < 3; ++w) shared += tp[u] == ta[w];
@@ -620,15 +636,18 @@ namespace {
 void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive,
                   const int32_t* build_ids, int64_t n_build, const int32_t* probe_ids, int64_t n_probe, int sym,
                   int mode, int32_t* pairs, uint64_t pair_cap, const int32_t* owner, const uint8_t* applied,
-                  uint8_t* revert) {
+                  uint8_t* revert, bool boxes_current = false) {
   cudaStream_t st = ctx.stream;
   S.ds.ensure(1, st);
   PCU_CUDA(cudaMemsetAsync(S.ds.get(), 0, sizeof(DetectScalars), st));
-  S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), st);
   const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
-  S.degen.ensure(static_cast<size_t>(nf > 0 ? nf : 1), st);
-  PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()),
-             S.degen.get());
+  if (!boxes_current) {
+    S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), st);
+    S.degen.ensure(static_cast<size_t>(nf > 0 ? nf : 1), st);
+    B = reinterpret_cast<const FBox*>(S.fbox.get());
+    PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()),
+               S.degen.get(), nullptr);
+  }
   PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n_build, 256), ctx.num_sms * 4)), 256, 0,
              B, build_ids, n_build, d_alive, S.ds.get());
   PCU_LAUNCH(ctx, k_set_invh, 1, 1, 0, S.ds.get(), n_build);
@@ -664,7 +683,7 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
              S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids);
   S.cls.ensure(3 * S.cand_cap, st);
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
-  PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
+  PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
              S.cls.get(), pairs, pair_cap, owner, applied, revert);
   PCU_LAUNCH(ctx, k_narrow<2>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
              applied, revert);
@@ -726,7 +745,7 @@ void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_
                        const uint8_t* d_applied, uint8_t* d_revert) {
   // round 1: grid over the faces owned by applied collapses, probed by every alive face
   detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner, d_applied,
-               d_revert);
+               d_revert, true);
 }
 
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
@@ -735,7 +754,22 @@ void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, con
                                 const uint8_t* d_applied, uint8_t* d_revert) {
   // later rounds: only (restored face, applied-owned face) pairs can be new
   detect_round(ctx, S, dV, dF, nf, d_falive, d_restored, n_restored, d_owned, n_owned, 0, 1, nullptr, 0, d_owner,
-               d_applied, d_revert);
+               d_applied, d_revert, true);
+}
+
+// Persistent face boxes for the QEM loop: computed once, then refreshed only for the faces a
+// collapse batch or a revert touched (every other face keeps its geometry).
+void boxes_init(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive) {
+  S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), ctx.stream);
+  S.degen.ensure(static_cast<size_t>(nf > 0 ? nf : 1), ctx.stream);
+  PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()),
+             S.degen.get(), nullptr);
+}
+void boxes_update(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, const int32_t* ids, int64_t n,
+                  const uint8_t* d_alive) {
+  if (n <= 0) return;
+  PCU_LAUNCH(ctx, k_fboxes, grid_for(n, 256), 256, 0, dV, dF, n, d_alive, reinterpret_cast<FBox*>(S.fbox.get()),
+             S.degen.get(), ids);
 }
 
 const void* detect_scalars_ptr(IsectScratch& S) { return S.ds.get(); }

@@ -45,6 +45,9 @@ void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, con
                                 const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
                                 const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
                                 const uint8_t* d_applied, uint8_t* d_revert);
+void boxes_init(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive);
+void boxes_update(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, const int32_t* ids, int64_t n,
+                  const uint8_t* d_alive);
 const void* detect_scalars_ptr(IsectScratch& S);
 size_t detect_scalars_size();
 void detect_grow(IsectScratch& S, unsigned long long ncand);

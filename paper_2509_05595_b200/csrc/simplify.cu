@@ -672,6 +672,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
 
   ctx.prof.reset(st);
   build_incidence();
+  boxes_init(ctx, *isc, X, F, nf, falive.get());
   PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, off.get(), deg.get(), inc.get(), nv, Q.get());
 
   int64_t alive_faces = nf, alive_verts = nv;
@@ -751,6 +752,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
       h = sync_counters(false);  // ---- sync 2
       ctx.prof.mark(st, "collapse");
       int64_t nq = static_cast<int64_t>(h.query);
+      boxes_update(ctx, *isc, X, F, qf.get(), nq, falive.get());  // moved / renamed faces
       int32_t* qa = qf.get();
       int32_t* qb = qf2.get();
       bool first_round = true;
@@ -770,6 +772,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
         PCU_CUDA(cudaMemsetAsync(&cnt.get()->query, 0, 8, st));
         PCU_LAUNCH(ctx, k_requery, grid_for(nq, 256), 256, 0, qa, nq, owner.get(), B.applied, qb, cnt.get());
         h = sync_counters(true);  // ---- sync per round
+        boxes_update(ctx, *isc, X, F, rlist.get(), static_cast<int64_t>(h.restored), falive.get());  // restored faces
         unsigned long long found = 0, ncand = 0;
         int redo = 0;
         detect_read(ds_host.data(), &found, &redo, &ncand);
