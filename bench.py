@@ -337,17 +337,160 @@ def run_ours(args):
     return 0
 
 
+# ------------------------------------------------------------------ C4 / C5 (multi-GPU configs)
+def _dist_setup():
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return torch, dist, rank, world, local
+
+
+def _max_over_ranks(torch, dist, world, ms):
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_c4(args):
+    """C4: one 5.24M-triangle mesh, UDF 1024^3 as z-slabs (one per rank), one-plane halo
+    exchange + gather over NCCL, DMC on rank 0.  Strong scaling (fixed total work)."""
+    torch, dist, rank, world, local = _dist_setup()
+    from paper_2509_05595_b200 import api
+    from paper_2509_05595_b200 import distributed as D
+    v, f, R, _ = workload("c4")
+    ctx = api.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    mesh = api.DeviceMesh.upload(v, f, ctx)
+    fn = D.gpu_slab_fn(mesh, R)
+
+    def step():
+        halo, full = D.distributed_sdf(fn, R, rank, world, dist if world > 1 else None)
+        out_faces = 0
+        if rank == 0:
+            g = api.DeviceGrid.from_device(full.data_ptr(), R, ctx)
+            m = api.extract(g)
+            out_faces = m.size()[1]
+            m.free()
+            g.free()
+        return out_faces
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    total = 0.0
+    nf = 0
+    for _ in range(args.steps):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        nf = step()
+        ev1.record()
+        torch.cuda.synchronize()
+        total += ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    max_ms = _max_over_ranks(torch, dist, world, total)
+    if rank == 0:
+        n1 = (R + 1) ** 3
+        line = {"metric": "UDF+DMC ms per mesh (C4 z-slab)", "value": round(max_ms / args.steps, 3), "unit": "ms/mesh",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C4", "faces_in": int(len(f)), "R": R, "dmc_faces": int(nf),
+                           "parallelism": f"z-slabs x{world} + NCCL halo/gather"},
+                "udf_voxels_per_s": round(n1 / (max_ms / args.steps * 1e-3), 1), "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    mesh.free()
+    ctx.close()
+    _ = stream
+    return 0
+
+
+def run_c5(args):
+    """C5: a batch of mixed meshes, LPT-assigned one-per-GPU (no collective on the data path).
+    Weak-ish scaling: the batch is fixed, value = whole-job ms per mesh (makespan / meshes)."""
+    torch, dist, rank, world, local = _dist_setup()
+    from paper_2509_05595_b200 import api, fixtures as FX
+    from paper_2509_05595_b200 import distributed as D
+    meshes = FX.c5_batch(args.batch)
+    ctx = api.Context(local)
+    mine = D.lpt_assign([len(m[1]) for m in meshes], world)[rank]
+    dev = {i: api.DeviceMesh.upload(meshes[i][0], meshes[i][1], ctx) for i in mine}
+
+    def step():
+        for i in mine:
+            _, _, R, target = meshes[i]
+            out, st, tm = api.remesh_device(dev[i], R, target)
+            out.free()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total = 0.0
+    for _ in range(args.steps):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record()
+        step()
+        ev1.record()
+        torch.cuda.synchronize()
+        total += ev0.elapsed_time(ev1)
+    max_ms = _max_over_ranks(torch, dist, world, total)
+    if rank == 0:
+        line = {"metric": "end-to-end remesh ms per mesh (C5 batch makespan / meshes)",
+                "value": round(max_ms / args.steps / len(meshes), 3), "unit": "ms/mesh", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": "C5", "meshes": len(meshes), "faces_in_total": int(sum(len(m[1]) for m in meshes)),
+                           "parallelism": f"LPT one-mesh-per-GPU x{world}",
+                           "lpt_makespan_ratio": round(D.makespan([len(m[1]) for m in meshes], world), 3)}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    for m in dev.values():
+        m.free()
+    ctx.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--batch", type=int, default=64, help="C5 batch size")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     args = ap.parse_args()
     if args.impl == "reference":
+        if args.config in ("c4", "c5"):
+            print(json.dumps({"impl": "reference", "unavailable": "CPU arm is defined for the C1-C3 single-mesh "
+                              "configs only"}))
+            return 0
         return run_reference(args)
+    if args.config == "c4":
+        return run_c4(args)
+    if args.config == "c5":
+        return run_c5(args)
     return run_ours(args)
 
 

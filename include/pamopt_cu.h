@@ -102,6 +102,13 @@ int pamopt_cu_udf_to_sdf(pamopt_cu_grid grid, double eps);
 /* fused compute_udf + udf_to_sdf (the pipeline path) */
 int pamopt_cu_compute_sdf(pamopt_cu_ctx ctx, pamopt_cu_mesh mesh, int32_t R, double eps,
                           pamopt_cu_grid* out);
+/* z-slab of the SDF lattice: planes [z0, z1) only (multi-GPU slab decomposition) */
+int pamopt_cu_compute_sdf_slab(pamopt_cu_ctx ctx, pamopt_cu_mesh mesh, int32_t R, double eps, int32_t z0,
+                               int32_t z1, pamopt_cu_grid* out);
+int pamopt_cu_grid_slab(pamopt_cu_grid grid, int32_t* z0, int32_t* z1);
+/* device-to-device exchange with caller buffers (NCCL halo exchange / gather) */
+int pamopt_cu_grid_copy_to_device(pamopt_cu_grid grid, void* dst);
+int pamopt_cu_grid_from_device(pamopt_cu_ctx ctx, int32_t R, const float* src, pamopt_cu_grid* out);
 int pamopt_cu_grid_upload(pamopt_cu_ctx ctx, int32_t R, const float* samples, pamopt_cu_grid* out);
 int pamopt_cu_grid_resolution(pamopt_cu_grid grid, int32_t* R);
 int pamopt_cu_grid_download(pamopt_cu_grid grid, float* samples);

@@ -74,6 +74,10 @@ _SIGS = {
     "pamopt_cu_compute_udf": (C.c_int, [vp, vp, i32, P(vp)]),
     "pamopt_cu_udf_to_sdf": (C.c_int, [vp, dbl]),
     "pamopt_cu_compute_sdf": (C.c_int, [vp, vp, i32, dbl, P(vp)]),
+    "pamopt_cu_compute_sdf_slab": (C.c_int, [vp, vp, i32, dbl, i32, i32, P(vp)]),
+    "pamopt_cu_grid_slab": (C.c_int, [vp, P(i32), P(i32)]),
+    "pamopt_cu_grid_copy_to_device": (C.c_int, [vp, vp]),
+    "pamopt_cu_grid_from_device": (C.c_int, [vp, i32, vp, P(vp)]),
     "pamopt_cu_grid_upload": (C.c_int, [vp, i32, vp, P(vp)]),
     "pamopt_cu_grid_resolution": (C.c_int, [vp, P(i32)]),
     "pamopt_cu_grid_download": (C.c_int, [vp, vp]),

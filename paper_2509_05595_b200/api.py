@@ -115,12 +115,31 @@ class DeviceMesh:
 
 
 class DeviceGrid:
-    """Device-resident ScalarGrid ((R+1)^3 f32, x-fastest)."""
+    """Device-resident ScalarGrid ((R+1)^3 f32, x-fastest), or a z-slab of it
+    (lattice planes [z0, z1))."""
 
     def __init__(self, handle, ctx: Context, R: int):
         self.h = handle
         self.ctx = ctx
         self.R = R
+        z0, z1 = C.c_int32(), C.c_int32()
+        check(lib().pamopt_cu_grid_slab(handle, C.byref(z0), C.byref(z1)))
+        self.z0, self.z1 = z0.value, z1.value
+
+    @property
+    def planes(self) -> int:
+        return self.z1 - self.z0
+
+    @classmethod
+    def from_device(cls, ptr: int, R: int, ctx: Context | None = None) -> "DeviceGrid":
+        """Full (R+1)^3 grid copied from a device buffer (e.g. a torch tensor's data_ptr)."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib().pamopt_cu_grid_from_device(ctx.h, int(R), C.c_void_p(ptr), C.byref(h)))
+        return cls(h, ctx, R)
+
+    def copy_to_device(self, ptr: int) -> None:
+        check(lib().pamopt_cu_grid_copy_to_device(self.h, C.c_void_p(ptr)))
 
     @classmethod
     def upload(cls, samples, R: int, ctx: Context | None = None) -> "DeviceGrid":
@@ -132,7 +151,7 @@ class DeviceGrid:
         return cls(h, ctx, R)
 
     def download(self) -> np.ndarray:
-        out = np.empty((self.R + 1) ** 3, np.float32)
+        out = np.empty((self.R + 1) ** 2 * self.planes, np.float32)
         check(lib().pamopt_cu_grid_download(self.h, ptr(out)))
         return out
 
@@ -175,6 +194,16 @@ def compute_sdf(mesh, R: int, eps: float | None = None, ctx: Context | None = No
     h = C.c_void_p()
     check(lib().pamopt_cu_compute_sdf(m.ctx.h, m.h, int(R), default_eps(R) if eps is None else float(eps),
                                       C.byref(h)))
+    return DeviceGrid(h, m.ctx, R)
+
+
+def compute_sdf_slab(mesh, R: int, z0: int, z1: int, eps: float | None = None,
+                     ctx: Context | None = None) -> DeviceGrid:
+    """SDF lattice planes [z0, z1) only — one rank's share of the z-slab decomposition."""
+    m = _mesh(mesh, ctx)
+    h = C.c_void_p()
+    check(lib().pamopt_cu_compute_sdf_slab(m.ctx.h, m.h, int(R), default_eps(R) if eps is None else float(eps),
+                                           int(z0), int(z1), C.byref(h)))
     return DeviceGrid(h, m.ctx, R)
 
 

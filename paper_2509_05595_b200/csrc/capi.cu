@@ -42,6 +42,7 @@ struct pamopt_cu_mesh_s {
 struct pamopt_cu_grid_s {
   pamopt_cu_ctx owner;
   int32_t R = 0;
+  int32_t z0 = 0, z1 = 0;  // lattice planes [z0, z1) held (a z-slab, or the whole grid)
   pcu::DevBuf<float> g;
   pcu::DmcResult last;  // debug view of the last extract
 };
@@ -223,7 +224,8 @@ static void check_R(int32_t R) {
   PCU_REQUIRE(R >= 8 && R <= 2048 && (R & (R - 1)) == 0, PAMOPT_CU_EINVAL, "R must be a power of two in [8, 2048]");
 }
 
-static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, double eps, pamopt_cu_grid* out) {
+static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, double eps, pamopt_cu_grid* out,
+                     int32_t z0 = 0, int32_t z1 = -1) {
   return guarded([&] {
     check_ctx(c);
     PCU_REQUIRE(m && out, PAMOPT_CU_EINVAL, "null argument");
@@ -233,14 +235,18 @@ static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, dou
       PCU_REQUIRE(eps >= lo && eps <= hi, PAMOPT_CU_EINVAL, "udf_to_sdf: epsilon out of range");
     }
     pcu::DeviceGuard g(c->ctx.device);
+    if (z1 < 0) z1 = R + 1;
+    PCU_REQUIRE(z0 >= 0 && z0 < z1 && z1 <= R + 1, PAMOPT_CU_EINVAL, "bad slab plane range");
     auto* gr = new pamopt_cu_grid_s();
     gr->owner = c;
     ++c->refs;
     gr->R = R;
+    gr->z0 = z0;
+    gr->z1 = z1;
     const int64_t n1 = R + 1;
-    gr->g.alloc(n1 * n1 * n1, c->ctx.stream);
+    gr->g.alloc(n1 * n1 * (z1 - z0), c->ctx.stream);
     try {
-      pcu::udf_run(c->ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, mode, eps, gr->g.get());
+      pcu::udf_run(c->ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, mode, eps, gr->g.get(), z0, z1);
     } catch (...) {
       delete gr;
       ctx_unref(c);
@@ -258,6 +264,49 @@ int pamopt_cu_compute_sdf(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, double e
   return make_grid(c, m, R, 1, eps, out);
 }
 
+int pamopt_cu_compute_sdf_slab(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, double eps, int32_t z0, int32_t z1,
+                               pamopt_cu_grid* out) {
+  return make_grid(c, m, R, 1, eps, out, z0, z1);
+}
+
+int pamopt_cu_grid_slab(pamopt_cu_grid gr, int32_t* z0, int32_t* z1) {
+  return guarded([&] {
+    PCU_REQUIRE(gr != nullptr, PAMOPT_CU_EINVAL, "null grid");
+    if (z0) *z0 = gr->z0;
+    if (z1) *z1 = gr->z1;
+  });
+}
+
+int pamopt_cu_grid_copy_to_device(pamopt_cu_grid gr, void* dst) {
+  return guarded([&] {
+    PCU_REQUIRE(gr && dst, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    const int64_t n1 = gr->R + 1;
+    PCU_CUDA(cudaMemcpyAsync(dst, gr->g.get(), n1 * n1 * (gr->z1 - gr->z0) * sizeof(float), cudaMemcpyDeviceToDevice,
+                             ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+int pamopt_cu_grid_from_device(pamopt_cu_ctx c, int32_t R, const float* src, pamopt_cu_grid* out) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(R >= 8 && R <= 2048 && (R & (R - 1)) == 0 && src && out, PAMOPT_CU_EINVAL, "bad arguments");
+    pcu::DeviceGuard g(c->ctx.device);
+    auto* gr = new pamopt_cu_grid_s();
+    gr->owner = c;
+    ++c->refs;
+    gr->R = R;
+    gr->z0 = 0;
+    gr->z1 = R + 1;
+    const int64_t n1 = R + 1;
+    gr->g.alloc(n1 * n1 * n1, c->ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(gr->g.get(), src, n1 * n1 * n1 * sizeof(float), cudaMemcpyDeviceToDevice, c->ctx.stream));
+    *out = gr;
+  });
+}
+
 int pamopt_cu_udf_to_sdf(pamopt_cu_grid gr, double eps) {
   return guarded([&] {
     PCU_REQUIRE(gr != nullptr, PAMOPT_CU_EINVAL, "null grid");
@@ -267,7 +316,7 @@ int pamopt_cu_udf_to_sdf(pamopt_cu_grid gr, double eps) {
     pcu::Ctx& ctx = gr->owner->ctx;
     pcu::DeviceGuard g(ctx.device);
     const int64_t n1 = R + 1;
-    pcu::udf_to_sdf_inplace(ctx, gr->g.get(), n1 * n1 * n1, eps);
+    pcu::udf_to_sdf_inplace(ctx, gr->g.get(), n1 * n1 * (gr->z1 - gr->z0), eps);
   });
 }
 
@@ -281,6 +330,8 @@ int pamopt_cu_grid_upload(pamopt_cu_ctx c, int32_t R, const float* samples, pamo
     gr->owner = c;
     ++c->refs;
     gr->R = R;
+    gr->z0 = 0;
+    gr->z1 = R + 1;
     const int64_t n1 = R + 1;
     gr->g.alloc(n1 * n1 * n1, c->ctx.stream);
     PCU_CUDA(cudaMemcpyAsync(gr->g.get(), samples, n1 * n1 * n1 * sizeof(float), cudaMemcpyHostToDevice, c->ctx.stream));
@@ -301,7 +352,8 @@ int pamopt_cu_grid_download(pamopt_cu_grid gr, float* samples) {
     pcu::Ctx& ctx = gr->owner->ctx;
     pcu::DeviceGuard g(ctx.device);
     const int64_t n1 = gr->R + 1;
-    PCU_CUDA(cudaMemcpyAsync(samples, gr->g.get(), n1 * n1 * n1 * sizeof(float), cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaMemcpyAsync(samples, gr->g.get(), n1 * n1 * (gr->z1 - gr->z0) * sizeof(float), cudaMemcpyDeviceToHost,
+                             ctx.stream));
     PCU_CUDA(cudaStreamSynchronize(ctx.stream));
   });
 }
@@ -335,6 +387,7 @@ int pamopt_cu_dmc_extract(pamopt_cu_grid gr, double beta, pamopt_cu_mesh* out) {
   return guarded([&] {
     PCU_REQUIRE(gr && out, PAMOPT_CU_EINVAL, "null argument");
     PCU_REQUIRE(beta > 0.0, PAMOPT_CU_EINVAL, "beta must be positive");
+    PCU_REQUIRE(gr->z0 == 0 && gr->z1 == gr->R + 1, PAMOPT_CU_EINVAL, "extract: the grid is a z-slab; assemble it first");
     pcu::Ctx& ctx = gr->owner->ctx;
     pcu::DeviceGuard g(ctx.device);
     gr->last = pcu::DmcResult();

@@ -10,8 +10,9 @@ namespace pcu {
 
 // ---- stage 1a (udf.cu)
 // mode 0: UDF (+INF sentinel); mode 1: fused SDF (u - eps, sentinel +1.0)
+// z-slab: only lattice planes [z0, z1) are computed and written (z1 < 0: the whole grid)
 void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf, int R, int mode, double eps,
-             float* d_out);
+             float* d_out, int z0 = 0, int z1 = -1);
 void udf_to_sdf_inplace(Ctx& ctx, float* g, int64_t n, double eps);
 std::vector<int64_t> hierarchy_pairs(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf, int R, int r);
 

@@ -144,8 +144,15 @@ __device__ __forceinline__ void append(bool keep, uint64_t val, uint64_t* out, u
   }
 }
 
+// slab pruning: a level-r cell z covers lattice planes [z*R/r, (z+1)*R/r]; cells that touch no
+// plane of the slab [zp0, zp1] cannot change any slab sample and are not emitted
+__device__ __forceinline__ bool in_slab(int zc, int R, int r, int zp0, int zp1) {
+  const int s = R / r;
+  return zc * s <= zp1 && (zc + 1) * s >= zp0;
+}
+
 __global__ void k_level0(const TriD* __restrict__ T, int64_t nf, int R, uint64_t* out,
-                         unsigned long long* cnt, uint64_t cap) {
+                         unsigned long long* cnt, uint64_t cap, int zp0, int zp1) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const bool active = i < nf;
   TriD t;
@@ -170,7 +177,7 @@ __global__ void k_level0(const TriD* __restrict__ T, int64_t nf, int R, uint64_t
     uint64_t val = 0;
     if (j < n) {
       const int x = lo[0] + j % nx, y = lo[1] + (j / nx) % ny, z = lo[2] + j / (nx * ny);
-      keep = survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, thr);
+      keep = in_slab(z, R, r, zp0, zp1) && survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, thr);
       val = (static_cast<uint64_t>(x + r * (y + r * z)) << 32) | static_cast<uint64_t>(i);
     }
     append(keep, val, out, cnt, cap);
@@ -178,7 +185,7 @@ __global__ void k_level0(const TriD* __restrict__ T, int64_t nf, int R, uint64_t
 }
 
 __global__ void k_refine(const uint64_t* __restrict__ in, uint64_t n_in, const TriD* __restrict__ T,
-                         int R, int r, uint64_t* out, unsigned long long* cnt, uint64_t cap) {
+                         int R, int r, uint64_t* out, unsigned long long* cnt, uint64_t cap, int zp0, int zp1) {
   const uint64_t gid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   bool keep = false;
   uint64_t val = 0;
@@ -190,7 +197,7 @@ __global__ void k_refine(const uint64_t* __restrict__ in, uint64_t n_in, const T
     const int px = pc % rp, py = (pc / rp) % rp, pz = pc / (rp * rp);
     const int x = 2 * px + (ch & 1), y = 2 * py + ((ch >> 1) & 1), z = 2 * pz + ((ch >> 2) & 1);
     const TriD t = T[tri];
-    keep = survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, level_thr(R, r));
+    keep = in_slab(z, R, r, zp0, zp1) && survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, level_thr(R, r));
     val = (static_cast<uint64_t>(x + r * (y + r * z)) << 32) | tri;
   }
   append(keep, val, out, cnt, cap);
@@ -371,13 +378,13 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
 
 // mode 0: UDF (+INF sentinel); mode 1: SDF (u - eps, sentinel +1.0)
 __global__ void k_finalize(const unsigned long long* __restrict__ blocks, const int32_t* __restrict__ bmap, int R,
-                           int rb, int bs, int mode, double eps, float* __restrict__ out) {
+                           int rb, int bs, int mode, double eps, float* __restrict__ out, int z0, int z1) {
   const int64_t n1 = R + 1;
-  const int64_t total = n1 * n1 * n1;
+  const int64_t total = n1 * n1 * (z1 - z0);
   const int nv1 = bs + 1;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int x = static_cast<int>(i % n1), y = static_cast<int>((i / n1) % n1), z = static_cast<int>(i / (n1 * n1));
+    const int x = static_cast<int>(i % n1), y = static_cast<int>((i / n1) % n1), z = z0 + static_cast<int>(i / (n1 * n1));
     int bxs[2], bys[2], bzs[2], nbx = 0, nby = 0, nbz = 0;
     if (x / bs < rb) bxs[nbx++] = x / bs;
     if (x % bs == 0 && x > 0) bxs[nbx++] = x / bs - 1;
@@ -454,7 +461,7 @@ int ilog2(int x) {
 // Runs levels 8..r_b; returns the brick-level pairs (and the pairs of `keep_level` if >= 0).
 static DevBuf<uint64_t> hierarchy_to_bricks(Ctx& ctx, const TriD* T, int64_t nf, int R, int rb,
                                             uint64_t& n_out, int keep_r, DevBuf<uint64_t>* kept,
-                                            uint64_t* kept_n) {
+                                            uint64_t* kept_n, int zp0 = 0, int zp1 = 1 << 30) {
   DevBuf<unsigned long long> cnt(1, ctx.stream);
   uint64_t cap = static_cast<uint64_t>(nf) * 16 + (1 << 16);
   DevBuf<uint64_t> cur;
@@ -464,10 +471,10 @@ static DevBuf<uint64_t> hierarchy_to_bricks(Ctx& ctx, const TriD* T, int64_t nf,
       DevBuf<uint64_t> out(cap, ctx.stream);
       cnt.memset(0, ctx.stream);
       if (r == 8) {
-        PCU_LAUNCH(ctx, k_level0, grid_for(nf, 128), 128, 0, T, nf, R, out.get(), cnt.get(), cap);
+        PCU_LAUNCH(ctx, k_level0, grid_for(nf, 128), 128, 0, T, nf, R, out.get(), cnt.get(), cap, zp0, zp1);
       } else {
         PCU_LAUNCH(ctx, k_refine, grid_for(static_cast<int64_t>(n * 8), 256), 256, 0, cur.get(), n, T, R, r,
-                   out.get(), cnt.get(), cap);
+                   out.get(), cnt.get(), cap, zp0, zp1);
       }
       const uint64_t got = read_scalar(ctx, cnt.get());
       if (got > cap) {
@@ -490,7 +497,9 @@ static DevBuf<uint64_t> hierarchy_to_bricks(Ctx& ctx, const TriD* T, int64_t nf,
 }
 
 void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf, int R, int mode, double eps,
-             float* d_out) {
+             float* d_out, int z0, int z1) {
+  if (z1 < 0) z1 = R + 1;
+  PCU_REQUIRE(z0 >= 0 && z0 < z1 && z1 <= R + 1, PAMOPT_CU_EINVAL, "compute_udf: bad slab plane range");
   (void)nv;
   PCU_REQUIRE(R >= 8 && (R & (R - 1)) == 0 && R <= 2048, PAMOPT_CU_EINVAL, "compute_udf: R must be a power of two in [8, 2048]");
   const int rb = R >= 64 ? R / 8 : 8;
@@ -498,13 +507,14 @@ void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t 
   const int64_t n1 = R + 1;
   const int64_t nvert = n1 * n1 * n1;
   if (nf == 0) {
-    PCU_LAUNCH(ctx, k_finalize, static_cast<unsigned>(ctx.num_sms * 8), 256, 0, nullptr, nullptr, R, rb, bs, mode, eps, d_out);
+    PCU_LAUNCH(ctx, k_finalize, static_cast<unsigned>(ctx.num_sms * 8), 256, 0, nullptr, nullptr, R, rb, bs, mode, eps, d_out,
+               z0, z1);
     return;
   }
   DevBuf<TriD> T(nf, ctx.stream);
   PCU_LAUNCH(ctx, k_prep, grid_for(nf, 256), 256, 0, dV, dF, nf, T.get());
   uint64_t npairs = 0;
-  DevBuf<uint64_t> bp = hierarchy_to_bricks(ctx, T.get(), nf, R, rb, npairs, -1, nullptr, nullptr);
+  DevBuf<uint64_t> bp = hierarchy_to_bricks(ctx, T.get(), nf, R, rb, npairs, -1, nullptr, nullptr, z0, z1 - 1);
   const int64_t nb = static_cast<int64_t>(rb) * rb * rb;
   DevBuf<uint32_t> bcnt(nb, ctx.stream), boff(nb, ctx.stream), bcur(nb, ctx.stream);
   DevBuf<uint32_t> nitems(nb, ctx.stream), item_off(nb, ctx.stream), isact(nb, ctx.stream), act_off(nb, ctx.stream);
@@ -537,7 +547,7 @@ void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t 
     PCU_LAUNCH(ctx, k_brick, n_items, 256, 0, items.get(), tris.get(), T.get(), R, rb, bs, J, blocks.get());
   }
   PCU_LAUNCH(ctx, k_finalize, static_cast<unsigned>(ctx.num_sms * 16), 256, 0, blocks.get(), bmap.get(), R, rb, bs,
-             mode, eps, d_out);
+             mode, eps, d_out, z0, z1);
   (void)nvert;
 }
 
