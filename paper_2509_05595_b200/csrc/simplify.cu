@@ -261,11 +261,12 @@ __global__ void k_cost(const double* __restrict__ X, const int32_t* __restrict__
   bool ok = det != 0.0;
   D3 x{0.0, 0.0, 0.0};
   if (ok) {
-    const double i00 = (m11 * m22 - m12 * m21) / det, i01 = (m02 * m21 - m01 * m22) / det,
-                 i02 = (m01 * m12 - m02 * m11) / det, i10 = (m12 * m20 - m10 * m22) / det,
-                 i11 = (m00 * m22 - m02 * m20) / det, i12 = (m02 * m10 - m00 * m12) / det,
-                 i20 = (m10 * m21 - m11 * m20) / det, i21 = (m01 * m20 - m00 * m21) / det,
-                 i22 = (m00 * m11 - m01 * m10) / det;
+    const double rdet = 1.0 / det;  // adjugate * (1/det)
+    const double i00 = (m11 * m22 - m12 * m21) * rdet, i01 = (m02 * m21 - m01 * m22) * rdet,
+                 i02 = (m01 * m12 - m02 * m11) * rdet, i10 = (m12 * m20 - m10 * m22) * rdet,
+                 i11 = (m00 * m22 - m02 * m20) * rdet, i12 = (m02 * m10 - m00 * m12) * rdet,
+                 i20 = (m10 * m21 - m11 * m20) * rdet, i21 = (m01 * m20 - m00 * m21) * rdet,
+                 i22 = (m00 * m11 - m01 * m10) * rdet;
     const double nA = fmax(fmax((fabs(m00) + fabs(m10)) + fabs(m20), (fabs(m01) + fabs(m11)) + fabs(m21)),
                            (fabs(m02) + fabs(m12)) + fabs(m22));
     const double nI = fmax(fmax((fabs(i00) + fabs(i10)) + fabs(i20), (fabs(i01) + fabs(i11)) + fabs(i21)),

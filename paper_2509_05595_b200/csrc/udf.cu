@@ -34,40 +34,42 @@ constexpr int kChunk = 128;  // triangles per brick work item
 struct __align__(16) TriD {
   double a[3], b[3], c[3], lo[3], hi[3];
   float ab[3], ac[3];  // local frame (b-a, c-a computed in FP64, rounded to FP32)
+  float n[3];          // unit normal (FP32)
+  float binv[3];       // inverse Gram matrix of (ab, ac): [g11, -g01, g00] / det
+  float blo[3], bhi[3];  // AABB in the local frame (FP32)
   float L2;            // max squared edge length
   int wc;              // well conditioned: every corner angle has sin^2 >= 0.01
 };
 
 // FP32 point-triangle squared distance in the triangle's local frame (p relative to a).
-// Used only as a certified filter for well-conditioned triangles (see survives / k_brick):
-// its error is far below the 1e-4 * L^2 margin, so every decision it takes equals the FP64
-// decision; everything near a threshold is re-evaluated in FP64.
+// Used only as a certified filter for well-conditioned triangles (see survives / k_brick): its
+// error is far below the 1e-4 * L^2 + 1e-3 * d^2 margin, so every decision it takes equals the
+// FP64 decision; everything near a threshold is re-evaluated with the pinned FP64 routine.
+// (Explicit FMAs and approximate reciprocals: the file is built with --fmad=false for the FP64
+// parity arithmetic, but this filter only needs an error bound.)
+__device__ __forceinline__ float fdot(float ax, float ay, float az, float bx, float by, float bz) {
+  return __fmaf_rn(ax, bx, __fmaf_rn(ay, by, __fmul_rn(az, bz)));
+}
 __device__ __forceinline__ float fseg_sq(float px, float py, float pz, float ax, float ay, float az, float bx, float by,
                                          float bz) {
   const float ux = bx - ax, uy = by - ay, uz = bz - az;
-  const float den = ux * ux + uy * uy + uz * uz;
-  float t = den > 0.f ? ((px - ax) * ux + (py - ay) * uy + (pz - az) * uz) / den : 0.f;
+  const float wx = px - ax, wy = py - ay, wz = pz - az;
+  const float den = fdot(ux, uy, uz, ux, uy, uz);
+  float t = den > 0.f ? __fdividef(fdot(wx, wy, wz, ux, uy, uz), den) : 0.f;
   t = fminf(fmaxf(t, 0.f), 1.f);
-  const float qx = px - (ax + t * ux), qy = py - (ay + t * uy), qz = pz - (az + t * uz);
-  return qx * qx + qy * qy + qz * qz;
+  const float qx = __fmaf_rn(-t, ux, wx), qy = __fmaf_rn(-t, uy, wy), qz = __fmaf_rn(-t, uz, wz);
+  return fdot(qx, qy, qz, qx, qy, qz);
 }
 __device__ __forceinline__ float fptri_sq(const TriD& t, float px, float py, float pz) {
   const float bx = t.ab[0], by = t.ab[1], bz = t.ab[2], cx = t.ac[0], cy = t.ac[1], cz = t.ac[2];
-  const float nx = by * cz - bz * cy, ny = bz * cx - bx * cz, nz = bx * cy - by * cx;
-  const float nn = nx * nx + ny * ny + nz * nz;
   float best = __int_as_float(0x7f800000);
-  if (nn > 0.f) {
-    const float dn = px * nx + py * ny + pz * nz;
-    const float s = dn / nn;
-    const float qx = px - s * nx, qy = py - s * ny, qz = pz - s * nz;
-    const float d00 = bx * bx + by * by + bz * bz, d01 = bx * cx + by * cy + bz * cz, d11 = cx * cx + cy * cy + cz * cz;
-    const float d20 = qx * bx + qy * by + qz * bz, d21 = qx * cx + qy * cy + qz * cz;
-    const float den = d00 * d11 - d01 * d01;
-    if (den > 0.f) {
-      const float v = (d11 * d20 - d01 * d21) / den, w = (d00 * d21 - d01 * d20) / den;
-      if (v >= 0.f && w >= 0.f && v + w <= 1.f) best = dn * s;
-    }
-  }
+  // plane term with the precomputed unit normal: dn = p.n^, projection q = p - dn n^
+  const float nx = t.n[0], ny = t.n[1], nz = t.n[2];
+  const float dn = fdot(px, py, pz, nx, ny, nz);
+  const float qx = __fmaf_rn(-dn, nx, px), qy = __fmaf_rn(-dn, ny, py), qz = __fmaf_rn(-dn, nz, pz);
+  const float d20 = fdot(qx, qy, qz, bx, by, bz), d21 = fdot(qx, qy, qz, cx, cy, cz);
+  const float v = __fmaf_rn(t.binv[0], d20, t.binv[1] * d21), w = __fmaf_rn(t.binv[1], d20, t.binv[2] * d21);
+  if (v >= 0.f && w >= 0.f && v + w <= 1.f) best = dn * dn;
   best = fminf(best, fseg_sq(px, py, pz, 0.f, 0.f, 0.f, bx, by, bz));
   best = fminf(best, fseg_sq(px, py, pz, bx, by, bz, cx, cy, cz));
   best = fminf(best, fseg_sq(px, py, pz, cx, cy, cz, 0.f, 0.f, 0.f));
@@ -120,7 +122,23 @@ __global__ void k_prep(const double* __restrict__ V, const int32_t* __restrict__
   }
   const double lab = sqn(ab), lac = sqn(ac), lbc = sqn(bc);
   t.L2 = static_cast<float>(fmax(fmax(lab, lac), lbc));
-  const double n2 = sqn(cross(ab, ac));
+  const D3 nv = cross(ab, ac);
+  const double n2 = sqn(nv);
+  {
+    const double inv = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;
+    t.n[0] = static_cast<float>(nv.x * inv);
+    t.n[1] = static_cast<float>(nv.y * inv);
+    t.n[2] = static_cast<float>(nv.z * inv);
+    const double g00 = lab, g01 = dot(ab, ac), g11 = lac, gd = g00 * g11 - g01 * g01;
+    const double gi = gd > 0.0 ? 1.0 / gd : 0.0;
+    t.binv[0] = static_cast<float>(g11 * gi);
+    t.binv[1] = static_cast<float>(-g01 * gi);
+    t.binv[2] = static_cast<float>(g00 * gi);
+    for (int k = 0; k < 3; ++k) {
+      t.blo[k] = static_cast<float>(t.lo[k] - t.a[k]);
+      t.bhi[k] = static_cast<float>(t.hi[k] - t.a[k]);
+    }
+  }
   // sin^2 of the three corner angles: |n|^2 / (|e1|^2 |e2|^2)
   const bool wc = lab > 0.0 && lac > 0.0 && lbc > 0.0 && n2 >= 0.01 * lab * lac && n2 >= 0.01 * lab * lbc &&
                   n2 >= 0.01 * lac * lbc;
@@ -260,14 +278,21 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
   __shared__ uint16_t list[8][2][512];    // ping-pong survivor lists (local cell index at level j)
   __shared__ uint16_t vlist[8][729];      // needed vertices, packed x | y<<4 | z<<8
   __shared__ TriD tsh[8];
+  __shared__ unsigned next_tri;  // dynamic triangle distribution among the warps (load balance)
   const Item it = items[blockIdx.x];
+  if (threadIdx.x == 0) next_tri = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nv1 = bs + 1, nvb = nv1 * nv1 * nv1;
   for (int v = threadIdx.x; v < nvb; v += blockDim.x) vmin[v] = ~0ull;
   __syncthreads();
   const int bx = it.brick % rb, by = (it.brick / rb) % rb, bz = it.brick / (rb * rb);
   const unsigned lt = (1u << lane) - 1u;
-  for (uint32_t k = it.begin + warp; k < it.end; k += 8) {
+  for (;;) {
+    unsigned kk = 0;
+    if (lane == 0) kk = atomicAdd(&next_tri, 1u);
+    kk = __shfl_sync(0xffffffffu, kk, 0);
+    const uint32_t k = it.begin + kk;
+    if (k >= it.end) break;
     if (lane == 0) tsh[warp] = T[tris[k]];
     __syncwarp();
     const TriD& t = tsh[warp];
@@ -357,13 +382,20 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
       const D3 p{static_cast<double>(gx) / R, static_cast<double>(gy) / R, static_cast<double>(gz) / R};
       if (t.wc) {
         // this triangle cannot lower the vertex's running minimum: skip the FP64 evaluation
-        // (the minimum is order independent, so skipping never changes the result)
+        // (the minimum is order independent, so skipping never changes the result).  Cheap
+        // lower bounds first (plane distance, box distance), then the FP32 distance.
         const double curm = __longlong_as_double(static_cast<long long>(vmin[v]));  // NaN while unset
         const float px = static_cast<float>(p.x - t.a[0]), py = static_cast<float>(p.y - t.a[1]),
                     pz = static_cast<float>(p.z - t.a[2]);
-        const float d2f = fptri_sq(t, px, py, pz);
-        const float L2 = fmaxf(t.L2, px * px + py * py + pz * pz);
-        if (static_cast<double>(d2f) - 1e-4 * static_cast<double>(L2) > curm * (1.0 + 1e-3)) continue;
+        const float L2 = fmaxf(t.L2, fdot(px, py, pz, px, py, pz));
+        const float skip = __fmaf_rn(1e-4f, L2, static_cast<float>(curm * (1.0 + 1e-3)));  // NaN: never skip
+        const float dn = fdot(px, py, pz, t.n[0], t.n[1], t.n[2]);
+        if (dn * dn > skip) continue;
+        const float ex = fmaxf(fmaxf(t.blo[0] - px, px - t.bhi[0]), 0.f),
+                    ey = fmaxf(fmaxf(t.blo[1] - py, py - t.bhi[1]), 0.f),
+                    ez = fmaxf(fmaxf(t.blo[2] - pz, pz - t.bhi[2]), 0.f);
+        if (fdot(ex, ey, ez, ex, ey, ez) > skip) continue;
+        if (fptri_sq(t, px, py, pz) > skip) continue;
       }
       const double d2 = ptri_sq(p, A, Bv, Cv);
       atomicMin(&vmin[v], static_cast<unsigned long long>(__double_as_longlong(d2)));
