@@ -293,10 +293,17 @@ def run_ours(args):
         dmc_bytes = 4 * n1 + 12 * tm["dmc_vertices"] + 12 * tm["dmc_faces"]
         qem_bytes = st["alg_bytes"]
 
-        def roof(bytes_, ms):
+        def roof(bytes_, ms, traffic=None):
             ach = bytes_ / (ms * 1e-3) / 1e9
             return {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
-                    "frac": round(ach / hbm, 5), "traffic": None, "alg_bytes": int(bytes_), "ms": round(ms, 3)}
+                    "frac": round(ach / hbm, 5), "traffic": traffic, "alg_bytes": int(bytes_), "ms": round(ms, 3)}
+
+        # DRAM bytes of the UDF stage's kernels from the committed ncu capture of the same config
+        udf_traffic = None
+        tp = os.path.join(ROOT, "profiles", f"r01_udf_traffic_{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as fh:
+                udf_traffic = json.load(fh).get("dram_bytes")
 
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -317,8 +324,8 @@ def run_ours(args):
                        "dmc_faces": int(tm["dmc_faces"]), "faces_out": int(nf), "qem_iterations": st["iterations"],
                        "parallelism": f"replicas x{world} (one mesh per GPU)",
                        "l2": "flushed (256 MB write) before every timed step"},
-            "roofline": roof(udf_bytes, udf_ms),
-            "stages": {"udf": roof(udf_bytes, udf_ms), "dmc": roof(dmc_bytes, dmc_ms), "qem": roof(qem_bytes, qem_ms),
+            "roofline": roof(udf_bytes, udf_ms, udf_traffic),
+            "stages": {"udf": roof(udf_bytes, udf_ms, udf_traffic), "dmc": roof(dmc_bytes, dmc_ms), "qem": roof(qem_bytes, qem_ms),
                        "udf_voxels_per_s": round(n1 / (udf_ms * 1e-3), 1),
                        "undo_hist": st["undo_hist"][:4]},
             "peak_source": peak_kind,
