@@ -623,6 +623,35 @@ __global__ void k_compact(const double* __restrict__ X, const int32_t* __restric
     for (int k = 0; k < 3; ++k) Fo[3 * fmap[i] + k] = static_cast<int32_t>(vmap[F[3 * i + k]]);
 }
 
+// Mid-run compaction: drop dead faces/vertices, renumbering both order-preservingly. Edge ids
+// (lexicographic ranks over alive edges), incidence order, collapse direction (a < b) and the
+// invalid-pair order are all invariant under a monotone renumbering, so results are unchanged.
+__global__ void k_compact_state(const double* __restrict__ X, const double* __restrict__ Q,
+                                const int32_t* __restrict__ F, int64_t nv, int64_t nf,
+                                const uint32_t* __restrict__ vkeep, const uint32_t* __restrict__ vmap,
+                                const uint32_t* __restrict__ fkeep, const uint32_t* __restrict__ fmap,
+                                double* __restrict__ Xo, double* __restrict__ Qo, int32_t* __restrict__ Fo) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < nv && vkeep[i]) {
+    const uint32_t j = vmap[i];
+    for (int k = 0; k < 3; ++k) Xo[3 * j + k] = X[3 * i + k];
+    for (int k = 0; k < 10; ++k) Qo[10 * j + k] = Q[10 * i + k];
+  }
+  if (i < nf && fkeep[i])
+    for (int k = 0; k < 3; ++k) Fo[3 * fmap[i] + k] = static_cast<int32_t>(vmap[F[3 * i + k]]);
+}
+__global__ void k_u8_to_u32(const uint8_t* __restrict__ a, int64_t n, uint32_t* __restrict__ o) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) o[i] = a[i] ? 1u : 0u;
+}
+__global__ void k_inv_remap(uint64_t* __restrict__ inv, int64_t n, const uint32_t* __restrict__ vkeep,
+                            const uint32_t* __restrict__ vmap) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t a = static_cast<uint32_t>(inv[i] >> 32), b = static_cast<uint32_t>(inv[i]);
+  inv[i] = (vkeep[a] && vkeep[b]) ? (static_cast<uint64_t>(vmap[a]) << 32) | vmap[b] : ~0ull;
+}
+
 }  // namespace
 
 void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv, int64_t& nf, int64_t target,
@@ -663,10 +692,10 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
   DevBuf<uint8_t> sort_tmp;
 
   auto build_incidence = [&]() {
-    deg.memset(0, st);
+    PCU_CUDA(cudaMemsetAsync(deg.get(), 0, nv * sizeof(uint32_t), st));
     PCU_LAUNCH(ctx, k_deg, grid_for(nf, 256), 256, 0, F, falive.get(), nf, deg.get());
     exclusive_scan_u32(ctx, deg.get(), off.get(), nv);
-    cur.memset(0, st);
+    PCU_CUDA(cudaMemsetAsync(cur.get(), 0, nv * sizeof(uint32_t), st));
     PCU_LAUNCH(ctx, k_fill, grid_for(nf, 256), 256, 0, F, falive.get(), nf, off.get(), cur.get(), inc.get());
     PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
   };
@@ -692,9 +721,39 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     return h;
   };
   const unsigned gs_grid = static_cast<unsigned>(ctx.num_sms * 16);
+  // shrink the working set once a sizeable fraction of it is dead (one host sync per compaction)
+  auto compact_state = [&]() {
+    DevBuf<uint32_t> vk(nv, st), vmap(nv, st), fk(nf, st), fmap(nf, st);
+    PCU_LAUNCH(ctx, k_u8_to_u32, grid_for(nv, 256), 256, 0, valive.get(), nv, vk.get());
+    PCU_LAUNCH(ctx, k_u8_to_u32, grid_for(nf, 256), 256, 0, falive.get(), nf, fk.get());
+    exclusive_scan_u32(ctx, vk.get(), vmap.get(), nv);
+    exclusive_scan_u32(ctx, fk.get(), fmap.get(), nf);
+    const int64_t nv2 = static_cast<int64_t>(read_scalar(ctx, vmap.get() + nv - 1)) + read_scalar(ctx, vk.get() + nv - 1);
+    const int64_t nf2 = static_cast<int64_t>(read_scalar(ctx, fmap.get() + nf - 1)) + read_scalar(ctx, fk.get() + nf - 1);
+    DevBuf<double> Xo(3 * (nv2 ? nv2 : 1), st), Qo(10 * (nv2 ? nv2 : 1), st);
+    DevBuf<int32_t> Fo(3 * (nf2 ? nf2 : 1), st);
+    PCU_LAUNCH(ctx, k_compact_state, grid_for(std::max(nv, nf), 256), 256, 0, X, Q.get(), F, nv, nf, vk.get(),
+               vmap.get(), fk.get(), fmap.get(), Xo.get(), Qo.get(), Fo.get());
+    if (ninv) {
+      PCU_LAUNCH(ctx, k_inv_remap, grid_for(ninv, 256), 256, 0, inv.get(), ninv, vk.get(), vmap.get());
+      sort_pairs_u64(ctx, inv.get(), ninv);  // dropped pairs (~0) sort last and never match
+    }
+    V = std::move(Xo);
+    Q = std::move(Qo);
+    Fb = std::move(Fo);
+    X = V.get();
+    F = Fb.get();
+    nv = nv2;
+    nf = nf2;
+    PCU_CUDA(cudaMemsetAsync(falive.get(), 1, nf, st));
+    PCU_CUDA(cudaMemsetAsync(valive.get(), 1, nv, st));
+    boxes_init(ctx, *isc, X, F, nf, falive.get());
+  };
   while (alive_faces > target && zero_run < P.stall) {
     S.iterations++;
     ctx.prof.mark(st, "misc");
+    if (alive_faces * 5 < nf * 3 && nf > 4096) compact_state();
+    ctx.prof.mark(st, "compact_state");
     if (S.iterations > 1) build_incidence();
     ctx.prof.mark(st, "incidence");
     cnt.memset(0, st);
@@ -711,8 +770,8 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     PCU_LAUNCH(ctx, k_cost, eg, 128, 0, X, F, Q.get(), off.get(), deg.get(), inc.get(), ea.get(), eb.get(), valid.get(),
                d_ne, P.we, P.ws, key.get(), place.get(), cnt.get());
     ctx.prof.mark(st, "cost");
-    vmin.memset(0xFF, st);
-    vfmin.memset(0xFF, st);
+    PCU_CUDA(cudaMemsetAsync(vmin.get(), 0xFF, nv * 8, st));
+    PCU_CUDA(cudaMemsetAsync(vfmin.get(), 0xFF, nv * 8, st));
     PCU_LAUNCH(ctx, k_prop_edges, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vmin.get());
     PCU_LAUNCH(ctx, k_prop_faces, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vmin.get(), vfmin.get());
     PCU_LAUNCH(ctx, k_mark, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vfmin.get(), marked.get(),
@@ -759,7 +818,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
       bool first_round = true;
       int64_t nrest = 0;
       while (nq > 0) {
-        revert.memset(0, st);
+        PCU_CUDA(cudaMemsetAsync(revert.get(), 0, nm, st));
         PCU_CUDA(cudaMemsetAsync(&cnt.get()->restored, 0, 8, st));
         if (first_round)
           undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get());
