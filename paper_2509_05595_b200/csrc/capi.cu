@@ -81,7 +81,9 @@ void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n) 
   size_t need = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, n, ctx.stream);
   void* t = tmp_storage(ctx, need);
+  cudaEvent_t e = ctx.prof.kt ? ctx.prof.kbegin(ctx.stream) : nullptr;
   PCU_CUDA(cub::DeviceScan::ExclusiveSum(t, need, in, out, n, ctx.stream));
+  if (e) ctx.prof.kend("cub_scan_u32", e, ctx.stream);
   ++ctx.launches;
 }
 
@@ -101,7 +103,9 @@ void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit) {
   size_t need = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, need, db, static_cast<int>(n), 0, end_bit, ctx.stream);
   void* t = tmp_storage(ctx, need);
+  cudaEvent_t e = ctx.prof.kt ? ctx.prof.kbegin(ctx.stream) : nullptr;
   PCU_CUDA(cub::DeviceRadixSort::SortKeys(t, need, db, static_cast<int>(n), 0, end_bit, ctx.stream));
+  if (e) ctx.prof.kend("cub_sort_pairs_u64", e, ctx.stream);
   ++ctx.launches;
   if (db.Current() != keys)
     PCU_CUDA(cudaMemcpyAsync(keys, db.Current(), n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
@@ -128,6 +132,7 @@ int pamopt_cu_ctx_create(int32_t device, pamopt_cu_ctx* out) {
     c->ctx.device = device;
     const char* pe = std::getenv("PAMOPT_PROFILE");
     c->ctx.prof.on = pe && pe[0] == '1';
+    c->ctx.prof.kt = pe && pe[0] == '2';
     pcu::DeviceGuard g(device);
     PCU_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
     PCU_CUDA(cudaDeviceGetAttribute(&c->ctx.num_sms, cudaDevAttrMultiProcessorCount, device));

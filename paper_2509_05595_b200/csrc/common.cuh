@@ -47,6 +47,39 @@ void set_last_error(const std::string& m);
 // (diagnostics only; never enabled in timed runs).
 struct Prof {
   bool on = false;
+  bool kt = false;  // PAMOPT_PROFILE=2: per-kernel device time (events around every launch)
+  struct Pending {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pend;
+  std::map<std::string, double> kms;
+  std::map<std::string, int64_t> kn;
+  cudaEvent_t kbegin(cudaStream_t s) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    return e;
+  }
+  void kend(const char* name, cudaEvent_t a, cudaStream_t s) {
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, s);
+    pend.push_back({name, a, b});
+    if (pend.size() > 8192) kflush();
+  }
+  void kflush() {
+    for (auto& p : pend) {
+      cudaEventSynchronize(p.b);
+      float ms_ = 0.f;
+      cudaEventElapsedTime(&ms_, p.a, p.b);
+      kms[p.name] += ms_;
+      kn[p.name] += 1;
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    pend.clear();
+  }
   std::map<std::string, double> ms;
   std::map<std::string, int64_t> n;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
@@ -64,6 +97,16 @@ struct Prof {
     t = std::chrono::steady_clock::now();
   }
   void dump(const char* title) {
+    if (kt) {
+      kflush();
+      double tot = 0;
+      for (auto& kv : kms) tot += kv.second;
+      std::fprintf(stderr, "[pamopt kernels] %s device total %.2f ms\n", title, tot);
+      for (auto& kv : kms)
+        std::fprintf(stderr, "  %-34s %10.3f ms  %8lld launches\n", kv.first.c_str(), kv.second, (long long)kn[kv.first]);
+      kms.clear();
+      kn.clear();
+    }
     if (!on) return;
     double tot = 0;
     for (auto& kv : ms) tot += kv.second;
@@ -153,7 +196,9 @@ inline unsigned grid_for(int64_t n, int block) {
 
 #define PCU_LAUNCH(ctx, kernel, grid, block, smem, ...)                       \
   do {                                                                        \
+    cudaEvent_t pcu_ev_ = (ctx).prof.kt ? (ctx).prof.kbegin((ctx).stream) : nullptr; \
     kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);           \
+    if (pcu_ev_) (ctx).prof.kend(#kernel, pcu_ev_, (ctx).stream);              \
     ++(ctx).launches;                                                         \
     PCU_CUDA(cudaGetLastError());                                             \
   } while (0)

@@ -798,8 +798,10 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
         sort_tmp.alloc(need, st);
         sort_tmp_bytes = need;
       }
+      cudaEvent_t sev = ctx.prof.kt ? ctx.prof.kbegin(st) : nullptr;
       cub::DeviceRadixSort::SortKeys(sort_tmp.get(), sort_tmp_bytes, marked.get(), marked_sorted.get(),
                                      static_cast<int>(nm), 0, 64, st);
+      if (sev) ctx.prof.kend("cub_sort_marked", sev, st);
       PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, marked_sorted.get(), nm, ea.get(), eb.get(), enf.get(), F,
                  off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get());
       exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
