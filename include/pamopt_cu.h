@@ -92,6 +92,8 @@ int pamopt_cu_mesh_from_device(pamopt_cu_ctx ctx, const double* d_vertices, int6
                                const int32_t* d_faces, int64_t nf, pamopt_cu_mesh* out);
 int pamopt_cu_mesh_size(pamopt_cu_mesh mesh, int64_t* nv, int64_t* nf);
 int pamopt_cu_mesh_download(pamopt_cu_mesh mesh, double* vertices, int32_t* faces);
+/* device-to-device copy into caller buffers (NCCL gather of slab meshes); either may be NULL */
+int pamopt_cu_mesh_copy_to_device(pamopt_cu_mesh mesh, double* d_vertices, int32_t* d_faces);
 int pamopt_cu_mesh_free(pamopt_cu_mesh mesh);
 
 /* ---- stage 1a: voxel_field --------------------------------------------------------- */
@@ -109,6 +111,11 @@ int pamopt_cu_grid_slab(pamopt_cu_grid grid, int32_t* z0, int32_t* z1);
 /* device-to-device exchange with caller buffers (NCCL halo exchange / gather) */
 int pamopt_cu_grid_copy_to_device(pamopt_cu_grid grid, void* dst);
 int pamopt_cu_grid_from_device(pamopt_cu_ctx ctx, int32_t R, const float* src, pamopt_cu_grid* out);
+/* a z-slab grid holding lattice planes [z0, z1) from device (src) or host (samples) memory */
+int pamopt_cu_grid_slab_from_device(pamopt_cu_ctx ctx, int32_t R, int32_t z0, int32_t z1, const float* src,
+                                    pamopt_cu_grid* out);
+int pamopt_cu_grid_slab_upload(pamopt_cu_ctx ctx, int32_t R, int32_t z0, int32_t z1, const float* samples,
+                               pamopt_cu_grid* out);
 int pamopt_cu_grid_upload(pamopt_cu_ctx ctx, int32_t R, const float* samples, pamopt_cu_grid* out);
 int pamopt_cu_grid_resolution(pamopt_cu_grid grid, int32_t* R);
 int pamopt_cu_grid_download(pamopt_cu_grid grid, float* samples);
@@ -120,6 +127,17 @@ int pamopt_cu_hierarchy_pairs(pamopt_cu_ctx ctx, pamopt_cu_mesh mesh, int32_t R,
 
 /* ---- stage 1b: dual_mc -------------------------------------------------------------- */
 int pamopt_cu_dmc_extract(pamopt_cu_grid sdf, double beta, pamopt_cu_mesh* out);
+/* slab-local extract: the grid holds planes [z0, z1) covering [own_z0-2,
+ * own_z1+2) clipped to the lattice; cells of layers [own_z0, own_z1) emit the faces of their
+ * corner-0 edges, in the same order as the whole-grid extract.  out mesh V = [own patch
+ * vertices (counts[0]), 4-split vertices (counts[1])]; face indices are relative to the first own
+ * patch vertex, negative ones naming the previous slab's top layer.  Assemble with
+ * pamopt_cu_mesh_rebase: concatenating every slab's patch vertices, then every slab's split
+ * vertices, reproduces the whole-grid mesh bit for bit. */
+int pamopt_cu_dmc_extract_slab(pamopt_cu_grid sdf, int32_t own_z0, int32_t own_z1, double beta,
+                               pamopt_cu_mesh* out, int64_t counts[2]);
+/* in place: F -> patch_base + F if F < nvp_own, else extra_base + (F - nvp_own) */
+int pamopt_cu_mesh_rebase(pamopt_cu_mesh mesh, int64_t patch_base, int64_t nvp_own, int64_t extra_base);
 /* active cells of the last extract on this grid: linear cell index, case, flip mask */
 int pamopt_cu_dmc_active_cells(pamopt_cu_grid sdf, int64_t* cells, uint8_t* cases,
                                uint8_t* flips, int64_t cap, int64_t* n);

@@ -56,6 +56,7 @@ def lib():
         L.orc_dmc_patches.argtypes = [C.c_int, C.c_int, i32p]
         L.orc_dmc_extract.argtypes = [f32p, C.c_int, C.c_double, i64p]
         L.orc_dmc_fetch.argtypes = [C.c_void_p] * 5
+        L.orc_dmc_extract_slab.argtypes = [f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, i64p]
         L.orc_tri_tri_pairs.argtypes = [f64p, i32p, i32p, C.c_int64, i32p]
         L.orc_orient3d.restype = C.c_int
         L.orc_orient3d.argtypes = [f64p, f64p, f64p, f64p]
@@ -172,6 +173,20 @@ def dmc_extract(sdf, R: int, beta: float = 5.0) -> dict:
                         faces.ctypes.data)
     return dict(cells=cells, cases=cases, flips=flips, vertices=verts, faces=faces,
                 n_quads=int(sizes[3]), n_split4=int(sizes[4]))
+
+
+def dmc_extract_slab(planes, R: int, pz0: int, own_z0: int, own_z1: int, beta: float = 5.0) -> dict:
+    """Slab-local DMC over resident planes [pz0, pz0 + len(planes)): vertices =
+    [own patch vertices, 4-split vertices]; face indices relative to the first own patch vertex."""
+    planes = np.ascontiguousarray(planes, np.float32)
+    pz1 = pz0 + planes.size // ((R + 1) * (R + 1))
+    sizes = np.zeros(7, np.int64)
+    lib().orc_dmc_extract_slab(planes.ravel(), R, pz0, pz1, own_z0, own_z1, beta, sizes)
+    na, nv, nf = int(sizes[0]), int(sizes[1]), int(sizes[2])
+    verts = np.empty((nv, 3), np.float64)
+    faces = np.empty((nf, 3), np.int32)
+    lib().orc_dmc_fetch(None, None, None, verts.ctypes.data, faces.ctypes.data)
+    return dict(vertices=verts, faces=faces, nvp_own=int(sizes[5]), n_extra=int(sizes[6]))
 
 
 # ---------------------------------------------------------------- tri_isect

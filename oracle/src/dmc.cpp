@@ -183,7 +183,8 @@ struct Grid {
   const float* s;
   int R;
   int64_t n1;
-  float at(int64_t x, int64_t y, int64_t z) const { return s[x + n1 * (y + n1 * z)]; }
+  int64_t zb;  // global z of the first resident plane (z-slab restatement)
+  float at(int64_t x, int64_t y, int64_t z) const { return s[x + n1 * (y + n1 * (z - zb))]; }
   int case_of(int64_t x, int64_t y, int64_t z) const {
     int cs = 0;
     for (int c = 0; c < 8; ++c)
@@ -229,17 +230,26 @@ struct DmcOut {
   std::vector<int32_t> faces;
   int64_t nquads = 0;
   int64_t nsplit4 = 0;
+  int64_t nvp_own = 0;  // patch vertices of the own layers (slab mode)
+  int64_t n_extra = 0;
 };
 
-void run_dmc(const float* sdf, int R, double beta, DmcOut& out) {
-  Grid g{sdf, R, static_cast<int64_t>(R) + 1};
-  const int64_t ncell = static_cast<int64_t>(R) * R * R;
+// Whole grid: pz0 = 0, own layers [0, R).  Slab: the resident planes start at pz0; cells of layers
+// [own_z0, own_z1) emit quads, the layer below only provides vertex ids; the output drops the
+// vertices below the own layers and shifts every face index by their count.
+void run_dmc(const float* sdf, int R, double beta, DmcOut& out, int64_t pz0 = 0, int64_t own_z0 = 0,
+             int64_t own_z1 = -1) {
+  if (own_z1 < 0) own_z1 = R;
+  Grid g{sdf, R, static_cast<int64_t>(R) + 1, pz0};
+  const int64_t cz0 = own_z0 > 0 ? own_z0 - 1 : 0;
+  const int64_t cbeg = static_cast<int64_t>(R) * R * cz0;
+  const int64_t ncell = static_cast<int64_t>(R) * R * own_z1;
   // classify (dense scan, per-thread chunks then ordered concatenation)
   const int64_t chunk = 1 << 16;
-  const int64_t nchunks = (ncell + chunk - 1) / chunk;
+  const int64_t nchunks = (ncell - cbeg + chunk - 1) / chunk;
   std::vector<std::vector<int64_t>> part(nchunks);
   parallel_for(nchunks, [&](int64_t ci) {
-    for (int64_t c = ci * chunk; c < std::min(ncell, (ci + 1) * chunk); ++c) {
+    for (int64_t c = cbeg + ci * chunk; c < std::min(ncell, cbeg + (ci + 1) * chunk); ++c) {
       const int64_t x = c % R, y = (c / R) % R, z = c / (static_cast<int64_t>(R) * R);
       const int cs = g.case_of(x, y, z);
       if (cs != 0 && cs != 255) part[ci].push_back(c);
@@ -306,7 +316,7 @@ void run_dmc(const float* sdf, int R, double beta, DmcOut& out) {
   parallel_for(na, [&](int64_t i) {
     const int64_t c = out.cells[i];
     const int64_t xyz[3] = {c % R, (c / R) % R, c / (static_cast<int64_t>(R) * R)};
-    for (int a = 0; a < 3; ++a) {
+    for (int a = 0; a < 3 && xyz[2] >= own_z0; ++a) {
       const int b = (a + 1) % 3, cc = (a + 2) % 3;
       if (xyz[b] < 1 || xyz[cc] < 1) continue;  // lower vertex coordinate must be in [1, R-1]
       int64_t up[3] = {xyz[0], xyz[1], xyz[2]};
@@ -395,6 +405,14 @@ void run_dmc(const float* sdf, int R, double beta, DmcOut& out) {
         for (int t = 0; t < Q.ntri; ++t)
           for (int k = 0; k < 3; ++k) out.faces.push_back(static_cast<int32_t>(ids[Q.tri[t][k]]));
       }
+  // drop the lending layer's vertices (slab mode); whole grid: shift = 0
+  const int64_t cown = static_cast<int64_t>(R) * R * own_z0;
+  const int64_t i0 = std::lower_bound(out.cells.begin(), out.cells.end(), cown) - out.cells.begin();
+  const int64_t shift = out.vbase[i0];
+  out.verts.erase(out.verts.begin(), out.verts.begin() + 3 * shift);
+  for (auto& x : out.faces) x = static_cast<int32_t>(x - shift);
+  out.nvp_own = nv_patch - shift;
+  out.n_extra = extra;
 }
 
 }  // namespace
@@ -431,6 +449,22 @@ void orc_dmc_extract(const float* sdf, int R, double beta, int64_t* sizes) {
   sizes[2] = static_cast<int64_t>(g_last.faces.size() / 3);
   sizes[3] = g_last.nquads;
   sizes[4] = g_last.nsplit4;
+}
+
+// slab-local extract: planes [pz0, pz1) resident; sizes as orc_dmc_extract plus
+// {nvp_own, n_extra}
+void orc_dmc_extract_slab(const float* planes, int R, int pz0, int pz1, int own_z0, int own_z1, double beta,
+                          int64_t* sizes) {
+  (void)pz1;
+  g_last = DmcOut();
+  run_dmc(planes, R, beta, g_last, pz0, own_z0, own_z1);
+  sizes[0] = static_cast<int64_t>(g_last.cells.size());
+  sizes[1] = static_cast<int64_t>(g_last.verts.size() / 3);
+  sizes[2] = static_cast<int64_t>(g_last.faces.size() / 3);
+  sizes[3] = g_last.nquads;
+  sizes[4] = g_last.nsplit4;
+  sizes[5] = g_last.nvp_own;
+  sizes[6] = g_last.n_extra;
 }
 
 void orc_dmc_fetch(int64_t* cells, uint8_t* cases, uint8_t* flips, double* verts, int32_t* faces) {

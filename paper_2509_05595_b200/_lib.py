@@ -70,6 +70,7 @@ _SIGS = {
     "pamopt_cu_mesh_from_device": (C.c_int, [vp, vp, i64, vp, i64, P(vp)]),
     "pamopt_cu_mesh_size": (C.c_int, [vp, P(i64), P(i64)]),
     "pamopt_cu_mesh_download": (C.c_int, [vp, vp, vp]),
+    "pamopt_cu_mesh_copy_to_device": (C.c_int, [vp, vp, vp]),
     "pamopt_cu_mesh_free": (C.c_int, [vp]),
     "pamopt_cu_compute_udf": (C.c_int, [vp, vp, i32, P(vp)]),
     "pamopt_cu_udf_to_sdf": (C.c_int, [vp, dbl]),
@@ -79,11 +80,15 @@ _SIGS = {
     "pamopt_cu_grid_copy_to_device": (C.c_int, [vp, vp]),
     "pamopt_cu_grid_from_device": (C.c_int, [vp, i32, vp, P(vp)]),
     "pamopt_cu_grid_upload": (C.c_int, [vp, i32, vp, P(vp)]),
+    "pamopt_cu_grid_slab_from_device": (C.c_int, [vp, i32, i32, i32, vp, P(vp)]),
+    "pamopt_cu_grid_slab_upload": (C.c_int, [vp, i32, i32, i32, vp, P(vp)]),
     "pamopt_cu_grid_resolution": (C.c_int, [vp, P(i32)]),
     "pamopt_cu_grid_download": (C.c_int, [vp, vp]),
     "pamopt_cu_grid_free": (C.c_int, [vp]),
     "pamopt_cu_hierarchy_pairs": (C.c_int, [vp, vp, i32, i32, vp, i64, P(i64)]),
     "pamopt_cu_dmc_extract": (C.c_int, [vp, dbl, P(vp)]),
+    "pamopt_cu_dmc_extract_slab": (C.c_int, [vp, i32, i32, dbl, P(vp), P(i64)]),
+    "pamopt_cu_mesh_rebase": (C.c_int, [vp, i64, i64, i64]),
     "pamopt_cu_dmc_active_cells": (C.c_int, [vp, vp, vp, vp, i64, P(i64)]),
     "pamopt_cu_dmc_table": (C.c_int, [vp]),
     "pamopt_cu_self_intersections": (C.c_int, [vp, vp, i64, P(i64)]),

@@ -102,6 +102,14 @@ class DeviceMesh:
         check(lib().pamopt_cu_mesh_download(self.h, ptr(v), ptr(f)))
         return v, f
 
+    def rebase(self, patch_base: int, nvp_own: int, extra_base: int) -> None:
+        """Face indices -> global ids of the assembled slab mesh (pamopt_cu_mesh_rebase)."""
+        check(lib().pamopt_cu_mesh_rebase(self.h, int(patch_base), int(nvp_own), int(extra_base)))
+
+    def copy_to_device(self, vptr: int | None, fptr: int | None) -> None:
+        check(lib().pamopt_cu_mesh_copy_to_device(self.h, C.c_void_p(vptr) if vptr else None,
+                                                   C.c_void_p(fptr) if fptr else None))
+
     def free(self):
         if self.h:
             lib().pamopt_cu_mesh_free(self.h)
@@ -140,6 +148,25 @@ class DeviceGrid:
 
     def copy_to_device(self, ptr: int) -> None:
         check(lib().pamopt_cu_grid_copy_to_device(self.h, C.c_void_p(ptr)))
+
+    @classmethod
+    def slab_from_device(cls, ptr: int, R: int, z0: int, z1: int, ctx: Context | None = None) -> "DeviceGrid":
+        """z-slab (lattice planes [z0, z1)) copied from a device buffer."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib().pamopt_cu_grid_slab_from_device(ctx.h, int(R), int(z0), int(z1), C.c_void_p(ptr), C.byref(h)))
+        return cls(h, ctx, R)
+
+    @classmethod
+    def slab_upload(cls, planes, R: int, z0: int, ctx: Context | None = None) -> "DeviceGrid":
+        """z-slab from host samples: planes [z0, z0 + len) of the (R+1)^3 lattice."""
+        ctx = ctx or default_context()
+        s = np.ascontiguousarray(planes, np.float32).ravel()
+        n = s.size // ((R + 1) * (R + 1))
+        assert s.size == n * (R + 1) * (R + 1)
+        h = C.c_void_p()
+        check(lib().pamopt_cu_grid_slab_upload(ctx.h, int(R), int(z0), int(z0 + n), ptr(s), C.byref(h)))
+        return cls(h, ctx, R)
 
     @classmethod
     def upload(cls, samples, R: int, ctx: Context | None = None) -> "DeviceGrid":
@@ -223,6 +250,16 @@ def extract(grid: DeviceGrid, beta: float = DEFAULT_BETA) -> DeviceMesh:
     h = C.c_void_p()
     check(lib().pamopt_cu_dmc_extract(grid.h, float(beta), C.byref(h)))
     return DeviceMesh(h, grid.ctx)
+
+
+def extract_slab(grid: DeviceGrid, own_z0: int, own_z1: int, beta: float = DEFAULT_BETA):
+    """Slab-local extract.  Returns (DeviceMesh, nvp_own, n_extra); the mesh's
+    vertices are [own patch vertices, 4-split vertices] and its face indices are relative to the
+    first own patch vertex until DeviceMesh.rebase."""
+    h = C.c_void_p()
+    counts = (C.c_int64 * 2)()
+    check(lib().pamopt_cu_dmc_extract_slab(grid.h, int(own_z0), int(own_z1), float(beta), C.byref(h), counts))
+    return DeviceMesh(h, grid.ctx), int(counts[0]), int(counts[1])
 
 
 def dmc_active_cells(grid: DeviceGrid):

@@ -212,6 +212,19 @@ int pamopt_cu_mesh_download(pamopt_cu_mesh m, double* v, int32_t* f) {
   });
 }
 
+int pamopt_cu_mesh_copy_to_device(pamopt_cu_mesh m, double* v, int32_t* f) {
+  return guarded([&] {
+    PCU_REQUIRE(m != nullptr, PAMOPT_CU_EINVAL, "null mesh");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    if (v && m->nv)
+      PCU_CUDA(cudaMemcpyAsync(v, m->V.get(), 3 * m->nv * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+    if (f && m->nf)
+      PCU_CUDA(cudaMemcpyAsync(f, m->F.get(), 3 * m->nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
 int pamopt_cu_mesh_free(pamopt_cu_mesh m) {
   return guarded([&] {
     if (!m) return;
@@ -312,6 +325,37 @@ int pamopt_cu_grid_from_device(pamopt_cu_ctx c, int32_t R, const float* src, pam
   });
 }
 
+static int grid_slab_make(pamopt_cu_ctx c, int32_t R, int32_t z0, int32_t z1, const float* src, cudaMemcpyKind kind,
+                          pamopt_cu_grid* out) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(R >= 8 && R <= 2048 && (R & (R - 1)) == 0 && src && out, PAMOPT_CU_EINVAL, "bad arguments");
+    PCU_REQUIRE(0 <= z0 && z0 < z1 && z1 <= R + 1, PAMOPT_CU_EINVAL, "slab planes must satisfy 0 <= z0 < z1 <= R+1");
+    pcu::DeviceGuard g(c->ctx.device);
+    auto* gr = new pamopt_cu_grid_s();
+    gr->owner = c;
+    ++c->refs;
+    gr->R = R;
+    gr->z0 = z0;
+    gr->z1 = z1;
+    const int64_t n = static_cast<int64_t>(R + 1) * (R + 1) * (z1 - z0);
+    gr->g.alloc(n, c->ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(gr->g.get(), src, n * sizeof(float), kind, c->ctx.stream));
+    if (kind == cudaMemcpyHostToDevice) PCU_CUDA(cudaStreamSynchronize(c->ctx.stream));
+    *out = gr;
+  });
+}
+
+int pamopt_cu_grid_slab_from_device(pamopt_cu_ctx c, int32_t R, int32_t z0, int32_t z1, const float* src,
+                                    pamopt_cu_grid* out) {
+  return grid_slab_make(c, R, z0, z1, src, cudaMemcpyDeviceToDevice, out);
+}
+
+int pamopt_cu_grid_slab_upload(pamopt_cu_ctx c, int32_t R, int32_t z0, int32_t z1, const float* samples,
+                               pamopt_cu_grid* out) {
+  return grid_slab_make(c, R, z0, z1, samples, cudaMemcpyHostToDevice, out);
+}
+
 int pamopt_cu_udf_to_sdf(pamopt_cu_grid gr, double eps) {
   return guarded([&] {
     PCU_REQUIRE(gr != nullptr, PAMOPT_CU_EINVAL, "null grid");
@@ -405,6 +449,39 @@ int pamopt_cu_dmc_extract(pamopt_cu_grid gr, double beta, pamopt_cu_mesh* out) {
     m->V = std::move(gr->last.V);
     m->F = std::move(gr->last.F);
     *out = m;
+  });
+}
+
+int pamopt_cu_dmc_extract_slab(pamopt_cu_grid gr, int32_t own_z0, int32_t own_z1, double beta, pamopt_cu_mesh* out,
+                               int64_t counts[2]) {
+  return guarded([&] {
+    PCU_REQUIRE(gr && out && counts, PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(beta > 0.0, PAMOPT_CU_EINVAL, "beta must be positive");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    gr->last = pcu::DmcResult();
+    pcu::dmc_extract_slab(ctx, gr->g.get(), gr->R, gr->z0, gr->z1, own_z0, own_z1, beta, gr->last);
+    auto* m = new pamopt_cu_mesh_s();
+    m->owner = gr->owner;
+    ++gr->owner->refs;
+    m->nv = static_cast<int64_t>(gr->last.nv);
+    m->nf = static_cast<int64_t>(gr->last.nf);
+    m->V = std::move(gr->last.V);
+    m->F = std::move(gr->last.F);
+    counts[0] = static_cast<int64_t>(gr->last.nvp_own);
+    counts[1] = static_cast<int64_t>(gr->last.n_extra);
+    *out = m;
+  });
+}
+
+int pamopt_cu_mesh_rebase(pamopt_cu_mesh m, int64_t patch_base, int64_t nvp_own, int64_t extra_base) {
+  return guarded([&] {
+    PCU_REQUIRE(m != nullptr, PAMOPT_CU_EINVAL, "null mesh");
+    PCU_REQUIRE(patch_base >= 0 && nvp_own >= 0 && extra_base >= 0 && extra_base < (int64_t(1) << 31),
+                PAMOPT_CU_EINVAL, "rebase: bad offsets");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    pcu::mesh_rebase(ctx, m->F.get(), 3 * m->nf, patch_base, nvp_own, extra_base);
   });
 }
 

@@ -150,7 +150,10 @@ struct GridView {
   const float* s;
   int R;
   int64_t n1;
-  __device__ __forceinline__ float at(int64_t x, int64_t y, int64_t z) const { return s[x + n1 * (y + n1 * z)]; }
+  int64_t zb;  // global z of the first resident lattice plane (0 for a whole grid)
+  __device__ __forceinline__ float at(int64_t x, int64_t y, int64_t z) const {
+    return s[x + n1 * (y + n1 * (z - zb))];
+  }
   __device__ __forceinline__ int case_of(int64_t x, int64_t y, int64_t z) const {
     int cs = 0;
 #pragma unroll
@@ -166,7 +169,8 @@ __device__ __forceinline__ void cell_xyz(int64_t c, int R, int64_t& x, int64_t& 
   z = c / (static_cast<int64_t>(R) * R);
 }
 
-__global__ void __launch_bounds__(256) k_classify_count(GridView g, int64_t ncell, uint32_t* __restrict__ bcount) {
+__global__ void __launch_bounds__(256) k_classify_count(GridView g, int64_t c0, int64_t ncell,
+                                                        uint32_t* __restrict__ bcount) {
   typedef cub::BlockReduce<uint32_t, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kCellsPerBlock;
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(256) k_classify_count(GridView g, int64_t ncel
     const int64_t c = base + k * 256 + threadIdx.x;
     if (c < ncell) {
       int64_t x, y, z;
-      cell_xyz(c, g.R, x, y, z);
+      cell_xyz(c0 + c, g.R, x, y, z);
       const int cs = g.case_of(x, y, z);
       cnt += (cs != 0 && cs != 255);
     }
@@ -184,7 +188,8 @@ __global__ void __launch_bounds__(256) k_classify_count(GridView g, int64_t ncel
   if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(256) k_classify_write(GridView g, int64_t ncell, const uint32_t* __restrict__ boff,
+__global__ void __launch_bounds__(256) k_classify_write(GridView g, int64_t c0, int64_t ncell,
+                                                        const uint32_t* __restrict__ boff,
                                                         uint32_t* __restrict__ cells, uint8_t* __restrict__ cases) {
   typedef cub::BlockScan<uint32_t, 256> BS;
   __shared__ typename BS::TempStorage tmp;
@@ -195,14 +200,14 @@ __global__ void __launch_bounds__(256) k_classify_write(GridView g, int64_t ncel
     int cs = 0;
     if (c < ncell) {
       int64_t x, y, z;
-      cell_xyz(c, g.R, x, y, z);
+      cell_xyz(c0 + c, g.R, x, y, z);
       cs = g.case_of(x, y, z);
     }
     const uint32_t flag = (c < ncell && cs != 0 && cs != 255) ? 1u : 0u;
     uint32_t pos, tot;
     BS(tmp).ExclusiveSum(flag, pos, tot);
     if (flag) {
-      cells[run + pos] = static_cast<uint32_t>(c);
+      cells[run + pos] = static_cast<uint32_t>(c0 + c);
       cases[run + pos] = static_cast<uint8_t>(cs);
     }
     run += tot;
@@ -214,7 +219,7 @@ __device__ __forceinline__ const PatchSet& patches_of(int cs, int flip) { return
 
 __global__ void k_patch_count(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
                               int64_t na, uint8_t* __restrict__ flips, uint32_t* __restrict__ npatch,
-                              uint32_t* __restrict__ cellmap) {
+                              uint32_t* __restrict__ cellmap, int64_t c0) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= na) return;
   const int cs = cases[i];
@@ -233,7 +238,7 @@ __global__ void k_patch_count(GridView g, const uint32_t* __restrict__ cells, co
   }
   flips[i] = static_cast<uint8_t>(flip);
   npatch[i] = patches_of(cs, flip).n;
-  cellmap[cells[i]] = static_cast<uint32_t>(i);
+  cellmap[cells[i] - c0] = static_cast<uint32_t>(i);
 }
 
 __device__ __forceinline__ D3 gpoint(int64_t x, int64_t y, int64_t z, int R) {
@@ -294,7 +299,7 @@ struct QuadGeo {
 __device__ __forceinline__ bool make_quad(GridView g, int64_t x, int64_t y, int64_t z, int a,
                                           const uint32_t* __restrict__ cellmap, const uint8_t* __restrict__ cases,
                                           const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase,
-                                          QuadGeo& Q) {
+                                          int64_t cbase, QuadGeo& Q) {
   const int64_t xyz[3] = {x, y, z};
   const int b = (a + 1) % 3, c = (a + 2) % 3;
   if (xyz[b] < 1 || xyz[c] < 1) return false;
@@ -313,7 +318,7 @@ __device__ __forceinline__ bool make_quad(GridView g, int64_t x, int64_t y, int6
     if (offs[k][1] == -1) c0 |= 1 << c;
     const int cx = c0 & 1, cy = (c0 >> 1) & 1, cz = (c0 >> 2) & 1;
     const int e = a == 0 ? cy + 2 * cz : (a == 1 ? 4 + cx + 2 * cz : 8 + cx + 2 * cy);
-    const uint32_t j = cellmap[cl[0] + g.R * (cl[1] + static_cast<int64_t>(g.R) * cl[2])];
+    const uint32_t j = cellmap[cl[0] + g.R * (cl[1] + static_cast<int64_t>(g.R) * cl[2]) - cbase];
     Q.q[k] = vbase[j] + patches_of(cases[j], flips[j]).edge_patch[e];
   }
   if (!(Q.f0 < 0.0f)) {  // lower endpoint positive: reverse so the normal points - -> +
@@ -362,17 +367,18 @@ __device__ __forceinline__ int split_code(const QuadGeo& Q, const double* __rest
 
 __global__ void k_quad_count(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
                              const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase,
-                             const uint32_t* __restrict__ cellmap, int64_t na, const double* __restrict__ V,
-                             uint64_t* __restrict__ counts, uint8_t* __restrict__ codes) {
+                             const uint32_t* __restrict__ cellmap, int64_t c0, int64_t own_z0, int64_t na,
+                             const double* __restrict__ V, uint64_t* __restrict__ counts,
+                             uint8_t* __restrict__ codes) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= na) return;
   int64_t x, y, z;
   cell_xyz(cells[i], g.R, x, y, z);
   uint32_t nfaces = 0, nextra = 0;
   uint8_t code = 0;
-  for (int a = 0; a < 3; ++a) {
+  for (int a = 0; a < 3 && z >= own_z0; ++a) {  // the layer below a slab only lends vertex ids
     QuadGeo Q;
-    if (!make_quad(g, x, y, z, a, cellmap, cases, flips, vbase, Q)) continue;
+    if (!make_quad(g, x, y, z, a, cellmap, cases, flips, vbase, c0, Q)) continue;
     const int sc = split_code(Q, V);
     code |= static_cast<uint8_t>(sc << (2 * a));
     nfaces += sc == 3 ? 4 : 2;
@@ -384,9 +390,9 @@ __global__ void k_quad_count(GridView g, const uint32_t* __restrict__ cells, con
 
 __global__ void k_quad_write(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
                              const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase,
-                             const uint32_t* __restrict__ cellmap, int64_t na, const uint8_t* __restrict__ codes,
-                             const uint64_t* __restrict__ offs, uint64_t nv_patch, double beta,
-                             double* __restrict__ V, int32_t* __restrict__ Fo) {
+                             const uint32_t* __restrict__ cellmap, int64_t c0, int64_t na,
+                             const uint8_t* __restrict__ codes, const uint64_t* __restrict__ offs, uint64_t nv_patch,
+                             int64_t shift, double beta, double* __restrict__ V, int32_t* __restrict__ Fo) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= na || codes[i] == 0) return;
   int64_t x, y, z;
@@ -396,8 +402,9 @@ __global__ void k_quad_write(GridView g, const uint32_t* __restrict__ cells, con
     const int sc = (codes[i] >> (2 * a)) & 3;
     if (!sc) continue;
     QuadGeo Q;
-    make_quad(g, x, y, z, a, cellmap, cases, flips, vbase, Q);
-    const uint32_t* q = Q.q;
+    make_quad(g, x, y, z, a, cellmap, cases, flips, vbase, c0, Q);
+    for (int k = 0; k < 4; ++k) Q.q[k] -= static_cast<uint32_t>(shift);  // ids relative to the first own vertex
+    const int32_t* q = reinterpret_cast<const int32_t*>(Q.q);
     int32_t* o = Fo + 3 * fo;
     if (sc == 1) {
       const int32_t t[6] = {(int32_t)q[0], (int32_t)q[1], (int32_t)q[2], (int32_t)q[0], (int32_t)q[2], (int32_t)q[3]};
@@ -408,7 +415,7 @@ __global__ void k_quad_write(GridView g, const uint32_t* __restrict__ cells, con
       for (int k = 0; k < 6; ++k) o[k] = t[k];
       fo += 2;
     } else {
-      const uint64_t ve = nv_patch + eo;
+      const uint64_t ve = nv_patch - shift + eo;
       const D3 p = crossing(Q.plo, Q.phi, Q.f0, Q.f1, beta);
       V[3 * ve] = p.x;
       V[3 * ve + 1] = p.y;
@@ -434,21 +441,40 @@ void dmc_table_host(int32_t* out) {
   }
 }
 
-void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res) {
+namespace {
+// first own patch vertex: vbase of the first active cell at or above the own layers
+__global__ void k_own_split(const uint32_t* __restrict__ cells, const uint32_t* __restrict__ vbase, int64_t na,
+                            uint64_t cthr, uint32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na) return;
+  if (cells[i] >= cthr && (i == 0 || cells[i - 1] < cthr)) *out = vbase[i];
+}
+}  // namespace
+
+void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, int own_z0, int own_z1, double beta,
+                      DmcResult& res) {
   upload_table(ctx.device);
-  GridView g{d_sdf, R, static_cast<int64_t>(R) + 1};
-  const int64_t ncell = static_cast<int64_t>(R) * R * R;
+  const int cz0 = own_z0 > 0 ? own_z0 - 1 : 0;  // the layer below lends its patch-vertex ids
+  PCU_REQUIRE(R >= 2 && own_z0 >= 0 && own_z0 < own_z1 && own_z1 <= R, PAMOPT_CU_EINVAL,
+              "dmc slab: own cell layers must satisfy 0 <= z0 < z1 <= R");
+  PCU_REQUIRE(pz0 <= std::max(own_z0 - 2, 0) && pz1 >= std::min(own_z1 + 2, R + 1) && pz0 >= 0 && pz1 <= R + 1,
+              PAMOPT_CU_EINVAL, "dmc slab: resident planes must cover [z0-2, z1+2) clipped to the lattice");
+  GridView g{d_planes, R, static_cast<int64_t>(R) + 1, pz0};
+  const int64_t rr = static_cast<int64_t>(R) * R;
+  const int64_t c0 = rr * cz0;
+  const int64_t ncell = rr * (own_z1 - cz0);
   const int64_t nblk = (ncell + kCellsPerBlock - 1) / kCellsPerBlock;
   DevBuf<uint32_t> bcount(nblk, ctx.stream), boff(nblk, ctx.stream);
-  PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, ncell, bcount.get());
+  PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, c0, ncell, bcount.get());
   exclusive_scan_u32(ctx, bcount.get(), boff.get(), nblk);
   const uint32_t na = read_scalar(ctx, boff.get() + nblk - 1) + read_scalar(ctx, bcount.get() + nblk - 1);
   res.cells.alloc(na ? na : 1, ctx.stream);
   res.cases.alloc(na ? na : 1, ctx.stream);
   res.flips.alloc(na ? na : 1, ctx.stream);
   res.n_active = na;
-  PCU_LAUNCH(ctx, k_classify_write, static_cast<unsigned>(nblk), 256, 0, g, ncell, boff.get(), res.cells.get(),
+  PCU_LAUNCH(ctx, k_classify_write, static_cast<unsigned>(nblk), 256, 0, g, c0, ncell, boff.get(), res.cells.get(),
              res.cases.get());
+  res.nvp_own = res.n_extra = 0;
   if (na == 0) {
     res.nv = res.nf = 0;
     res.V.alloc(1, ctx.stream);
@@ -458,9 +484,18 @@ void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& re
   DevBuf<uint32_t> npatch(na, ctx.stream), vbase(na, ctx.stream);
   DevBuf<uint32_t> cellmap(ncell, ctx.stream);  // only active entries are written / read
   PCU_LAUNCH(ctx, k_patch_count, grid_for(na, 256), 256, 0, g, res.cells.get(), res.cases.get(), na, res.flips.get(),
-             npatch.get(), cellmap.get());
+             npatch.get(), cellmap.get(), c0);
   exclusive_scan_u32(ctx, npatch.get(), vbase.get(), na);
   const uint64_t nv_patch = static_cast<uint64_t>(read_scalar(ctx, vbase.get() + na - 1)) + read_scalar(ctx, npatch.get() + na - 1);
+  uint64_t shift = 0;
+  if (own_z0 > cz0) {
+    DevBuf<uint32_t> split(1, ctx.stream);
+    const uint32_t init = static_cast<uint32_t>(nv_patch);
+    PCU_CUDA(cudaMemcpyAsync(split.get(), &init, 4, cudaMemcpyHostToDevice, ctx.stream));
+    PCU_LAUNCH(ctx, k_own_split, grid_for(na, 256), 256, 0, res.cells.get(), vbase.get(), na,
+               static_cast<uint64_t>(rr * own_z0), split.get());
+    shift = read_scalar(ctx, split.get());
+  }
   DevBuf<uint64_t> counts(na, ctx.stream), offs(na, ctx.stream);
   DevBuf<uint8_t> codes(na, ctx.stream);
   // patch vertices first (the quad pass reads them); extra vertices appended after
@@ -468,18 +503,41 @@ void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& re
   PCU_LAUNCH(ctx, k_patch_vertices, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
              vbase.get(), na, beta, Vp.get());
   PCU_LAUNCH(ctx, k_quad_count, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
-             vbase.get(), cellmap.get(), na, Vp.get(), counts.get(), codes.get());
+             vbase.get(), cellmap.get(), c0, static_cast<int64_t>(own_z0), na, Vp.get(), counts.get(), codes.get());
   exclusive_scan_u64(ctx, counts.get(), offs.get(), na);
   const uint64_t last = read_scalar(ctx, offs.get() + na - 1) + read_scalar(ctx, counts.get() + na - 1);
   const uint64_t nf = last >> 32, nextra = last & 0xffffffffu;
-  res.nv = nv_patch + nextra;
+  res.nvp_own = nv_patch - shift;
+  res.n_extra = nextra;
+  res.nv = res.nvp_own + nextra;
   res.nf = nf;
   res.n_quads = 0;
-  res.V.alloc(3 * res.nv, ctx.stream);
+  res.V.alloc(3 * (res.nv ? res.nv : 1), ctx.stream);
   res.F.alloc(3 * (nf ? nf : 1), ctx.stream);
-  PCU_CUDA(cudaMemcpyAsync(res.V.get(), Vp.get(), 3 * nv_patch * sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+  if (res.nvp_own)
+    PCU_CUDA(cudaMemcpyAsync(res.V.get(), Vp.get() + 3 * shift, 3 * res.nvp_own * sizeof(double),
+                             cudaMemcpyDeviceToDevice, ctx.stream));
   PCU_LAUNCH(ctx, k_quad_write, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
-             vbase.get(), cellmap.get(), na, codes.get(), offs.get(), nv_patch, beta, res.V.get(), res.F.get());
+             vbase.get(), cellmap.get(), c0, na, codes.get(), offs.get(), nv_patch, static_cast<int64_t>(shift), beta,
+             res.V.get(), res.F.get());
+}
+
+namespace {
+__global__ void k_rebase(int32_t* __restrict__ F, int64_t n, int64_t patch_base, int64_t nvp_own, int64_t extra_base) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int64_t v = F[i];
+  F[i] = static_cast<int32_t>(v < nvp_own ? patch_base + v : extra_base + (v - nvp_own));
+}
+}  // namespace
+
+void mesh_rebase(Ctx& ctx, int32_t* dF, int64_t nidx, int64_t patch_base, int64_t nvp_own, int64_t extra_base) {
+  if (nidx <= 0) return;
+  PCU_LAUNCH(ctx, k_rebase, grid_for(nidx, 256), 256, 0, dF, nidx, patch_base, nvp_own, extra_base);
+}
+
+void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res) {
+  dmc_extract_slab(ctx, d_sdf, R, 0, R + 1, 0, R, beta, res);
 }
 
 }  // namespace pcu

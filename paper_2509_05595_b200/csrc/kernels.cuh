@@ -24,8 +24,16 @@ struct DmcResult {
   DevBuf<double> V;
   DevBuf<int32_t> F;
   uint64_t nv = 0, nf = 0, n_quads = 0;
+  uint64_t nvp_own = 0, n_extra = 0;  // V = [own patch vertices, extra (4-split) vertices]
 };
 void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res);
+// z-slab extraction: d_planes holds lattice planes [pz0, pz1); cells of layers
+// [own_z0, own_z1) emit faces; the layer below only lends vertex ids.  Face indices are relative
+// to the first own patch vertex (negative = the previous slab's top layer); see mesh_rebase.
+void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, int own_z0, int own_z1, double beta,
+                      DmcResult& res);
+// F[i] -> patch_base + F[i] if F[i] < nvp_own, else extra_base + (F[i] - nvp_own)
+void mesh_rebase(Ctx& ctx, int32_t* dF, int64_t nidx, int64_t patch_base, int64_t nvp_own, int64_t extra_base);
 void dmc_table_host(int32_t* out);
 
 // ---- tri_isect (isect.cu)
