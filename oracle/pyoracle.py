@@ -68,6 +68,13 @@ def lib():
         L.orc_simplify.argtypes = [f64p, C.c_int64, i32p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int, i64p]
         L.orc_simplify_fetch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_link_condition.argtypes = [f64p, C.c_int64, i32p, C.c_int64, i32p, C.c_int64, i32p]
+        L.orc_topology.argtypes = [i32p, C.c_int64, C.c_int64, i64p]
+        L.orc_topology_lists.argtypes = [C.c_void_p, C.c_void_p]
+        L.orc_nearest.argtypes = [f64p, i32p, C.c_int64, f64p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_sample.restype = C.c_int
+        L.orc_sample.argtypes = [f64p, i32p, C.c_int64, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_max_corner_cos.restype = C.c_double
+        L.orc_max_corner_cos.argtypes = [f64p, i32p, C.c_int64]
         _LIB = L
     return _LIB
 
@@ -93,6 +100,11 @@ def ref():
         L.ref_bvh_overlap_pairs.argtypes = [f64p, C.c_int64, i32p, C.c_int64, C.c_void_p, C.c_int64]
         L.ref_normalize_unit_cube.restype = C.c_int
         L.ref_normalize_unit_cube.argtypes = [f64p, C.c_int64, C.c_double, f64p]
+        L.ref_analyze_topology_lists.restype = C.c_int
+        L.ref_analyze_topology_lists.argtypes = [f64p, C.c_int64, i32p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_nearest_primitive.restype = C.c_int
+        L.ref_nearest_primitive.argtypes = [f64p, C.c_int64, i32p, C.c_int64, f64p, C.c_int64, C.c_void_p,
+                                            C.c_void_p, C.c_void_p]
         _REF = L
     return _REF
 
@@ -301,3 +313,97 @@ def ref_normalize_unit_cube(v, padding: float):
     st = np.zeros(4, np.float64)
     assert ref().ref_normalize_unit_cube(v.ravel(), len(v), padding, st) == 0
     return v, st
+
+
+# ---------------------------------------------------------------- certification / metrics
+SAMPLE_SEED_B = 0x632BE59BD9B4E019  # seed offset of the second mesh's samples (chamfer/hausdorff)
+
+
+def topology(f, nv: int) -> dict:
+    """analyze_topology restatement (mesh.cpp:113-150) with the non-manifold lists."""
+    f = np.ascontiguousarray(f, np.int32).reshape(-1, 3)
+    out = np.zeros(6, np.int64)
+    lib().orc_topology(f, len(f), int(nv), out)
+    edges = np.empty(int(out[4]), np.int64)
+    verts = np.empty(int(out[5]), np.int32)
+    lib().orc_topology_lists(edges.ctypes.data, verts.ctypes.data)
+    return dict(manifold=bool(out[0]), watertight=bool(out[1]), euler=int(out[2]), boundary_edges=int(out[3]),
+                nonmanifold_edges=np.stack([edges >> 32, edges & 0xffffffff], 1).astype(np.int32),
+                nonmanifold_vertices=verts)
+
+
+def nearest(v, f, pts):
+    """Brute-force nearest face per point (lbvh.cpp:192-237 semantics): (face, dist, closest)."""
+    v, f = _vf(v, f)
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    face = np.empty(len(pts), np.int32)
+    dist = np.empty(len(pts))
+    clo = np.empty((len(pts), 3))
+    lib().orc_nearest(v, f, len(f), pts.ravel(), len(pts), face.ctypes.data, dist.ctypes.data, clo.ctypes.data)
+    return face, dist, clo
+
+
+def sample(v, f, n: int, seed: int):
+    """Pinned area-weighted sampler -> (points [n,3], face ids, total area); None for zero area."""
+    v, f = _vf(v, f)
+    pts = np.empty((n, 3))
+    fid = np.empty(n, np.int32)
+    area = C.c_double()
+    rc = lib().orc_sample(v, f, len(f), int(n), int(seed) & (2**64 - 1), pts.ctypes.data, fid.ctypes.data,
+                          C.byref(area))
+    if rc != 0:
+        return None
+    return pts, fid, area.value
+
+
+def _directed(va, fa, vb, fb, n, seed):
+    s = sample(va, fa, n, seed)
+    if s is None:
+        raise ValueError("zero-area mesh")
+    _, d, _ = nearest(vb, fb, s[0])
+    return d, s[2]
+
+
+def chamfer(va, fa, vb, fb, n: int = 16384, seed: int = 42) -> float:
+    """(A(a)/n) sum d^2(s_i(a), b) + (A(b)/n) sum d^2(t_j(b), a) (SPEC quality_metrics)."""
+    da, aa = _directed(va, fa, vb, fb, n, seed)
+    db, ab = _directed(vb, fb, va, fa, n, seed + SAMPLE_SEED_B)
+    return aa / n * float(np.sum(da * da)) + ab / n * float(np.sum(db * db))
+
+
+def hausdorff(va, fa, vb, fb, n: int = 16384, seed: int = 42) -> float:
+    da, _ = _directed(va, fa, vb, fb, n, seed)
+    db, _ = _directed(vb, fb, va, fa, n, seed + SAMPLE_SEED_B)
+    return float(max(da.max(), db.max()))
+
+
+def min_internal_angle(v, f) -> float:
+    v, f = _vf(v, f)
+    c = lib().orc_max_corner_cos(v, f, len(f))
+    return float(np.degrees(np.arccos(c)))
+
+
+def ref_topology_full(v, f) -> dict:
+    v, f = _vf(v, f)
+    out = np.zeros(6, np.int64)
+    rc = ref().ref_analyze_topology(v, len(v), f, len(f), out)
+    assert rc == 0
+    edges = np.empty(int(out[4]), np.int64)
+    verts = np.empty(int(out[5]), np.int32)
+    rc = ref().ref_analyze_topology_lists(v, len(v), f, len(f), edges.ctypes.data, verts.ctypes.data)
+    assert rc == 0
+    return dict(manifold=bool(out[0]), watertight=bool(out[1]), euler=int(out[2]), boundary_edges=int(out[3]),
+                nonmanifold_edges=np.stack([edges >> 32, edges & 0xffffffff], 1).astype(np.int32),
+                nonmanifold_vertices=verts)
+
+
+def ref_nearest(v, f, pts):
+    v, f = _vf(v, f)
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    face = np.empty(len(pts), np.int32)
+    dist = np.empty(len(pts))
+    clo = np.empty((len(pts), 3))
+    rc = ref().ref_nearest_primitive(v, len(v), f, len(f), pts.ravel(), len(pts), face.ctypes.data,
+                                     dist.ctypes.data, clo.ctypes.data)
+    assert rc == 0
+    return face, dist, clo

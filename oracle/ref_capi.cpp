@@ -70,6 +70,39 @@ int ref_analyze_topology(const double* v, int64_t nv, const int32_t* f, int64_t 
   }
 }
 
+// mesh.cpp:113-150, the lists: nonmanifold edges as (a<<32|b) in std::map order, vertices ascending
+int ref_analyze_topology_lists(const double* v, int64_t nv, const int32_t* f, int64_t nf, int64_t* edges,
+                               int32_t* verts) {
+  try {
+    IndexedMesh m = make_mesh(v, nv, f, nf);
+    TopologySummary s = analyze_topology(m);
+    for (size_t i = 0; i < s.nonmanifold_edges.size(); ++i)
+      edges[i] = (static_cast<int64_t>(s.nonmanifold_edges[i].a) << 32) | static_cast<uint32_t>(s.nonmanifold_edges[i].b);
+    for (size_t i = 0; i < s.nonmanifold_vertices.size(); ++i) verts[i] = s.nonmanifold_vertices[i];
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// lbvh.cpp:192-237: TriangleBvh::nearest_primitive for a batch of points
+int ref_nearest_primitive(const double* v, int64_t nv, const int32_t* f, int64_t nf, const double* pts, int64_t n,
+                          int32_t* face, double* dist, double* closest) {
+  try {
+    IndexedMesh m = make_mesh(v, nv, f, nf);
+    const TriangleBvh bvh = TriangleBvh::build(m);
+    for (int64_t i = 0; i < n; ++i) {
+      const NearestHit h = bvh.nearest_primitive(m, Vec3d(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]));
+      face[i] = h.primitive;
+      dist[i] = h.distance;
+      for (int k = 0; k < 3; ++k) closest[3 * i + k] = h.point[k];
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 // mesh.cpp:301-358 for a list of edges (a,b); result 1/0, -1 = unknown edge (invalid_argument).
 int ref_link_condition(const double* v, int64_t nv, const int32_t* f, int64_t nf,
                        const int32_t* edges, int64_t ne, int32_t* out) {
