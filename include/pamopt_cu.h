@@ -157,6 +157,49 @@ int pamopt_cu_simplify(pamopt_cu_mesh mesh, int64_t target_faces,
                        const pamopt_cu_simplify_params* params, pamopt_cu_simplify_stats* stats,
                        int64_t* per_iter_collapses, int64_t per_iter_cap);
 
+/* ---- certification and quality metrics ---------------------------- */
+/* analyze_topology (mesh.cpp:113-150; TopologySummary mesh.hpp:44-51) */
+typedef struct {
+  int32_t manifold;
+  int32_t watertight;
+  int64_t euler_characteristic;
+  int64_t boundary_edge_count;
+  int64_t n_nonmanifold_edges;
+  int64_t n_nonmanifold_vertices;
+} pamopt_cu_topology;
+/* lists (count-then-fill): nonmanifold_edges = int32[2*cap_edges] (a<b, ascending),
+ * nonmanifold_vertices = int32[cap_vertices] (ascending); either may be NULL */
+int pamopt_cu_analyze_topology(pamopt_cu_mesh mesh, pamopt_cu_topology* out, int32_t* nonmanifold_edges,
+                               int64_t cap_edges, int32_t* nonmanifold_vertices, int64_t cap_vertices);
+/* TriangleBvh::nearest_primitive (lbvh.cpp:192-237) for n host points: face (-1 for an empty
+ * mesh), distance, closest point (double[3n]); ties go to the lower face id.  Any output may be NULL. */
+int pamopt_cu_nearest_primitive(pamopt_cu_mesh mesh, const double* points, int64_t n, int32_t* face,
+                                double* distance, double* closest);
+/* the pinned area-weighted sampler: points double[3n], faces int32[n] (may be NULL) */
+int pamopt_cu_sample_points(pamopt_cu_mesh mesh, int64_t n, uint64_t seed, double* points, int32_t* faces,
+                            double* total_area);
+/* quality_metrics: squared-distance Chamfer and sampled symmetric Hausdorff with n
+ * samples per direction (mesh a uses seed, mesh b seed + 0x632BE59BD9B4E019); EINVAL for a
+ * zero-area mesh */
+int pamopt_cu_chamfer(pamopt_cu_mesh a, pamopt_cu_mesh b, int64_t n_samples, uint64_t seed, double* out);
+int pamopt_cu_hausdorff(pamopt_cu_mesh a, pamopt_cu_mesh b, int64_t n_samples, uint64_t seed, double* out);
+/* minimum corner angle in degrees; a zero-area face counts as 0 */
+int pamopt_cu_min_internal_angle(pamopt_cu_mesh mesh, double* degrees);
+/* MeshReport (SPEC.md quality_metrics): every field in one call; reference may be NULL (cd/hd = NaN) */
+typedef struct {
+  double cd;
+  double hd;
+  double min_angle_deg;
+  int32_t manifold;
+  int32_t watertight;
+  int32_t intersection_free;
+  int32_t pad_;
+  int64_t n_faces;
+  int64_t n_vertices;
+} pamopt_cu_mesh_report;
+int pamopt_cu_report(pamopt_cu_mesh reference, pamopt_cu_mesh mesh, int64_t n_samples, uint64_t seed,
+                     pamopt_cu_mesh_report* out);
+
 /* ---- pipeline: UDF -> SDF -> DMC -> QEM ------------------------------------------------ */
 int pamopt_cu_remesh(pamopt_cu_ctx ctx, pamopt_cu_mesh input, int32_t R, double eps, double beta,
                      int64_t target_faces, const pamopt_cu_simplify_params* params,

@@ -40,6 +40,21 @@ class StageTimes(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class Topology(C.Structure):
+    _fields_ = [("manifold", C.c_int32), ("watertight", C.c_int32), ("euler_characteristic", C.c_int64),
+                ("boundary_edge_count", C.c_int64), ("n_nonmanifold_edges", C.c_int64),
+                ("n_nonmanifold_vertices", C.c_int64)]
+
+
+class MeshReport(C.Structure):
+    _fields_ = [("cd", C.c_double), ("hd", C.c_double), ("min_angle_deg", C.c_double), ("manifold", C.c_int32),
+                ("watertight", C.c_int32), ("intersection_free", C.c_int32), ("pad_", C.c_int32),
+                ("n_faces", C.c_int64), ("n_vertices", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
 class PamoptError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
@@ -94,6 +109,13 @@ _SIGS = {
     "pamopt_cu_self_intersections": (C.c_int, [vp, vp, i64, P(i64)]),
     "pamopt_cu_tri_tri_pairs": (C.c_int, [vp, vp, i64, vp]),
     "pamopt_cu_simplify": (C.c_int, [vp, i64, P(SimplifyParams), P(SimplifyStats), vp, i64]),
+    "pamopt_cu_analyze_topology": (C.c_int, [vp, P(Topology), vp, i64, vp, i64]),
+    "pamopt_cu_nearest_primitive": (C.c_int, [vp, vp, i64, vp, vp, vp]),
+    "pamopt_cu_sample_points": (C.c_int, [vp, i64, C.c_uint64, vp, vp, P(dbl)]),
+    "pamopt_cu_chamfer": (C.c_int, [vp, vp, i64, C.c_uint64, P(dbl)]),
+    "pamopt_cu_hausdorff": (C.c_int, [vp, vp, i64, C.c_uint64, P(dbl)]),
+    "pamopt_cu_min_internal_angle": (C.c_int, [vp, P(dbl)]),
+    "pamopt_cu_report": (C.c_int, [vp, vp, i64, C.c_uint64, P(MeshReport)]),
     "pamopt_cu_remesh": (C.c_int, [vp, vp, i32, dbl, dbl, i64, P(SimplifyParams), P(vp), P(SimplifyStats),
                                    P(StageTimes)]),
     "pamopt_cu_remesh_host": (C.c_int, [vp, vp, i64, vp, i64, i32, dbl, dbl, i64, P(SimplifyParams), P(i64),

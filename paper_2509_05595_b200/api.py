@@ -355,3 +355,75 @@ def remesh_device(mesh: DeviceMesh, R: int, target_faces: int, eps: float | None
     check(lib().pamopt_cu_remesh(mesh.ctx.h, mesh.h, int(R), default_eps(R) if eps is None else float(eps),
                                  float(beta), int(target_faces), C.byref(p), C.byref(h), C.byref(st), C.byref(tm)))
     return DeviceMesh(h, mesh.ctx), st.as_dict(), tm.as_dict()
+
+
+# ------------------------------------------------------- certification / quality metrics
+SAMPLE_SEED_B = 0x632BE59BD9B4E019
+
+
+def analyze_topology(mesh, ctx: Context | None = None) -> dict:
+    """analyze_topology (mesh.cpp:113-150) on the GPU: TopologySummary with the lists."""
+    m = _mesh(mesh, ctx)
+    t = _lib.Topology()
+    check(lib().pamopt_cu_analyze_topology(m.h, C.byref(t), None, 0, None, 0))
+    e = np.empty((t.n_nonmanifold_edges, 2), np.int32)
+    v = np.empty(t.n_nonmanifold_vertices, np.int32)
+    check(lib().pamopt_cu_analyze_topology(m.h, C.byref(t), ptr(e), len(e), ptr(v), len(v)))
+    return dict(manifold=bool(t.manifold), watertight=bool(t.watertight), euler=int(t.euler_characteristic),
+                boundary_edges=int(t.boundary_edge_count), nonmanifold_edges=e, nonmanifold_vertices=v)
+
+
+def nearest_primitive(mesh, points, ctx: Context | None = None):
+    """TriangleBvh::nearest_primitive (lbvh.cpp:192-237) per point: (face, distance, closest)."""
+    m = _mesh(mesh, ctx)
+    p = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    face = np.empty(len(p), np.int32)
+    dist = np.empty(len(p))
+    clo = np.empty((len(p), 3))
+    check(lib().pamopt_cu_nearest_primitive(m.h, ptr(p), len(p), ptr(face), ptr(dist), ptr(clo)))
+    return face, dist, clo
+
+
+def sample_points(mesh, n: int, seed: int, ctx: Context | None = None):
+    """The pinned area-weighted sampler: (points [n,3], face ids, total area)."""
+    m = _mesh(mesh, ctx)
+    pts = np.empty((n, 3))
+    fid = np.empty(n, np.int32)
+    area = C.c_double()
+    check(lib().pamopt_cu_sample_points(m.h, int(n), int(seed) & (2**64 - 1), ptr(pts), ptr(fid), C.byref(area)))
+    return pts, fid, area.value
+
+
+def chamfer(a, b, n_samples: int = 16384, seed: int = 42, ctx: Context | None = None) -> float:
+    ma, mb = _mesh(a, ctx), _mesh(b, ctx)
+    out = C.c_double()
+    check(lib().pamopt_cu_chamfer(ma.h, mb.h, int(n_samples), int(seed) & (2**64 - 1), C.byref(out)))
+    return out.value
+
+
+def hausdorff(a, b, n_samples: int = 16384, seed: int = 42, ctx: Context | None = None) -> float:
+    ma, mb = _mesh(a, ctx), _mesh(b, ctx)
+    out = C.c_double()
+    check(lib().pamopt_cu_hausdorff(ma.h, mb.h, int(n_samples), int(seed) & (2**64 - 1), C.byref(out)))
+    return out.value
+
+
+def min_internal_angle(mesh, ctx: Context | None = None) -> float:
+    m = _mesh(mesh, ctx)
+    out = C.c_double()
+    check(lib().pamopt_cu_min_internal_angle(m.h, C.byref(out)))
+    return out.value
+
+
+def mesh_report(mesh, reference=None, n_samples: int = 16384, seed: int = 42, ctx: Context | None = None) -> dict:
+    """MeshReport (SPEC quality_metrics): cd/hd vs reference (NaN without one), min angle,
+    manifold, watertight, intersection_free, counts."""
+    m = _mesh(mesh, ctx)
+    r = _mesh(reference, m.ctx) if reference is not None else None  # keep alive across the call
+    out = _lib.MeshReport()
+    check(lib().pamopt_cu_report(r.h if r is not None else None, m.h, int(n_samples), int(seed) & (2**64 - 1),
+                                 C.byref(out)))
+    d = out.as_dict()
+    for k in ("manifold", "watertight", "intersection_free"):
+        d[k] = bool(d[k])
+    return d

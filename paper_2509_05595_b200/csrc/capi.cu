@@ -4,6 +4,8 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <cmath>
+#include <limits>
 #include <cstring>
 #include <string>
 
@@ -482,6 +484,158 @@ int pamopt_cu_mesh_rebase(pamopt_cu_mesh m, int64_t patch_base, int64_t nvp_own,
     pcu::Ctx& ctx = m->owner->ctx;
     pcu::DeviceGuard g(ctx.device);
     pcu::mesh_rebase(ctx, m->F.get(), 3 * m->nf, patch_base, nvp_own, extra_base);
+  });
+}
+
+// ------------------------------------------------------------ certification / metrics
+static constexpr uint64_t kSeedB = 0x632BE59BD9B4E019ull;
+
+static void check_indices(pcu::Ctx& ctx, const pamopt_cu_mesh_s* m) {
+  if (m->nf == 0) return;
+  const std::vector<int32_t> mm = pcu::index_range(ctx, m->F.get(), 3 * m->nf);
+  PCU_REQUIRE(mm[0] >= 0 && mm[1] < m->nv, PAMOPT_CU_EINVAL, "invalid mesh: face index out of range");
+}
+
+int pamopt_cu_analyze_topology(pamopt_cu_mesh m, pamopt_cu_topology* out, int32_t* edges, int64_t cap_e,
+                               int32_t* verts, int64_t cap_v) {
+  return guarded([&] {
+    PCU_REQUIRE(m && out, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    check_indices(ctx, m);
+    pcu::TopologyResult t;
+    pcu::analyze_topology(ctx, m->F.get(), m->nf, m->nv, t);
+    out->manifold = t.manifold;
+    out->watertight = t.watertight;
+    out->euler_characteristic = t.euler;
+    out->boundary_edge_count = t.boundary;
+    out->n_nonmanifold_edges = static_cast<int64_t>(t.nm_edges.size());
+    out->n_nonmanifold_vertices = static_cast<int64_t>(t.nm_verts.size());
+    if (edges)
+      for (int64_t i = 0; i < std::min<int64_t>(cap_e, out->n_nonmanifold_edges); ++i) {
+        edges[2 * i] = static_cast<int32_t>(t.nm_edges[i] >> 32);
+        edges[2 * i + 1] = static_cast<int32_t>(t.nm_edges[i] & 0xffffffffu);
+      }
+    if (verts)
+      for (int64_t i = 0; i < std::min<int64_t>(cap_v, out->n_nonmanifold_vertices); ++i) verts[i] = t.nm_verts[i];
+  });
+}
+
+int pamopt_cu_nearest_primitive(pamopt_cu_mesh m, const double* pts, int64_t n, int32_t* face, double* dist,
+                                double* closest) {
+  return guarded([&] {
+    PCU_REQUIRE(m && (n == 0 || pts) && n >= 0, PAMOPT_CU_EINVAL, "bad arguments");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    if (n == 0) return;
+    if (m->nf == 0) {  // empty tree: primitive -1, distance +INF (lbvh.cpp:194-197)
+      for (int64_t i = 0; i < n; ++i) {
+        if (face) face[i] = -1;
+        if (dist) dist[i] = std::numeric_limits<double>::infinity();
+        if (closest) closest[3 * i] = closest[3 * i + 1] = closest[3 * i + 2] = 0.0;
+      }
+      return;
+    }
+    check_indices(ctx, m);
+    pcu::DevBuf<double> dp(3 * n, ctx.stream), d2(n, ctx.stream), dc(3 * n, ctx.stream);
+    pcu::DevBuf<int32_t> df(n, ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(dp.get(), pts, 3 * n * sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+    pcu::nearest_primitive(ctx, m->V.get(), m->F.get(), m->nf, dp.get(), n, df.get(), d2.get(), dc.get());
+    std::vector<double> h2(n);
+    PCU_CUDA(cudaMemcpyAsync(h2.data(), d2.get(), n * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (face) PCU_CUDA(cudaMemcpyAsync(face, df.get(), n * 4, cudaMemcpyDeviceToHost, ctx.stream));
+    if (closest) PCU_CUDA(cudaMemcpyAsync(closest, dc.get(), 3 * n * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (dist)
+      for (int64_t i = 0; i < n; ++i) dist[i] = std::sqrt(h2[i]);
+  });
+}
+
+int pamopt_cu_sample_points(pamopt_cu_mesh m, int64_t n, uint64_t seed, double* pts, int32_t* faces,
+                            double* total_area) {
+  return guarded([&] {
+    PCU_REQUIRE(m && n >= 0 && (n == 0 || pts), PAMOPT_CU_EINVAL, "bad arguments");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    check_indices(ctx, m);
+    pcu::DevBuf<double> dp(3 * (n ? n : 1), ctx.stream);
+    pcu::DevBuf<int32_t> df(n ? n : 1, ctx.stream);
+    double area = 0.0;
+    PCU_REQUIRE(pcu::sample_points(ctx, m->V.get(), m->F.get(), m->nf, n, seed, dp.get(), df.get(), &area),
+                PAMOPT_CU_EINVAL, "sample_points: zero-area mesh");
+    if (n) PCU_CUDA(cudaMemcpyAsync(pts, dp.get(), 3 * n * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (n && faces) PCU_CUDA(cudaMemcpyAsync(faces, df.get(), n * 4, cudaMemcpyDeviceToHost, ctx.stream));
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (total_area) *total_area = area;
+  });
+}
+
+static void two_sided(pamopt_cu_mesh a, pamopt_cu_mesh b, int64_t n, uint64_t seed, double& cd, double& hd) {
+  PCU_REQUIRE(a && b && n > 0, PAMOPT_CU_EINVAL, "bad arguments");
+  PCU_REQUIRE(a->owner == b->owner, PAMOPT_CU_EINVAL, "metrics: meshes belong to different contexts");
+  pcu::Ctx& ctx = a->owner->ctx;
+  pcu::DeviceGuard g(ctx.device);
+  check_indices(ctx, a);
+  check_indices(ctx, b);
+  double sa, ma, aa, sb, mb, ab;
+  pcu::directed_d2(ctx, a->V.get(), a->F.get(), a->nf, b->V.get(), b->F.get(), b->nf, n, seed, sa, ma, aa);
+  pcu::directed_d2(ctx, b->V.get(), b->F.get(), b->nf, a->V.get(), a->F.get(), a->nf, n, seed + kSeedB, sb, mb, ab);
+  cd = aa / static_cast<double>(n) * sa + ab / static_cast<double>(n) * sb;
+  hd = std::sqrt(std::max(ma, mb));
+}
+
+int pamopt_cu_chamfer(pamopt_cu_mesh a, pamopt_cu_mesh b, int64_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    PCU_REQUIRE(out, PAMOPT_CU_EINVAL, "null argument");
+    double cd, hd;
+    two_sided(a, b, n, seed, cd, hd);
+    *out = cd;
+  });
+}
+
+int pamopt_cu_hausdorff(pamopt_cu_mesh a, pamopt_cu_mesh b, int64_t n, uint64_t seed, double* out) {
+  return guarded([&] {
+    PCU_REQUIRE(out, PAMOPT_CU_EINVAL, "null argument");
+    double cd, hd;
+    two_sided(a, b, n, seed, cd, hd);
+    *out = hd;
+  });
+}
+
+int pamopt_cu_min_internal_angle(pamopt_cu_mesh m, double* deg) {
+  return guarded([&] {
+    PCU_REQUIRE(m && deg, PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(m->nf > 0, PAMOPT_CU_EINVAL, "min_internal_angle: empty mesh");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    check_indices(ctx, m);
+    const double c = pcu::max_corner_cos(ctx, m->V.get(), m->F.get(), m->nf);
+    *deg = std::acos(c) * (180.0 / 3.14159265358979323846);
+  });
+}
+
+int pamopt_cu_report(pamopt_cu_mesh ref, pamopt_cu_mesh m, int64_t n, uint64_t seed, pamopt_cu_mesh_report* out) {
+  return guarded([&] {
+    PCU_REQUIRE(m && out, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    check_indices(ctx, m);
+    *out = pamopt_cu_mesh_report{};
+    out->n_faces = m->nf;
+    out->n_vertices = m->nv;
+    out->cd = out->hd = std::numeric_limits<double>::quiet_NaN();
+    if (ref) two_sided(ref, m, n, seed, out->cd, out->hd);
+    out->min_angle_deg = m->nf ? std::acos(pcu::max_corner_cos(ctx, m->V.get(), m->F.get(), m->nf)) *
+                                     (180.0 / 3.14159265358979323846)
+                               : 0.0;
+    pcu::TopologyResult t;
+    pcu::analyze_topology(ctx, m->F.get(), m->nf, m->nv, t);
+    out->manifold = t.manifold;
+    out->watertight = t.watertight;
+    const std::vector<int32_t> pairs =
+        m->nf >= 2 ? pcu::self_intersections(ctx, m->V.get(), m->nv, m->F.get(), m->nf, nullptr, nullptr)
+                   : std::vector<int32_t>();
+    out->intersection_free = pairs.empty() ? 1 : 0;
   });
 }
 

@@ -36,6 +36,25 @@ void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, 
 void mesh_rebase(Ctx& ctx, int32_t* dF, int64_t nidx, int64_t patch_base, int64_t nvp_own, int64_t extra_base);
 void dmc_table_host(int32_t* out);
 
+// ---- certification / quality metrics (metrics.cu)
+struct TopologyResult {
+  int32_t manifold = 0, watertight = 0;
+  int64_t euler = 0, boundary = 0;
+  std::vector<uint64_t> nm_edges;  // (a<<32|b), ascending
+  std::vector<int32_t> nm_verts;   // ascending
+};
+void analyze_topology(Ctx& ctx, const int32_t* dF, int64_t nf, int64_t nv, TopologyResult& out);
+// nearest face per point (lbvh.cpp:192-237 semantics): squared distance, face (-1: none), closest
+void nearest_primitive(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf, const double* d_pts, int64_t n,
+                       int32_t* d_face, double* d_d2, double* d_closest);
+// pinned area-weighted sampler; false for a zero-area (or empty) mesh
+bool sample_points(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf, int64_t n, uint64_t seed,
+                   double* d_pts, int32_t* d_fid, double* total_area);
+void directed_d2(Ctx& ctx, const double* Va, const int32_t* Fa, int64_t nfa, const double* Vb, const int32_t* Fb,
+                 int64_t nfb, int64_t n, uint64_t seed, double& sum_d2, double& max_d2, double& area_a);
+double max_corner_cos(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf);
+std::vector<int32_t> index_range(Ctx& ctx, const int32_t* d, int64_t n);  // {min, max}
+
 // ---- tri_isect (isect.cu)
 // all intersecting pairs (i<j) among faces with alive[i] (alive may be null); if `query` is
 // non-null only pairs with at least one query face are reported.  Result sorted (host).
