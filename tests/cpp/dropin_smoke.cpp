@@ -7,9 +7,11 @@
 #include <map>
 
 #include "pamopt/dual_mc.hpp"
+#include "pamopt/lbvh.hpp"
 #include "pamopt/mesh.hpp"
 #include "pamopt/mesh_io.hpp"
 #include "pamopt/pipeline.hpp"
+#include "pamopt/quality_metrics.hpp"
 #include "pamopt/simplify.hpp"
 #include "pamopt/tri_isect.hpp"
 #include "pamopt/voxel_field.hpp"
@@ -68,14 +70,32 @@ int main() {
   StageTimings tm;
   IndexedMesh e = remesh(in, R, 1000, SimplifyParams{}, 0.0, 5.0, nullptr, &tm);
   const bool same = e.faces == s.faces && e.vertices == s.vertices;
+  // GPU certification twins vs the reference's own CPU implementations
+  const TopologySummary tg = cuda::analyze_topology(d);
+  const bool topo_same = tg.manifold == td.manifold && tg.watertight == td.watertight &&
+                         tg.euler_characteristic == td.euler_characteristic &&
+                         tg.boundary_edge_count == td.boundary_edge_count &&
+                         tg.nonmanifold_edges == td.nonmanifold_edges &&
+                         tg.nonmanifold_vertices == td.nonmanifold_vertices;
+  const TriangleBvh bvh = TriangleBvh::build(s);
+  std::vector<Vec3d> q;
+  for (int i = 0; i < 512; ++i) q.push_back(d.vertices[(i * 7919) % d.vertex_count()] * 1.01);
+  const std::vector<NearestHit> hg = cuda::nearest_primitives(s, q);
+  bool near_same = true;
+  for (size_t i = 0; i < q.size(); ++i) {
+    const NearestHit h = bvh.nearest_primitive(s, q[i]);  // reference lbvh.cpp:192-237
+    near_same = near_same && h.primitive == hg[i].primitive && h.distance == hg[i].distance && h.point == hg[i].point;
+  }
+  const MeshReport rep = mesh_report(s, &in, 4096);
   std::printf("{\"dmc_faces\": %d, \"dmc_manifold\": %d, \"dmc_watertight\": %d, \"dmc_euler\": %d, "
               "\"dmc_isect\": %zu, \"out_faces\": %d, \"out_manifold\": %d, \"out_euler\": %d, \"out_isect\": %zu, "
-              "\"iterations\": %lld, \"pipeline_equal\": %d, \"total_ms\": %.3f}\n",
+              "\"iterations\": %lld, \"pipeline_equal\": %d, \"total_ms\": %.3f, \"topology_equal\": %d, "
+              "\"nearest_equal\": %d, \"cd\": %.3e, \"hd\": %.3e, \"min_angle\": %.2f}\n",
               d.face_count(), td.manifold, td.watertight, td.euler_characteristic, pd.size(), s.face_count(),
               ts.manifold, ts.euler_characteristic, ps.size(), static_cast<long long>(st.iterations), same,
-              tm.total_ms);
+              tm.total_ms, topo_same, near_same, rep.cd, rep.hd, rep.min_angle_deg);
   const bool ok = td.manifold && td.watertight && pd.empty() && ts.manifold && ps.empty() && s.face_count() <= 1000 &&
-                  same;
+                  same && topo_same && near_same && rep.watertight && rep.intersection_free;
   std::fflush(stdout);
   std::_Exit(ok ? 0 : 1);  // parallel.cpp pool: never run static destructors
 }
