@@ -31,7 +31,7 @@ namespace {
 constexpr double kHalfSqrt3 = 0.8660254037844386;
 constexpr int kChunk = 128;  // triangles per brick work item
 
-struct __align__(16) TriD {
+struct __align__(16) TriD {  // loaded as sizeof/16 int4 words by k_brick
   double a[3], b[3], c[3], lo[3], hi[3];
   float ab[3], ac[3];  // local frame (b-a, c-a computed in FP64, rounded to FP32)
   float n[3];          // unit normal (FP32)
@@ -39,7 +39,9 @@ struct __align__(16) TriD {
   float blo[3], bhi[3];  // AABB in the local frame (FP32)
   float L2;            // max squared edge length
   int wc;              // well conditioned: every corner angle has sin^2 >= 0.01
+  float ie[3];         // FP32 1/|ab|^2, 1/|bc|^2, 1/|ca|^2 (0 for a zero-length edge; filter only)
 };
+static_assert(sizeof(TriD) % 16 == 0 && sizeof(TriD) / 16 <= 32, "TriD is copied by one warp in int4 words");
 
 // FP32 point-triangle squared distance in the triangle's local frame (p relative to a).
 // Used only as a certified filter for well-conditioned triangles (see survives / k_brick): its
@@ -51,11 +53,10 @@ __device__ __forceinline__ float fdot(float ax, float ay, float az, float bx, fl
   return __fmaf_rn(ax, bx, __fmaf_rn(ay, by, __fmul_rn(az, bz)));
 }
 __device__ __forceinline__ float fseg_sq(float px, float py, float pz, float ax, float ay, float az, float bx, float by,
-                                         float bz) {
+                                         float bz, float inv_den) {
   const float ux = bx - ax, uy = by - ay, uz = bz - az;
   const float wx = px - ax, wy = py - ay, wz = pz - az;
-  const float den = fdot(ux, uy, uz, ux, uy, uz);
-  float t = den > 0.f ? __fdividef(fdot(wx, wy, wz, ux, uy, uz), den) : 0.f;
+  float t = fdot(wx, wy, wz, ux, uy, uz) * inv_den;  // inv_den = 0 for a zero-length edge
   t = fminf(fmaxf(t, 0.f), 1.f);
   const float qx = __fmaf_rn(-t, ux, wx), qy = __fmaf_rn(-t, uy, wy), qz = __fmaf_rn(-t, uz, wz);
   return fdot(qx, qy, qz, qx, qy, qz);
@@ -70,9 +71,9 @@ __device__ __forceinline__ float fptri_sq(const TriD& t, float px, float py, flo
   const float d20 = fdot(qx, qy, qz, bx, by, bz), d21 = fdot(qx, qy, qz, cx, cy, cz);
   const float v = __fmaf_rn(t.binv[0], d20, t.binv[1] * d21), w = __fmaf_rn(t.binv[1], d20, t.binv[2] * d21);
   if (v >= 0.f && w >= 0.f && v + w <= 1.f) best = dn * dn;
-  best = fminf(best, fseg_sq(px, py, pz, 0.f, 0.f, 0.f, bx, by, bz));
-  best = fminf(best, fseg_sq(px, py, pz, bx, by, bz, cx, cy, cz));
-  best = fminf(best, fseg_sq(px, py, pz, cx, cy, cz, 0.f, 0.f, 0.f));
+  best = fminf(best, fseg_sq(px, py, pz, 0.f, 0.f, 0.f, bx, by, bz, t.ie[0]));
+  best = fminf(best, fseg_sq(px, py, pz, bx, by, bz, cx, cy, cz, t.ie[1]));
+  best = fminf(best, fseg_sq(px, py, pz, cx, cy, cz, 0.f, 0.f, 0.f, t.ie[2]));
   return best;
 }
 
@@ -97,8 +98,15 @@ __device__ __forceinline__ bool survives(const TriD& t, double cx, double cy, do
   return sqrt(d2) <= thr;
 }
 
+// 1/r for a power of two r, exactly (exponent bits): x * inv_pow2(r) == x / r bit for bit
+__device__ __forceinline__ double inv_pow2(int r) {
+  return __longlong_as_double(static_cast<long long>(1023 - (__ffs(r) - 1)) << 52);
+}
+
+// 3/R + (sqrt(3)/2)/r with R, r powers of two: the products by exact reciprocals equal the
+// quotients bit for bit, and avoid two FP64 divisions per call
 __device__ __forceinline__ double level_thr(int R, int r) {
-  return 3.0 / static_cast<double>(R) + kHalfSqrt3 / static_cast<double>(r);
+  return 3.0 * inv_pow2(R) + kHalfSqrt3 * inv_pow2(r);
 }
 
 __global__ void k_prep(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t nf,
@@ -122,6 +130,10 @@ __global__ void k_prep(const double* __restrict__ V, const int32_t* __restrict__
   }
   const double lab = sqn(ab), lac = sqn(ac), lbc = sqn(bc);
   t.L2 = static_cast<float>(fmax(fmax(lab, lac), lbc));
+  {
+    const float fl[3] = {static_cast<float>(lab), static_cast<float>(lbc), static_cast<float>(lac)};
+    for (int k = 0; k < 3; ++k) t.ie[k] = fl[k] > 0.f ? 1.0f / fl[k] : 0.f;
+  }
   const D3 nv = cross(ab, ac);
   const double n2 = sqn(nv);
   {
@@ -195,7 +207,8 @@ __global__ void k_level0(const TriD* __restrict__ T, int64_t nf, int R, uint64_t
     uint64_t val = 0;
     if (j < n) {
       const int x = lo[0] + j % nx, y = lo[1] + (j / nx) % ny, z = lo[2] + j / (nx * ny);
-      keep = in_slab(z, R, r, zp0, zp1) && survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, thr);
+      const double ir = inv_pow2(r);
+      keep = in_slab(z, R, r, zp0, zp1) && survives(t, (x + 0.5) * ir, (y + 0.5) * ir, (z + 0.5) * ir, thr);
       val = (static_cast<uint64_t>(x + r * (y + r * z)) << 32) | static_cast<uint64_t>(i);
     }
     append(keep, val, out, cnt, cap);
@@ -215,7 +228,8 @@ __global__ void k_refine(const uint64_t* __restrict__ in, uint64_t n_in, const T
     const int px = pc % rp, py = (pc / rp) % rp, pz = pc / (rp * rp);
     const int x = 2 * px + (ch & 1), y = 2 * py + ((ch >> 1) & 1), z = 2 * pz + ((ch >> 2) & 1);
     const TriD t = T[tri];
-    keep = in_slab(z, R, r, zp0, zp1) && survives(t, (x + 0.5) / r, (y + 0.5) / r, (z + 0.5) / r, level_thr(R, r));
+    const double ir = inv_pow2(r);
+    keep = in_slab(z, R, r, zp0, zp1) && survives(t, (x + 0.5) * ir, (y + 0.5) * ir, (z + 0.5) * ir, level_thr(R, r));
     val = (static_cast<uint64_t>(x + r * (y + r * z)) << 32) | tri;
   }
   append(keep, val, out, cnt, cap);
@@ -293,7 +307,11 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
     kk = __shfl_sync(0xffffffffu, kk, 0);
     const uint32_t k = it.begin + kk;
     if (k >= it.end) break;
-    if (lane == 0) tsh[warp] = T[tris[k]];
+    {  // cooperative 16-byte copy of the triangle record
+      constexpr int kW = static_cast<int>(sizeof(TriD) / 16);
+      const int4* src = reinterpret_cast<const int4*>(T + tris[k]);
+      if (lane < kW) reinterpret_cast<int4*>(&tsh[warp])[lane] = __ldg(src + lane);
+    }
     __syncwarp();
     const TriD& t = tsh[warp];
     // level 0 inside the brick: the brick itself survived (the pair exists)
@@ -303,7 +321,7 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
     for (int j = 1; j <= J; ++j) {
       const int lp = j - 1;  // log2 of the parent side
       const int r = rb << j;
-      const double thr = level_thr(R, r);
+      const double thr = level_thr(R, r), ir = inv_pow2(r);
       const int ncand = nsurv * 8;
       int nout = 0;
       for (int base = 0; base < ncand; base += 32) {
@@ -316,7 +334,7 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
           const int x = 2 * px + (ch & 1), y = 2 * py + ((ch >> 1) & 1), z = 2 * pz + ((ch >> 2) & 1);
           cell = x | (y << j) | (z << (2 * j));
           const int gx = (bx << j) + x, gy = (by << j) + y, gz = (bz << j) + z;
-          keep = survives(t, (gx + 0.5) / r, (gy + 0.5) / r, (gz + 0.5) / r, thr);
+          keep = survives(t, (gx + 0.5) * ir, (gy + 0.5) * ir, (gz + 0.5) * ir, thr);
         }
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         if (keep) list[warp][cur ^ 1][nout + __popc(m & lt)] = static_cast<uint16_t>(cell);
@@ -374,12 +392,13 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
     }
     __syncwarp();
     const D3 A{t.a[0], t.a[1], t.a[2]}, Bv{t.b[0], t.b[1], t.b[2]}, Cv{t.c[0], t.c[1], t.c[2]};
+    const double iR = inv_pow2(R);
     for (int i = lane; i < nneed; i += 32) {
       const int pk = vlist[warp][i];
       const int vx = pk & 15, vy = (pk >> 4) & 15, vz = pk >> 8;
       const int v = vx + nv1 * (vy + nv1 * vz);
       const int gx = bx * bs + vx, gy = by * bs + vy, gz = bz * bs + vz;
-      const D3 p{static_cast<double>(gx) / R, static_cast<double>(gy) / R, static_cast<double>(gz) / R};
+      const D3 p{static_cast<double>(gx) * iR, static_cast<double>(gy) * iR, static_cast<double>(gz) * iR};
       if (t.wc) {
         // this triangle cannot lower the vertex's running minimum: skip the FP64 evaluation
         // (the minimum is order independent, so skipping never changes the result).  Cheap
@@ -473,7 +492,8 @@ __global__ void k_debug_pairs(const uint64_t* __restrict__ bpairs, uint64_t n, c
     for (int j = 1; j <= jt && keep; ++j) {
       const int sh = jt - j, r = rb << j;
       const int gx = bx * (1 << j) + (x >> sh), gy = by * (1 << j) + (y >> sh), gz = bz * (1 << j) + (z >> sh);
-      keep = survives(t, (gx + 0.5) / r, (gy + 0.5) / r, (gz + 0.5) / r, level_thr(R, r));
+      const double ir = inv_pow2(r);
+      keep = survives(t, (gx + 0.5) * ir, (gy + 0.5) * ir, (gz + 0.5) * ir, level_thr(R, r));
     }
     const int r = rb << jt;
     const uint64_t gx = bx * side + x, gy = by * side + y, gz = bz * side + z;
