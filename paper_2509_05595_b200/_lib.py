@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpamopt_cu.so")
+LIB_PATH = os.environ.get("PAMOPT_LIB") or os.path.join(HERE, "libpamopt_cu.so")  # PAMOPT_LIB: A/B variants only
 
 OK, EINVAL, ECUDA, ENOMEM, ENUMERIC, ECAP = 0, -1, -2, -3, -4, -5
 

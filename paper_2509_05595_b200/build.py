@@ -28,18 +28,23 @@ def _stale(src_files, target):
     return any(os.path.getmtime(s) > t for s in src_files)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), tag: str = "") -> str:
+    """defines/tag: an A/B variant (-D flags) built into build_obj/<tag>/ and libpamopt_cu_<tag>.so;
+    select it at run time with PAMOPT_LIB=<path> (experiments only)."""
+    out = OUT if not tag else OUT.replace(".so", f"_{tag}.so")
+    obj_dir = OBJ if not tag else os.path.join(OBJ, tag)
+    os.makedirs(obj_dir, exist_ok=True)
+    extra = [f"-D{d}" for d in defines]
     headers = [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))]
     headers.append(os.path.join(HERE, "..", "include", "pamopt_cu.h"))
     objs = []
     jobs = []
     for s in SOURCES:
         src = os.path.join(CSRC, s)
-        obj = os.path.join(OBJ, s.replace(".cu", ".o"))
+        obj = os.path.join(obj_dir, s.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale([src] + headers, obj):
-            jobs.append([NVCC, *FLAGS, "-c", src, "-o", obj])
+            jobs.append([NVCC, *FLAGS, *extra, "-c", src, "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -50,10 +55,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs) or 1)) as ex:
         list(ex.map(run, jobs))
-    if jobs or _stale(objs, OUT):
-        run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs, "-lcudart"])
-    return OUT
+    if jobs or _stale(objs, out):
+        run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs, "-lcudart"])
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    tags = [a[6:] for a in sys.argv[1:] if a.startswith("--tag=")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=defs, tag=tags[0] if tags else ""))

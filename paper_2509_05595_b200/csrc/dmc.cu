@@ -241,8 +241,10 @@ __global__ void k_patch_count(GridView g, const uint32_t* __restrict__ cells, co
   cellmap[cells[i] - c0] = static_cast<uint32_t>(i);
 }
 
+// x / R for the power-of-two R: the product by the exact reciprocal is the same double
 __device__ __forceinline__ D3 gpoint(int64_t x, int64_t y, int64_t z, int R) {
-  return D3{static_cast<double>(x) / R, static_cast<double>(y) / R, static_cast<double>(z) / R};
+  const double iR = __longlong_as_double(static_cast<long long>(1023 - (__ffs(R) - 1)) << 52);
+  return D3{static_cast<double>(x) * iR, static_cast<double>(y) * iR, static_cast<double>(z) * iR};
 }
 
 __device__ __forceinline__ D3 crossing(D3 p0, D3 p1, float f0, float f1, double beta) {

@@ -562,7 +562,10 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
 }
 
 template <int SHARED>
-__global__ void __launch_bounds__(128) k_narrow(const double* __restrict__ V, const int32_t* __restrict__ F,
+#ifndef PCU_NARROW_MINB
+#define PCU_NARROW_MINB 1
+#endif
+__global__ void __launch_bounds__(128, PCU_NARROW_MINB) k_narrow(const double* __restrict__ V, const int32_t* __restrict__ F,
                                                 const uint64_t* __restrict__ cls, uint64_t cap,
                                                 DetectScalars* __restrict__ ds, int mode, int32_t* __restrict__ pairs,
                                                 uint64_t pair_cap, const int32_t* __restrict__ owner,

@@ -214,31 +214,58 @@ __device__ double qeval(const double* q, D3 p) {
 
 __device__ double ring_skinny(const double* X, const int32_t* F, const int32_t* ia, int na, const int32_t* ib, int nb,
                               int a, int b, D3 x) {
+  // faces of ring(a) U ring(b) in ascending id order (the pinned summation order); the next
+  // face's index triple is fetched one step ahead so its load overlaps the current face's math
   int i = 0, j = 0;
-  double cs = 0.0;
-  while (i < na || j < nb) {
-    int f;
-    if (j == nb || (i < na && ia[i] < ib[j])) f = ia[i++];
-    else if (i == na || ib[j] < ia[i]) f = ib[j++];
-    else {
-      f = ia[i++];
+  auto next = [&]() -> int {
+    if (i < na || j < nb) {
+      if (j == nb || (i < na && ia[i] < ib[j])) return ia[i++];
+      if (i == na || ib[j] < ia[i]) return ib[j++];
       ++j;
+      return ia[i++];
     }
-    const int32_t* t = F + 3 * f;
-    if (has(t, a) && has(t, b)) continue;
-    D3 P[3];
-    for (int k = 0; k < 3; ++k) P[k] = (t[k] == a || t[k] == b) ? x : P3(X, t[k]);
-    const D3 n = cross(sub(P[1], P[0]), sub(P[2], P[0]));
-    const double area = 0.5 * sqrt(sqn(n));
-    const double l01 = sqn(sub(P[1], P[0])), l12 = sqn(sub(P[2], P[1])), l20 = sqn(sub(P[0], P[2]));
-    const double den = (l01 + l12) + l20;
-    const double c = den > 0.0 ? (k4Sqrt3 * area) / den : 0.0;
-    cs = cs + (1.0 - c);
+    return -1;
+  };
+  double cs = 0.0;
+  int f = next();
+  int t0 = 0, t1 = 0, t2 = 0;
+  if (f >= 0) {
+    t0 = F[3 * f];
+    t1 = F[3 * f + 1];
+    t2 = F[3 * f + 2];
+  }
+  while (f >= 0) {
+    const int fn = next();
+    int u0 = 0, u1 = 0, u2 = 0;
+    if (fn >= 0) {
+      u0 = F[3 * fn];
+      u1 = F[3 * fn + 1];
+      u2 = F[3 * fn + 2];
+    }
+    const bool ha = t0 == a || t1 == a || t2 == a, hb = t0 == b || t1 == b || t2 == b;
+    if (!(ha && hb)) {
+      const int tt[3] = {t0, t1, t2};
+      D3 P[3];
+      for (int k = 0; k < 3; ++k) P[k] = (tt[k] == a || tt[k] == b) ? x : P3(X, tt[k]);
+      const D3 n = cross(sub(P[1], P[0]), sub(P[2], P[0]));
+      const double area = 0.5 * sqrt(sqn(n));
+      const double l01 = sqn(sub(P[1], P[0])), l12 = sqn(sub(P[2], P[1])), l20 = sqn(sub(P[0], P[2]));
+      const double den = (l01 + l12) + l20;
+      const double c = den > 0.0 ? (k4Sqrt3 * area) / den : 0.0;
+      cs = cs + (1.0 - c);
+    }
+    f = fn;
+    t0 = u0;
+    t1 = u1;
+    t2 = u2;
   }
   return cs;
 }
 
-__global__ void k_cost(const double* __restrict__ X, const int32_t* __restrict__ F, const double* __restrict__ Q,
+#ifndef PCU_COST_MINB
+#define PCU_COST_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PCU_COST_MINB) k_cost(const double* __restrict__ X, const int32_t* __restrict__ F, const double* __restrict__ Q,
                        const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
                        const int32_t* __restrict__ inc, const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
                        const uint8_t* __restrict__ valid, const unsigned long long* __restrict__ d_ne, double we,
