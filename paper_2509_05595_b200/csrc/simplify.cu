@@ -386,22 +386,6 @@ __global__ void k_total(const uint32_t* __restrict__ off, const uint32_t* __rest
 
 // ---------------------------------------------------------------------- link condition
 // restatement of mesh.cpp:301-358 on the CSR incidence (-2 = the virtual boundary vertex)
-__device__ bool is_boundary_vertex(int v, const int32_t* F, const uint32_t* off, const uint32_t* deg,
-                                   const int32_t* inc) {
-  const int d = static_cast<int>(deg[v]);
-  for (int i = 0; i < d; ++i) {
-    const int32_t* t = F + 3 * inc[off[v] + i];
-    for (int k = 0; k < 3; ++k) {
-      const int x = t[k];
-      if (x == v) continue;
-      int c = 0;
-      for (int j = 0; j < d && c < 2; ++j) c += has(F + 3 * inc[off[v] + j], x);
-      if (c == 1) return true;
-    }
-  }
-  return false;
-}
-
 __device__ int faces_of_edge(int a, int b, const int32_t* F, const uint32_t* off, const uint32_t* deg,
                              const int32_t* inc) {
   int c = 0;
@@ -409,17 +393,22 @@ __device__ int faces_of_edge(int a, int b, const int32_t* F, const uint32_t* off
   return c;
 }
 
-// sorted unique link vertex set of v (+ -2 if boundary); returns size
+// sorted unique link vertex set of v (+ -2 if boundary); returns size.  One pass over the
+// incident faces builds the multiset of their other vertices (a vertex counted once per face);
+// after sorting, v is a boundary vertex (mesh.cpp:298-356: some ring vertex lies in exactly one
+// incident face) iff some value occurs once — the same verdict without the O(deg^2) rescans.
 __device__ int link_set(int v, const int32_t* F, const uint32_t* off, const uint32_t* deg, const int32_t* inc,
                         int32_t* out) {
   int n = 0;
   const int d = min(static_cast<int>(deg[v]), kMaxDeg);
+  const int32_t* L = inc + off[v];
   for (int i = 0; i < d; ++i) {
-    const int32_t* t = F + 3 * inc[off[v] + i];
-    for (int k = 0; k < 3; ++k)
-      if (t[k] != v) out[n++] = t[k];
+    const int32_t* t = F + 3 * L[i];
+    const int32_t t0 = t[0], t1 = t[1], t2 = t[2];
+    if (t0 != v) out[n++] = t0;
+    if (t1 != v && t1 != t0) out[n++] = t1;
+    if (t2 != v && t2 != t0 && t2 != t1) out[n++] = t2;
   }
-  if (is_boundary_vertex(v, F, off, deg, inc)) out[n++] = -2;
   for (int i = 1; i < n; ++i) {
     const int32_t x = out[i];
     int j = i - 1;
@@ -429,9 +418,20 @@ __device__ int link_set(int v, const int32_t* F, const uint32_t* off, const uint
     }
     out[j + 1] = x;
   }
+  bool boundary = false;
   int u = 0;
-  for (int i = 0; i < n; ++i)
-    if (u == 0 || out[u - 1] != out[i]) out[u++] = out[i];
+  for (int i = 0; i < n;) {
+    int k = i + 1;
+    while (k < n && out[k] == out[i]) ++k;
+    boundary |= (k - i) == 1;
+    out[u++] = out[i];
+    i = k;
+  }
+  if (boundary) {  // -2 sorts first
+    for (int i = u; i > 0; --i) out[i] = out[i - 1];
+    out[0] = -2;
+    ++u;
+  }
   return u;
 }
 
