@@ -280,6 +280,14 @@ def run_ours(args):
     e2e_val = float(te.item()) / (args.steps * world)
     h2d = v.nbytes + f.nbytes
 
+    # ---- one extra, untimed step with CUDA events around every launch: per-kernel device time
+    # (the share of the step each kernel takes; the committed ncu launch list corroborates it)
+    ctx.profile(True)
+    one_step()
+    ctx.synchronize()
+    ktimes = ctx.kernel_times()
+    ctx.profile(False)
+
     if rank == 0:
         peaks, peak_kind = load_peaks()
         hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
@@ -335,6 +343,12 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        ktot = sum(ms for ms, _ in ktimes.values()) or 1.0
+        top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:12]
+        line["kernels"] = {"source": "one untimed step, CUDA events around every launch",
+                           "device_ms_total": round(ktot, 3),
+                           "top": [{"name": k, "ms": round(ms, 3), "launches": n, "share": round(ms / ktot, 4)}
+                                   for k, (ms, n) in top]}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -81,6 +81,8 @@ _SIGS = {
     "pamopt_cu_ctx_stream": (vp, [vp]),
     "pamopt_cu_ctx_synchronize": (C.c_int, [vp]),
     "pamopt_cu_ctx_launches": (i64, [vp]),
+    "pamopt_cu_ctx_profile": (C.c_int, [vp, i32]),
+    "pamopt_cu_ctx_kernel_times": (i64, [vp, vp, i64]),
     "pamopt_cu_mesh_upload": (C.c_int, [vp, vp, i64, vp, i64, P(vp)]),
     "pamopt_cu_mesh_from_device": (C.c_int, [vp, vp, i64, vp, i64, P(vp)]),
     "pamopt_cu_mesh_size": (C.c_int, [vp, P(i64), P(i64)]),

@@ -45,6 +45,21 @@ class Context:
     def launches(self) -> int:
         return int(lib().pamopt_cu_ctx_launches(self.h))
 
+    def profile(self, on: bool = True) -> None:
+        """Per-kernel device-time accounting (events around every launch; perturbs timing)."""
+        check(lib().pamopt_cu_ctx_profile(self.h, 1 if on else 0))
+
+    def kernel_times(self) -> dict:
+        """{kernel: (ms, launches)} accumulated since profile(True)."""
+        n = lib().pamopt_cu_ctx_kernel_times(self.h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        lib().pamopt_cu_ctx_kernel_times(self.h, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, ms, cnt = line.split("\t")
+            out[name] = (float(ms), int(cnt))
+        return out
+
     def close(self) -> None:
         if self.h:
             lib().pamopt_cu_ctx_destroy(self.h)

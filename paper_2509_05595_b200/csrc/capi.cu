@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -134,7 +135,7 @@ int pamopt_cu_ctx_create(int32_t device, pamopt_cu_ctx* out) {
     c->ctx.device = device;
     const char* pe = std::getenv("PAMOPT_PROFILE");
     c->ctx.prof.on = pe && pe[0] == '1';
-    c->ctx.prof.kt = pe && pe[0] == '2';
+    c->ctx.prof.kt = c->ctx.prof.kt_print = pe && pe[0] == '2';
     pcu::DeviceGuard g(device);
     PCU_CUDA(cudaStreamCreateWithFlags(&c->ctx.stream, cudaStreamNonBlocking));
     PCU_CUDA(cudaDeviceGetAttribute(&c->ctx.num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -164,6 +165,36 @@ int pamopt_cu_ctx_synchronize(pamopt_cu_ctx c) {
 }
 
 int64_t pamopt_cu_ctx_launches(pamopt_cu_ctx c) { return c ? c->ctx.launches : 0; }
+
+int pamopt_cu_ctx_profile(pamopt_cu_ctx c, int on) {
+  return guarded([&] {
+    check_ctx(c);
+    pcu::DeviceGuard g(c->ctx.device);
+    c->ctx.prof.kflush();
+    c->ctx.prof.kms.clear();
+    c->ctx.prof.kn.clear();
+    c->ctx.prof.kt = on != 0;
+  });
+}
+
+int64_t pamopt_cu_ctx_kernel_times(pamopt_cu_ctx c, char* buf, int64_t cap) {
+  if (!c) return 0;
+  pcu::DeviceGuard g(c->ctx.device);
+  c->ctx.prof.kflush();
+  std::string out;
+  char line[256];
+  for (auto& kv : c->ctx.prof.kms) {
+    std::snprintf(line, sizeof(line), "%s\t%.6f\t%lld\n", kv.first.c_str(), kv.second,
+                  static_cast<long long>(c->ctx.prof.kn[kv.first]));
+    out += line;
+  }
+  if (buf && cap > 0) {
+    const int64_t k = std::min<int64_t>(cap - 1, static_cast<int64_t>(out.size()));
+    std::memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+  return static_cast<int64_t>(out.size());
+}
 
 // ---------------------------------------------------------------------------- meshes
 static int mesh_create(pamopt_cu_ctx c, const double* v, int64_t nv, const int32_t* f, int64_t nf,

@@ -47,7 +47,8 @@ void set_last_error(const std::string& m);
 // (diagnostics only; never enabled in timed runs).
 struct Prof {
   bool on = false;
-  bool kt = false;  // PAMOPT_PROFILE=2: per-kernel device time (events around every launch)
+  bool kt = false;        // per-kernel device time (events around every launch)
+  bool kt_print = false;  // PAMOPT_PROFILE=2: print the tally at the end of each simplify
   struct Pending {
     const char* name;
     cudaEvent_t a, b;
@@ -97,7 +98,7 @@ struct Prof {
     t = std::chrono::steady_clock::now();
   }
   void dump(const char* title) {
-    if (kt) {
+    if (kt && kt_print) {
       kflush();
       double tot = 0;
       for (auto& kv : kms) tot += kv.second;

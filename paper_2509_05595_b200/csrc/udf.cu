@@ -77,12 +77,14 @@ __device__ __forceinline__ float fptri_sq(const TriD& t, float px, float py, flo
   return best;
 }
 
-__device__ __forceinline__ bool survives(const TriD& t, double cx, double cy, double cz, double thr) {
+// 0: fails, 1: survives, 2: undecided (needs survives_exact).  The box test is exact; the FP32
+// decision is certified away from the threshold for well-conditioned triangles.
+__device__ __forceinline__ int survives_fast(const TriD& t, double cx, double cy, double cz, double thr) {
   const double tb = thr + 1e-9;
   const double dx = fmax(fmax(t.lo[0] - cx, cx - t.hi[0]), 0.0);
   const double dy = fmax(fmax(t.lo[1] - cy, cy - t.hi[1]), 0.0);
   const double dz = fmax(fmax(t.lo[2] - cz, cz - t.hi[2]), 0.0);
-  if ((dx * dx + dy * dy) + dz * dz > tb * tb) return false;
+  if ((dx * dx + dy * dy) + dz * dz > tb * tb) return 0;
   if (t.wc) {  // certified FP32 decision away from the threshold
     const float px = static_cast<float>(cx - t.a[0]), py = static_cast<float>(cy - t.a[1]),
                 pz = static_cast<float>(cz - t.a[2]);
@@ -90,12 +92,22 @@ __device__ __forceinline__ bool survives(const TriD& t, double cx, double cy, do
     const float L2 = fmaxf(t.L2, px * px + py * py + pz * pz);
     const float th2 = static_cast<float>(thr * thr);
     const float m = 1e-4f * L2 + 1e-3f * th2;
-    if (d2 < th2 - m) return true;
-    if (d2 > th2 + m) return false;
+    if (d2 < th2 - m) return 1;
+    if (d2 > th2 + m) return 0;
   }
+  return 2;
+}
+
+// the pinned predicate itself: sqrt(ptri_sq) <= thr in FP64
+__device__ __forceinline__ bool survives_exact(const TriD& t, double cx, double cy, double cz, double thr) {
   const double d2 = ptri_sq(D3{cx, cy, cz}, D3{t.a[0], t.a[1], t.a[2]}, D3{t.b[0], t.b[1], t.b[2]},
                             D3{t.c[0], t.c[1], t.c[2]});
   return sqrt(d2) <= thr;
+}
+
+__device__ __forceinline__ bool survives(const TriD& t, double cx, double cy, double cz, double thr) {
+  const int s = survives_fast(t, cx, cy, cz, thr);
+  return s == 2 ? survives_exact(t, cx, cy, cz, thr) : s == 1;
 }
 
 // 1/r for a power of two r, exactly (exponent bits): x * inv_pow2(r) == x / r bit for bit
@@ -291,6 +303,7 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
   __shared__ uint32_t rows[8][16];        // finest-level survivor bit rows: byte (y + bs z) holds x bits
   __shared__ uint16_t list[8][2][512];    // ping-pong survivor lists (local cell index at level j)
   __shared__ uint16_t vlist[8][729];      // needed vertices, packed x | y<<4 | z<<8
+  __shared__ uint16_t equeue[8][64];      // vertices queued for the FP64 evaluation
   __shared__ TriD tsh[8];
   __shared__ unsigned next_tri;  // dynamic triangle distribution among the warps (load balance)
   const Item it = items[blockIdx.x];
@@ -393,32 +406,60 @@ __global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items
     __syncwarp();
     const D3 A{t.a[0], t.a[1], t.a[2]}, Bv{t.b[0], t.b[1], t.b[2]}, Cv{t.c[0], t.c[1], t.c[2]};
     const double iR = inv_pow2(R);
-    for (int i = lane; i < nneed; i += 32) {
-      const int pk = vlist[warp][i];
+    // Pass over the needed vertices: the certified FP32 filter decides which vertices this
+    // triangle may lower; those are queued (warp ballot) and evaluated in FP64 32 at a time, so
+    // the expensive pinned routine always runs with a full warp.
+    int qn = 0;
+    auto eval = [&](int pk) {
       const int vx = pk & 15, vy = (pk >> 4) & 15, vz = pk >> 8;
       const int v = vx + nv1 * (vy + nv1 * vz);
-      const int gx = bx * bs + vx, gy = by * bs + vy, gz = bz * bs + vz;
-      const D3 p{static_cast<double>(gx) * iR, static_cast<double>(gy) * iR, static_cast<double>(gz) * iR};
-      if (t.wc) {
-        // this triangle cannot lower the vertex's running minimum: skip the FP64 evaluation
-        // (the minimum is order independent, so skipping never changes the result).  Cheap
-        // lower bounds first (plane distance, box distance), then the FP32 distance.
-        const double curm = __longlong_as_double(static_cast<long long>(vmin[v]));  // NaN while unset
-        const float px = static_cast<float>(p.x - t.a[0]), py = static_cast<float>(p.y - t.a[1]),
-                    pz = static_cast<float>(p.z - t.a[2]);
-        const float L2 = fmaxf(t.L2, fdot(px, py, pz, px, py, pz));
-        const float skip = __fmaf_rn(1e-4f, L2, static_cast<float>(curm * (1.0 + 1e-3)));  // NaN: never skip
-        const float dn = fdot(px, py, pz, t.n[0], t.n[1], t.n[2]);
-        if (dn * dn > skip) continue;
-        const float ex = fmaxf(fmaxf(t.blo[0] - px, px - t.bhi[0]), 0.f),
-                    ey = fmaxf(fmaxf(t.blo[1] - py, py - t.bhi[1]), 0.f),
-                    ez = fmaxf(fmaxf(t.blo[2] - pz, pz - t.bhi[2]), 0.f);
-        if (fdot(ex, ey, ez, ex, ey, ez) > skip) continue;
-        if (fptri_sq(t, px, py, pz) > skip) continue;
-      }
+      const D3 p{static_cast<double>(bx * bs + vx) * iR, static_cast<double>(by * bs + vy) * iR,
+                 static_cast<double>(bz * bs + vz) * iR};
       const double d2 = ptri_sq(p, A, Bv, Cv);
       atomicMin(&vmin[v], static_cast<unsigned long long>(__double_as_longlong(d2)));
+    };
+    for (int base = 0; base < nneed; base += 32) {
+      const int i = base + lane;
+      bool need = false;
+      int pk = 0;
+      if (i < nneed) {
+        pk = vlist[warp][i];
+        need = true;
+        if (t.wc) {
+          const int vx = pk & 15, vy = (pk >> 4) & 15, vz = pk >> 8;
+          const int v = vx + nv1 * (vy + nv1 * vz);
+          const double px64 = static_cast<double>(bx * bs + vx) * iR, py64 = static_cast<double>(by * bs + vy) * iR,
+                       pz64 = static_cast<double>(bz * bs + vz) * iR;
+          // this triangle cannot lower the vertex's running minimum: skip the FP64 evaluation
+          // (the minimum is order independent, so skipping never changes the result).  Cheap
+          // lower bounds first (plane distance, box distance), then the FP32 distance.
+          const double curm = __longlong_as_double(static_cast<long long>(vmin[v]));  // NaN while unset
+          const float px = static_cast<float>(px64 - t.a[0]), py = static_cast<float>(py64 - t.a[1]),
+                      pz = static_cast<float>(pz64 - t.a[2]);
+          const float L2 = fmaxf(t.L2, fdot(px, py, pz, px, py, pz));
+          const float skip = __fmaf_rn(1e-4f, L2, static_cast<float>(curm * (1.0 + 1e-3)));  // NaN: never skip
+          const float dn = fdot(px, py, pz, t.n[0], t.n[1], t.n[2]);
+          if (dn * dn > skip) {
+            need = false;
+          } else {
+            const float ex = fmaxf(fmaxf(t.blo[0] - px, px - t.bhi[0]), 0.f),
+                        ey = fmaxf(fmaxf(t.blo[1] - py, py - t.bhi[1]), 0.f),
+                        ez = fmaxf(fmaxf(t.blo[2] - pz, pz - t.bhi[2]), 0.f);
+            if (fdot(ex, ey, ez, ex, ey, ez) > skip || fptri_sq(t, px, py, pz) > skip) need = false;
+          }
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, need);
+      if (need) equeue[warp][qn + __popc(m & lt)] = static_cast<uint16_t>(pk);
+      qn += __popc(m);
+      __syncwarp();
+      if (qn >= 32) {
+        eval(equeue[warp][qn - 32 + lane]);
+        qn -= 32;
+        __syncwarp();
+      }
     }
+    if (lane < qn) eval(equeue[warp][lane]);
     __syncwarp();
   }
   __syncthreads();
