@@ -144,9 +144,12 @@ __device__ int upper_neighbours(int a, const int32_t* __restrict__ F, const uint
   return u;
 }
 
+// per vertex a: its upper neighbours b > a (ascending) with the face count of edge ab; the
+// sorted list is parked in the CSR-aligned scratch (2 slots per incident face) for k_edge_fill
 __global__ void k_edge_count(const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
                              const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int64_t nv,
-                             uint32_t* __restrict__ ecount, Counters* cnt) {
+                             uint32_t* __restrict__ ecount, int32_t* __restrict__ snb, uint8_t* __restrict__ smult,
+                             Counters* cnt) {
   const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (a >= nv) return;
   int32_t nb[2 * kMaxDeg];
@@ -158,24 +161,29 @@ __global__ void k_edge_count(const int32_t* __restrict__ F, const uint32_t* __re
     return;
   }
   int bad = 0;
-  for (int i = 0; i < u; ++i) bad |= (mult[i] != 1 && mult[i] != 2);
+  const int64_t s0 = 2 * static_cast<int64_t>(off[a]);
+  for (int i = 0; i < u; ++i) {
+    bad |= (mult[i] != 1 && mult[i] != 2);
+    snb[s0 + i] = nb[i];
+    smult[s0 + i] = mult[i];
+  }
   if (bad) atomicAdd(&cnt->err, 1ull);  // non-manifold edge: input must come from stage 1
   ecount[a] = static_cast<uint32_t>(u);
 }
 
-__global__ void k_edge_fill(const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
-                            const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int64_t nv,
-                            const uint32_t* __restrict__ eoff, int32_t* __restrict__ ea, int32_t* __restrict__ eb,
+__global__ void k_edge_fill(const uint32_t* __restrict__ off, const uint32_t* __restrict__ ecount, int64_t nv,
+                            const uint32_t* __restrict__ eoff, const int32_t* __restrict__ snb,
+                            const uint8_t* __restrict__ smult, int32_t* __restrict__ ea, int32_t* __restrict__ eb,
                             uint8_t* __restrict__ enf) {
   const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (a >= nv || !deg[a]) return;
-  int32_t nb[2 * kMaxDeg];
-  uint8_t mult[2 * kMaxDeg];
-  const int u = upper_neighbours(static_cast<int>(a), F, off, deg, inc, nb, mult);
+  if (a >= nv) return;
+  const int u = static_cast<int>(ecount[a]);
+  const int64_t s0 = 2 * static_cast<int64_t>(off[a]);
+  const uint32_t e0 = eoff[a];
   for (int i = 0; i < u; ++i) {
-    ea[eoff[a] + i] = static_cast<int32_t>(a);
-    eb[eoff[a] + i] = nb[i];
-    enf[eoff[a] + i] = mult[i];
+    ea[e0 + i] = static_cast<int32_t>(a);
+    eb[e0 + i] = snb[s0 + i];
+    enf[e0 + i] = smult[s0 + i];
   }
 }
 
@@ -698,6 +706,8 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
   DevBuf<int32_t> inc(3 * nf, st), ea(ecap, st), eb(ecap, st), owner(nf, st), qf(3 * nf + 16, st),
       qf2(3 * nf + 16, st), Fprev(3 * nf, st);
   DevBuf<uint8_t> enf(ecap, st), valid(ecap, st), revert(ecap, st);
+  DevBuf<int32_t> snb(6 * nf + 16, st);  // upper-neighbour scratch, 2 slots per incidence entry
+  DevBuf<uint8_t> smult(6 * nf + 16, st);
   DevBuf<uint64_t> key(ecap, st), marked(ecap, st), marked_sorted(ecap, st);
   DevBuf<double> place(3 * ecap, st);
   DevBuf<unsigned long long> vmin(nv, st), vfmin(nv, st);
@@ -786,11 +796,11 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     cnt.memset(0, st);
     // edges (device-side count; kernels below stride over it)
     PCU_LAUNCH(ctx, k_edge_count, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, ecount.get(),
-               cnt.get());
+               snb.get(), smult.get(), cnt.get());
     exclusive_scan_u32(ctx, ecount.get(), eoff.get(), nv);
     PCU_LAUNCH(ctx, k_total, 1, 1, 0, eoff.get(), ecount.get(), nv, d_ne);
-    PCU_LAUNCH(ctx, k_edge_fill, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, eoff.get(), ea.get(),
-               eb.get(), enf.get());
+    PCU_LAUNCH(ctx, k_edge_fill, grid_for(nv, 128), 128, 0, off.get(), ecount.get(), nv, eoff.get(), snb.get(),
+               smult.get(), ea.get(), eb.get(), enf.get());
     ctx.prof.mark(st, "edges");
     const unsigned eg = std::min<unsigned>(grid_for(ne_hint, 128), gs_grid);
     PCU_LAUNCH(ctx, k_mark_invalid, eg, 128, 0, ea.get(), eb.get(), d_ne, inv.get(), ninv, valid.get());
