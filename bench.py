@@ -288,6 +288,17 @@ def run_ours(args):
     ktimes = ctx.kernel_times()
     ctx.profile(False)
 
+    # ---- certification of this run's output (untimed, GPU): SPEC MeshReport vs the input soup
+    cert = None
+    if rank == 0:
+        out, _, _ = api.remesh_device(mesh, R, target)
+        r = api.mesh_report(out, mesh, n_samples=16384, seed=42)
+        out.free()
+        cert = {"manifold": r["manifold"], "watertight": r["watertight"],
+                "intersection_free": r["intersection_free"], "faces": int(r["n_faces"]),
+                "min_angle_deg": round(r["min_angle_deg"], 3), "chamfer_vs_input": r["cd"],
+                "hausdorff_vs_input": r["hd"], "samples_per_side": 16384}
+
     if rank == 0:
         peaks, peak_kind = load_peaks()
         hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
@@ -343,6 +354,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+        line["certification"] = cert
         ktot = sum(ms for ms, _ in ktimes.values()) or 1.0
         top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:12]
         line["kernels"] = {"source": "one untimed step, CUDA events around every launch",
