@@ -99,8 +99,43 @@ void exclusive_scan_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n) 
   ++ctx.launches;
 }
 
+// Small sorts (the QEM loop's marked keys and invalid pairs late in a run): one CTA bitonic
+// sort in shared memory replaces CUB's multi-kernel radix sort, whose fixed launch chain
+// dominates at these sizes.  Keys are unique or ties are identical values, so the result equals
+// any other correct ascending sort.
+constexpr int kSmallSort = 4096;
+__global__ void __launch_bounds__(1024) k_small_sort(const uint64_t* __restrict__ in, int n, uint64_t* __restrict__ out) {
+  __shared__ uint64_t sh[kSmallSort];
+  int N = 1;
+  while (N < n) N <<= 1;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) sh[i] = i < n ? in[i] : ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= N; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = sh[i], b = sh[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            sh[i] = b;
+            sh[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = sh[i];
+}
+
+bool small_sort_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n) {
+  if (n > kSmallSort) return false;
+  if (n > 0) PCU_LAUNCH(ctx, k_small_sort, 1, 1024, 0, in, static_cast<int>(n), out);
+  return true;
+}
+
 void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit) {
   if (n <= 1) return;
+  if (small_sort_u64(ctx, keys, keys, n)) return;
   DevBuf<uint64_t> alt(n, ctx.stream);
   cub::DoubleBuffer<uint64_t> db(keys, alt.get());
   size_t need = 0;

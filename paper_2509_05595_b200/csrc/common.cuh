@@ -209,6 +209,8 @@ inline unsigned grid_for(int64_t n, int block) {
 void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n);
 void exclusive_scan_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n);
 void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit = 64);
+// one-CTA sort for n <= 4096 (in may alias out); false (nothing launched) if n is larger
+bool small_sort_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n);
 template <class T>
 T read_scalar(Ctx& ctx, const T* dptr) {
   T h;

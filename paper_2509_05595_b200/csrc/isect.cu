@@ -335,6 +335,7 @@ struct DetectScalars {
   unsigned long long found;
   unsigned long long npairs;
   unsigned long long ncls[3];
+  unsigned long long nhuge;  // probes covering > kMaxCells cells, handed to k_probe_huge
   int redo;  // candidate buffer overflowed: the round's outputs are void, the caller repeats it
   int pad;
 };
@@ -424,7 +425,8 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
                                                const uint32_t* __restrict__ occ, int sym,
                                                const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
                                                uint64_t cap, unsigned long long* __restrict__ ncand,
-                                               const int32_t* __restrict__ probe_ids) {
+                                               const int32_t* __restrict__ probe_ids, int32_t* __restrict__ huge,
+                                               unsigned long long* __restrict__ nhuge) {
   // candidates are staged in shared memory and flushed with one global atomic per block
   // (a single-address counter bumped per candidate serialises in the L2 atomic unit)
   constexpr int kBuf = 2048;
@@ -459,13 +461,9 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
       }
     };
     if (cp.count() > kMaxCells) {
-      // huge probe: scan the whole build set, each entry once (in the bucket of its first cell)
-      for (uint32_t h = 0; h <= mask; ++h)
-        for (uint32_t e = boff[h]; e < boff[h] + bcount[h]; ++e) {
-          const int4 en = entries[e];
-          if (cell_hash(en.y, en.z, en.w, mask) != h) continue;
-          consider(en.x, B[en.x]);
-        }
+      // huge probe: k_probe_huge scans the build set for it with a whole warp
+      huge[agg_inc(nhuge)] = p;
+      p = -1;
     } else {
       for (int64_t z = cp.lo[2]; z <= cp.hi[2]; ++z)
         for (int64_t y = cp.lo[1]; y <= cp.hi[1]; ++y)
@@ -483,7 +481,8 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
             }
           }
     }
-    for (int64_t b = 0; b < nbig; ++b) consider(big[b], B[big[b]]);
+    if (p >= 0)
+      for (int64_t b = 0; b < nbig; ++b) consider(big[b], B[big[b]]);
   }
   __syncthreads();
   const unsigned m = min(nbuf, static_cast<unsigned>(kBuf));
@@ -491,6 +490,33 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
   __syncthreads();
   for (unsigned i = threadIdx.x; i < m; i += blockDim.x)
     if (gbase + i < cap) cand[gbase + i] = buf[i];
+}
+
+// Huge probes (their box covers more than kMaxCells grid cells): one warp per probe, lanes
+// stride over the build set (ids, or every alive face) — every build face is met exactly once,
+// with the same emission rules as k_probe.
+__global__ void __launch_bounds__(128) k_probe_huge(const FBox* __restrict__ B, const int32_t* __restrict__ huge,
+                                                    const unsigned long long* __restrict__ nhuge,
+                                                    const int32_t* __restrict__ build_ids, int64_t n_build,
+                                                    const uint8_t* __restrict__ alive, int sym,
+                                                    const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
+                                                    uint64_t cap, unsigned long long* __restrict__ ncand) {
+  const unsigned long long nh = *nhuge;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); w < nh; w += nw) {
+    const int32_t p = huge[w];
+    const bool p_build = sym || (in_build && in_build[p]);
+    const FBox bp = B[p];
+    for (int64_t k = lane; k < n_build; k += 32) {
+      const int32_t a = build_ids ? build_ids[k] : static_cast<int32_t>(k);
+      if (alive && !alive[a]) continue;
+      if (a == p || (p_build && a < p)) continue;
+      if (!overlap(bp, B[a])) continue;
+      const unsigned long long g = agg_inc(ncand);
+      if (g < cap) cand[g] = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
+    }
+  }
 }
 
 __device__ __forceinline__ void report(DetectScalars* ds, int mode, int32_t p, int32_t a, int32_t* pairs,
@@ -619,6 +645,7 @@ struct IsectScratch {
   DevBuf<int4> entries;      // (face id, first cell x, y, z) by bucket
   DevBuf<uint32_t> occ;      // non-empty bucket bitmap
   DevBuf<int32_t> big;
+  DevBuf<int32_t> huge;      // huge probe ids
   DevBuf<uint8_t> in_build;
   DevBuf<uint64_t> cand;
   DevBuf<float> fbox;        // 6 floats per face
@@ -680,10 +707,13 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   }
   if (S.cand_cap == 0) S.cand_cap = static_cast<uint64_t>(nf) * 4 + 4096;
   S.cand.ensure(S.cand_cap, st);
+  S.huge.ensure(static_cast<size_t>(n_probe) + 16, st);
   PCU_LAUNCH(ctx, k_probe, grid_for(n_probe, 128), 128, 0, B, n_probe,
              d_alive, S.ds.get(), mask, S.bcount.get(), S.boff.get(), S.entries.get(), S.big.get(), S.occ.get(), sym,
              in_build,
-             S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids);
+             S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids, S.huge.get(), &S.ds.get()->nhuge);
+  PCU_LAUNCH(ctx, k_probe_huge, static_cast<unsigned>(ctx.num_sms * 2), 128, 0, B, S.huge.get(), &S.ds.get()->nhuge,
+             build_ids, n_build, d_alive, sym, in_build, S.cand.get(), S.cand_cap, &S.ds.get()->ncand);
   S.cls.ensure(3 * S.cand_cap, st);
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,

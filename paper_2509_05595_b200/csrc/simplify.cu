@@ -829,16 +829,19 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     int64_t nnew = 0;
     if (nm > 0) {
       // marked keys in ascending order (deterministic collapse ids + the trim order)
-      size_t need = 0;
-      cub::DeviceRadixSort::SortKeys(nullptr, need, marked.get(), marked_sorted.get(), static_cast<int>(nm), 0, 64, st);
-      if (need > sort_tmp_bytes) {
-        sort_tmp.alloc(need, st);
-        sort_tmp_bytes = need;
+      if (!small_sort_u64(ctx, marked.get(), marked_sorted.get(), nm)) {
+        size_t need = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, need, marked.get(), marked_sorted.get(), static_cast<int>(nm), 0, 64,
+                                       st);
+        if (need > sort_tmp_bytes) {
+          sort_tmp.alloc(need, st);
+          sort_tmp_bytes = need;
+        }
+        cudaEvent_t sev = ctx.prof.kt ? ctx.prof.kbegin(st) : nullptr;
+        cub::DeviceRadixSort::SortKeys(sort_tmp.get(), sort_tmp_bytes, marked.get(), marked_sorted.get(),
+                                       static_cast<int>(nm), 0, 64, st);
+        if (sev) ctx.prof.kend("cub_sort_marked", sev, st);
       }
-      cudaEvent_t sev = ctx.prof.kt ? ctx.prof.kbegin(st) : nullptr;
-      cub::DeviceRadixSort::SortKeys(sort_tmp.get(), sort_tmp_bytes, marked.get(), marked_sorted.get(),
-                                     static_cast<int>(nm), 0, 64, st);
-      if (sev) ctx.prof.kend("cub_sort_marked", sev, st);
       PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, marked_sorted.get(), nm, ea.get(), eb.get(), enf.get(), F,
                  off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get());
       exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
