@@ -443,7 +443,6 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
   }
   if (p >= 0) {
     const double inv_h = ds->inv_h;
-    const int64_t nbig = static_cast<int64_t>(ds->nbig);
     const bool p_build = sym || (in_build && in_build[p]);
     const FBox bp = B[p];
     const CellRange cp = cells_of(bp, inv_h);
@@ -481,8 +480,7 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
             }
           }
     }
-    if (p >= 0)
-      for (int64_t b = 0; b < nbig; ++b) consider(big[b], B[big[b]]);
+    // pairs with big build faces come from k_probe_big
   }
   __syncthreads();
   const unsigned m = min(nbuf, static_cast<unsigned>(kBuf));
@@ -492,29 +490,53 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
     if (gbase + i < cap) cand[gbase + i] = buf[i];
 }
 
-// Huge probes (their box covers more than kMaxCells grid cells): one warp per probe, lanes
-// stride over the build set (ids, or every alive face) — every build face is met exactly once,
-// with the same emission rules as k_probe.
-__global__ void __launch_bounds__(128) k_probe_huge(const FBox* __restrict__ B, const int32_t* __restrict__ huge,
-                                                    const unsigned long long* __restrict__ nhuge,
-                                                    const int32_t* __restrict__ build_ids, int64_t n_build,
-                                                    const uint8_t* __restrict__ alive, int sym,
-                                                    const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
-                                                    uint64_t cap, unsigned long long* __restrict__ ncand) {
-  const unsigned long long nh = *nhuge;
+// Probes and build faces too large for the grid (their box covers more than kMaxCells cells),
+// one warp each, in one launch:
+//   * a huge probe p: lanes stride over the build set (ids, or every alive face), skipping the
+//     big build faces (handled below);
+//   * a big build face b: lanes stride over the probe set, pairs (x, b).
+// Each pair is met exactly once, with k_probe's emission rules.
+__global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B, const DetectScalars* __restrict__ ds,
+                                                     const int32_t* __restrict__ huge, const int32_t* __restrict__ big,
+                                                     const int32_t* __restrict__ build_ids, int64_t n_build,
+                                                     const int32_t* __restrict__ probe_ids, int64_t n_probe,
+                                                     const uint8_t* __restrict__ alive, int sym,
+                                                     const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
+                                                     uint64_t cap, unsigned long long* __restrict__ ncand) {
+  const unsigned long long nh = ds->nhuge, nb = ds->nbig;
+  const double inv_h = ds->inv_h;
   const int lane = threadIdx.x & 31;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); w < nh; w += nw) {
-    const int32_t p = huge[w];
-    const bool p_build = sym || (in_build && in_build[p]);
-    const FBox bp = B[p];
-    for (int64_t k = lane; k < n_build; k += 32) {
-      const int32_t a = build_ids ? build_ids[k] : static_cast<int32_t>(k);
-      if (alive && !alive[a]) continue;
-      if (a == p || (p_build && a < p)) continue;
-      if (!overlap(bp, B[a])) continue;
-      const unsigned long long g = agg_inc(ncand);
-      if (g < cap) cand[g] = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
+  auto emit = [&](int32_t p, int32_t a) {
+    const unsigned long long g = agg_inc(ncand);
+    if (g < cap) cand[g] = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
+  };
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); w < nh + nb; w += nw) {
+    if (w < nh) {
+      const int32_t p = huge[w];
+      const bool p_build = sym || (in_build && in_build[p]);
+      const FBox bp = B[p];
+      for (int64_t k = lane; k < n_build; k += 32) {
+        const int32_t a = build_ids ? build_ids[k] : static_cast<int32_t>(k);
+        if (alive && !alive[a]) continue;
+        if (a == p || (p_build && a < p)) continue;
+        const FBox ba = B[a];
+        if (!overlap(bp, ba)) continue;
+        if (cells_of(ba, inv_h).count() > kMaxCells) continue;  // big build face: second half
+        emit(p, a);
+      }
+    } else {
+      const int32_t b = big[w - nh];
+      const FBox bb = B[b];
+      for (int64_t k = lane; k < n_probe; k += 32) {
+        const int32_t x = probe_ids ? probe_ids[k] : static_cast<int32_t>(k);
+        if (alive && !alive[x]) continue;
+        if (x == b) continue;
+        const bool x_build = sym || (in_build && in_build[x]);
+        if (x_build && b < x) continue;  // emitted from probe b instead
+        if (!overlap(B[x], bb)) continue;
+        emit(x, b);
+      }
     }
   }
 }
@@ -712,8 +734,9 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
              d_alive, S.ds.get(), mask, S.bcount.get(), S.boff.get(), S.entries.get(), S.big.get(), S.occ.get(), sym,
              in_build,
              S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids, S.huge.get(), &S.ds.get()->nhuge);
-  PCU_LAUNCH(ctx, k_probe_huge, static_cast<unsigned>(ctx.num_sms * 2), 128, 0, B, S.huge.get(), &S.ds.get()->nhuge,
-             build_ids, n_build, d_alive, sym, in_build, S.cand.get(), S.cand_cap, &S.ds.get()->ncand);
+  PCU_LAUNCH(ctx, k_probe_large, static_cast<unsigned>(ctx.num_sms * 2), 128, 0, B, S.ds.get(), S.huge.get(),
+             S.big.get(), build_ids, n_build, probe_ids, n_probe, d_alive, sym, in_build, S.cand.get(), S.cand_cap,
+             &S.ds.get()->ncand);
   S.cls.ensure(3 * S.cand_cap, st);
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
