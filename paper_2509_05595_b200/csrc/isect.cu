@@ -418,6 +418,10 @@ __global__ void k_bin(const FBox* __restrict__ B, const int32_t* __restrict__ id
 // (p, a) with a in the build grid and overlapping (conservative float) boxes, in the first
 // common cell of the two cell ranges only.  `sym` = probe set == build set (each unordered pair
 // once); otherwise a pair of two build faces is emitted only from its smaller probe.
+// SIMT balance: probes differ wildly in work (0 .. 64 occupied cells), so lanes only enumerate
+// their occupied cells into a per-warp queue of (owner lane, cell) records; whenever 32 records
+// are queued the whole warp drains them, one cell's entry list per lane.  Probes covering more
+// than kMaxCells cells go to k_probe_large.
 __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64_t n, const uint8_t* __restrict__ alive,
                                                const DetectScalars* __restrict__ ds, uint32_t mask,
                                                const uint32_t* __restrict__ bcount, const uint32_t* __restrict__ boff,
@@ -429,64 +433,120 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
                                                unsigned long long* __restrict__ nhuge) {
   // candidates are staged in shared memory and flushed with one global atomic per block
   // (a single-address counter bumped per candidate serialises in the L2 atomic unit)
-  constexpr int kBuf = 2048;
+  constexpr int kBuf = 1024, kQ = 64;
   __shared__ uint64_t buf[kBuf];
   __shared__ unsigned int nbuf;
   __shared__ unsigned long long gbase;
+  __shared__ FBox sbox[4][32];
+  __shared__ int32_t sp[4][32];
+  __shared__ int32_t slo[4][32][3];
+  __shared__ uint8_t sbuild[4][32];
+  __shared__ int32_t qc[4][kQ][3];
+  __shared__ uint32_t qh[4][kQ];
+  __shared__ uint8_t qo[4][kQ];
+  (void)big;
   if (threadIdx.x == 0) nbuf = 0;
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   int32_t p = -1;
   if (k < n) {
     p = probe_ids ? probe_ids[k] : static_cast<int32_t>(k);
     if (alive && !alive[p]) p = -1;
   }
+  const double inv_h = ds->inv_h;
+  FBox bp{};
+  CellRange cp{};
+  bool p_build = false;
+  int64_t ncell = 0;
   if (p >= 0) {
-    const double inv_h = ds->inv_h;
-    const bool p_build = sym || (in_build && in_build[p]);
-    const FBox bp = B[p];
-    const CellRange cp = cells_of(bp, inv_h);
-    auto consider = [&](int32_t a, const FBox& ba) {
-      if (a == p) return;
-      if (p_build && a < p) return;  // the pair is emitted from probe a instead
-      if (!overlap(bp, ba)) return;
-      const uint64_t v = (static_cast<uint64_t>(static_cast<uint32_t>(p)) << 32) | static_cast<uint32_t>(a);
-      const unsigned slot = atomicAdd(&nbuf, 1u);
-      if (slot < kBuf) {
-        buf[slot] = v;
-      } else {  // block buffer full: direct global append
-        const unsigned long long g = agg_inc(ncand);
-        if (g < cap) cand[g] = v;
-      }
-    };
-    if (cp.count() > kMaxCells) {
-      // huge probe: k_probe_huge scans the build set for it with a whole warp
+    p_build = sym || (in_build && in_build[p]);
+    bp = B[p];
+    cp = cells_of(bp, inv_h);
+    ncell = cp.count();
+    if (ncell > kMaxCells) {  // huge probe: k_probe_large scans the build set for it
       huge[agg_inc(nhuge)] = p;
-      p = -1;
-    } else {
-      for (int64_t z = cp.lo[2]; z <= cp.hi[2]; ++z)
-        for (int64_t y = cp.lo[1]; y <= cp.hi[1]; ++y)
-          for (int64_t x = cp.lo[0]; x <= cp.hi[0]; ++x) {
-            const uint32_t h = cell_hash(x, y, z, mask);
-            if (!((occ[h >> 5] >> (h & 31)) & 1u)) continue;  // empty bucket (L2-resident bitmap)
-            const uint32_t e0 = boff[h], e1 = e0 + bcount[h];
-            for (uint32_t e = e0; e < e1; ++e) {
-              const int4 en = entries[e];  // face id + its first cell: the dedup test needs no box load
-              // first common cell of the two ranges (a hash collision can at worst duplicate a pair)
-              if (x != max(cp.lo[0], static_cast<int64_t>(en.y)) || y != max(cp.lo[1], static_cast<int64_t>(en.z)) ||
-                  z != max(cp.lo[2], static_cast<int64_t>(en.w)))
-                continue;
-              consider(en.x, B[en.x]);
-            }
-          }
+      ncell = 0;
     }
-    // pairs with big build faces come from k_probe_big
   }
+  sbox[warp][lane] = bp;
+  sp[warp][lane] = p;
+  for (int c = 0; c < 3; ++c) slo[warp][lane][c] = static_cast<int32_t>(cp.lo[c]);
+  sbuild[warp][lane] = p_build ? 1 : 0;
+  const int64_t nx = cp.hi[0] - cp.lo[0] + 1, ny = cp.hi[1] - cp.lo[1] + 1;
+  int64_t ci = 0;
+  int qn = 0;  // warp-uniform queue length
+  __syncwarp();
+  for (;;) {
+    // fill: every lane contributes its next occupied cell (empty buckets are skipped via the
+    // L2-resident occupancy bitmap)
+    bool got = false;
+    int32_t cx = 0, cy = 0, cz = 0;
+    uint32_t ch = 0;
+    while (ci < ncell) {
+      cx = static_cast<int32_t>(cp.lo[0] + ci % nx);
+      cy = static_cast<int32_t>(cp.lo[1] + (ci / nx) % ny);
+      cz = static_cast<int32_t>(cp.lo[2] + ci / (nx * ny));
+      ++ci;
+      ch = cell_hash(cx, cy, cz, mask);
+      if ((occ[ch >> 5] >> (ch & 31)) & 1u) {
+        got = true;
+        break;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, got);
+    if (got) {
+      const int pos = qn + __popc(m & lt);
+      qc[warp][pos][0] = cx;
+      qc[warp][pos][1] = cy;
+      qc[warp][pos][2] = cz;
+      qh[warp][pos] = ch;
+      qo[warp][pos] = static_cast<uint8_t>(lane);
+    }
+    qn += __popc(m);
+    const bool more = __any_sync(0xffffffffu, ci < ncell);
+    if (qn >= 32 || (!more && qn > 0)) {
+      __syncwarp();
+      const int take = min(qn, 32);
+      if (lane < take) {
+        const int r = qn - take + lane;
+        const int o = qo[warp][r];
+        const int32_t op = sp[warp][o];
+        const FBox ob = sbox[warp][o];
+        const bool obuild = sbuild[warp][o] != 0;
+        const int32_t x = qc[warp][r][0], y = qc[warp][r][1], z = qc[warp][r][2];
+        const int32_t lx = slo[warp][o][0], ly = slo[warp][o][1], lz = slo[warp][o][2];
+        const uint32_t h = qh[warp][r];
+        const uint32_t e0 = boff[h], e1 = e0 + bcount[h];
+        for (uint32_t e = e0; e < e1; ++e) {
+          const int4 en = entries[e];  // face id + its first cell: the dedup test needs no box load
+          // first common cell of the two ranges (a hash collision can at worst duplicate a pair)
+          if (x != max(lx, en.y) || y != max(ly, en.z) || z != max(lz, en.w)) continue;
+          const int32_t a = en.x;
+          if (a == op || (obuild && a < op)) continue;  // the pair is emitted from probe a instead
+          if (!overlap(ob, B[a])) continue;
+          const uint64_t v = (static_cast<uint64_t>(static_cast<uint32_t>(op)) << 32) | static_cast<uint32_t>(a);
+          const unsigned slot = atomicAdd(&nbuf, 1u);
+          if (slot < kBuf) {
+            buf[slot] = v;
+          } else {  // block buffer full: direct global append
+            const unsigned long long g = agg_inc(ncand);
+            if (g < cap) cand[g] = v;
+          }
+        }
+      }
+      __syncwarp();
+      qn -= take;
+    }
+    if (!more && qn == 0) break;
+  }
+  // pairs with big build faces come from k_probe_large
   __syncthreads();
-  const unsigned m = min(nbuf, static_cast<unsigned>(kBuf));
-  if (threadIdx.x == 0 && m) gbase = atomicAdd(ncand, static_cast<unsigned long long>(m));
+  const unsigned mm = min(nbuf, static_cast<unsigned>(kBuf));
+  if (threadIdx.x == 0 && mm) gbase = atomicAdd(ncand, static_cast<unsigned long long>(mm));
   __syncthreads();
-  for (unsigned i = threadIdx.x; i < m; i += blockDim.x)
+  for (unsigned i = threadIdx.x; i < mm; i += blockDim.x)
     if (gbase + i < cap) cand[gbase + i] = buf[i];
 }
 
