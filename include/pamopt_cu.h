@@ -83,6 +83,11 @@ void* pamopt_cu_ctx_stream(pamopt_cu_ctx ctx);
 int pamopt_cu_ctx_synchronize(pamopt_cu_ctx ctx);
 /* number of kernels this context launched since creation (telemetry) */
 int64_t pamopt_cu_ctx_launches(pamopt_cu_ctx ctx);
+/* per-kernel device-time accounting (CUDA events around every launch; diagnostics only, it
+ * perturbs timing): on != 0 starts a fresh tally.  kernel_times writes
+ * "name\tms\tlaunches\n" lines (NUL-terminated, truncated to cap) and returns the full length. */
+int pamopt_cu_ctx_profile(pamopt_cu_ctx ctx, int on);
+int64_t pamopt_cu_ctx_kernel_times(pamopt_cu_ctx ctx, char* buf, int64_t cap);
 
 /* ---- meshes (IndexedMesh) ------------------------------------------------------------ */
 int pamopt_cu_mesh_upload(pamopt_cu_ctx ctx, const double* vertices, int64_t nv,
@@ -95,6 +100,25 @@ int pamopt_cu_mesh_download(pamopt_cu_mesh mesh, double* vertices, int32_t* face
 /* device-to-device copy into caller buffers (NCCL gather of slab meshes); either may be NULL */
 int pamopt_cu_mesh_copy_to_device(pamopt_cu_mesh mesh, double* d_vertices, int32_t* d_faces);
 int pamopt_cu_mesh_free(pamopt_cu_mesh mesh);
+
+/* ---- ingest: file bytes in host memory -> device mesh --------------- */
+/* LoadStats (mesh_io.hpp:11-15) */
+typedef struct {
+  int64_t degenerate_faces_dropped;
+  int64_t polygons_triangulated;
+  int64_t vertices_welded;
+} pamopt_cu_load_stats;
+/* load_stl (mesh_io.cpp:309-366) for binary STL: corners welded by exact equality, vertices in
+ * first-occurrence order, repeated-index faces dropped.  ASCII STL -> EINVAL (host loader). */
+int pamopt_cu_load_stl(pamopt_cu_ctx ctx, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
+                       pamopt_cu_load_stats* stats);
+/* load_ply (mesh_io.cpp:135-255) for binary_little_endian PLY whose face lists hold exactly 3
+ * indices (the reference writer's layout); vertex x/y/z of any scalar type.  Other layouts and
+ * ASCII PLY -> EINVAL (host loader). */
+int pamopt_cu_load_ply(pamopt_cu_ctx ctx, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
+                       pamopt_cu_load_stats* stats);
+/* normalize_unit_cube (mesh_io.cpp:393-408), in place; scale_translation = {scale, tx, ty, tz} or NULL */
+int pamopt_cu_normalize_unit_cube(pamopt_cu_mesh mesh, double padding, double* scale_translation);
 
 /* ---- stage 1a: voxel_field --------------------------------------------------------- */
 /* R: power of two >= 8.  Returns the UDF lattice ((R+1)^3 f32, x-fastest, +INF sentinel). */

@@ -102,6 +102,9 @@ def ref():
         L.ref_normalize_unit_cube.argtypes = [f64p, C.c_int64, C.c_double, f64p]
         L.ref_analyze_topology_lists.restype = C.c_int
         L.ref_analyze_topology_lists.argtypes = [f64p, C.c_int64, i32p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_load_mesh.restype = C.c_int
+        L.ref_load_mesh.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), i64p]
+        L.ref_load_fetch.argtypes = [C.c_void_p, C.c_void_p]
         L.ref_nearest_primitive.restype = C.c_int
         L.ref_nearest_primitive.argtypes = [f64p, C.c_int64, i32p, C.c_int64, f64p, C.c_int64, C.c_void_p,
                                             C.c_void_p, C.c_void_p]
@@ -407,3 +410,45 @@ def ref_nearest(v, f, pts):
                                      dist.ctypes.data, clo.ctypes.data)
     assert rc == 0
     return face, dist, clo
+
+
+# ---------------------------------------------------------------- ingest (mesh_io.cpp)
+def ref_load_mesh(path: str):
+    """The reference's own load_mesh: (vertices, faces, stats dict) or None on a load error."""
+    nv, nf = C.c_int64(), C.c_int64()
+    st = np.zeros(3, np.int64)
+    if ref().ref_load_mesh(path.encode(), C.byref(nv), C.byref(nf), st) != 0:
+        return None
+    v = np.empty((nv.value, 3))
+    f = np.empty((nf.value, 3), np.int32)
+    ref().ref_load_fetch(v.ctypes.data, f.ctypes.data)
+    return v, f, dict(degenerate_faces_dropped=int(st[0]), polygons_triangulated=int(st[1]),
+                      vertices_welded=int(st[2]))
+
+
+def load_stl_binary(data: bytes):
+    """Restatement of load_stl's binary branch + StlWelder (mesh_io.cpp:291-366): corners welded
+    by exact equality (bit patterns; a NaN corner is never equal), first-occurrence numbering,
+    faces with repeated indices dropped (add_polygon, mesh_io.cpp:32-42)."""
+    count = int(np.frombuffer(data[80:84], np.uint32)[0])
+    rec = np.frombuffer(data[84:84 + 50 * count], np.uint8).reshape(count, 50)
+    pts = rec[:, 12:48].copy().view(np.float32).reshape(count * 3, 3)
+    ids, verts, welded = {}, [], 0
+    vid = np.empty(count * 3, np.int64)
+    for c, p in enumerate(pts):
+        if np.isnan(p).any():
+            vid[c] = len(verts)
+            verts.append(p.astype(np.float64))
+            continue
+        key = p.tobytes()
+        if key in ids:
+            vid[c] = ids[key]
+            welded += 1
+        else:
+            ids[key] = vid[c] = len(verts)
+            verts.append(p.astype(np.float64))
+    tri = vid.reshape(count, 3)
+    keep = (tri[:, 0] != tri[:, 1]) & (tri[:, 1] != tri[:, 2]) & (tri[:, 0] != tri[:, 2])
+    v = np.array(verts, np.float64).reshape(-1, 3)
+    return v, tri[keep].astype(np.int32), dict(degenerate_faces_dropped=int((~keep).sum()), polygons_triangulated=0,
+                                               vertices_welded=welded)

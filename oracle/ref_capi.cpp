@@ -85,6 +85,30 @@ int ref_analyze_topology_lists(const double* v, int64_t nv, const int32_t* f, in
   }
 }
 
+// mesh_io.cpp:372-385: load_mesh; the result is kept for ref_load_fetch.  stats = {degenerate
+// faces dropped, polygons triangulated, vertices welded}; returns 0, or -1 on a load error
+static IndexedMesh g_loaded;
+int ref_load_mesh(const char* path, int64_t* nv, int64_t* nf, int64_t* stats) {
+  try {
+    LoadStats st;
+    g_loaded = load_mesh(path, &st);
+    *nv = g_loaded.vertex_count();
+    *nf = g_loaded.face_count();
+    stats[0] = st.degenerate_faces_dropped;
+    stats[1] = st.polygons_triangulated;
+    stats[2] = st.vertices_welded;
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+void ref_load_fetch(double* v, int32_t* f) {
+  for (int i = 0; i < g_loaded.vertex_count(); ++i)
+    for (int k = 0; k < 3; ++k) v[3 * i + k] = g_loaded.vertices[i][k];
+  for (int i = 0; i < g_loaded.face_count(); ++i)
+    for (int k = 0; k < 3; ++k) f[3 * i + k] = g_loaded.faces[i][k];
+}
+
 // lbvh.cpp:192-237: TriangleBvh::nearest_primitive for a batch of points
 int ref_nearest_primitive(const double* v, int64_t nv, const int32_t* f, int64_t nf, const double* pts, int64_t n,
                           int32_t* face, double* dist, double* closest) {

@@ -40,6 +40,14 @@ class StageTimes(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class LoadStats(C.Structure):
+    _fields_ = [("degenerate_faces_dropped", C.c_int64), ("polygons_triangulated", C.c_int64),
+                ("vertices_welded", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Topology(C.Structure):
     _fields_ = [("manifold", C.c_int32), ("watertight", C.c_int32), ("euler_characteristic", C.c_int64),
                 ("boundary_edge_count", C.c_int64), ("n_nonmanifold_edges", C.c_int64),
@@ -89,6 +97,9 @@ _SIGS = {
     "pamopt_cu_mesh_download": (C.c_int, [vp, vp, vp]),
     "pamopt_cu_mesh_copy_to_device": (C.c_int, [vp, vp, vp]),
     "pamopt_cu_mesh_free": (C.c_int, [vp]),
+    "pamopt_cu_load_stl": (C.c_int, [vp, vp, i64, P(vp), P(LoadStats)]),
+    "pamopt_cu_load_ply": (C.c_int, [vp, vp, i64, P(vp), P(LoadStats)]),
+    "pamopt_cu_normalize_unit_cube": (C.c_int, [vp, dbl, vp]),
     "pamopt_cu_compute_udf": (C.c_int, [vp, vp, i32, P(vp)]),
     "pamopt_cu_udf_to_sdf": (C.c_int, [vp, dbl]),
     "pamopt_cu_compute_sdf": (C.c_int, [vp, vp, i32, dbl, P(vp)]),

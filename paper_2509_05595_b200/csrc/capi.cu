@@ -9,6 +9,9 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <vector>
+#include <sstream>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -422,6 +425,192 @@ int pamopt_cu_grid_slab_from_device(pamopt_cu_ctx c, int32_t R, int32_t z0, int3
 int pamopt_cu_grid_slab_upload(pamopt_cu_ctx c, int32_t R, int32_t z0, int32_t z1, const float* samples,
                                pamopt_cu_grid* out) {
   return grid_slab_make(c, R, z0, z1, samples, cudaMemcpyHostToDevice, out);
+}
+
+// ------------------------------------------------------------------------------ ingest
+static pamopt_cu_mesh mesh_from_ingest(pamopt_cu_ctx c, pcu::IngestResult& r) {
+  auto* m = new pamopt_cu_mesh_s();
+  m->owner = c;
+  ++c->refs;
+  m->nv = r.nv;
+  m->nf = r.nf;
+  m->V = std::move(r.V);
+  m->F = std::move(r.F);
+  return m;
+}
+
+int pamopt_cu_load_stl(pamopt_cu_ctx c, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
+                       pamopt_cu_load_stats* stats) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(bytes && out && nbytes >= 0, PAMOPT_CU_EINVAL, "null argument");
+    const char* b = static_cast<const char*>(bytes);
+    if (nbytes >= 5 && std::strncmp(b, "solid", 5) == 0) {
+      const std::string head(b, static_cast<size_t>(nbytes));
+      PCU_REQUIRE(head.find("facet") == std::string::npos, PAMOPT_CU_EINVAL,
+                  "load_stl: ascii stl (parse it with the host loader, mesh_io.cpp:320-342)");
+    }
+    PCU_REQUIRE(nbytes >= 84, PAMOPT_CU_EINVAL, "load_stl: truncated binary stl header");
+    uint32_t count = 0;
+    std::memcpy(&count, b + 80, 4);
+    pcu::DeviceGuard g(c->ctx.device);
+    pcu::DevBuf<uint8_t> d(static_cast<size_t>(nbytes), c->ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(d.get(), bytes, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, c->ctx.stream));
+    pcu::IngestResult r;
+    pcu::load_stl_binary(c->ctx, d.get(), nbytes, count, r);
+    PCU_REQUIRE(r.nf > 0, PAMOPT_CU_EINVAL, "load_stl: empty mesh (no faces)");
+    if (stats) *stats = pamopt_cu_load_stats{r.degenerate_dropped, 0, r.welded};
+    *out = mesh_from_ingest(c, r);
+  });
+}
+
+// PLY header (mesh_io.cpp:141-185) -> fixed-size body layout for the GPU decoder
+static pcu::PlyBinaryLayout ply_layout(const char* b, int64_t n, int64_t& body) {
+  auto type_of = [](const std::string& t, int& code) -> int {
+    if (t == "float" || t == "float32") { code = 0; return 4; }
+    if (t == "double" || t == "float64") { code = 1; return 8; }
+    if (t == "int" || t == "int32") { code = 2; return 4; }
+    if (t == "uint" || t == "uint32") { code = 3; return 4; }
+    if (t == "char" || t == "int8") { code = 4; return 1; }
+    if (t == "uchar" || t == "uint8") { code = 5; return 1; }
+    if (t == "short" || t == "int16") { code = 6; return 2; }
+    if (t == "ushort" || t == "uint16") { code = 7; return 2; }
+    throw pcu::Error(PAMOPT_CU_EINVAL, "load_ply: unknown ply type " + t);
+  };
+  const std::string text(b, static_cast<size_t>(std::min<int64_t>(n, 1 << 16)));
+  const size_t eh = text.find("end_header");
+  PCU_REQUIRE(text.compare(0, 3, "ply") == 0 && eh != std::string::npos, PAMOPT_CU_EINVAL,
+              "load_ply: missing ply magic or end_header");
+  const size_t nl = text.find('\n', eh);
+  PCU_REQUIRE(nl != std::string::npos, PAMOPT_CU_EINVAL, "load_ply: truncated header");
+  body = static_cast<int64_t>(nl + 1);
+  struct Prop { std::string name; int code = 0, size = 0; bool list = false; int ccode = 0, csize = 0; };
+  struct Elem { std::string name; int64_t count = 0; std::vector<Prop> props; };
+  std::vector<Elem> els;
+  std::string format;
+  size_t pos = text.find('\n') + 1;
+  while (pos < eh) {
+    size_t e = text.find('\n', pos);
+    std::string line = text.substr(pos, e - pos);
+    pos = e + 1;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    std::istringstream ss(line);
+    std::string tag;
+    ss >> tag;
+    if (tag == "format") {
+      ss >> format;
+    } else if (tag == "element") {
+      Elem el;
+      ss >> el.name >> el.count;
+      els.push_back(el);
+    } else if (tag == "property") {
+      PCU_REQUIRE(!els.empty(), PAMOPT_CU_EINVAL, "load_ply: property before element");
+      Prop p;
+      std::string t;
+      ss >> t;
+      if (t == "list") {
+        std::string ct, it;
+        ss >> ct >> it >> p.name;
+        p.list = true;
+        p.csize = type_of(ct, p.ccode);
+        p.size = type_of(it, p.code);
+      } else {
+        p.size = type_of(t, p.code);
+        ss >> p.name;
+      }
+      els.back().props.push_back(p);
+    }
+  }
+  PCU_REQUIRE(format == "binary_little_endian", PAMOPT_CU_EINVAL,
+              "load_ply: only binary_little_endian bodies are decoded on the GPU (ascii: host loader)");
+  pcu::PlyBinaryLayout L;
+  int64_t off = body;
+  bool have_v = false, have_f = false;
+  for (const Elem& el : els) {
+    int64_t stride = 0;
+    int list_props = 0;
+    for (const Prop& p : el.props) {
+      if (p.list) {
+        ++list_props;
+        stride += p.csize + 3 * p.size;  // fixed 3-entry lists (verified on the GPU)
+      } else {
+        stride += p.size;
+      }
+    }
+    if (el.name == "vertex") {
+      PCU_REQUIRE(list_props == 0, PAMOPT_CU_EINVAL, "load_ply: list property in the vertex element");
+      int64_t o = 0;
+      int found = 0;
+      for (const Prop& p : el.props) {
+        const int k = p.name == "x" ? 0 : (p.name == "y" ? 1 : (p.name == "z" ? 2 : -1));
+        if (k >= 0) {
+          L.off[k] = static_cast<int>(o);
+          L.type[k] = p.code;
+          found |= 1 << k;
+        }
+        o += p.size;
+      }
+      PCU_REQUIRE(found == 7, PAMOPT_CU_EINVAL, "load_ply: vertex element lacks x/y/z");
+      L.vbase = off;
+      L.vstride = stride;
+      L.nvert = el.count;
+      have_v = true;
+    } else if (el.name == "face") {
+      PCU_REQUIRE(have_v, PAMOPT_CU_EINVAL, "load_ply: face element before the vertex element");
+      PCU_REQUIRE(list_props == 1, PAMOPT_CU_EINVAL, "load_ply: face element needs exactly one list property");
+      int64_t o = 0;
+      for (const Prop& p : el.props) {
+        if (p.list) {
+          L.count_off = static_cast<int>(o);
+          L.count_type = p.ccode;
+          L.index_off = static_cast<int>(o + p.csize);
+          L.index_type = p.code;
+          o += p.csize + 3 * p.size;
+        } else {
+          o += p.size;
+        }
+      }
+      L.fbase = off;
+      L.fstride = stride;
+      L.nface = el.count;
+      have_f = true;
+    } else {
+      PCU_REQUIRE(list_props == 0 || have_f, PAMOPT_CU_EINVAL,
+                  "load_ply: variable-size element before the faces (host loader)");
+    }
+    if (list_props == 0 || el.name == "face") off += stride * el.count;
+  }
+  PCU_REQUIRE(have_v, PAMOPT_CU_EINVAL, "load_ply: no vertex element");
+  PCU_REQUIRE(!have_f || L.fbase + L.fstride * L.nface <= n, PAMOPT_CU_EINVAL, "load_ply: truncated binary body");
+  PCU_REQUIRE(L.vbase + L.vstride * L.nvert <= n, PAMOPT_CU_EINVAL, "load_ply: truncated binary body");
+  return L;
+}
+
+int pamopt_cu_load_ply(pamopt_cu_ctx c, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
+                       pamopt_cu_load_stats* stats) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(bytes && out && nbytes > 0, PAMOPT_CU_EINVAL, "null argument");
+    int64_t body = 0;
+    const pcu::PlyBinaryLayout L = ply_layout(static_cast<const char*>(bytes), nbytes, body);
+    pcu::DeviceGuard g(c->ctx.device);
+    pcu::DevBuf<uint8_t> d(static_cast<size_t>(nbytes), c->ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(d.get(), bytes, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, c->ctx.stream));
+    pcu::IngestResult r;
+    pcu::load_ply_binary(c->ctx, d.get(), L, r);
+    PCU_REQUIRE(r.nf > 0, PAMOPT_CU_EINVAL, "load_ply: empty mesh (no faces)");
+    if (stats) *stats = pamopt_cu_load_stats{r.degenerate_dropped, 0, 0};
+    *out = mesh_from_ingest(c, r);
+  });
+}
+
+int pamopt_cu_normalize_unit_cube(pamopt_cu_mesh m, double padding, double* st) {
+  return guarded([&] {
+    PCU_REQUIRE(m != nullptr, PAMOPT_CU_EINVAL, "null mesh");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    pcu::normalize_unit_cube(ctx, m->V.get(), m->nv, padding, st);
+  });
 }
 
 int pamopt_cu_udf_to_sdf(pamopt_cu_grid gr, double eps) {

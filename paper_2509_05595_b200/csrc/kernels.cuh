@@ -55,6 +55,24 @@ void directed_d2(Ctx& ctx, const double* Va, const int32_t* Fa, int64_t nfa, con
 double max_corner_cos(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf);
 std::vector<int32_t> index_range(Ctx& ctx, const int32_t* d, int64_t n);  // {min, max}
 
+// ---- ingest (ingest.cu)
+struct IngestResult {
+  DevBuf<double> V;
+  DevBuf<int32_t> F;
+  int64_t nv = 0, nf = 0, welded = 0, degenerate_dropped = 0;
+};
+// body offsets/types of a binary little-endian PLY (header parsed on the host); types: 0 float,
+// 1 double, 2 int32, 3 uint32, 4 int8, 5 uint8, 6 int16, 7 uint16
+struct PlyBinaryLayout {
+  int64_t vbase = 0, vstride = 0, nvert = 0;
+  int off[3] = {0, 0, 0}, type[3] = {0, 0, 0};
+  int64_t fbase = 0, fstride = 0, nface = 0;
+  int count_off = 0, count_type = 5, index_off = 1, index_type = 2;
+};
+void load_stl_binary(Ctx& ctx, const uint8_t* d_bytes, int64_t nbytes, uint32_t count, IngestResult& out);
+void load_ply_binary(Ctx& ctx, const uint8_t* d_bytes, const PlyBinaryLayout& layout, IngestResult& out);
+void normalize_unit_cube(Ctx& ctx, double* dV, int64_t nv, double padding, double* scale_translation);
+
 // ---- tri_isect (isect.cu)
 // all intersecting pairs (i<j) among faces with alive[i] (alive may be null); if `query` is
 // non-null only pairs with at least one query face are reported.  Result sorted (host).
