@@ -381,9 +381,13 @@ __global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict_
 }
 
 // cell size = mean box extent of the build set
+#ifndef PCU_CELL_SCALE
+#define PCU_CELL_SCALE 1.5
+#endif
+// grid cell edge = PCU_CELL_SCALE x the mean box extent of the build set
 __global__ void k_set_invh(DetectScalars* ds, int64_t n) {
   const double mean = n > 0 ? ds->ext_sum / static_cast<double>(n) : 1.0;
-  ds->inv_h = 1.0 / (mean > 0.0 ? mean : 1e-3);
+  ds->inv_h = 1.0 / (PCU_CELL_SCALE * (mean > 0.0 ? mean : 1e-3));
 }
 
 // pass 0: count bucket entries (or big); pass 1: fill
