@@ -1,3 +1,4 @@
+"""Aggregate an ncu --csv launch list (gpu__time_duration.sum) by kernel: usage agg_launches.py <csv> [top]"""
 import csv, collections, sys
 rows=list(csv.reader(open(sys.argv[1])))
 hi=[i for i,r in enumerate(rows) if 'Kernel Name' in r][0]

@@ -1,4 +1,4 @@
-"""Small driver for ncu captures: one C2 pipeline pass (device resident)."""
+"""Driver for ncu captures: one device-resident pipeline pass of a config (default c2)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_05595_b200 import api, fixtures as FX
