@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
   __shared__ int32_t qc[4][kQ][3];
   __shared__ uint32_t qh[4][kQ];
   __shared__ uint8_t qo[4][kQ];
+  __shared__ uint32_t spre[4][32], sbase[4][32];  // drain: inclusive entry-count prefix, first entry
   (void)big;
   if (threadIdx.x == 0) nbuf = 0;
   __syncthreads();
@@ -513,31 +514,49 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
     if (qn >= 32 || (!more && qn > 0)) {
       __syncwarp();
       const int take = min(qn, 32);
+      // lane r < take owns record qn - take + r; its cell's entry list is spread over the warp:
+      // flattened (record, entry) index t -> record by a 5-step search of the warp's prefix sums
+      uint32_t cnt = 0, e0 = 0;
       if (lane < take) {
-        const int r = qn - take + lane;
+        const uint32_t h = qh[warp][qn - take + lane];
+        e0 = boff[h];
+        cnt = bcount[h];
+      }
+      uint32_t incl = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      spre[warp][lane] = incl;
+      sbase[warp][lane] = e0;
+      __syncwarp();
+      for (uint32_t t = lane; t < total; t += 32) {
+        int lo = 0, hi = take - 1;  // first record whose inclusive prefix exceeds t
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (spre[warp][mid] > t) hi = mid;
+          else lo = mid + 1;
+        }
+        const int r = qn - take + lo;
+        const uint32_t e = sbase[warp][lo] + (t - (lo ? spre[warp][lo - 1] : 0u));
         const int o = qo[warp][r];
         const int32_t op = sp[warp][o];
-        const FBox ob = sbox[warp][o];
-        const bool obuild = sbuild[warp][o] != 0;
-        const int32_t x = qc[warp][r][0], y = qc[warp][r][1], z = qc[warp][r][2];
-        const int32_t lx = slo[warp][o][0], ly = slo[warp][o][1], lz = slo[warp][o][2];
-        const uint32_t h = qh[warp][r];
-        const uint32_t e0 = boff[h], e1 = e0 + bcount[h];
-        for (uint32_t e = e0; e < e1; ++e) {
-          const int4 en = entries[e];  // face id + its first cell: the dedup test needs no box load
-          // first common cell of the two ranges (a hash collision can at worst duplicate a pair)
-          if (x != max(lx, en.y) || y != max(ly, en.z) || z != max(lz, en.w)) continue;
-          const int32_t a = en.x;
-          if (a == op || (obuild && a < op)) continue;  // the pair is emitted from probe a instead
-          if (!overlap(ob, B[a])) continue;
-          const uint64_t v = (static_cast<uint64_t>(static_cast<uint32_t>(op)) << 32) | static_cast<uint32_t>(a);
-          const unsigned slot = atomicAdd(&nbuf, 1u);
-          if (slot < kBuf) {
-            buf[slot] = v;
-          } else {  // block buffer full: direct global append
-            const unsigned long long g = agg_inc(ncand);
-            if (g < cap) cand[g] = v;
-          }
+        const int4 en = entries[e];  // face id + its first cell: the dedup test needs no box load
+        // first common cell of the two ranges (a hash collision can at worst duplicate a pair)
+        if (qc[warp][r][0] != max(slo[warp][o][0], en.y) || qc[warp][r][1] != max(slo[warp][o][1], en.z) ||
+            qc[warp][r][2] != max(slo[warp][o][2], en.w))
+          continue;
+        const int32_t a = en.x;
+        if (a == op || (sbuild[warp][o] && a < op)) continue;  // the pair is emitted from probe a instead
+        if (!overlap(sbox[warp][o], B[a])) continue;
+        const uint64_t v = (static_cast<uint64_t>(static_cast<uint32_t>(op)) << 32) | static_cast<uint32_t>(a);
+        const unsigned slot = atomicAdd(&nbuf, 1u);
+        if (slot < kBuf) {
+          buf[slot] = v;
+        } else {  // block buffer full: direct global append
+          const unsigned long long g = agg_inc(ncand);
+          if (g < cap) cand[g] = v;
         }
       }
       __syncwarp();
