@@ -296,7 +296,10 @@ __global__ void k_make_items(const uint32_t* __restrict__ cnt, const uint32_t* _
 // so all 32 lanes evaluate distances on useful work.  Vertex distances: a certified FP32
 // evaluation first (well-conditioned triangles) skips every triangle that cannot lower the
 // vertex's running minimum; the rest are evaluated with the pinned FP64 routine.
-__global__ void __launch_bounds__(256, 3) k_brick(const Item* __restrict__ items, const uint32_t* __restrict__ tris,
+#ifndef PCU_BRICK_MINB
+#define PCU_BRICK_MINB 3
+#endif
+__global__ void __launch_bounds__(256, PCU_BRICK_MINB) k_brick(const Item* __restrict__ items, const uint32_t* __restrict__ tris,
                                                   const TriD* __restrict__ T, int R, int rb, int bs, int J,
                                                   unsigned long long* __restrict__ blocks) {
   __shared__ unsigned long long vmin[729];
