@@ -43,6 +43,8 @@ def test_c3_qem_properties(api, c3):
     out, st, tm = api.remesh_device(m, R, target)
     ov, of = out.download()
     assert target <= len(of) <= target + 200 and st["iterations"] < 1000
+    import bench
+    assert st["face_iterations"] == bench.FACE_ITERATIONS["c3"]  # the reference arm's work units
     t1 = api.analyze_topology(out)
     assert t1["manifold"] and t1["watertight"] and t1["euler"] == t0["euler"]
     assert len(api.detect_self_intersections(out)) == 0
