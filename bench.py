@@ -450,20 +450,38 @@ def run_c4(args):
 
 def run_c5(args):
     """C5: a batch of mixed meshes, LPT-assigned one-per-GPU (no collective on the data path).
-    Weak-ish scaling: the batch is fixed, value = whole-job ms per mesh (makespan / meshes)."""
+    Within a GPU, --streams host threads each drive their own context (stream): the long QEM
+    tails of small meshes are latency-bound, so concurrent meshes overlap on the device.
+    Strong scaling (the batch is fixed); value = whole-job ms per mesh (makespan / meshes)."""
+    import threading
+
     torch, dist, rank, world, local = _dist_setup()
     from paper_2509_05595_b200 import api, fixtures as FX
     from paper_2509_05595_b200 import distributed as D
     meshes = FX.c5_batch(args.batch)
-    ctx = api.Context(local)
     mine = D.lpt_assign([len(m[1]) for m in meshes], world)[rank]
-    dev = {i: api.DeviceMesh.upload(meshes[i][0], meshes[i][1], ctx) for i in mine}
+    K = max(1, args.streams)
+    ctxs = [api.Context(local) for _ in range(K)]
+    lanes = D.lpt_assign([len(meshes[i][1]) for i in mine], K)  # per-stream share (positions in mine)
+    dev = {}
+    for w in range(K):
+        for j in lanes[w]:
+            i = mine[j]
+            dev[i] = api.DeviceMesh.upload(meshes[i][0], meshes[i][1], ctxs[w])
 
-    def step():
-        for i in mine:
+    def worker(w):
+        for j in lanes[w]:
+            i = mine[j]
             _, _, R, target = meshes[i]
             out, st, tm = api.remesh_device(dev[i], R, target)
             out.free()
+
+    def step():
+        threads = [threading.Thread(target=worker, args=(w,)) for w in range(K)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
 
     for _ in range(args.warmup):
         step()
@@ -477,6 +495,7 @@ def run_c5(args):
         torch.cuda.synchronize()
         ev0.record()
         step()
+        torch.cuda.synchronize()  # device-wide: every stream's work precedes ev1
         ev1.record()
         torch.cuda.synchronize()
         total += ev0.elapsed_time(ev1)
@@ -488,7 +507,7 @@ def run_c5(args):
                 "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": "C5", "meshes": len(meshes), "faces_in_total": int(sum(len(m[1]) for m in meshes)),
-                           "parallelism": f"LPT one-mesh-per-GPU x{world}",
+                           "parallelism": f"LPT one-mesh-per-GPU x{world}, {K} concurrent streams per GPU",
                            "lpt_makespan_ratio": round(D.makespan([len(m[1]) for m in meshes], world), 3)}}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -496,7 +515,8 @@ def run_c5(args):
         dist.destroy_process_group()
     for m in dev.values():
         m.free()
-    ctx.close()
+    for c in ctxs:
+        c.close()
     return 0
 
 
@@ -507,6 +527,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--batch", type=int, default=64, help="C5 batch size")
+    ap.add_argument("--streams", type=int, default=8, help="C5: concurrent meshes (contexts) per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     args = ap.parse_args()

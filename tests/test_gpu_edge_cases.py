@@ -106,3 +106,31 @@ def test_hierarchy_levels_c1_scale(api, oracle, c1):
         got = api.build_hierarchy_pairs((c1["v"], c1["f"]), c1["R"], r)
         ref = oracle.hierarchy_pairs(c1["v"], c1["f"], c1["R"], r)
         assert np.array_equal(got, ref), r
+
+
+def test_concurrent_contexts_match_sequential(api):
+    """Distinct contexts on distinct host threads (the C5 batch path) give the same outputs as
+    sequential runs: contexts share nothing but the device."""
+    import threading
+    cases = [FX.make_config("c1")[:2] + (128, 3000), (FX.soup(6, 5000, seed=11)) + (128, 4000)]
+    cases = [(FX.normalize_unit_cube(v, 6.0 / R)[0], f, R, t) for v, f, R, t in cases]
+    seq = [api.run_pipeline(v, f, R, t) for v, f, R, t in cases]
+    out = [None] * len(cases)
+
+    def work(k):
+        ctx = api.Context(0)
+        v, f, R, t = cases[k]
+        m = api.DeviceMesh.upload(v, f, ctx)
+        o, st, tm = api.remesh_device(m, R, t)
+        out[k] = o.download()
+        o.free()
+        m.free()
+        ctx.close()
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(cases))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for s, (ov, of) in zip(seq, out):
+        assert np.array_equal(of, s.faces) and np.array_equal(bits(ov), bits(s.vertices))
