@@ -348,6 +348,18 @@ def run_ours(args):
             "clocks": clk,
         }
         line["certification"] = cert
+        # the limiter of the UDF's dominant kernel from the committed ncu capture: k_brick is
+        # instruction-issue bound (distance arithmetic), which is why the HBM fraction is small
+        cp = os.path.join(ROOT, "profiles", f"r01_ncu_counters_{args.config}.json")
+        if os.path.exists(cp):
+            with open(cp) as fh:
+                kb = json.load(fh)["kernels"].get("k_brick")
+            if kb:
+                line["roofline"]["compute"] = {
+                    "kernel": "k_brick", "bound": "issue", "issue_active_frac": round(kb["issue_active_pct"] / 100, 4),
+                    "fp64_pipe_frac": round(kb["fp64_pipe_pct"] / 100, 4), "fma_pipe_frac": round(kb["fma_pipe_pct"] / 100, 4),
+                    "simt_efficiency": round(kb["threads_per_warp_inst"] / 32, 4),
+                    "source": f"profiles/r01_ncu_counters_{args.config}.json"}
         ktot = sum(ms for ms, _ in ktimes.values()) or 1.0
         top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:12]
         line["kernels"] = {"source": "one untimed step, CUDA events around every launch",
