@@ -630,8 +630,10 @@ __device__ __forceinline__ void report(DetectScalars* ds, int mode, int32_t p, i
   if (mode == 1) {
     atomicAdd(&ds->found, 1ull);
     const int32_t op = owner[p], oa = owner[a];
-    if (op >= 0 && applied[op]) revert[op] = 1;
-    if (oa >= 0 && applied[oa]) revert[oa] = 1;
+    // owner[f] >= 0 exactly while its collapse is applied (k_collapse sets it only for applied
+    // collapses, k_revert clears it together with applied), so no applied[] lookup is needed
+    if (op >= 0) revert[op] = 1;
+    if (oa >= 0) revert[oa] = 1;
   } else {
     const unsigned long long k = atomicAdd(&ds->npairs, 1ull);
     if (k < pair_cap) {
@@ -673,7 +675,7 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
     const int32_t p = static_cast<int32_t>(cand[i] >> 32), a = static_cast<int32_t>(cand[i] & 0xffffffffu);
     if (mode == 1) {
       const int32_t op = owner[p], oa = owner[a];
-      if (!(op >= 0 && applied[op]) && !(oa >= 0 && applied[oa])) continue;
+      if (op < 0 && oa < 0) continue;  // owner >= 0 <=> applied (see report)
     }
     const int32_t* tp = F + 3 * p;
     const int32_t* ta = F + 3 * a;
@@ -709,7 +711,7 @@ __global__ void __launch_bounds__(128, PCU_NARROW_MINB) k_narrow(const double* _
     const int32_t p = static_cast<int32_t>(L[i] >> 32), a = static_cast<int32_t>(L[i] & 0xffffffffu);
     if (mode == 1) {
       const int32_t op = owner[p], oa = owner[a];
-      const bool rp = op >= 0 && applied[op], ra = oa >= 0 && applied[oa];
+      const bool rp = op >= 0, ra = oa >= 0;  // owner >= 0 <=> applied (see report)
       if ((!rp || revert[op]) && (!ra || revert[oa])) continue;  // nothing left to flag
     }
     const int32_t* tp = F + 3 * p;
