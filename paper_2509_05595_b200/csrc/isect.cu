@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B,
 }
 
 __device__ __forceinline__ void report(DetectScalars* ds, int mode, int32_t p, int32_t a, int32_t* pairs,
-                                       uint64_t pair_cap, const int32_t* owner, const uint8_t* applied,
+                                       uint64_t pair_cap, const int32_t* owner,
                                        uint8_t* revert) {
   if (mode == 1) {
     atomicAdd(&ds->found, 1ull);
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
                                                   uint64_t cap, DetectScalars* __restrict__ ds, int mode,
                                                   uint64_t* __restrict__ cls, int32_t* __restrict__ pairs,
                                                   uint64_t pair_cap, const int32_t* __restrict__ owner,
-                                                  const uint8_t* __restrict__ applied, uint8_t* __restrict__ revert) {
+                                                  uint8_t* __restrict__ revert) {
   const unsigned long long n = ds->ncand;
   if (n > cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) ds->redo = 1;
@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
     for (int u = 0; u < 3; ++u)
       for (int w = 0; w < 3; ++w) shared += tp[u] == ta[w];
     if (shared == 3 || degen[p] || degen[a]) {
-      report(ds, mode, p, a, pairs, pair_cap, owner, applied, revert);
+      report(ds, mode, p, a, pairs, pair_cap, owner, revert);
       continue;
     }
     const unsigned long long slot = agg_inc_labeled(&ds->ncls[shared], static_cast<unsigned>(shared));
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(128, PCU_NARROW_MINB) k_narrow(const double* _
                                                 const uint64_t* __restrict__ cls, uint64_t cap,
                                                 DetectScalars* __restrict__ ds, int mode, int32_t* __restrict__ pairs,
                                                 uint64_t pair_cap, const int32_t* __restrict__ owner,
-                                                const uint8_t* __restrict__ applied, uint8_t* __restrict__ revert) {
+                                                uint8_t* __restrict__ revert) {
   if (ds->redo) return;
   const unsigned long long n = ds->ncls[SHARED];
   const uint64_t* L = cls + SHARED * cap;
@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(128, PCU_NARROW_MINB) k_narrow(const double* _
       const PairInfo I = pair_info(tp, ta);
       hit = SHARED == 1 ? verdict1(V, tp, ta, I) : verdict2(V, tp, ta, I);
     }
-    if (hit) report(ds, mode, p, a, pairs, pair_cap, owner, applied, revert);
+    if (hit) report(ds, mode, p, a, pairs, pair_cap, owner, revert);
   }
 }
 
@@ -772,7 +772,7 @@ namespace {
 //   (ids, or every alive face) -> narrow phase.  Results stay in S.ds (found / npairs / redo).
 void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive,
                   const int32_t* build_ids, int64_t n_build, const int32_t* probe_ids, int64_t n_probe, int sym,
-                  int mode, int32_t* pairs, uint64_t pair_cap, const int32_t* owner, const uint8_t* applied,
+                  int mode, int32_t* pairs, uint64_t pair_cap, const int32_t* owner,
                   uint8_t* revert, bool boxes_current = false) {
   cudaStream_t st = ctx.stream;
   S.ds.ensure(1, st);
@@ -825,13 +825,13 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   S.cls.ensure(3 * S.cand_cap, st);
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
-             S.cls.get(), pairs, pair_cap, owner, applied, revert);
+             S.cls.get(), pairs, pair_cap, owner, revert);
   PCU_LAUNCH(ctx, k_narrow<2>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
-             applied, revert);
+             revert);
   PCU_LAUNCH(ctx, k_narrow<1>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
-             applied, revert);
+             revert);
   PCU_LAUNCH(ctx, k_narrow<0>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
-             applied, revert);
+             revert);
 }
 
 }  // namespace
@@ -846,8 +846,7 @@ std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, 
   uint64_t pair_cap = static_cast<uint64_t>(nf) + 1024;
   DevBuf<int32_t> pairs(2 * pair_cap, ctx.stream);
   while (true) {
-    detect_round(ctx, S, dV, dF, nf, d_alive, nullptr, nf, nullptr, nf, 1, 0, pairs.get(), pair_cap, nullptr, nullptr,
-                 nullptr);
+    detect_round(ctx, S, dV, dF, nf, d_alive, nullptr, nf, nullptr, nf, 1, 0, pairs.get(), pair_cap, nullptr, nullptr);
     const DetectScalars ds = read_scalar(ctx, S.ds.get());
     if (ds.redo) {
       S.cand_cap = ds.ncand + ds.ncand / 4 + 4096;
@@ -883,19 +882,19 @@ void tri_tri_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t*
 
 void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                        const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
-                       const uint8_t* d_applied, uint8_t* d_revert) {
+                       uint8_t* d_revert) {
   // round 1: grid over the faces owned by applied collapses, probed by every alive face
-  detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner, d_applied,
+  detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner,
                d_revert, true);
 }
 
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                                 const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
                                 const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
-                                const uint8_t* d_applied, uint8_t* d_revert) {
+                                uint8_t* d_revert) {
   // later rounds: only (restored face, applied-owned face) pairs can be new
   detect_round(ctx, S, dV, dF, nf, d_falive, d_restored, n_restored, d_owned, n_owned, 0, 1, nullptr, 0, d_owner,
-               d_applied, d_revert, true);
+               d_revert, true);
 }
 
 // Persistent face boxes for the QEM loop: computed once, then refreshed only for the faces a

@@ -82,15 +82,16 @@ void tri_tri_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t*
 
 // Broad phase + narrow phase of the QEM undo loop, asynchronous: results (found pairs, buffer
 // overflow) are left in device scalars; detect_scalars_ptr/size let the caller fetch them in
-// the same host synchronisation as its own counters.
+// the same host synchronisation as its own counters.  d_owner[f] >= 0 names the applied collapse
+// that modified face f (owner is set only for applied collapses and cleared on revert).
 struct IsectScratch;
 void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                        const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
-                       const uint8_t* d_applied, uint8_t* d_revert);
+                       uint8_t* d_revert);
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                                 const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
                                 const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
-                                const uint8_t* d_applied, uint8_t* d_revert);
+                                uint8_t* d_revert);
 void boxes_init(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive);
 void boxes_update(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, const int32_t* ids, int64_t n,
                   const uint8_t* d_alive);

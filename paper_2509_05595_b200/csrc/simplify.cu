@@ -863,10 +863,10 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
         PCU_CUDA(cudaMemsetAsync(revert.get(), 0, nm, st));
         PCU_CUDA(cudaMemsetAsync(&cnt.get()->restored, 0, 8, st));
         if (first_round)
-          undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), B.applied, revert.get());
+          undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), revert.get());
         else
           undo_detect_restored_async(ctx, *isc, X, F, nf, falive.get(), rlist.get(), nrest, qa, nq, owner.get(),
-                                     B.applied, revert.get());
+                                     revert.get());
         PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
                    Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get(),
                    rlist.get());
