@@ -224,6 +224,27 @@ typedef struct {
 int pamopt_cu_report(pamopt_cu_mesh reference, pamopt_cu_mesh mesh, int64_t n_samples, uint64_t seed,
                      pamopt_cu_mesh_report* out);
 
+/* ---- stage 3: safe projection (SPEC.md safe_project; Algorithm 2) --------------- */
+typedef struct {
+  int32_t iterations;  /* T = 50 */
+  int32_t refresh;     /* nearest-target refresh period, 10 */
+  int32_t cg_max;      /* 1000 */
+  int32_t elas_power;  /* 1 = |F^T F - I|_F as printed (C1-smoothed below elas_tau); 2 = squared */
+  int64_t samples;     /* m = 16384 surface samples of the input mesh */
+  uint64_t seed;
+  double kdis, kelas, kbend, kbar, dhat, cg_tol, elas_tau;
+} pamopt_cu_project_params;
+typedef struct {
+  int64_t iterations, cg_iterations, refreshes, converged;
+  double energy0, energy, grad_norm, last_alpha;
+} pamopt_cu_project_stats;
+int pamopt_cu_project_defaults(pamopt_cu_project_params* out);
+/* project(mesh_s, mesh_in): deforms mesh_s's vertices in place toward mesh_in along an
+ * intersection-free piecewise-linear trajectory; connectivity unchanged.  EINVAL if mesh_s
+ * self-intersects or has a degenerate face. */
+int pamopt_cu_safe_project(pamopt_cu_mesh mesh_s, pamopt_cu_mesh mesh_in, const pamopt_cu_project_params* params,
+                           pamopt_cu_project_stats* stats);
+
 /* ---- pipeline: UDF -> SDF -> DMC -> QEM ------------------------------------------------ */
 int pamopt_cu_remesh(pamopt_cu_ctx ctx, pamopt_cu_mesh input, int32_t R, double eps, double beta,
                      int64_t target_faces, const pamopt_cu_simplify_params* params,

@@ -48,6 +48,22 @@ class LoadStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ProjectParams(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("refresh", C.c_int32), ("cg_max", C.c_int32), ("elas_power", C.c_int32),
+                ("samples", C.c_int64), ("seed", C.c_uint64), ("kdis", C.c_double), ("kelas", C.c_double),
+                ("kbend", C.c_double), ("kbar", C.c_double), ("dhat", C.c_double), ("cg_tol", C.c_double),
+                ("elas_tau", C.c_double)]
+
+
+class ProjectStats(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("cg_iterations", C.c_int64), ("refreshes", C.c_int64),
+                ("converged", C.c_int64), ("energy0", C.c_double), ("energy", C.c_double),
+                ("grad_norm", C.c_double), ("last_alpha", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Topology(C.Structure):
     _fields_ = [("manifold", C.c_int32), ("watertight", C.c_int32), ("euler_characteristic", C.c_int64),
                 ("boundary_edge_count", C.c_int64), ("n_nonmanifold_edges", C.c_int64),
@@ -129,6 +145,8 @@ _SIGS = {
     "pamopt_cu_hausdorff": (C.c_int, [vp, vp, i64, C.c_uint64, P(dbl)]),
     "pamopt_cu_min_internal_angle": (C.c_int, [vp, P(dbl)]),
     "pamopt_cu_report": (C.c_int, [vp, vp, i64, C.c_uint64, P(MeshReport)]),
+    "pamopt_cu_project_defaults": (C.c_int, [P(ProjectParams)]),
+    "pamopt_cu_safe_project": (C.c_int, [vp, vp, P(ProjectParams), P(ProjectStats)]),
     "pamopt_cu_remesh": (C.c_int, [vp, vp, i32, dbl, dbl, i64, P(SimplifyParams), P(vp), P(SimplifyStats),
                                    P(StageTimes)]),
     "pamopt_cu_remesh_host": (C.c_int, [vp, vp, i64, vp, i64, i32, dbl, dbl, i64, P(SimplifyParams), P(i64),

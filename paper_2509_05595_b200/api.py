@@ -469,3 +469,23 @@ def normalize_unit_cube(mesh: DeviceMesh, padding: float):
     out = (C.c_double * 4)()
     check(lib().pamopt_cu_normalize_unit_cube(mesh.h, float(padding), out))
     return out[0], (out[1], out[2], out[3])
+
+
+# ------------------------------------------------------------------ stage 3 (SPEC.md safe_project)
+def project_defaults() -> dict:
+    p = _lib.ProjectParams()
+    check(lib().pamopt_cu_project_defaults(C.byref(p)))
+    return {k: getattr(p, k) for k, _ in p._fields_}
+
+
+def safe_project(mesh_s: DeviceMesh, mesh_in, **overrides):
+    """project(mesh_s, mesh_in, params): deforms mesh_s in place (intersection-free trajectory);
+    returns the stats dict.  Keyword overrides: iterations, refresh, samples, kdis, ..."""
+    p = _lib.ProjectParams()
+    check(lib().pamopt_cu_project_defaults(C.byref(p)))
+    for k, v in overrides.items():
+        setattr(p, k, v)
+    mi = _mesh(mesh_in, mesh_s.ctx)
+    st = _lib.ProjectStats()
+    check(lib().pamopt_cu_safe_project(mesh_s.h, mi.h, C.byref(p), C.byref(st)))
+    return st.as_dict()

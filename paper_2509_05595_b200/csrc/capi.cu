@@ -894,6 +894,56 @@ int pamopt_cu_report(pamopt_cu_mesh ref, pamopt_cu_mesh m, int64_t n, uint64_t s
   });
 }
 
+// ------------------------------------------------------------------------------ stage 3
+static pcu::ProjectParams to_pp(const pamopt_cu_project_params& p) {
+  pcu::ProjectParams q;
+  q.iterations = p.iterations;
+  q.refresh = p.refresh;
+  q.cg_max = p.cg_max;
+  q.elas_power = p.elas_power;
+  q.samples = p.samples;
+  q.seed = p.seed;
+  q.kdis = p.kdis;
+  q.kelas = p.kelas;
+  q.kbend = p.kbend;
+  q.kbar = p.kbar;
+  q.dhat = p.dhat;
+  q.cg_tol = p.cg_tol;
+  q.elas_tau = p.elas_tau;
+  return q;
+}
+
+int pamopt_cu_project_defaults(pamopt_cu_project_params* out) {
+  return guarded([&] {
+    PCU_REQUIRE(out, PAMOPT_CU_EINVAL, "null argument");
+    const pcu::ProjectParams d;
+    *out = pamopt_cu_project_params{d.iterations, d.refresh, d.cg_max, d.elas_power, d.samples, d.seed, d.kdis,
+                                    d.kelas, d.kbend, d.kbar, d.dhat, d.cg_tol, d.elas_tau};
+  });
+}
+
+int pamopt_cu_safe_project(pamopt_cu_mesh ms, pamopt_cu_mesh mi, const pamopt_cu_project_params* params,
+                           pamopt_cu_project_stats* stats) {
+  return guarded([&] {
+    PCU_REQUIRE(ms && mi, PAMOPT_CU_EINVAL, "null mesh");
+    PCU_REQUIRE(ms->owner == mi->owner, PAMOPT_CU_EINVAL, "safe_project: meshes belong to different contexts");
+    pamopt_cu_project_params p;
+    if (params) p = *params;
+    else pamopt_cu_project_defaults(&p);
+    PCU_REQUIRE(p.iterations >= 0 && p.refresh >= 1 && p.samples >= 1 && p.dhat > 0.0 && p.cg_max >= 1,
+                PAMOPT_CU_EINVAL, "safe_project: bad parameters");
+    pcu::Ctx& ctx = ms->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    check_indices(ctx, ms);
+    check_indices(ctx, mi);
+    pcu::ProjectStats st;
+    pcu::safe_project(ctx, ms->V.get(), ms->nv, ms->F.get(), ms->nf, mi->V.get(), mi->F.get(), mi->nf, to_pp(p), st);
+    if (stats)
+      *stats = pamopt_cu_project_stats{st.iterations, st.cg_iterations, st.refreshes, st.converged, st.energy0,
+                                       st.energy, st.grad_norm, st.last_alpha};
+  });
+}
+
 int pamopt_cu_dmc_active_cells(pamopt_cu_grid gr, int64_t* cells, uint8_t* cases, uint8_t* flips, int64_t cap,
                                int64_t* n) {
   return guarded([&] {

@@ -55,6 +55,21 @@ void directed_d2(Ctx& ctx, const double* Va, const int32_t* Fa, int64_t nfa, con
 double max_corner_cos(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf);
 std::vector<int32_t> index_range(Ctx& ctx, const int32_t* d, int64_t n);  // {min, max}
 
+// ---- stage 3: safe projection (project.cu, SPEC.md safe_project)
+struct ProjectParams {
+  int iterations = 50, refresh = 10, cg_max = 1000, elas_power = 1;
+  int64_t samples = 16384;
+  uint64_t seed = 42;
+  double kdis = 1e3, kelas = 1e-1, kbend = 1e-2, kbar = 1e2, dhat = 1e-3, cg_tol = 1e-3, elas_tau = 1e-12;
+};
+struct ProjectStats {
+  int64_t iterations = 0, cg_iterations = 0, refreshes = 0, converged = 0;
+  double energy0 = 0, energy = 0, grad_norm = 0, last_alpha = 0;
+};
+// deforms dV (mesh_s vertices) in place; connectivity unchanged
+void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t nf, const double* dVin,
+                  const int32_t* dFin, int64_t nfin, const ProjectParams& params, ProjectStats& stats);
+
 // ---- ingest (ingest.cu)
 struct IngestResult {
   DevBuf<double> V;
