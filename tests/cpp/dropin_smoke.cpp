@@ -12,6 +12,7 @@
 #include "pamopt/mesh_io.hpp"
 #include "pamopt/pipeline.hpp"
 #include "pamopt/quality_metrics.hpp"
+#include "pamopt/safe_project.hpp"
 #include "pamopt/simplify.hpp"
 #include "pamopt/tri_isect.hpp"
 #include "pamopt/voxel_field.hpp"
@@ -87,15 +88,21 @@ int main() {
     near_same = near_same && h.primitive == hg[i].primitive && h.distance == hg[i].distance && h.point == hg[i].point;
   }
   const MeshReport rep = mesh_report(s, &in, 4096);
+  pamopt_cu_project_params pp = default_projection_params();
+  pp.iterations = 10;
+  const IndexedMesh pj = project(s, in, pp);  // stage 3 (SPEC safe_project)
+  const MeshReport rep3 = mesh_report(pj, &in, 4096);
+  const bool proj_ok = pj.faces == s.faces && rep3.intersection_free && rep3.cd < rep.cd;
   std::printf("{\"dmc_faces\": %d, \"dmc_manifold\": %d, \"dmc_watertight\": %d, \"dmc_euler\": %d, "
               "\"dmc_isect\": %zu, \"out_faces\": %d, \"out_manifold\": %d, \"out_euler\": %d, \"out_isect\": %zu, "
               "\"iterations\": %lld, \"pipeline_equal\": %d, \"total_ms\": %.3f, \"topology_equal\": %d, "
-              "\"nearest_equal\": %d, \"cd\": %.3e, \"hd\": %.3e, \"min_angle\": %.2f}\n",
+              "\"nearest_equal\": %d, \"cd\": %.3e, \"hd\": %.3e, \"min_angle\": %.2f, \"projected_cd\": %.3e, "
+              "\"projection_ok\": %d}\n",
               d.face_count(), td.manifold, td.watertight, td.euler_characteristic, pd.size(), s.face_count(),
               ts.manifold, ts.euler_characteristic, ps.size(), static_cast<long long>(st.iterations), same,
-              tm.total_ms, topo_same, near_same, rep.cd, rep.hd, rep.min_angle_deg);
+              tm.total_ms, topo_same, near_same, rep.cd, rep.hd, rep.min_angle_deg, rep3.cd, proj_ok);
   const bool ok = td.manifold && td.watertight && pd.empty() && ts.manifold && ps.empty() && s.face_count() <= 1000 &&
-                  same && topo_same && near_same && rep.watertight && rep.intersection_free;
+                  same && topo_same && near_same && rep.watertight && rep.intersection_free && proj_ok;
   std::fflush(stdout);
   std::_Exit(ok ? 0 : 1);  // parallel.cpp pool: never run static destructors
 }
