@@ -16,13 +16,15 @@ struct J2 {
   double g[N];
   double h[N][N];
   __host__ __device__ J2() : v(0.0) {
-    for (int i = 0; i < N; ++i) {
+    #pragma unroll 1
+  for (int i = 0; i < N; ++i) {
       g[i] = 0.0;
       for (int j = 0; j < N; ++j) h[i][j] = 0.0;
     }
   }
   __host__ __device__ J2(double c) : v(c) {  // NOLINT: constants promote implicitly
-    for (int i = 0; i < N; ++i) {
+    #pragma unroll 1
+  for (int i = 0; i < N; ++i) {
       g[i] = 0.0;
       for (int j = 0; j < N; ++j) h[i][j] = 0.0;
     }
@@ -38,6 +40,7 @@ template <int N>
 __host__ __device__ inline J2<N> operator+(const J2<N>& a, const J2<N>& b) {
   J2<N> r;
   r.v = a.v + b.v;
+  #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = a.g[i] + b.g[i];
     for (int j = 0; j < N; ++j) r.h[i][j] = a.h[i][j] + b.h[i][j];
@@ -48,6 +51,7 @@ template <int N>
 __host__ __device__ inline J2<N> operator-(const J2<N>& a, const J2<N>& b) {
   J2<N> r;
   r.v = a.v - b.v;
+  #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = a.g[i] - b.g[i];
     for (int j = 0; j < N; ++j) r.h[i][j] = a.h[i][j] - b.h[i][j];
@@ -58,6 +62,7 @@ template <int N>
 __host__ __device__ inline J2<N> operator-(const J2<N>& a) {
   J2<N> r;
   r.v = -a.v;
+  #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = -a.g[i];
     for (int j = 0; j < N; ++j) r.h[i][j] = -a.h[i][j];
@@ -68,6 +73,7 @@ template <int N>
 __host__ __device__ inline J2<N> operator*(const J2<N>& a, const J2<N>& b) {
   J2<N> r;
   r.v = a.v * b.v;
+  #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = a.v * b.g[i] + b.v * a.g[i];
     for (int j = 0; j < N; ++j)
@@ -79,6 +85,7 @@ template <int N>
 __host__ __device__ inline J2<N> operator*(double c, const J2<N>& a) {
   J2<N> r;
   r.v = c * a.v;
+  #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = c * a.g[i];
     for (int j = 0; j < N; ++j) r.h[i][j] = c * a.h[i][j];
@@ -111,6 +118,7 @@ template <int N>
 __host__ __device__ inline J2<N> chain(const J2<N>& a, double f, double d1, double d2) {
   J2<N> r;
   r.v = f;
+  #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = d1 * a.g[i];
     for (int j = 0; j < N; ++j) r.h[i][j] = d1 * a.h[i][j] + d2 * a.g[i] * a.g[j];
@@ -147,6 +155,7 @@ __host__ __device__ inline J2<N> atan2(const J2<N>& y, const J2<N>& x) {
   const double fyy = -2.0 * x.v * y.v / r4, fxx = 2.0 * x.v * y.v / r4, fxy = (y.v * y.v - x.v * x.v) / r4;
   J2<N> r;
   r.v = ::atan2(y.v, x.v);
+  #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = fy * y.g[i] + fx * x.g[i];
     for (int j = 0; j < N; ++j)

@@ -215,18 +215,22 @@ __device__ T barrier_of_d2(const T& d2, double dhat) {
 }
 
 // ------------------------------------------------------------------------- the terms
-template <class T>
+// G selects the terms compiled into an instantiation (0: all, for values; 1: the 1-vertex term;
+// 3: the triangle terms; 4: the 4-vertex terms) so each jet size only carries its own stencils
+template <class T, int G>
 __device__ T term_value(const Stencil& S, const V<T>* x, const TermData& D, const Params& P) {
-  switch (S.term) {
-    case kS2M: {
+  if constexpr (G == 0 || G == 1) {
+    if (S.term == kS2M) {
       const V<T> y{T(D.ytgt[3 * S.v[0]]), T(D.ytgt[3 * S.v[0] + 1]), T(D.ytgt[3 * S.v[0] + 2])};
       return (P.kdis * D.s0[S.v[0]]) * d2_pp(x[0], y);
     }
-    case kM2S: {
+  }
+  if constexpr (G == 0 || G == 3) {
+    if (S.term == kM2S) {
       const V<T> y{T(D.ys[3 * S.param]), T(D.ys[3 * S.param + 1]), T(D.ys[3 * S.param + 2])};
       return (P.kdis * D.m2s_w) * d2_pt_class(y, x, S.cls);
     }
-    case kElas: {
+    if (S.term == kElas) {
       // F = Ds Dm^-1 (3x2); C = F^T F; E = 1/4 A0 |C - I|_F^p
       const double* mi = D.dminv + 4 * S.param;
       const V<T> e1 = x[1] - x[0], e2 = x[2] - x[0];
@@ -242,7 +246,9 @@ __device__ T term_value(const Stencil& S, const V<T>* x, const TermData& D, cons
       if (ad::value(s) < tau) return w * (s * (3.0 * tau - s)) * (0.5 / (tau * ::sqrt(tau)));
       return w * ad::sqrt(s);
     }
-    case kBend: {
+  }
+  if constexpr (G == 0 || G == 4) {
+    if (S.term == kBend) {
       // hinge (i, j | k, l): faces (i, j, k) and (j, i, l); signed dihedral, flat = 0
       const V<T> e = x[1] - x[0];
       const V<T> n0 = ad::cross(e, x[2] - x[0]), n1 = ad::cross(x[3] - x[0], e);
@@ -252,15 +258,10 @@ __device__ T term_value(const Stencil& S, const V<T>* x, const TermData& D, cons
       const T dth = th - D.theta0[S.param];
       return (0.5 * P.kbend * D.l0[S.param]) * (dth * dth);
     }
-    case kPT: {
-      const T d2 = d2_pt_class(x[0], x + 1, S.cls);
-      return P.kbar * barrier_of_d2(d2, P.dhat);
-    }
-    default: {
-      const T d2 = d2_ee_class(x[0], x[1], x[2], x[3], S.cls);
-      return P.kbar * barrier_of_d2(d2, P.dhat);
-    }
+    if (S.term == kPT) return P.kbar * barrier_of_d2(d2_pt_class(x[0], x + 1, S.cls), P.dhat);
+    if (S.term == kEE) return P.kbar * barrier_of_d2(d2_ee_class(x[0], x[1], x[2], x[3], S.cls), P.dhat);
   }
+  return T(0.0);
 }
 
 // Jacobi eigen-decomposition of a symmetric n x n block (in place) and the SPD clamp
@@ -322,7 +323,7 @@ __device__ void eval_stencil(const Stencil& S, const double* X, const TermData& 
   for (int a = 0; a < S.nv; ++a)
     x[a] = V<J2<N>>{J2<N>::var(3 * a, X[3 * S.v[a]]), J2<N>::var(3 * a + 1, X[3 * S.v[a] + 1]),
                     J2<N>::var(3 * a + 2, X[3 * S.v[a] + 2])};
-  const J2<N> e = term_value<J2<N>>(S, x, D, P);
+  const J2<N> e = term_value<J2<N>, (N == 3 ? 1 : (N == 9 ? 3 : 4))>(S, x, D, P);
   *val = e.v;
   for (int i = 0; i < N; ++i) gslot[i] = e.g[i];
   for (int i = 0; i < N; ++i)
@@ -349,7 +350,7 @@ __global__ void k_values(const Stencil* __restrict__ st, int64_t ns, const doubl
   const Stencil S = st[s];
   V<double> x[4];
   for (int a = 0; a < S.nv; ++a) x[a] = V<double>{X[3 * S.v[a]], X[3 * S.v[a] + 1], X[3 * S.v[a] + 2]};
-  const double e = term_value<double>(S, x, D, P);
+  const double e = term_value<double, 0>(S, x, D, P);
   val[s] = e;
   if (!(e == e) || isinf(e)) atomicOr(bad, 1ull);
 }
