@@ -437,6 +437,109 @@ __global__ void k_step(int64_t n, const double* __restrict__ x, double a, const 
   if (i < n) o[i] = x[i] + a * p[i];
 }
 
+// ---- global block-sparse (BSR, 3x3 blocks) matrix from the projected stencil blocks: the
+// sparsity is every (vertex, vertex) pair of every stencil; contributions to a block are summed
+// in stencil order (a stable key sort), so the matrix is deterministic.
+__global__ void k_pair_keys(const Stencil* __restrict__ st, int64_t ns, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (s >= ns) return;
+  const Stencil S = st[s];
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) {
+      const int64_t k = 16 * s + 4 * a + b;
+      const bool on = a < S.nv && b < S.nv;
+      keys[k] = on ? (static_cast<uint64_t>(S.v[a]) << 32) | static_cast<uint32_t>(S.v[b]) : ~0ull;
+      vals[k] = static_cast<uint32_t>(k);
+    }
+}
+__global__ void k_key_heads(const uint64_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ head) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) head[i] = (keys[i] != ~0ull && (i == 0 || keys[i] != keys[i - 1])) ? 1u : 0u;
+}
+__global__ void k_bsr_fill(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                           const uint32_t* __restrict__ head, const uint32_t* __restrict__ hpos, int64_t n,
+                           const Stencil* __restrict__ st, const double* __restrict__ blk, int32_t* __restrict__ bcol,
+                           int32_t* __restrict__ brow, double* __restrict__ bval) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n || !head[i]) return;
+  const uint32_t b = hpos[i];
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t j = i; j < n && keys[j] == keys[i]; ++j) {
+    const uint32_t v = vals[j];
+    const int64_t s = v >> 4;
+    const int a = (v >> 2) & 3, c = v & 3;
+    const int m = 3 * st[s].nv;
+    const double* B = blk + kBlk * s;
+    for (int r = 0; r < 3; ++r)
+      for (int q = 0; q < 3; ++q) acc[3 * r + q] += B[(3 * a + r) * m + 3 * c + q];
+  }
+  brow[b] = static_cast<int32_t>(keys[i] >> 32);
+  bcol[b] = static_cast<int32_t>(keys[i] & 0xffffffffu);
+  for (int k = 0; k < 9; ++k) bval[9 * static_cast<int64_t>(b) + k] = acc[k];
+}
+__global__ void k_row_start(const int32_t* __restrict__ brow, int64_t nb, int64_t nv, uint32_t* __restrict__ rs) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i > nb) return;
+  const int64_t vi = i < nb ? brow[i] : nv;
+  const int64_t vp = i == 0 ? -1 : brow[i - 1];
+  for (int64_t v = vp + 1; v <= vi && v <= nv; ++v) rs[v] = static_cast<uint32_t>(i);
+}
+__global__ void k_bsr_mv(const uint32_t* __restrict__ rs, const int32_t* __restrict__ bcol,
+                         const double* __restrict__ bval, int64_t nv, const double* __restrict__ x,
+                         double* __restrict__ y) {
+  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (v >= nv) return;
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (uint32_t k = rs[v]; k < rs[v + 1]; ++k) {
+    const double* B = bval + 9 * static_cast<int64_t>(k);
+    const int j = bcol[k];
+    const double x0 = x[3 * j], x1 = x[3 * j + 1], x2 = x[3 * j + 2];
+    a += (B[0] * x0 + B[1] * x1) + B[2] * x2;
+    b += (B[3] * x0 + B[4] * x1) + B[5] * x2;
+    c += (B[6] * x0 + B[7] * x1) + B[8] * x2;
+  }
+  y[3 * v] = a;
+  y[3 * v + 1] = b;
+  y[3 * v + 2] = c;
+}
+__global__ void k_bsr_diag(const uint32_t* __restrict__ rs, const int32_t* __restrict__ bcol,
+                           const double* __restrict__ bval, int64_t nv, double* __restrict__ d) {
+  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (v >= nv) return;
+  double e[3] = {0, 0, 0};
+  for (uint32_t k = rs[v]; k < rs[v + 1]; ++k)
+    if (bcol[k] == v)
+      for (int r = 0; r < 3; ++r) e[r] += bval[9 * static_cast<int64_t>(k) + 4 * r];
+  for (int r = 0; r < 3; ++r) d[3 * v + r] = e[r];
+}
+
+// CG with device-resident scalars (no host round trip per iteration).  sc[0] = rz, sc[1] = qAq,
+// sc[2] = rz_new, sc[3] = rr; every scalar comes from a CUB reduction of elementwise products.
+__global__ void k_cg_step(int64_t n, const double* __restrict__ sc, const double* __restrict__ q,
+                          const double* __restrict__ Ap, const double* __restrict__ d, double* __restrict__ x,
+                          double* __restrict__ r, double* __restrict__ z, double* __restrict__ prz,
+                          double* __restrict__ prr) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double qaq = sc[1];
+  const double alpha = qaq > 0.0 ? sc[0] / qaq : 0.0;
+  x[i] += alpha * q[i];
+  const double ri = r[i] - alpha * Ap[i];
+  r[i] = ri;
+  const double zi = ri / (d[i] > 0.0 ? d[i] : 1.0);
+  z[i] = zi;
+  prz[i] = ri * zi;
+  prr[i] = ri * ri;
+}
+__global__ void k_cg_dir(int64_t n, const double* __restrict__ sc, const double* __restrict__ z, double* __restrict__ q) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double beta = sc[0] != 0.0 ? sc[2] / sc[0] : 0.0;
+  q[i] = z[i] + beta * q[i];
+}
+__global__ void k_cg_shift(double* __restrict__ sc) { sc[0] = sc[2]; }
+
 // --------------------------------------------------------------------- broad phase
 // face boxes over [X, X + p] inflated by `pad` (p may be null)
 __global__ void k_swept_boxes(const double* __restrict__ X, const double* __restrict__ p, const int32_t* __restrict__ F,
@@ -540,6 +643,16 @@ __device__ double accd_pair(const double* X, const double* p, const int* v, doub
   }
   const double lp = m0 + m1;
   if (!(lp > 0.0)) return 1.0;
+  // margin: the SPEC's 0.1 d̂, or 10% of the current gap when the pair is already closer than that
+  // (the standard ACCD slack), so a close pair still lets the step advance
+  {
+    V<double> q[4];
+    for (int a = 0; a < 4; ++a) q[a] = V<double>{x[a][0], x[a][1], x[a][2]};
+    const double d0 = ::sqrt(fmax(EE ? d2_ee_class(q[0], q[1], q[2], q[3], ee_class(x[0], x[1], x[2], x[3]))
+                                     : d2_pt_class(q[0], q + 1, pt_class(x[0], x[1], x[2], x[3])),
+                                  0.0));
+    margin = fmin(margin, 0.1 * d0);
+  }
   double t = 0.0;
   for (int it = 0; it < 64; ++it) {
     double y[4][3];
@@ -898,6 +1011,23 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
   auto gather = [&](const double* slots, double* out) {
     PCU_LAUNCH(ctx, k_gather, grid_for(nv, 256), 256, 0, A.keys2.get(), A.vstart.get(), nv, slots, out);
   };
+  DevBuf<double> sc(4, st), tmp2(n3, st), bval;
+  DevBuf<uint64_t> bk, bk2;
+  DevBuf<uint32_t> bvl, bvl2, bhead, bhpos, rstart;
+  DevBuf<int32_t> bcol, brow;
+  int64_t nblk = 0;
+  DevBuf<uint8_t> red_tmp;
+  size_t red_bytes = 0;
+  auto dev_sum_to = [&](const double* d, int64_t n, double* out) {  // deterministic CUB sum into device memory
+    size_t need = 0;
+    cub::DeviceReduce::Sum(nullptr, need, d, out, n, st);
+    if (need > red_bytes) {
+      red_tmp.alloc(need, st);
+      red_bytes = need;
+    }
+    PCU_CUDA(cub::DeviceReduce::Sum(red_tmp.get(), need, d, out, n, st));
+    ++ctx.launches;
+  };
   auto dot = [&](const double* a, const double* b) {
     PCU_LAUNCH(ctx, k_mul, grid_for(n3, 256), 256, 0, n3, a, b, tmpv.get());
     return dev_sum(ctx, tmpv.get(), n3);
@@ -933,37 +1063,69 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     sort_pairs_u64(ctx, A.keys2.get(), 4 * ns);
     PCU_LAUNCH(ctx, k_slot_csr, grid_for(4 * ns + 1, 256), 256, 0, A.keys2.get(), 4 * ns, nv, A.vstart.get());
     gather(A.gslot.get(), g.get());
-    PCU_LAUNCH(ctx, k_blk_diag, grid_for(ns, 256), 256, 0, stc.get(), ns, A.blk.get(), A.slot2.get());
-    gather(A.slot2.get(), diag.get());
+    {  // global BSR matrix (3x3 blocks), deterministic summation in stencil order
+      const int64_t np = 16 * ns;
+      bk.ensure(np, st);
+      bk2.ensure(np, st);
+      bvl.ensure(np, st);
+      bvl2.ensure(np, st);
+      bhead.ensure(np, st);
+      bhpos.ensure(np, st);
+      PCU_LAUNCH(ctx, k_pair_keys, grid_for(ns, 128), 128, 0, stc.get(), ns, bk.get(), bvl.get());
+      size_t need = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, need, bk.get(), bk2.get(), bvl.get(), bvl2.get(), static_cast<int>(np), 0,
+                                      64, st);
+      if (need > red_bytes) {
+        red_tmp.alloc(need, st);
+        red_bytes = need;
+      }
+      PCU_CUDA(cub::DeviceRadixSort::SortPairs(red_tmp.get(), need, bk.get(), bk2.get(), bvl.get(), bvl2.get(),
+                                               static_cast<int>(np), 0, 64, st));
+      ++ctx.launches;
+      PCU_LAUNCH(ctx, k_key_heads, grid_for(np, 256), 256, 0, bk2.get(), np, bhead.get());
+      exclusive_scan_u32(ctx, bhead.get(), bhpos.get(), np);
+      nblk = static_cast<int64_t>(read_scalar(ctx, bhpos.get() + np - 1)) + read_scalar(ctx, bhead.get() + np - 1);
+      bcol.ensure(nblk, st);
+      brow.ensure(nblk, st);
+      bval.ensure(9 * nblk, st);
+      rstart.ensure(nv + 1, st);
+      PCU_LAUNCH(ctx, k_bsr_fill, grid_for(np, 128), 128, 0, bk2.get(), bvl2.get(), bhead.get(), bhpos.get(), np,
+                 stc.get(), A.blk.get(), bcol.get(), brow.get(), bval.get());
+      PCU_LAUNCH(ctx, k_row_start, grid_for(nblk + 1, 256), 256, 0, brow.get(), nblk, nv, rstart.get());
+      PCU_LAUNCH(ctx, k_bsr_diag, grid_for(nv, 256), 256, 0, rstart.get(), bcol.get(), bval.get(), nv, diag.get());
+    }
     // ---- PCG: H p = -g
     const double gnorm = ::sqrt(dot(g.get(), g.get()));
     stats.grad_norm = gnorm;
     if (!(gnorm > 0.0)) break;
     PCU_CUDA(cudaMemsetAsync(pdir.get(), 0, n3 * 8, st));
     PCU_CUDA(cudaMemcpyAsync(r.get(), g.get(), n3 * 8, cudaMemcpyDeviceToDevice, st));
-    {  // r = -g
-      PCU_LAUNCH(ctx, k_xpay, grid_for(n3, 256), 256, 0, n3, pdir.get(), -1.0, r.get());
-    }
+    PCU_LAUNCH(ctx, k_xpay, grid_for(n3, 256), 256, 0, n3, pdir.get(), -1.0, r.get());  // r = -g
     PCU_LAUNCH(ctx, k_precond, grid_for(n3, 256), 256, 0, n3, r.get(), diag.get(), z.get());
     PCU_CUDA(cudaMemcpyAsync(q.get(), z.get(), n3 * 8, cudaMemcpyDeviceToDevice, st));
-    double rz = dot(r.get(), z.get());
+    PCU_LAUNCH(ctx, k_mul, grid_for(n3, 256), 256, 0, n3, r.get(), z.get(), tmpv.get());
+    dev_sum_to(tmpv.get(), n3, sc.get());
+    const double tol2 = PP.cg_tol * PP.cg_tol * gnorm * gnorm;
     int cg = 0;
     for (; cg < PP.cg_max; ++cg) {
-      PCU_LAUNCH(ctx, k_blk_mul, grid_for(ns, 128), 128, 0, stc.get(), ns, A.blk.get(), q.get(), A.slot2.get());
-      gather(A.slot2.get(), Ap.get());
-      const double qAq = dot(q.get(), Ap.get());
-      if (!(qAq > 0.0)) break;
-      const double alpha = rz / qAq;
-      PCU_LAUNCH(ctx, k_axpy, grid_for(n3, 256), 256, 0, n3, alpha, q.get(), pdir.get());
-      PCU_LAUNCH(ctx, k_axpy, grid_for(n3, 256), 256, 0, n3, -alpha, Ap.get(), r.get());
-      if (::sqrt(dot(r.get(), r.get())) <= PP.cg_tol * gnorm) {
-        ++cg;
-        break;
+      PCU_LAUNCH(ctx, k_bsr_mv, grid_for(nv, 128), 128, 0, rstart.get(), bcol.get(), bval.get(), nv, q.get(), Ap.get());
+      PCU_LAUNCH(ctx, k_mul, grid_for(n3, 256), 256, 0, n3, q.get(), Ap.get(), tmpv.get());
+      dev_sum_to(tmpv.get(), n3, sc.get() + 1);
+      PCU_LAUNCH(ctx, k_cg_step, grid_for(n3, 256), 256, 0, n3, sc.get(), q.get(), Ap.get(), diag.get(), pdir.get(),
+                 r.get(), z.get(), tmpv.get(), tmp2.get());
+      dev_sum_to(tmpv.get(), n3, sc.get() + 2);
+      dev_sum_to(tmp2.get(), n3, sc.get() + 3);
+      PCU_LAUNCH(ctx, k_cg_dir, grid_for(n3, 256), 256, 0, n3, sc.get(), z.get(), q.get());
+      PCU_LAUNCH(ctx, k_cg_shift, 1, 1, 0, sc.get());
+      if ((cg & 15) == 15 || cg + 1 == PP.cg_max) {  // convergence check every 16 iterations
+        double h[4];
+        PCU_CUDA(cudaMemcpyAsync(h, sc.get(), 32, cudaMemcpyDeviceToHost, st));
+        PCU_CUDA(cudaStreamSynchronize(st));
+        if (h[3] <= tol2 || !(h[1] > 0.0)) {
+          ++cg;
+          break;
+        }
       }
-      PCU_LAUNCH(ctx, k_precond, grid_for(n3, 256), 256, 0, n3, r.get(), diag.get(), z.get());
-      const double rz2 = dot(r.get(), z.get());
-      PCU_LAUNCH(ctx, k_xpay, grid_for(n3, 256), 256, 0, n3, z.get(), rz2 / rz, q.get());
-      rz = rz2;
     }
     stats.cg_iterations += cg;
     // ---- ACCD step bound over the swept primitives
