@@ -503,22 +503,48 @@ __global__ void k_bsr_mv(const uint32_t* __restrict__ rs, const int32_t* __restr
   y[3 * v + 1] = b;
   y[3 * v + 2] = c;
 }
-__global__ void k_bsr_diag(const uint32_t* __restrict__ rs, const int32_t* __restrict__ bcol,
-                           const double* __restrict__ bval, int64_t nv, double* __restrict__ d) {
+// block-Jacobi preconditioner: the inverse of every vertex's 3x3 diagonal block (SPD)
+__global__ void k_bsr_dinv(const uint32_t* __restrict__ rs, const int32_t* __restrict__ bcol,
+                           const double* __restrict__ bval, int64_t nv, double* __restrict__ dinv) {
   const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (v >= nv) return;
-  double e[3] = {0, 0, 0};
+  double a[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (uint32_t k = rs[v]; k < rs[v + 1]; ++k)
     if (bcol[k] == v)
-      for (int r = 0; r < 3; ++r) e[r] += bval[9 * static_cast<int64_t>(k) + 4 * r];
-  for (int r = 0; r < 3; ++r) d[3 * v + r] = e[r];
+      for (int q = 0; q < 9; ++q) a[q] += bval[9 * static_cast<int64_t>(k) + q];
+  const double c00 = a[4] * a[8] - a[5] * a[7], c01 = a[5] * a[6] - a[3] * a[8], c02 = a[3] * a[7] - a[4] * a[6];
+  const double det = a[0] * c00 + a[1] * c01 + a[2] * c02;
+  double* o = dinv + 9 * v;
+  if (!(det > 0.0)) {  // isolated vertex: identity
+    for (int q = 0; q < 9; ++q) o[q] = (q % 4 == 0) ? 1.0 : 0.0;
+    return;
+  }
+  const double id = 1.0 / det;
+  o[0] = c00 * id;
+  o[1] = (a[2] * a[7] - a[1] * a[8]) * id;
+  o[2] = (a[1] * a[5] - a[2] * a[4]) * id;
+  o[3] = c01 * id;
+  o[4] = (a[0] * a[8] - a[2] * a[6]) * id;
+  o[5] = (a[2] * a[3] - a[0] * a[5]) * id;
+  o[6] = c02 * id;
+  o[7] = (a[1] * a[6] - a[0] * a[7]) * id;
+  o[8] = (a[0] * a[4] - a[1] * a[3]) * id;
+}
+__global__ void k_bprecond(int64_t nv, const double* __restrict__ dinv, const double* __restrict__ r,
+                           double* __restrict__ z) {
+  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (v >= nv) return;
+  const double* M = dinv + 9 * v;
+  const double r0 = r[3 * v], r1 = r[3 * v + 1], r2 = r[3 * v + 2];
+  z[3 * v] = (M[0] * r0 + M[1] * r1) + M[2] * r2;
+  z[3 * v + 1] = (M[3] * r0 + M[4] * r1) + M[5] * r2;
+  z[3 * v + 2] = (M[6] * r0 + M[7] * r1) + M[8] * r2;
 }
 
 // CG with device-resident scalars (no host round trip per iteration).  sc[0] = rz, sc[1] = qAq,
 // sc[2] = rz_new, sc[3] = rr; every scalar comes from a CUB reduction of elementwise products.
 __global__ void k_cg_step(int64_t n, const double* __restrict__ sc, const double* __restrict__ q,
-                          const double* __restrict__ Ap, const double* __restrict__ d, double* __restrict__ x,
-                          double* __restrict__ r, double* __restrict__ z, double* __restrict__ prz,
+                          const double* __restrict__ Ap, double* __restrict__ x, double* __restrict__ r,
                           double* __restrict__ prr) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
@@ -527,9 +553,6 @@ __global__ void k_cg_step(int64_t n, const double* __restrict__ sc, const double
   x[i] += alpha * q[i];
   const double ri = r[i] - alpha * Ap[i];
   r[i] = ri;
-  const double zi = ri / (d[i] > 0.0 ? d[i] : 1.0);
-  z[i] = zi;
-  prz[i] = ri * zi;
   prr[i] = ri * ri;
 }
 __global__ void k_cg_dir(int64_t n, const double* __restrict__ sc, const double* __restrict__ z, double* __restrict__ q) {
@@ -1011,7 +1034,7 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
   auto gather = [&](const double* slots, double* out) {
     PCU_LAUNCH(ctx, k_gather, grid_for(nv, 256), 256, 0, A.keys2.get(), A.vstart.get(), nv, slots, out);
   };
-  DevBuf<double> sc(4, st), tmp2(n3, st), bval;
+  DevBuf<double> sc(4, st), tmp2(n3, st), bval, dinv;
   DevBuf<uint64_t> bk, bk2;
   DevBuf<uint32_t> bvl, bvl2, bhead, bhpos, rstart;
   DevBuf<int32_t> bcol, brow;
@@ -1092,7 +1115,8 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
       PCU_LAUNCH(ctx, k_bsr_fill, grid_for(np, 128), 128, 0, bk2.get(), bvl2.get(), bhead.get(), bhpos.get(), np,
                  stc.get(), A.blk.get(), bcol.get(), brow.get(), bval.get());
       PCU_LAUNCH(ctx, k_row_start, grid_for(nblk + 1, 256), 256, 0, brow.get(), nblk, nv, rstart.get());
-      PCU_LAUNCH(ctx, k_bsr_diag, grid_for(nv, 256), 256, 0, rstart.get(), bcol.get(), bval.get(), nv, diag.get());
+      dinv.ensure(9 * nv, st);
+      PCU_LAUNCH(ctx, k_bsr_dinv, grid_for(nv, 256), 256, 0, rstart.get(), bcol.get(), bval.get(), nv, dinv.get());
     }
     // ---- PCG: H p = -g
     const double gnorm = ::sqrt(dot(g.get(), g.get()));
@@ -1101,7 +1125,7 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     PCU_CUDA(cudaMemsetAsync(pdir.get(), 0, n3 * 8, st));
     PCU_CUDA(cudaMemcpyAsync(r.get(), g.get(), n3 * 8, cudaMemcpyDeviceToDevice, st));
     PCU_LAUNCH(ctx, k_xpay, grid_for(n3, 256), 256, 0, n3, pdir.get(), -1.0, r.get());  // r = -g
-    PCU_LAUNCH(ctx, k_precond, grid_for(n3, 256), 256, 0, n3, r.get(), diag.get(), z.get());
+    PCU_LAUNCH(ctx, k_bprecond, grid_for(nv, 256), 256, 0, nv, dinv.get(), r.get(), z.get());
     PCU_CUDA(cudaMemcpyAsync(q.get(), z.get(), n3 * 8, cudaMemcpyDeviceToDevice, st));
     PCU_LAUNCH(ctx, k_mul, grid_for(n3, 256), 256, 0, n3, r.get(), z.get(), tmpv.get());
     dev_sum_to(tmpv.get(), n3, sc.get());
@@ -1111,8 +1135,10 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
       PCU_LAUNCH(ctx, k_bsr_mv, grid_for(nv, 128), 128, 0, rstart.get(), bcol.get(), bval.get(), nv, q.get(), Ap.get());
       PCU_LAUNCH(ctx, k_mul, grid_for(n3, 256), 256, 0, n3, q.get(), Ap.get(), tmpv.get());
       dev_sum_to(tmpv.get(), n3, sc.get() + 1);
-      PCU_LAUNCH(ctx, k_cg_step, grid_for(n3, 256), 256, 0, n3, sc.get(), q.get(), Ap.get(), diag.get(), pdir.get(),
-                 r.get(), z.get(), tmpv.get(), tmp2.get());
+      PCU_LAUNCH(ctx, k_cg_step, grid_for(n3, 256), 256, 0, n3, sc.get(), q.get(), Ap.get(), pdir.get(), r.get(),
+                 tmp2.get());
+      PCU_LAUNCH(ctx, k_bprecond, grid_for(nv, 256), 256, 0, nv, dinv.get(), r.get(), z.get());
+      PCU_LAUNCH(ctx, k_mul, grid_for(n3, 256), 256, 0, n3, r.get(), z.get(), tmpv.get());
       dev_sum_to(tmpv.get(), n3, sc.get() + 2);
       dev_sum_to(tmp2.get(), n3, sc.get() + 3);
       PCU_LAUNCH(ctx, k_cg_dir, grid_for(n3, 256), 256, 0, n3, sc.get(), z.get(), q.get());
