@@ -355,30 +355,6 @@ __global__ void k_values(const Stencil* __restrict__ st, int64_t ns, const doubl
   if (!(e == e) || isinf(e)) atomicOr(bad, 1ull);
 }
 
-// block-vector products into slots: out[s][i] = sum_j B_s[i][j] in[v_s(j)]
-__global__ void k_blk_mul(const Stencil* __restrict__ st, int64_t ns, const double* __restrict__ blk,
-                          const double* __restrict__ in, double* __restrict__ out) {
-  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (s >= ns) return;
-  const Stencil S = st[s];
-  const int n = 3 * S.nv;
-  double x[kMaxN];
-  for (int a = 0; a < S.nv; ++a)
-    for (int k = 0; k < 3; ++k) x[3 * a + k] = in[3 * S.v[a] + k];
-  const double* B = blk + kBlk * s;
-  for (int i = 0; i < n; ++i) {
-    double sum = 0.0;
-    for (int j = 0; j < n; ++j) sum += B[i * n + j] * x[j];
-    out[kMaxN * s + i] = sum;
-  }
-}
-__global__ void k_blk_diag(const Stencil* __restrict__ st, int64_t ns, const double* __restrict__ blk,
-                           double* __restrict__ out) {
-  const int64_t s = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (s >= ns) return;
-  const int n = 3 * st[s].nv;
-  for (int i = 0; i < n; ++i) out[kMaxN * s + i] = blk[kBlk * s + i * n + i];
-}
 
 // slot keys (vertex << 32 | stencil * 4 + local) for the deterministic per-vertex gather
 __global__ void k_slot_keys(const Stencil* __restrict__ st, int64_t ns, uint64_t* __restrict__ keys) {
@@ -415,17 +391,9 @@ __global__ void k_gather(const uint64_t* __restrict__ keys, const uint32_t* __re
 }
 
 // ------------------------------------------------------------------------ vector ops
-__global__ void k_axpy(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) y[i] += a * x[i];
-}
 __global__ void k_xpay(int64_t n, const double* __restrict__ x, double a, double* __restrict__ y) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) y[i] = x[i] + a * y[i];
-}
-__global__ void k_precond(int64_t n, const double* __restrict__ r, const double* __restrict__ d, double* __restrict__ z) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) z[i] = r[i] / (d[i] > 0.0 ? d[i] : 1.0);
 }
 __global__ void k_mul(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -861,7 +829,7 @@ double dev_sum(Ctx& ctx, const double* d, int64_t n) {
 struct Assembly {
   DevBuf<Stencil> st;
   int64_t ns = 0;
-  DevBuf<double> val, gslot, blk, slot2, diag;
+  DevBuf<double> val, gslot, blk;
   DevBuf<uint64_t> keys, keys2;
   DevBuf<uint32_t> vstart;
 };
@@ -1029,7 +997,7 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     return dev_sum(ctx, A.val.get(), ns);
   };
   const int64_t n3 = 3 * nv;
-  DevBuf<double> g(n3, st), diag(n3, st), pdir(n3, st), r(n3, st), z(n3, st), q(n3, st), Ap(n3, st), tmpv(n3, st),
+  DevBuf<double> g(n3, st), pdir(n3, st), r(n3, st), z(n3, st), q(n3, st), Ap(n3, st), tmpv(n3, st),
       Xn(n3, st);
   auto gather = [&](const double* slots, double* out) {
     PCU_LAUNCH(ctx, k_gather, grid_for(nv, 256), 256, 0, A.keys2.get(), A.vstart.get(), nv, slots, out);
@@ -1073,7 +1041,6 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     // ---- assemble gradient + projected Hessian blocks
     A.val.ensure(ns, st);
     A.gslot.ensure(kMaxN * ns, st);
-    A.slot2.ensure(kMaxN * ns, st);
     A.blk.ensure(kBlk * ns, st);
     A.keys.ensure(4 * ns, st);
     A.keys2.ensure(4 * ns, st);
