@@ -199,7 +199,7 @@ int pamopt_cu_analyze_topology(pamopt_cu_mesh mesh, pamopt_cu_topology* out, int
  * mesh), distance, closest point (double[3n]); ties go to the lower face id.  Any output may be NULL. */
 int pamopt_cu_nearest_primitive(pamopt_cu_mesh mesh, const double* points, int64_t n, int32_t* face,
                                 double* distance, double* closest);
-/* the pinned area-weighted sampler (DESIGN.md §9): points double[3n], faces int32[n] (may be NULL) */
+/* the pinned area-weighted sampler (DESIGN.md §8): points double[3n], faces int32[n] (may be NULL) */
 int pamopt_cu_sample_points(pamopt_cu_mesh mesh, int64_t n, uint64_t seed, double* points, int32_t* faces,
                             double* total_area);
 /* quality_metrics: squared-distance Chamfer and sampled symmetric Hausdorff with n
