@@ -673,10 +673,8 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int32_t p = static_cast<int32_t>(cand[i] >> 32), a = static_cast<int32_t>(cand[i] & 0xffffffffu);
-    if (mode == 1) {
-      const int32_t op = owner[p], oa = owner[a];
-      if (op < 0 && oa < 0) continue;  // owner >= 0 <=> applied (see report)
-    }
+    // (undo mode: every candidate already has an applied-owned face — round 1 builds the grid over
+    // the owned faces, later rounds probe with them — so no owner filter is needed here)
     const int32_t* tp = F + 3 * p;
     const int32_t* ta = F + 3 * a;
     // the float boxes enclose the double boxes within one f32 ulp per side: an overlap deeper
