@@ -245,6 +245,13 @@ int pamopt_cu_project_defaults(pamopt_cu_project_params* out);
 int pamopt_cu_safe_project(pamopt_cu_mesh mesh_s, pamopt_cu_mesh mesh_in, const pamopt_cu_project_params* params,
                            pamopt_cu_project_stats* stats);
 
+/* one stage-3 energy stencil on the GPU (unit checks of the terms).  term: 0 S2M, 1 M2S,
+ * 2 elastic, 3 bending, 4 point-triangle barrier, 5 edge-edge barrier; cls: the frozen distance
+ * class (M2S / barrier); coords: nv (1, 3 or 4) vertices; rest[16] = {s0, ytgt[3], ys[3], m2s_w,
+ * dminv[4], a0, theta0, l0, -}; out = {value, gradient[12], SPD-projected Hessian[144]} */
+int pamopt_cu_project_term(pamopt_cu_ctx ctx, int32_t term, int32_t cls, const double* coords, int32_t nv,
+                           const double* rest, const pamopt_cu_project_params* params, double* out);
+
 /* ---- pipeline: UDF -> SDF -> DMC -> QEM ------------------------------------------------ */
 int pamopt_cu_remesh(pamopt_cu_ctx ctx, pamopt_cu_mesh input, int32_t R, double eps, double beta,
                      int64_t target_faces, const pamopt_cu_simplify_params* params,

@@ -147,6 +147,7 @@ _SIGS = {
     "pamopt_cu_report": (C.c_int, [vp, vp, i64, C.c_uint64, P(MeshReport)]),
     "pamopt_cu_project_defaults": (C.c_int, [P(ProjectParams)]),
     "pamopt_cu_safe_project": (C.c_int, [vp, vp, P(ProjectParams), P(ProjectStats)]),
+    "pamopt_cu_project_term": (C.c_int, [vp, i32, i32, vp, i32, vp, P(ProjectParams), vp]),
     "pamopt_cu_remesh": (C.c_int, [vp, vp, i32, dbl, dbl, i64, P(SimplifyParams), P(vp), P(SimplifyStats),
                                    P(StageTimes)]),
     "pamopt_cu_remesh_host": (C.c_int, [vp, vp, i64, vp, i64, i32, dbl, dbl, i64, P(SimplifyParams), P(i64),

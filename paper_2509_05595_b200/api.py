@@ -489,3 +489,23 @@ def safe_project(mesh_s: DeviceMesh, mesh_in, **overrides):
     st = _lib.ProjectStats()
     check(lib().pamopt_cu_safe_project(mesh_s.h, mi.h, C.byref(p), C.byref(st)))
     return st.as_dict()
+
+
+TERMS = {"s2m": 0, "m2s": 1, "elastic": 2, "bending": 3, "pt": 4, "ee": 5}
+
+
+def project_term(term: str, coords, rest=None, cls: int = 0, ctx: Context | None = None, **overrides):
+    """One stage-3 energy stencil on the GPU: (value, gradient, SPD-projected Hessian)."""
+    ctx = ctx or default_context()
+    x = np.ascontiguousarray(coords, np.float64).reshape(-1, 3)
+    r = np.zeros(16)
+    if rest is not None:
+        r[:len(rest)] = rest
+    p = _lib.ProjectParams()
+    check(lib().pamopt_cu_project_defaults(C.byref(p)))
+    for k, v in overrides.items():
+        setattr(p, k, v)
+    out = np.zeros(1 + 12 + 144)
+    check(lib().pamopt_cu_project_term(ctx.h, TERMS[term], int(cls), ptr(x), len(x), ptr(r), C.byref(p), ptr(out)))
+    n = 3 * len(x)
+    return out[0], out[1:1 + n].copy(), out[13:13 + n * n].reshape(n, n).copy()

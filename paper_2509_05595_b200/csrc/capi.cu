@@ -944,6 +944,19 @@ int pamopt_cu_safe_project(pamopt_cu_mesh ms, pamopt_cu_mesh mi, const pamopt_cu
   });
 }
 
+int pamopt_cu_project_term(pamopt_cu_ctx c, int32_t term, int32_t cls, const double* coords, int32_t nv,
+                           const double* rest, const pamopt_cu_project_params* params, double* out) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(coords && rest && out && term >= 0 && term <= 5, PAMOPT_CU_EINVAL, "bad arguments");
+    pamopt_cu_project_params p;
+    if (params) p = *params;
+    else pamopt_cu_project_defaults(&p);
+    pcu::DeviceGuard g(c->ctx.device);
+    pcu::project_term_probe(c->ctx, term, cls, coords, nv, rest, to_pp(p), out);
+  });
+}
+
 int pamopt_cu_dmc_active_cells(pamopt_cu_grid gr, int64_t* cells, uint8_t* cases, uint8_t* flips, int64_t cap,
                                int64_t* n) {
   return guarded([&] {

@@ -70,6 +70,10 @@ struct ProjectStats {
 void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t nf, const double* dVin,
                   const int32_t* dFin, int64_t nfin, const ProjectParams& params, ProjectStats& stats);
 
+// one term stencil evaluated on the GPU (unit checks): out = {value, grad[12], projected H[144]}
+void project_term_probe(Ctx& ctx, int term, int cls, const double* coords, int nv, const double* rest,
+                        const ProjectParams& params, double* out);
+
 // ---- ingest (ingest.cu)
 struct IngestResult {
   DevBuf<double> V;

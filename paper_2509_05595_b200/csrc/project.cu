@@ -797,6 +797,20 @@ __global__ void k_rest_faces(const double* __restrict__ X, const int32_t* __rest
   a0[f] = 0.5 * nl;
 }
 
+// one stencil on one thread (unit checks of the terms, tests/test_gpu_project.py): the rest
+// data arrive in small device arrays laid out like the solver's (X holds the stencil vertices
+// 0..nv-1, X0 their rest positions)
+__global__ void k_term_probe(Stencil S, const double* __restrict__ X, TermData D, Params P, double* __restrict__ out) {
+  double val = 0.0, g[kMaxN], H[kBlk];
+  if (S.nv == 1) eval_stencil<3>(S, X, D, P, &val, g, H);
+  else if (S.nv == 3) eval_stencil<9>(S, X, D, P, &val, g, H);
+  else eval_stencil<12>(S, X, D, P, &val, g, H);
+  out[0] = val;
+  const int n = 3 * S.nv;
+  for (int i = 0; i < n; ++i) out[1 + i] = g[i];
+  for (int i = 0; i < n * n; ++i) out[1 + kMaxN + i] = H[i];
+}
+
 // hinge rest state: theta0 (same signed dihedral as the bending term) and |x_i - x_j|
 __global__ void k_hinge_rest(const double* __restrict__ X, const int32_t* __restrict__ hinge, int64_t nh,
                              double* __restrict__ theta0, double* __restrict__ l0) {
@@ -1161,6 +1175,23 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     PCU_CUDA(cudaMemcpyAsync(dV, Xn.get(), n3 * 8, cudaMemcpyDeviceToDevice, st));
     stats.last_alpha = alpha;
   }
+  PCU_CUDA(cudaStreamSynchronize(st));
+}
+
+void project_term_probe(Ctx& ctx, int term, int cls, const double* coords, int nv, const double* rest,
+                        const ProjectParams& PP, double* out) {
+  // rest: {s0, ytgt[3], ys[3], m2s_w}  (S2M / M2S), {dminv[4], a0} (elastic), {theta0, l0} (bending)
+  cudaStream_t st = ctx.stream;
+  PCU_REQUIRE(nv == 1 || nv == 3 || nv == 4, PAMOPT_CU_EINVAL, "term probe: 1, 3 or 4 vertices");
+  DevBuf<double> X(3 * nv, st), R(16, st), o(1 + kMaxN + kBlk, st);
+  PCU_CUDA(cudaMemcpyAsync(X.get(), coords, 3 * nv * 8, cudaMemcpyHostToDevice, st));
+  PCU_CUDA(cudaMemcpyAsync(R.get(), rest, 16 * 8, cudaMemcpyHostToDevice, st));
+  const double* r = R.get();
+  TermData D{X.get(), r + 0, r + 1, r + 4, rest[7], r + 8, r + 12, r + 13, r + 14};
+  Params P{PP.kdis, PP.kelas, PP.kbend, PP.kbar, PP.dhat, PP.elas_tau, PP.elas_power};
+  Stencil S{term, nv, {0, nv > 1 ? 1 : -1, nv > 2 ? 2 : -1, nv > 3 ? 3 : -1}, 0, cls};
+  PCU_LAUNCH(ctx, k_term_probe, 1, 1, 0, S, X.get(), D, P, o.get());
+  PCU_CUDA(cudaMemcpyAsync(out, o.get(), (1 + kMaxN + kBlk) * 8, cudaMemcpyDeviceToHost, st));
   PCU_CUDA(cudaStreamSynchronize(st));
 }
 

@@ -76,3 +76,54 @@ def test_initial_energy_matches_oracle_distance_terms(api, oracle):
     _, d2, _ = oracle.nearest(lv, lf, ys)
     expect = 1e3 * (float(np.sum(s0 * d * d)) + ain / 16384 * float(np.sum(d2 * d2)))
     assert abs(st["energy0"] - expect) <= 1e-10 * expect
+
+
+# ----------------------------------------------------------------- term unit checks (SPEC)
+def _fd_grad(api, term, x, rest, cls=0, h=1e-6):
+    g = np.zeros(x.size)
+    for i in range(x.size):
+        xp, xm = x.copy().ravel(), x.copy().ravel()
+        xp[i] += h
+        xm[i] -= h
+        g[i] = (api.project_term(term, xp, rest, cls)[0] - api.project_term(term, xm, rest, cls)[0]) / (2 * h)
+    return g
+
+
+def _check_grad_and_spd(api, term, x, rest, cls=0):
+    val, g, H = api.project_term(term, x, rest, cls)
+    fd = _fd_grad(api, term, np.asarray(x, float), rest, cls)
+    assert np.allclose(g, fd, rtol=1e-5, atol=1e-7 * max(1.0, np.abs(g).max())), term
+    assert np.array_equal(H, H.T) or np.abs(H - H.T).max() <= 1e-12 * max(1.0, np.abs(H).max())
+    assert np.linalg.eigvalsh(0.5 * (H + H.T)).min() >= 1e-10 * (1 - 1e-6) - 1e-12 * np.abs(H).max()
+    return val, g
+
+
+def test_term_s2m_and_barrier_known_answers(api):
+    d = 0.3
+    val, g = _check_grad_and_spd(api, "s2m", [[0.0, 0.0, d]], [2.0, 0.0, 0.0, 0.0])
+    assert abs(val - 1e3 * 2.0 * d * d) < 1e-12 and abs(g[2] - 1e3 * 4.0 * d) < 1e-9
+    dh = 1e-3
+    tri = [[0.0, 0.0, 0.0], [1e-2, 0.0, 0.0], [0.0, 1e-2, 0.0]]
+    val, _ = _check_grad_and_spd(api, "pt", [[2e-3, 2e-3, dh / 2]] + tri, None, cls=6)  # point-plane class
+    assert abs(val - 1e2 * (dh * dh / 4) * np.log(2)) < 1e-15
+    ee = [[-1e-2, 0.0, 0.0], [1e-2, 0.0, 0.0], [0.0, -1e-2, dh / 2], [0.0, 1e-2, dh / 2]]
+    val, _ = _check_grad_and_spd(api, "ee", ee, None, cls=8)  # line-line class
+    assert abs(val - 1e2 * (dh * dh / 4) * np.log(2)) < 1e-15
+
+
+def test_term_elastic_and_bending_known_answers(api):
+    rest = [0, 0, 0, 0, 0, 0, 0, 0, 1.0, 0.0, 0.0, 1.0, 0.5]  # Dm^-1 = I, A0 = 1/2
+    x0 = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0]])
+    lam = 1.2
+    val, _ = _check_grad_and_spd(api, "elastic", lam * x0, rest)
+    assert abs(val - 1e-1 * 0.25 * 0.5 * np.sqrt(2) * (lam * lam - 1)) < 1e-14
+    c, s_ = np.cos(0.7), np.sin(0.7)
+    Rm = np.array([[c, -s_, 0], [s_, c, 0], [0, 0, 1]])
+    assert abs(api.project_term("elastic", x0 @ Rm.T + np.array([0.3, -0.2, 0.5]), rest)[0]) < 1e-18  # rigid
+    th = 0.4
+    hinge = np.array([[0.0, 0, 0], [1, 0, 0], [0.5, 1, 0], [0.5, -np.cos(th), np.sin(th)]])
+    brest = [0] * 13 + [0.0, 1.0]  # theta0 = 0 (flat), l0 = 1
+    val, _ = _check_grad_and_spd(api, "bending", hinge, brest)
+    assert abs(val - 1e-2 * 0.5 * th * th) < 1e-12
+    flat = np.array([[0.0, 0, 0], [1, 0, 0], [0.5, 1, 0], [0.5, -1, 0]])
+    assert abs(api.project_term("bending", flat @ Rm.T, brest)[0]) < 1e-20  # rigid motion of the rest hinge
