@@ -1112,7 +1112,7 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     dev_sum_to(tmpv.get(), n3, sc.get());
     const double tol2 = PP.cg_tol * PP.cg_tol * gnorm * gnorm;
     int cg = 0;
-    for (; cg < PP.cg_max; ++cg) {
+    auto cg_iter = [&]() {
       PCU_LAUNCH(ctx, k_bsr_mv, grid_for(nv, 128), 128, 0, rstart.get(), bcol.get(), bval.get(), nv, q.get(), Ap.get());
       PCU_LAUNCH(ctx, k_mul, grid_for(n3, 256), 256, 0, n3, q.get(), Ap.get(), tmpv.get());
       dev_sum_to(tmpv.get(), n3, sc.get() + 1);
@@ -1124,14 +1124,35 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
       dev_sum_to(tmp2.get(), n3, sc.get() + 3);
       PCU_LAUNCH(ctx, k_cg_dir, grid_for(n3, 256), 256, 0, n3, sc.get(), z.get(), q.get());
       PCU_LAUNCH(ctx, k_cg_shift, 1, 1, 0, sc.get());
-      if ((cg & 15) == 15 || cg + 1 == PP.cg_max) {  // convergence check every 16 iterations
-        double h[4];
-        PCU_CUDA(cudaMemcpyAsync(h, sc.get(), 32, cudaMemcpyDeviceToHost, st));
-        PCU_CUDA(cudaStreamSynchronize(st));
-        if (h[3] <= tol2 || !(h[1] > 0.0)) {
-          ++cg;
-          break;
-        }
+    };
+    auto converged = [&]() {
+      double h[4];
+      PCU_CUDA(cudaMemcpyAsync(h, sc.get(), 32, cudaMemcpyDeviceToHost, st));
+      PCU_CUDA(cudaStreamSynchronize(st));
+      return h[3] <= tol2 || !(h[1] > 0.0);
+    };
+    constexpr int kChunk = 16;  // CG iterations per convergence check
+    if (!ctx.prof.kt) {
+      // the 16-iteration chunk is captured once per Newton step into a CUDA graph and replayed:
+      // the CG kernels are tiny, so launch latency, not work, bounds them
+      cudaGraph_t graph = nullptr;
+      cudaGraphExec_t exec = nullptr;
+      PCU_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      for (int k = 0; k < kChunk; ++k) cg_iter();
+      PCU_CUDA(cudaStreamEndCapture(st, &graph));
+      PCU_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      for (; cg < PP.cg_max;) {
+        PCU_CUDA(cudaGraphLaunch(exec, st));
+        cg += kChunk;
+        if (converged()) break;
+      }
+      cudaGraphExecDestroy(exec);
+      cudaGraphDestroy(graph);
+    } else {
+      for (; cg < PP.cg_max;) {
+        for (int k = 0; k < kChunk; ++k) cg_iter();
+        cg += kChunk;
+        if (converged()) break;
       }
     }
     stats.cg_iterations += cg;
