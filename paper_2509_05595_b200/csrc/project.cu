@@ -446,6 +446,11 @@ __global__ void k_bsr_fill(const uint64_t* __restrict__ keys, const uint32_t* __
   bcol[b] = static_cast<int32_t>(keys[i] & 0xffffffffu);
   for (int k = 0; k < 9; ++k) bval[9 * static_cast<int64_t>(b) + k] = acc[k];
 }
+__global__ void k_compact_u64(const uint64_t* __restrict__ in, const uint32_t* __restrict__ keep,
+                              const uint32_t* __restrict__ pos, int64_t n, uint64_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n && keep[i]) out[pos[i]] = in[i];
+}
 __global__ void k_row_start(const int32_t* __restrict__ brow, int64_t nb, int64_t nv, uint32_t* __restrict__ rs) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i > nb) return;
@@ -940,7 +945,8 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
   // ---- broad phase -> contact primitives (deduplicated) for positions X (+ p when sweeping)
   DevBuf<double> box(6 * nf, st);
   DevBuf<uint64_t> bkey(nf, st), bkey2(nf, st);
-  DevBuf<uint64_t> fpairs, pt, ee;
+  DevBuf<uint64_t> fpairs, pt, ee, ubuf;
+  DevBuf<uint32_t> uhead, upos;
   int64_t npt = 0, nee = 0;
   auto primitives = [&](const double* X, const double* p, double pad) {
     PCU_LAUNCH(ctx, k_swept_boxes, grid_for(nf, 256), 256, 0, X, p, dF, nf, pad, box.get(), bkey.get());
@@ -961,15 +967,19 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
         unsigned long long h2[2];
         PCU_CUDA(cudaMemcpyAsync(h2, c2.get(), 16, cudaMemcpyDeviceToHost, st));
         PCU_CUDA(cudaStreamSynchronize(st));
-        // dedup (sorted unique) — a primitive pair can come from several face pairs
+        // dedup on the device (sort, head flags, scan, compact) — a primitive pair can come from
+        // several face pairs
         auto uniq = [&](DevBuf<uint64_t>& a, int64_t n) -> int64_t {
           if (n <= 1) return n;
           sort_pairs_u64(ctx, a.get(), n);
-          std::vector<uint64_t> h(n);
-          PCU_CUDA(cudaMemcpyAsync(h.data(), a.get(), n * 8, cudaMemcpyDeviceToHost, st));
-          PCU_CUDA(cudaStreamSynchronize(st));
-          const int64_t u = std::unique(h.begin(), h.end()) - h.begin();
-          PCU_CUDA(cudaMemcpyAsync(a.get(), h.data(), u * 8, cudaMemcpyHostToDevice, st));
+          uhead.ensure(n, st);
+          upos.ensure(n, st);
+          ubuf.ensure(n, st);
+          PCU_LAUNCH(ctx, k_key_heads, grid_for(n, 256), 256, 0, a.get(), n, uhead.get());
+          exclusive_scan_u32(ctx, uhead.get(), upos.get(), n);
+          const int64_t u = static_cast<int64_t>(read_scalar(ctx, upos.get() + n - 1)) + read_scalar(ctx, uhead.get() + n - 1);
+          PCU_LAUNCH(ctx, k_compact_u64, grid_for(n, 256), 256, 0, a.get(), uhead.get(), upos.get(), n, ubuf.get());
+          PCU_CUDA(cudaMemcpyAsync(a.get(), ubuf.get(), u * 8, cudaMemcpyDeviceToDevice, st));
           return u;
         };
         npt = uniq(pt, static_cast<int64_t>(h2[0]));
