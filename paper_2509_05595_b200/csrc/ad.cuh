@@ -1,7 +1,8 @@
 // ad.cuh — forward-mode second-order automatic differentiation for the stage-3 energy stencils
 // (SPEC.md safe_project; Appendix 2.2).  J2<N> carries a value, its gradient and its
-// full (symmetric) Hessian with respect to N stencil coordinates, so every term's gradient and
-// Hessian block are exact derivatives of one closed-form expression.  The same templates
+// symmetric Hessian with respect to N stencil coordinates (only the upper triangle h[i][j],
+// j >= i, is propagated; read it through hess()), so every term's gradient and Hessian block
+// are exact derivatives of one closed-form expression.  The same templates
 // instantiated on `double` give value-only evaluations (line search).
 #pragma once
 
@@ -19,14 +20,14 @@ struct J2 {
     #pragma unroll 1
   for (int i = 0; i < N; ++i) {
       g[i] = 0.0;
-      for (int j = 0; j < N; ++j) h[i][j] = 0.0;
+      for (int j = i; j < N; ++j) h[i][j] = 0.0;
     }
   }
   __host__ __device__ J2(double c) : v(c) {  // NOLINT: constants promote implicitly
     #pragma unroll 1
   for (int i = 0; i < N; ++i) {
       g[i] = 0.0;
-      for (int j = 0; j < N; ++j) h[i][j] = 0.0;
+      for (int j = i; j < N; ++j) h[i][j] = 0.0;
     }
   }
   __host__ __device__ static J2 var(int i, double x) {
@@ -43,7 +44,7 @@ __host__ __device__ inline J2<N> operator+(const J2<N>& a, const J2<N>& b) {
   #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = a.g[i] + b.g[i];
-    for (int j = 0; j < N; ++j) r.h[i][j] = a.h[i][j] + b.h[i][j];
+    for (int j = i; j < N; ++j) r.h[i][j] = a.h[i][j] + b.h[i][j];
   }
   return r;
 }
@@ -54,7 +55,7 @@ __host__ __device__ inline J2<N> operator-(const J2<N>& a, const J2<N>& b) {
   #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = a.g[i] - b.g[i];
-    for (int j = 0; j < N; ++j) r.h[i][j] = a.h[i][j] - b.h[i][j];
+    for (int j = i; j < N; ++j) r.h[i][j] = a.h[i][j] - b.h[i][j];
   }
   return r;
 }
@@ -65,7 +66,7 @@ __host__ __device__ inline J2<N> operator-(const J2<N>& a) {
   #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = -a.g[i];
-    for (int j = 0; j < N; ++j) r.h[i][j] = -a.h[i][j];
+    for (int j = i; j < N; ++j) r.h[i][j] = -a.h[i][j];
   }
   return r;
 }
@@ -76,7 +77,7 @@ __host__ __device__ inline J2<N> operator*(const J2<N>& a, const J2<N>& b) {
   #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = a.v * b.g[i] + b.v * a.g[i];
-    for (int j = 0; j < N; ++j)
+    for (int j = i; j < N; ++j)
       r.h[i][j] = a.v * b.h[i][j] + b.v * a.h[i][j] + a.g[i] * b.g[j] + b.g[i] * a.g[j];
   }
   return r;
@@ -88,7 +89,7 @@ __host__ __device__ inline J2<N> operator*(double c, const J2<N>& a) {
   #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = c * a.g[i];
-    for (int j = 0; j < N; ++j) r.h[i][j] = c * a.h[i][j];
+    for (int j = i; j < N; ++j) r.h[i][j] = c * a.h[i][j];
   }
   return r;
 }
@@ -121,7 +122,7 @@ __host__ __device__ inline J2<N> chain(const J2<N>& a, double f, double d1, doub
   #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = d1 * a.g[i];
-    for (int j = 0; j < N; ++j) r.h[i][j] = d1 * a.h[i][j] + d2 * a.g[i] * a.g[j];
+    for (int j = i; j < N; ++j) r.h[i][j] = d1 * a.h[i][j] + d2 * a.g[i] * a.g[j];
   }
   return r;
 }
@@ -158,7 +159,7 @@ __host__ __device__ inline J2<N> atan2(const J2<N>& y, const J2<N>& x) {
   #pragma unroll 1
   for (int i = 0; i < N; ++i) {
     r.g[i] = fy * y.g[i] + fx * x.g[i];
-    for (int j = 0; j < N; ++j)
+    for (int j = i; j < N; ++j)
       r.h[i][j] = fy * y.h[i][j] + fx * x.h[i][j] + fyy * y.g[i] * y.g[j] + fxx * x.g[i] * x.g[j] +
                   fxy * (y.g[i] * x.g[j] + x.g[i] * y.g[j]);
   }
@@ -169,6 +170,11 @@ __host__ __device__ inline J2<N> atan2(const J2<N>& y, const J2<N>& x) {
 __host__ __device__ inline double sqrt(double a) { return ::sqrt(a); }
 __host__ __device__ inline double log(double a) { return ::log(a); }
 __host__ __device__ inline double atan2(double y, double x) { return ::atan2(y, x); }
+
+template <int N>
+__host__ __device__ inline double hess(const J2<N>& a, int i, int j) {
+  return i <= j ? a.h[i][j] : a.h[j][i];
+}
 
 __host__ __device__ inline double value(double a) { return a; }
 template <int N>

@@ -327,7 +327,7 @@ __device__ void eval_stencil(const Stencil& S, const double* X, const TermData& 
   *val = e.v;
   for (int i = 0; i < N; ++i) gslot[i] = e.g[i];
   for (int i = 0; i < N; ++i)
-    for (int j = 0; j < N; ++j) blk[i * N + j] = e.h[i][j];
+    for (int j = 0; j < N; ++j) blk[i * N + j] = ad::hess(e, i, j);
   spd_project(blk, N);
 }
 
