@@ -129,11 +129,12 @@ __device__ bool gd_3d(D3 p1, D3 q1, D3 r1, D3 p2, D3 q2, D3 r2, int dp2, int dq2
   return true;
 }
 
-// T1=(A,B,C), T2=(A,D,E) non-coplanar: intersection longer than the shared point?
-__device__ bool shared_vertex_3d(D3 A, D3 B, D3 C, D3 D, D3 E) {
-  if (o3(B, A, D, E) * o3(C, A, D, E) > 0) return false;
-  const int oD = o3(D, A, B, C), oE = o3(E, A, B, C);
+// T1=(A,B,C), T2=(A,D,E) non-coplanar: intersection longer than the shared point?  oD, oE are
+// the exact orientations of D and E against T1's plane (the caller's coplanarity test made them;
+// a cyclic rotation of T1 keeps their signs), so a same-side pair costs no further predicate.
+__device__ bool shared_vertex_3d(D3 A, D3 B, D3 C, D3 D, D3 E, int oD, int oE) {
   if (oD * oE > 0) return false;
+  if (o3(B, A, D, E) * o3(C, A, D, E) > 0) return false;
   const D3 Z = oD != 0 ? D : E;   // a vertex of T2 off the plane of T1
   const D3 P = oD != 0 ? E : D;   // the side of the crossing point of DE with that plane
   const int sP = o3(A, B, P, Z), sC = o3(A, B, C, Z);
@@ -277,11 +278,9 @@ __device__ __noinline__ bool verdict1(const double* __restrict__ V, const int32_
   int i1 = 0;
   while (I.s1[i1] < 0) ++i1;
   const int j1 = I.s1[i1];
-  bool coplanar = true;
-  for (int j = 0; j < 3 && coplanar; ++j)
-    if (I.s2[j] < 0 && o3(T2[j], T1[0], T1[1], T1[2]) != 0) coplanar = false;
-  if (!coplanar)
-    return shared_vertex_3d(T1[i1], T1[(i1 + 1) % 3], T1[(i1 + 2) % 3], T2[(j1 + 1) % 3], T2[(j1 + 2) % 3]);
+  const int oD = o3(T2[(j1 + 1) % 3], T1[0], T1[1], T1[2]), oE = o3(T2[(j1 + 2) % 3], T1[0], T1[1], T1[2]);
+  if (oD != 0 || oE != 0)
+    return shared_vertex_3d(T1[i1], T1[(i1 + 1) % 3], T1[(i1 + 2) % 3], T2[(j1 + 1) % 3], T2[(j1 + 2) % 3], oD, oE);
   const int drop = drop_axis(T1);
   const P2 A = proj2(T1[i1], drop);
   P2 B = proj2(T1[(i1 + 1) % 3], drop), C = proj2(T1[(i1 + 2) % 3], drop);
