@@ -82,8 +82,51 @@ static void* tmp_storage(Ctx& ctx, size_t bytes) {
   return ctx.scratch;
 }
 
+// Small scans (most of the QEM loop's late iterations): one CTA, 16 items per thread, replaces
+// CUB's two-launch chain.  Integer sums, so the result equals CUB's bit for bit; each thread
+// reads its items before the block barrier and writes only its own, so in == out is safe.
+constexpr int kSmallScanItems = 16, kSmallScan = 1024 * kSmallScanItems;
+__global__ void __launch_bounds__(1024) k_small_scan(const uint32_t* in, int n, uint32_t* out) {
+  __shared__ uint32_t wsum[32];
+  const int base = threadIdx.x * kSmallScanItems;
+  uint32_t v[kSmallScanItems];
+  uint32_t tot = 0;
+#pragma unroll
+  for (int k = 0; k < kSmallScanItems; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0u;
+    tot += v[k];
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = wsum[lane], wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    wsum[lane] = wi - w;
+  }
+  __syncthreads();
+  uint32_t run = wsum[warp] + incl - tot;
+#pragma unroll
+  for (int k = 0; k < kSmallScanItems; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += v[k];
+  }
+}
+
 void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n) {
   if (n <= 0) return;
+  if (n <= kSmallScan) {
+    PCU_LAUNCH(ctx, k_small_scan, 1, 1024, 0, in, static_cast<int>(n), out);
+    return;
+  }
   size_t need = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, need, in, out, n, ctx.stream);
   void* t = tmp_storage(ctx, need);
