@@ -644,8 +644,9 @@ __device__ __forceinline__ void report(DetectScalars* ds, int mode, int32_t p, i
 
 // Narrow phase, stage 1 (grid-stride over the device-side candidate count): the exact
 // inflated double-box test (the reference's candidate set), duplicates and degenerate faces
-// (always intersecting), then bucketing by shared-vertex count so stage 2 runs one uniform code
-// path per warp.  mode 1 (QEM undo) skips pairs none of whose owners can still be reverted.
+// (always intersecting) and the 2-shared verdict inline, then bucketing the 0/1-shared pairs so
+// stage 2 runs one uniform code path per warp.  mode 1 (QEM undo): stage 2 skips pairs none of
+// whose owners can still be reverted.
 __device__ __forceinline__ bool deep_overlap(const FBox& a, const FBox& b) {
   bool ok = true;
   for (int k = 0; k < 3; ++k) {
@@ -684,6 +685,10 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
       for (int w = 0; w < 3; ++w) shared += tp[u] == ta[w];
     if (shared == 3 || degen[p] || degen[a]) {
       report(ds, mode, p, a, pairs, pair_cap, owner, revert);
+      continue;
+    }
+    if (shared == 2) {  // edge neighbours: one orientation decides almost every pair, so no bucket
+      if (verdict2(V, tp, ta, pair_info(tp, ta))) report(ds, mode, p, a, pairs, pair_cap, owner, revert);
       continue;
     }
     const unsigned long long slot = agg_inc_labeled(&ds->ncls[shared], static_cast<unsigned>(shared));
@@ -823,8 +828,6 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
              S.cls.get(), pairs, pair_cap, owner, revert);
-  PCU_LAUNCH(ctx, k_narrow<2>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
-             revert);
   PCU_LAUNCH(ctx, k_narrow<1>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
              revert);
   PCU_LAUNCH(ctx, k_narrow<0>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
