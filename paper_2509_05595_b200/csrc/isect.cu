@@ -677,12 +677,13 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
     // the owned faces, later rounds probe with them — so no owner filter is needed here)
     const int32_t* tp = F + 3 * p;
     const int32_t* ta = F + 3 * a;
-    // the float boxes enclose the double boxes within one f32 ulp per side: an overlap deeper
-    // than that margin in every axis certifies the double-box overlap without the vertex loads
-    if (!deep_overlap(B[p], B[a]) && !overlap(face_box(V, tp), face_box(V, ta))) continue;
     int shared = 0;
     for (int u = 0; u < 3; ++u)
       for (int w = 0; w < 3; ++w) shared += tp[u] == ta[w];
+    // faces sharing a vertex: both (inflated) double boxes contain it, so they overlap.  Otherwise
+    // the float boxes enclose the double boxes within one f32 ulp per side: an overlap deeper
+    // than that margin in every axis certifies the double-box overlap without the vertex loads
+    if (shared == 0 && !deep_overlap(B[p], B[a]) && !overlap(face_box(V, tp), face_box(V, ta))) continue;
     if (shared == 3 || degen[p] || degen[a]) {
       report(ds, mode, p, a, pairs, pair_cap, owner, revert);
       continue;
