@@ -274,17 +274,16 @@ __device__ __noinline__ bool verdict0(const double* __restrict__ V, const int32_
 __device__ __noinline__ bool verdict1(const double* __restrict__ V, const int32_t* t1, const int32_t* t2,
                                       const PairInfo& I) {
   const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
-  const D3 T2[3] = {vtx(V, t2[0]), vtx(V, t2[1]), vtx(V, t2[2])};
   int i1 = 0;
   while (I.s1[i1] < 0) ++i1;
   const int j1 = I.s1[i1];
-  const int oD = o3(T2[(j1 + 1) % 3], T1[0], T1[1], T1[2]), oE = o3(T2[(j1 + 2) % 3], T1[0], T1[1], T1[2]);
-  if (oD != 0 || oE != 0)
-    return shared_vertex_3d(T1[i1], T1[(i1 + 1) % 3], T1[(i1 + 2) % 3], T2[(j1 + 1) % 3], T2[(j1 + 2) % 3], oD, oE);
+  const D3 D3d = vtx(V, t2[(j1 + 1) % 3]), E3d = vtx(V, t2[(j1 + 2) % 3]);  // T2's shared vertex is T1[i1]
+  const int oD = o3(D3d, T1[0], T1[1], T1[2]), oE = o3(E3d, T1[0], T1[1], T1[2]);
+  if (oD != 0 || oE != 0) return shared_vertex_3d(T1[i1], T1[(i1 + 1) % 3], T1[(i1 + 2) % 3], D3d, E3d, oD, oE);
   const int drop = drop_axis(T1);
   const P2 A = proj2(T1[i1], drop);
   P2 B = proj2(T1[(i1 + 1) % 3], drop), C = proj2(T1[(i1 + 2) % 3], drop);
-  P2 D = proj2(T2[(j1 + 1) % 3], drop), E = proj2(T2[(j1 + 2) % 3], drop);
+  P2 D = proj2(D3d, drop), E = proj2(E3d, drop);
   if (o2(A, B, C) < 0) {
     const P2 t = B;
     B = C;
