@@ -126,6 +126,27 @@ __device__ __noinline__ int orient3d_exact(D3 a, D3 b, D3 c, D3 d) {
   return xp::sign_of(an, acc);
 }
 
+// The certified part of orient3d: the sign where the floating-point filter (or coincident
+// points) decides it, else 2.  Kernels that call only this carry none of the expansion
+// arithmetic's registers.
+__device__ __forceinline__ int orient3d_filtered(D3 a, D3 b, D3 c, D3 d) {
+  const double adx = a.x - d.x, bdx = b.x - d.x, cdx = c.x - d.x;
+  const double ady = a.y - d.y, bdy = b.y - d.y, cdy = c.y - d.y;
+  const double adz = a.z - d.z, bdz = b.z - d.z, cdz = c.z - d.z;
+  const double bdxcdy = bdx * cdy, cdxbdy = cdx * bdy;
+  const double cdxady = cdx * ady, adxcdy = adx * cdy;
+  const double adxbdy = adx * bdy, bdxady = bdx * ady;
+  const double det = adz * (bdxcdy - cdxbdy) + bdz * (cdxady - adxcdy) + cdz * (adxbdy - bdxady);
+  const double perm = (fabs(bdxcdy) + fabs(cdxbdy)) * fabs(adz) + (fabs(cdxady) + fabs(adxcdy)) * fabs(bdz) +
+                      (fabs(adxbdy) + fabs(bdxady)) * fabs(cdz);
+  const double bound = (7.0 + 56.0 * 1.1102230246251565e-16) * 1.1102230246251565e-16 * perm;
+  if (det > bound) return 1;
+  if (-det > bound) return -1;
+  auto same = [](D3 p, D3 q) { return p.x == q.x && p.y == q.y && p.z == q.z; };
+  if (same(a, b) || same(a, c) || same(a, d) || same(b, c) || same(b, d) || same(c, d)) return 0;
+  return 2;
+}
+
 // orient3d(a,b,c,d) = sign det[a-d, b-d, c-d]
 __device__ __forceinline__ int orient3d(D3 a, D3 b, D3 c, D3 d) {
   const double adx = a.x - d.x, bdx = b.x - d.x, cdx = c.x - d.x;

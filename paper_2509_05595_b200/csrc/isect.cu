@@ -297,6 +297,32 @@ __device__ __noinline__ bool verdict1(const double* __restrict__ V, const int32_
   return ray_in(A, B, C, D) || ray_in(A, B, C, E) || ray_in(A, D, E, B) || ray_in(A, D, E, C);
 }
 
+// verdict1 from filtered orientations only: 0/1 = the verdict (every predicate it needed was
+// certified, so it equals verdict1's), 2 = undecided (an uncertain orientation, or a coplanar
+// pair) -> the pair is re-run through verdict1 by a second pass.
+__device__ __forceinline__ int verdict1_fast(const double* __restrict__ V, const int32_t* t1, const int32_t* t2,
+                                             const PairInfo& I) {
+  const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
+  int i1 = 0;
+  while (I.s1[i1] < 0) ++i1;
+  const int j1 = I.s1[i1];
+  const D3 D = vtx(V, t2[(j1 + 1) % 3]), E = vtx(V, t2[(j1 + 2) % 3]);
+  const int oD = orient3d_filtered(D, T1[0], T1[1], T1[2]), oE = orient3d_filtered(E, T1[0], T1[1], T1[2]);
+  if (oD == 2 || oE == 2 || (oD == 0 && oE == 0)) return 2;
+  // shared_vertex_3d, predicate for predicate
+  if (oD * oE > 0) return 0;
+  const D3 A = T1[i1], B = T1[(i1 + 1) % 3], C = T1[(i1 + 2) % 3];
+  const int b1 = orient3d_filtered(B, A, D, E), c1 = orient3d_filtered(C, A, D, E);
+  if (b1 == 2 || c1 == 2) return 2;
+  if (b1 * c1 > 0) return 0;
+  const D3 Z = oD != 0 ? D : E;
+  const D3 P = oD != 0 ? E : D;
+  const int sP = orient3d_filtered(A, B, P, Z), sC = orient3d_filtered(A, B, C, Z);
+  const int tP = orient3d_filtered(A, C, P, Z), tB = orient3d_filtered(A, C, B, Z);
+  if (sP == 2 || sC == 2 || tP == 2 || tB == 2) return 2;
+  return sP * sC >= 0 && tP * tB >= 0 ? 1 : 0;
+}
+
 // non-degenerate, exactly 2 shared vertices
 __device__ __noinline__ bool verdict2(const double* __restrict__ V, const int32_t* t1, const int32_t* t2,
                                       const PairInfo& I) {
@@ -696,7 +722,41 @@ __global__ void __launch_bounds__(256) k_classify(const double* __restrict__ V, 
   }
 }
 
-template <int SHARED>
+// Stage 2a for the 1-shared bucket: certified-filter verdicts only (a small register budget,
+// so high occupancy for these latency-bound gathers); undecided pairs go to list 2 (empty:
+// 2-shared pairs are decided in k_classify) for the exact k_narrow<1, 2>.
+#ifndef PCU_NARROW1_FAST_MINB
+#define PCU_NARROW1_FAST_MINB 6
+#endif
+__global__ void __launch_bounds__(128, PCU_NARROW1_FAST_MINB) k_narrow1_fast(const double* __restrict__ V, const int32_t* __restrict__ F,
+                                                      uint64_t* __restrict__ cls, uint64_t cap,
+                                                      DetectScalars* __restrict__ ds, int mode,
+                                                      int32_t* __restrict__ pairs, uint64_t pair_cap,
+                                                      const int32_t* __restrict__ owner, uint8_t* __restrict__ revert) {
+  if (ds->redo) return;
+  const unsigned long long n = ds->ncls[1];
+  const uint64_t* L = cls + cap;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t c = L[i];
+    const int32_t p = static_cast<int32_t>(c >> 32), a = static_cast<int32_t>(c & 0xffffffffu);
+    if (mode == 1) {
+      const int32_t op = owner[p], oa = owner[a];
+      if ((op < 0 || revert[op]) && (oa < 0 || revert[oa])) continue;
+    }
+    const int32_t* tp = F + 3 * p;
+    const int32_t* ta = F + 3 * a;
+    const int v = verdict1_fast(V, tp, ta, pair_info(tp, ta));
+    if (v == 1) {
+      report(ds, mode, p, a, pairs, pair_cap, owner, revert);
+    } else if (v == 2) {
+      const unsigned long long slot = agg_inc_labeled(&ds->ncls[2], 2u);
+      cls[2 * cap + slot] = c;
+    }
+  }
+}
+
+template <int SHARED, int LIST = SHARED>
 #ifndef PCU_NARROW_MINB
 #define PCU_NARROW_MINB 1
 #endif
@@ -706,8 +766,8 @@ __global__ void __launch_bounds__(128, PCU_NARROW_MINB) k_narrow(const double* _
                                                 uint64_t pair_cap, const int32_t* __restrict__ owner,
                                                 uint8_t* __restrict__ revert) {
   if (ds->redo) return;
-  const unsigned long long n = ds->ncls[SHARED];
-  const uint64_t* L = cls + SHARED * cap;
+  const unsigned long long n = ds->ncls[LIST];
+  const uint64_t* L = cls + LIST * cap;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int32_t p = static_cast<int32_t>(L[i] >> 32), a = static_cast<int32_t>(L[i] & 0xffffffffu);
@@ -828,8 +888,11 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
              S.cls.get(), pairs, pair_cap, owner, revert);
-  PCU_LAUNCH(ctx, k_narrow<1>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
-             revert);
+  PCU_LAUNCH(ctx, k_narrow1_fast, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap,
+             owner, revert);
+  // the undecided remainder is a small fraction of the bucket: one CTA per SM
+  PCU_LAUNCH(ctx, (k_narrow<1, 2>), static_cast<unsigned>(ctx.num_sms), 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap,
+             owner, revert);
   PCU_LAUNCH(ctx, k_narrow<0>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
              revert);
 }
