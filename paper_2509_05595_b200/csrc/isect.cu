@@ -555,32 +555,45 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
       spre[warp][lane] = incl;
       sbase[warp][lane] = e0;
       __syncwarp();
-      for (uint32_t t = lane; t < total; t += 32) {
-        int lo = 0, hi = take - 1;  // first record whose inclusive prefix exceeds t
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (spre[warp][mid] > t) hi = mid;
-          else lo = mid + 1;
+      // warp-uniform trip count, so emitting lanes reserve their buffer slots with one shared
+      // atomic per warp step instead of one per candidate
+      for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        bool emit = false;
+        uint64_t v = 0;
+        if (t < total) {
+          int lo = 0, hi = take - 1;  // first record whose inclusive prefix exceeds t
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (spre[warp][mid] > t) hi = mid;
+            else lo = mid + 1;
+          }
+          const int r = qn - take + lo;
+          const uint32_t e = sbase[warp][lo] + (t - (lo ? spre[warp][lo - 1] : 0u));
+          const int o = qo[warp][r];
+          const int32_t op = sp[warp][o];
+          const int4 en = entries[e];  // face id + its first cell: the dedup test needs no box load
+          // first common cell of the two ranges (a hash collision can at worst duplicate a pair)
+          const int32_t a = en.x;
+          emit = qc[warp][r][0] == max(slo[warp][o][0], en.y) && qc[warp][r][1] == max(slo[warp][o][1], en.z) &&
+                 qc[warp][r][2] == max(slo[warp][o][2], en.w) &&
+                 !(a == op || (sbuild[warp][o] && a < op)) &&  // else emitted from probe a instead
+                 overlap(sbox[warp][o], B[a]);
+          v = (static_cast<uint64_t>(static_cast<uint32_t>(op)) << 32) | static_cast<uint32_t>(a);
         }
-        const int r = qn - take + lo;
-        const uint32_t e = sbase[warp][lo] + (t - (lo ? spre[warp][lo - 1] : 0u));
-        const int o = qo[warp][r];
-        const int32_t op = sp[warp][o];
-        const int4 en = entries[e];  // face id + its first cell: the dedup test needs no box load
-        // first common cell of the two ranges (a hash collision can at worst duplicate a pair)
-        if (qc[warp][r][0] != max(slo[warp][o][0], en.y) || qc[warp][r][1] != max(slo[warp][o][1], en.z) ||
-            qc[warp][r][2] != max(slo[warp][o][2], en.w))
-          continue;
-        const int32_t a = en.x;
-        if (a == op || (sbuild[warp][o] && a < op)) continue;  // the pair is emitted from probe a instead
-        if (!overlap(sbox[warp][o], B[a])) continue;
-        const uint64_t v = (static_cast<uint64_t>(static_cast<uint32_t>(op)) << 32) | static_cast<uint32_t>(a);
-        const unsigned slot = atomicAdd(&nbuf, 1u);
-        if (slot < kBuf) {
-          buf[slot] = v;
-        } else {  // block buffer full: direct global append
-          const unsigned long long g = agg_inc(ncand);
-          if (g < cap) cand[g] = v;
+        const unsigned em = __ballot_sync(0xffffffffu, emit);
+        if (em == 0u) continue;
+        unsigned base = 0;
+        if (lane == __ffs(em) - 1) base = atomicAdd(&nbuf, static_cast<unsigned>(__popc(em)));
+        base = __shfl_sync(0xffffffffu, base, __ffs(em) - 1);
+        if (emit) {
+          const unsigned slot = base + __popc(em & lt);
+          if (slot < kBuf) {
+            buf[slot] = v;
+          } else {  // block buffer full: direct global append
+            const unsigned long long g = agg_inc(ncand);
+            if (g < cap) cand[g] = v;
+          }
         }
       }
       __syncwarp();
