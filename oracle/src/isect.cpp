@@ -273,37 +273,133 @@ bool box_overlap(const Box& a, const Box& b) {
          a.hi.y >= b.lo.y && a.hi.z >= b.lo.z;
 }
 
-// Intersecting pairs (i<j) among `alive` faces where at least one of i,j has query[i]!=0.
-// Sort-and-sweep on lo.x; the candidate set equals the closed inflated-AABB overlap set.
+// Intersecting pairs (i<j) among `alive` faces where at least one of i,j has query[i]!=0
+// (query == nullptr: every alive face).  The candidate set is the closed inflated-AABB overlap
+// set (lbvh.cpp:182-190 semantics): a uniform hashed grid over the query faces (cell edge 1.5x
+// their mean box extent) is probed by every alive face, each pair examined in the first common
+// cell of the two cell ranges; faces covering more than kMaxCells cells are paired by a direct
+// scan.  Only the set matters (it is sorted and deduplicated), never the grid.
 std::vector<std::pair<int32_t, int32_t>> detect_pairs(const double* v, const int32_t* f, int64_t nf,
                                                       const uint8_t* alive, const uint8_t* query) {
+  constexpr int64_t kMaxCells = 64;
+  struct Range {
+    int64_t lo[3], hi[3];
+    int64_t count() const { return (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1); }
+  };
   std::vector<Box> boxes(nf);
-  std::vector<int32_t> ids;
+  parallel_for(nf, [&](int64_t i) {
+    if (!alive || alive[i]) boxes[i] = face_box(f + 3 * i, v);
+  }, 4096);
+  std::vector<int32_t> build, probe;
+  std::vector<uint8_t> in_build(nf, 0);
   for (int64_t i = 0; i < nf; ++i) {
     if (alive && !alive[i]) continue;
-    boxes[i] = face_box(f + 3 * i, v);
-    ids.push_back(static_cast<int32_t>(i));
-  }
-  std::sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) {
-    return boxes[a].lo.x < boxes[b].lo.x || (boxes[a].lo.x == boxes[b].lo.x && a < b);
-  });
-  const int64_t n = static_cast<int64_t>(ids.size());
-  std::vector<std::vector<std::pair<int32_t, int32_t>>> found(n);
-  parallel_for(n, [&](int64_t k) {
-    const int32_t i = ids[k];
-    const Box& bi = boxes[i];
-    for (int64_t m = k + 1; m < n; ++m) {
-      const int32_t j = ids[m];
-      if (boxes[j].lo.x > bi.hi.x) break;
-      if (query && !query[i] && !query[j]) continue;
-      if (!box_overlap(bi, boxes[j])) continue;
-      if (tri_tri_verdict(f + 3 * i, f + 3 * j, v))
-        found[k].emplace_back(std::min(i, j), std::max(i, j));
+    probe.push_back(static_cast<int32_t>(i));
+    if (!query || query[i]) {
+      build.push_back(static_cast<int32_t>(i));
+      in_build[i] = 1;
     }
-  }, 64);
+  }
+  if (build.empty()) return {};
+  double ext = 0.0;
+  for (int32_t b : build) {
+    const Box& x = boxes[b];
+    ext += std::max(std::max(x.hi.x - x.lo.x, x.hi.y - x.lo.y), x.hi.z - x.lo.z);
+  }
+  const double mean = ext / static_cast<double>(build.size());
+  const double inv_h = 1.0 / (1.5 * (mean > 0.0 ? mean : 1e-3));
+  auto range_of = [&](const Box& b) {
+    Range r;
+    const double lo[3] = {b.lo.x, b.lo.y, b.lo.z}, hi[3] = {b.hi.x, b.hi.y, b.hi.z};
+    for (int k = 0; k < 3; ++k) {
+      r.lo[k] = static_cast<int64_t>(std::floor(lo[k] * inv_h));
+      r.hi[k] = static_cast<int64_t>(std::floor(hi[k] * inv_h));
+    }
+    return r;
+  };
+  auto hash = [](int64_t x, int64_t y, int64_t z, uint64_t mask) {
+    uint64_t h = static_cast<uint64_t>(x) * 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(y) * 0xC2B2AE3D27D4EB4Full ^
+                 static_cast<uint64_t>(z) * 0x165667B19E3779F9ull;
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    return h & mask;
+  };
+  // counting sort of (cell, build face) entries into hash buckets
+  std::vector<Range> brange(build.size());
+  std::vector<int32_t> big;
+  int64_t nent = 0;
+  for (size_t k = 0; k < build.size(); ++k) {
+    brange[k] = range_of(boxes[build[k]]);
+    const int64_t c = brange[k].count();
+    if (c > kMaxCells) big.push_back(build[k]);
+    else nent += c;
+  }
+  uint64_t nb = 1024;
+  while (nb < static_cast<uint64_t>(2 * nent + 1)) nb <<= 1;
+  const uint64_t mask = nb - 1;
+  std::vector<uint32_t> boff(nb + 1, 0);
+  struct Entry {
+    int32_t face;
+    int64_t lo[3];
+  };
+  std::vector<Entry> ent(static_cast<size_t>(nent));
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<uint32_t> cur;
+    if (pass == 1) cur.assign(boff.begin(), boff.end() - 1);
+    for (size_t k = 0; k < build.size(); ++k) {
+      const Range& r = brange[k];
+      if (r.count() > kMaxCells) continue;
+      for (int64_t z = r.lo[2]; z <= r.hi[2]; ++z)
+        for (int64_t y = r.lo[1]; y <= r.hi[1]; ++y)
+          for (int64_t x = r.lo[0]; x <= r.hi[0]; ++x) {
+            const uint64_t h = hash(x, y, z, mask);
+            if (pass == 0) boff[h + 1]++;
+            else ent[cur[h]++] = Entry{build[k], {r.lo[0], r.lo[1], r.lo[2]}};
+          }
+    }
+    if (pass == 0)
+      for (uint64_t h = 0; h < nb; ++h) boff[h + 1] += boff[h];
+  }
+  // probe: every alive face against the grid; (p, b) with both in the build set only from p < b
+  const int64_t np = static_cast<int64_t>(probe.size());
+  constexpr int64_t kChunk = 2048;
+  const int64_t nchunk = (np + kChunk - 1) / kChunk;
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> found(nchunk);
+  parallel_for(nchunk, [&](int64_t ch) {
+    auto& out = found[ch];
+    for (int64_t k = ch * kChunk; k < std::min(np, (ch + 1) * kChunk); ++k) {
+      const int32_t p = probe[k];
+      const Box& bp = boxes[p];
+      auto consider = [&](int32_t b) {
+        if (b == p || (in_build[p] && b < p)) return;
+        if (!box_overlap(bp, boxes[b])) return;
+        if (tri_tri_verdict(f + 3 * p, f + 3 * b, v)) out.emplace_back(std::min(p, b), std::max(p, b));
+      };
+      const Range rp = range_of(bp);
+      if (rp.count() > kMaxCells) {  // huge probe: scan the build set (big build faces below)
+        for (size_t j = 0; j < build.size(); ++j)
+          if (brange[j].count() <= kMaxCells) consider(build[j]);
+      } else {
+        for (int64_t z = rp.lo[2]; z <= rp.hi[2]; ++z)
+          for (int64_t y = rp.lo[1]; y <= rp.hi[1]; ++y)
+            for (int64_t x = rp.lo[0]; x <= rp.hi[0]; ++x) {
+              const uint64_t h = hash(x, y, z, mask);
+              for (uint32_t e = boff[h]; e < boff[h + 1]; ++e) {
+                const Entry& en = ent[e];
+                if (x == std::max(rp.lo[0], en.lo[0]) && y == std::max(rp.lo[1], en.lo[1]) &&
+                    z == std::max(rp.lo[2], en.lo[2]))
+                  consider(en.face);
+              }
+            }
+      }
+      for (int32_t b : big) consider(b);
+    }
+  }, 1);
   std::vector<std::pair<int32_t, int32_t>> out;
   for (auto& x : found) out.insert(out.end(), x.begin(), x.end());
   std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
   return out;
 }
 

@@ -316,9 +316,9 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
     S.face_iterations += m.alive_faces;
     const Incidence I = build_incidence(m);
     // edges in lexicographic order
-    std::vector<std::pair<int32_t, int32_t>> edges;
-    for (int64_t v = 0; v < m.nv; ++v) {
-      std::vector<int32_t> nb;
+    // (per vertex: sorted unique upper neighbours, counted then written at scanned offsets)
+    auto upper = [&](int64_t v, std::vector<int32_t>& nb) {
+      nb.clear();
       for (const int32_t* p = I.begin(static_cast<int>(v)); p != I.end(static_cast<int>(v)); ++p) {
         const int32_t* t = m.face(*p);
         for (int k = 0; k < 3; ++k)
@@ -326,15 +326,35 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
       }
       std::sort(nb.begin(), nb.end());
       nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
-      for (int32_t b : nb) edges.emplace_back(static_cast<int32_t>(v), b);
-    }
+    };
+    std::vector<int64_t> eoff(m.nv + 1, 0);
+    constexpr int64_t kVChunk = 4096;
+    const int64_t nvc = (m.nv + kVChunk - 1) / kVChunk;
+    parallel_for(nvc, [&](int64_t c) {
+      std::vector<int32_t> nb;
+      for (int64_t v = c * kVChunk; v < std::min<int64_t>(m.nv, (c + 1) * kVChunk); ++v) {
+        upper(v, nb);
+        eoff[v + 1] = static_cast<int64_t>(nb.size());
+      }
+    }, 1);
+    for (int64_t v = 0; v < m.nv; ++v) eoff[v + 1] += eoff[v];
+    std::vector<std::pair<int32_t, int32_t>> edges(eoff[m.nv]);
+    parallel_for(nvc, [&](int64_t c) {
+      std::vector<int32_t> nb;
+      for (int64_t v = c * kVChunk; v < std::min<int64_t>(m.nv, (c + 1) * kVChunk); ++v) {
+        upper(v, nb);
+        for (size_t i = 0; i < nb.size(); ++i) edges[eoff[v] + i] = {static_cast<int32_t>(v), nb[i]};
+      }
+    }, 1);
     const int64_t ne = static_cast<int64_t>(edges.size());
     std::vector<uint64_t> key(ne, ~0ull);
     std::vector<V3> place(ne);
     std::vector<uint8_t> valid(ne, 1);
     int err = 0;
-    for (int64_t e = 0; e < ne; ++e)
-      if (invalid.count(edges[e])) valid[e] = 0;
+    if (!invalid.empty())
+      parallel_for(ne, [&](int64_t e) {
+        if (invalid.count(edges[e])) valid[e] = 0;
+      }, 4096);
     parallel_for(ne, [&](int64_t e) {
       if (!valid[e]) return;
       const CostOut c = edge_cost(m, I, edges[e].first, edges[e].second, P);

@@ -17,13 +17,17 @@
 #include "kernels.cuh"
 
 #include <atomic>
+#include <memory>
+#include <mutex>
 
 // Handles keep their context alive: pamopt_cu_ctx_destroy on a context that still owns meshes or
-// grids only marks it; the last handle freed releases it (no use-after-free at teardown).
+// grids only marks it; the last handle freed releases it (no use-after-free at teardown).  The
+// refcount and the dead/released flags change under one mutex, so exactly one caller releases.
 struct pamopt_cu_ctx_s {
   pcu::Ctx ctx;
-  std::atomic<int> refs{0};
-  std::atomic<bool> dead{false};
+  std::mutex mu;
+  int refs = 0;
+  bool dead = false, released = false;
 };
 
 static void ctx_release(pamopt_cu_ctx c) {
@@ -34,8 +38,30 @@ static void ctx_release(pamopt_cu_ctx c) {
   delete c;
 }
 
+static void ctx_ref(pamopt_cu_ctx c) {
+  std::lock_guard<std::mutex> l(c->mu);
+  ctx_ref(c);
+}
+
 static void ctx_unref(pamopt_cu_ctx c) {
-  if (--c->refs == 0 && c->dead) ctx_release(c);
+  bool rel;
+  {
+    std::lock_guard<std::mutex> l(c->mu);
+    rel = --c->refs == 0 && c->dead && !c->released;
+    if (rel) c->released = true;
+  }
+  if (rel) ctx_release(c);
+}
+
+static void ctx_mark_dead(pamopt_cu_ctx c) {
+  bool rel;
+  {
+    std::lock_guard<std::mutex> l(c->mu);
+    c->dead = true;
+    rel = c->refs == 0 && !c->released;
+    if (rel) c->released = true;
+  }
+  if (rel) ctx_release(c);
 }
 
 struct pamopt_cu_mesh_s {
@@ -231,8 +257,7 @@ int pamopt_cu_ctx_create(int32_t device, pamopt_cu_ctx* out) {
 int pamopt_cu_ctx_destroy(pamopt_cu_ctx c) {
   return guarded([&] {
     if (!c) return;
-    c->dead = true;
-    if (c->refs == 0) ctx_release(c);
+    ctx_mark_dead(c);
   });
 }
 
@@ -284,16 +309,16 @@ static int mesh_create(pamopt_cu_ctx c, const double* v, int64_t nv, const int32
     check_ctx(c);
     PCU_REQUIRE(out && nv >= 0 && nf >= 0 && (nv == 0 || v) && (nf == 0 || f), PAMOPT_CU_EINVAL, "bad mesh arguments");
     pcu::DeviceGuard g(c->ctx.device);
-    auto* m = new pamopt_cu_mesh_s();
-    m->owner = c;
-    ++c->refs;
+    std::unique_ptr<pamopt_cu_mesh_s> m(new pamopt_cu_mesh_s());  // freed (with its buffers) on a throw
     m->nv = nv;
     m->nf = nf;
     m->V.alloc(3 * (nv ? nv : 1), c->ctx.stream);
     m->F.alloc(3 * (nf ? nf : 1), c->ctx.stream);
     if (nv) PCU_CUDA(cudaMemcpyAsync(m->V.get(), v, 3 * nv * sizeof(double), kind, c->ctx.stream));
     if (nf) PCU_CUDA(cudaMemcpyAsync(m->F.get(), f, 3 * nf * sizeof(int32_t), kind, c->ctx.stream));
-    *out = m;
+    m->owner = c;
+    ctx_ref(c);
+    *out = m.release();
   });
 }
 
@@ -352,8 +377,18 @@ int pamopt_cu_mesh_free(pamopt_cu_mesh m) {
 }
 
 // ---------------------------------------------------------------------------- stage 1a
+static void check_indices(pcu::Ctx& ctx, const pamopt_cu_mesh_s* m) {
+  if (m->nf == 0) return;
+  const std::vector<int32_t> mm = pcu::index_range(ctx, m->F.get(), 3 * m->nf);
+  PCU_REQUIRE(mm[0] >= 0 && mm[1] < m->nv, PAMOPT_CU_EINVAL, "invalid mesh: face index out of range");
+}
+
+// IndexedMesh::validate (mesh.cpp:31-43, thrown as std::invalid_argument at mesh.cpp:186-187):
+// every hot-path entry rejects out-of-range and repeated face indices before any kernel reads them
+static void validate(pcu::Ctx& ctx, const pamopt_cu_mesh_s* m) { pcu::validate_mesh(ctx, m->F.get(), m->nf, m->nv); }
+
 static void check_R(int32_t R) {
-  PCU_REQUIRE(R >= 8 && R <= 2048 && (R & (R - 1)) == 0, PAMOPT_CU_EINVAL, "R must be a power of two in [8, 2048]");
+  PCU_REQUIRE(R >= 8 && R <= 1024 && (R & (R - 1)) == 0, PAMOPT_CU_EINVAL, "R must be a power of two in [8, 1024] (DMC cell ids are 32-bit)");
 }
 
 static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, double eps, pamopt_cu_grid* out,
@@ -369,15 +404,17 @@ static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, dou
     pcu::DeviceGuard g(c->ctx.device);
     if (z1 < 0) z1 = R + 1;
     PCU_REQUIRE(z0 >= 0 && z0 < z1 && z1 <= R + 1, PAMOPT_CU_EINVAL, "bad slab plane range");
+    PCU_REQUIRE(m->owner == c, PAMOPT_CU_EINVAL, "mesh belongs to another context");
+    validate(c->ctx, m);
     auto* gr = new pamopt_cu_grid_s();
     gr->owner = c;
-    ++c->refs;
+    ctx_ref(c);
     gr->R = R;
     gr->z0 = z0;
     gr->z1 = z1;
     const int64_t n1 = R + 1;
-    gr->g.alloc(n1 * n1 * (z1 - z0), c->ctx.stream);
     try {
+      gr->g.alloc(n1 * n1 * (z1 - z0), c->ctx.stream);
       pcu::udf_run(c->ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, mode, eps, gr->g.get(), z0, z1);
     } catch (...) {
       delete gr;
@@ -424,11 +461,11 @@ int pamopt_cu_grid_copy_to_device(pamopt_cu_grid gr, void* dst) {
 int pamopt_cu_grid_from_device(pamopt_cu_ctx c, int32_t R, const float* src, pamopt_cu_grid* out) {
   return guarded([&] {
     check_ctx(c);
-    PCU_REQUIRE(R >= 8 && R <= 2048 && (R & (R - 1)) == 0 && src && out, PAMOPT_CU_EINVAL, "bad arguments");
+    PCU_REQUIRE(R >= 8 && R <= 1024 && (R & (R - 1)) == 0 && src && out, PAMOPT_CU_EINVAL, "bad arguments (R: power of two in [8, 1024])");
     pcu::DeviceGuard g(c->ctx.device);
     auto* gr = new pamopt_cu_grid_s();
     gr->owner = c;
-    ++c->refs;
+    ctx_ref(c);
     gr->R = R;
     gr->z0 = 0;
     gr->z1 = R + 1;
@@ -443,12 +480,12 @@ static int grid_slab_make(pamopt_cu_ctx c, int32_t R, int32_t z0, int32_t z1, co
                           pamopt_cu_grid* out) {
   return guarded([&] {
     check_ctx(c);
-    PCU_REQUIRE(R >= 8 && R <= 2048 && (R & (R - 1)) == 0 && src && out, PAMOPT_CU_EINVAL, "bad arguments");
+    PCU_REQUIRE(R >= 8 && R <= 1024 && (R & (R - 1)) == 0 && src && out, PAMOPT_CU_EINVAL, "bad arguments (R: power of two in [8, 1024])");
     PCU_REQUIRE(0 <= z0 && z0 < z1 && z1 <= R + 1, PAMOPT_CU_EINVAL, "slab planes must satisfy 0 <= z0 < z1 <= R+1");
     pcu::DeviceGuard g(c->ctx.device);
     auto* gr = new pamopt_cu_grid_s();
     gr->owner = c;
-    ++c->refs;
+    ctx_ref(c);
     gr->R = R;
     gr->z0 = z0;
     gr->z1 = z1;
@@ -474,7 +511,7 @@ int pamopt_cu_grid_slab_upload(pamopt_cu_ctx c, int32_t R, int32_t z0, int32_t z
 static pamopt_cu_mesh mesh_from_ingest(pamopt_cu_ctx c, pcu::IngestResult& r) {
   auto* m = new pamopt_cu_mesh_s();
   m->owner = c;
-  ++c->refs;
+  ctx_ref(c);
   m->nv = r.nv;
   m->nf = r.nf;
   m->V = std::move(r.V);
@@ -677,7 +714,7 @@ int pamopt_cu_grid_upload(pamopt_cu_ctx c, int32_t R, const float* samples, pamo
     pcu::DeviceGuard g(c->ctx.device);
     auto* gr = new pamopt_cu_grid_s();
     gr->owner = c;
-    ++c->refs;
+    ctx_ref(c);
     gr->R = R;
     gr->z0 = 0;
     gr->z1 = R + 1;
@@ -725,6 +762,7 @@ int pamopt_cu_hierarchy_pairs(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int3
     check_ctx(c);
     PCU_REQUIRE(m && n, PAMOPT_CU_EINVAL, "null argument");
     pcu::DeviceGuard g(c->ctx.device);
+    validate(c->ctx, m);
     const std::vector<int64_t> h = pcu::hierarchy_pairs(c->ctx, m->V.get(), m->F.get(), m->nf, R, r);
     *n = static_cast<int64_t>(h.size() / 2);
     if (pairs) std::memcpy(pairs, h.data(), std::min<int64_t>(cap, *n) * 2 * sizeof(int64_t));
@@ -743,7 +781,7 @@ int pamopt_cu_dmc_extract(pamopt_cu_grid gr, double beta, pamopt_cu_mesh* out) {
     pcu::dmc_extract(ctx, gr->g.get(), gr->R, beta, gr->last);
     auto* m = new pamopt_cu_mesh_s();
     m->owner = gr->owner;
-    ++gr->owner->refs;
+    ctx_ref(gr->owner);
     m->nv = static_cast<int64_t>(gr->last.nv);
     m->nf = static_cast<int64_t>(gr->last.nf);
     m->V = std::move(gr->last.V);
@@ -763,7 +801,7 @@ int pamopt_cu_dmc_extract_slab(pamopt_cu_grid gr, int32_t own_z0, int32_t own_z1
     pcu::dmc_extract_slab(ctx, gr->g.get(), gr->R, gr->z0, gr->z1, own_z0, own_z1, beta, gr->last);
     auto* m = new pamopt_cu_mesh_s();
     m->owner = gr->owner;
-    ++gr->owner->refs;
+    ctx_ref(gr->owner);
     m->nv = static_cast<int64_t>(gr->last.nv);
     m->nf = static_cast<int64_t>(gr->last.nf);
     m->V = std::move(gr->last.V);
@@ -788,11 +826,6 @@ int pamopt_cu_mesh_rebase(pamopt_cu_mesh m, int64_t patch_base, int64_t nvp_own,
 // ------------------------------------------------------------ certification / metrics
 static constexpr uint64_t kSeedB = 0x632BE59BD9B4E019ull;
 
-static void check_indices(pcu::Ctx& ctx, const pamopt_cu_mesh_s* m) {
-  if (m->nf == 0) return;
-  const std::vector<int32_t> mm = pcu::index_range(ctx, m->F.get(), 3 * m->nf);
-  PCU_REQUIRE(mm[0] >= 0 && mm[1] < m->nv, PAMOPT_CU_EINVAL, "invalid mesh: face index out of range");
-}
 
 int pamopt_cu_analyze_topology(pamopt_cu_mesh m, pamopt_cu_topology* out, int32_t* edges, int64_t cap_e,
                                int32_t* verts, int64_t cap_v) {
@@ -1033,6 +1066,7 @@ int pamopt_cu_self_intersections(pamopt_cu_mesh m, int32_t* pairs, int64_t cap, 
     PCU_REQUIRE(m && n, PAMOPT_CU_EINVAL, "null argument");
     pcu::Ctx& ctx = m->owner->ctx;
     pcu::DeviceGuard g(ctx.device);
+    check_indices(ctx, m);
     const std::vector<int32_t> h = pcu::self_intersections(ctx, m->V.get(), m->nv, m->F.get(), m->nf, nullptr, nullptr);
     *n = static_cast<int64_t>(h.size() / 2);
     if (pairs) std::memcpy(pairs, h.data(), std::min<int64_t>(cap, *n) * 2 * sizeof(int32_t));
@@ -1047,6 +1081,7 @@ int pamopt_cu_tri_tri_pairs(pamopt_cu_mesh m, const int32_t* pairs, int64_t n, i
     pcu::DeviceGuard g(ctx.device);
     for (int64_t i = 0; i < 2 * n; ++i)
       PCU_REQUIRE(pairs[i] >= 0 && pairs[i] < m->nf, PAMOPT_CU_EINVAL, "face index out of range");
+    check_indices(ctx, m);
     pcu::DevBuf<int32_t> dp(2 * n, ctx.stream), dout(n, ctx.stream);
     PCU_CUDA(cudaMemcpyAsync(dp.get(), pairs, 2 * n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx.stream));
     pcu::tri_tri_pairs(ctx, m->V.get(), m->F.get(), dp.get(), n, dout.get());
@@ -1087,6 +1122,7 @@ int pamopt_cu_simplify(pamopt_cu_mesh m, int64_t target, const pamopt_cu_simplif
     const pcu::SimplifyParams P = to_params(params);
     pcu::Ctx& ctx = m->owner->ctx;
     pcu::DeviceGuard g(ctx.device);
+    validate(ctx, m);
     pcu::SimplifyStats S;
     pcu::simplify_run(ctx, m->V, m->F, m->nv, m->nf, target, P, S);
     PCU_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -1107,10 +1143,19 @@ static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double ep
   const double lo = 0.8660254037844386 / R, hi = 3.0 / R - 0.8660254037844386 / R;
   PCU_REQUIRE(eps >= lo && eps <= hi, PAMOPT_CU_EINVAL, "udf_to_sdf: epsilon out of range");
   const pcu::SimplifyParams P = to_params(params);
+  PCU_REQUIRE(in->owner == c, PAMOPT_CU_EINVAL, "mesh belongs to another context");
   pcu::Ctx& ctx = c->ctx;
   pcu::DeviceGuard g(ctx.device);
-  cudaEvent_t ev[4];
-  for (auto& e : ev) PCU_CUDA(cudaEventCreate(&e));
+  validate(ctx, in);
+  struct Events {  // destroyed on every exit path, including a throw from a stage
+    cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+    ~Events() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } evs;
+  cudaEvent_t* ev = evs.e;
+  for (int i = 0; i < 4; ++i) PCU_CUDA(cudaEventCreate(&ev[i]));
   PCU_CUDA(cudaEventRecord(ev[0], ctx.stream));
   const int64_t n1 = R + 1;
   pcu::DevBuf<float> sdf(n1 * n1 * n1, ctx.stream);
@@ -1122,7 +1167,7 @@ static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double ep
   PCU_CUDA(cudaEventRecord(ev[2], ctx.stream));
   auto* m = new pamopt_cu_mesh_s();
   m->owner = c;
-  ++c->refs;
+  ctx_ref(c);
   m->nv = static_cast<int64_t>(d.nv);
   m->nf = static_cast<int64_t>(d.nf);
   m->V = std::move(d.V);
@@ -1145,7 +1190,6 @@ static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double ep
     times->dmc_faces = static_cast<int64_t>(d.nf);
     times->dmc_vertices = static_cast<int64_t>(d.nv);
   }
-  for (auto& e : ev) cudaEventDestroy(e);
   to_stats(S, stats);
   *out = m;
 }

@@ -457,7 +457,7 @@ void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, 
                       DmcResult& res) {
   upload_table(ctx.device);
   const int cz0 = own_z0 > 0 ? own_z0 - 1 : 0;  // the layer below lends its patch-vertex ids
-  PCU_REQUIRE(R >= 2 && own_z0 >= 0 && own_z0 < own_z1 && own_z1 <= R, PAMOPT_CU_EINVAL,
+  PCU_REQUIRE(R >= 2 && R <= 1024 && own_z0 >= 0 && own_z0 < own_z1 && own_z1 <= R, PAMOPT_CU_EINVAL,
               "dmc slab: own cell layers must satisfy 0 <= z0 < z1 <= R");
   PCU_REQUIRE(pz0 <= std::max(own_z0 - 2, 0) && pz1 >= std::min(own_z1 + 2, R + 1) && pz0 >= 0 && pz1 <= R + 1,
               PAMOPT_CU_EINVAL, "dmc slab: resident planes must cover [z0-2, z1+2) clipped to the lattice");
@@ -539,6 +539,7 @@ void mesh_rebase(Ctx& ctx, int32_t* dF, int64_t nidx, int64_t patch_base, int64_
 }
 
 void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res) {
+  PCU_REQUIRE(R >= 2 && R <= 1024, PAMOPT_CU_EINVAL, "extract: R must be <= 1024 (32-bit cell ids)");
   dmc_extract_slab(ctx, d_sdf, R, 0, R + 1, 0, R, beta, res);
 }
 

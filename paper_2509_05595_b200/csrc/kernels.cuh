@@ -54,6 +54,8 @@ void directed_d2(Ctx& ctx, const double* Va, const int32_t* Fa, int64_t nfa, con
                  int64_t nfb, int64_t n, uint64_t seed, double& sum_d2, double& max_d2, double& area_a);
 double max_corner_cos(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf);
 std::vector<int32_t> index_range(Ctx& ctx, const int32_t* d, int64_t n);  // {min, max}
+// IndexedMesh::validate (mesh.cpp:31-43): throws EINVAL naming the first invalid face
+void validate_mesh(Ctx& ctx, const int32_t* dF, int64_t nf, int64_t nv);
 
 // ---- stage 3: safe projection (project.cu, SPEC.md safe_project)
 struct ProjectParams {

@@ -10,6 +10,8 @@
 //     Hausdorff and the minimum internal angle (SPEC quality_metrics).
 #include <cub/cub.cuh>
 
+#include <string>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -672,6 +674,44 @@ void directed_d2(Ctx& ctx, const double* Va, const int32_t* Fa, int64_t nfa, con
   sum_d2 = 0.0;
   for (double x : hp) sum_d2 += x;
   std::memcpy(&max_d2, &hm, 8);
+}
+
+// IndexedMesh::validate (mesh.cpp:31-43): the first face (lowest id) that references a vertex
+// outside [0, nv) or repeats an index.  key = f << 2 | reason (1 = out of range, 2 = repeated),
+// reduced with one 64-bit atomicMin, so the reported face is the reference's first offender.
+__global__ void k_validate(const int32_t* __restrict__ F, int64_t nf, int64_t nv, unsigned long long* __restrict__ key) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nf) return;
+  const int32_t a = F[3 * f], b = F[3 * f + 1], c = F[3 * f + 2];
+  const bool range = a < 0 || a >= nv || b < 0 || b >= nv || c < 0 || c >= nv;
+  const bool rep = a == b || b == c || a == c;
+  if (range || rep) atomicMin(key, (static_cast<unsigned long long>(f) << 2) | (range ? 1ull : 2ull));
+}
+
+void validate_mesh(Ctx& ctx, const int32_t* dF, int64_t nf, int64_t nv) {
+  if (nf <= 0) return;
+  DevBuf<unsigned long long> k(1, ctx.stream);
+  PCU_CUDA(cudaMemsetAsync(k.get(), 0xFF, 8, ctx.stream));
+  PCU_LAUNCH(ctx, k_validate, grid_for(nf, 256), 256, 0, dF, nf, nv, k.get());
+  const unsigned long long key = read_scalar(ctx, k.get());
+  if (key == ~0ull) return;
+  const int64_t f = static_cast<int64_t>(key >> 2);
+  int32_t t[3];
+  PCU_CUDA(cudaMemcpyAsync(t, dF + 3 * f, sizeof(t), cudaMemcpyDeviceToHost, ctx.stream));
+  PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  std::string msg = "invalid mesh: face " + std::to_string(f);
+  if ((key & 3) == 1) {
+    int32_t bad = t[0];
+    for (int i = 0; i < 3; ++i)
+      if (t[i] < 0 || t[i] >= nv) {
+        bad = t[i];
+        break;
+      }
+    msg += " references vertex " + std::to_string(bad);
+  } else {
+    msg += " has repeated vertex indices";
+  }
+  throw Error(PAMOPT_CU_EINVAL, msg);
 }
 
 std::vector<int32_t> index_range(Ctx& ctx, const int32_t* d, int64_t n) {

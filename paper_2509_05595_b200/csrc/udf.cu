@@ -597,7 +597,7 @@ void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t 
   if (z1 < 0) z1 = R + 1;
   PCU_REQUIRE(z0 >= 0 && z0 < z1 && z1 <= R + 1, PAMOPT_CU_EINVAL, "compute_udf: bad slab plane range");
   (void)nv;
-  PCU_REQUIRE(R >= 8 && (R & (R - 1)) == 0 && R <= 2048, PAMOPT_CU_EINVAL, "compute_udf: R must be a power of two in [8, 2048]");
+  PCU_REQUIRE(R >= 8 && (R & (R - 1)) == 0 && R <= 1024, PAMOPT_CU_EINVAL, "compute_udf: R must be a power of two in [8, 1024]");
   const int rb = R >= 64 ? R / 8 : 8;
   const int bs = R / rb, J = ilog2(bs);
   const int64_t n1 = R + 1;
