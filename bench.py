@@ -13,7 +13,7 @@ collective; the timing is the max over ranks and `value` = whole-job ms per mesh
 `e2e`:   the same metric through pamopt_cu_remesh_host (host arrays in pinned memory, the
          H2D copy and the D2H read of the result inside the timed region).
 `--impl reference`: the CPU implementation of the path (the oracle port of the reference's
-         algorithm, all host threads), a bounded sample per step scaled to ms per mesh.
+         algorithm, all host threads): one complete measured remesh of the same workload.
 """
 from __future__ import annotations
 
@@ -102,85 +102,55 @@ class Clocks:
                 "samples": len(sm)}
 
 
-# ------------------------------------------------------------------ CPU (oracle) estimate
-_C1_CACHE = {}
-
-
-def cpu_estimate(v, f, R, target, sdf_host, face_iterations_target):
-    """Bounded-sample CPU time of the reference algorithm (oracle port, all host threads),
-    scaled to ms per mesh.  Returns (ms, sample description, cores)."""
+# ------------------------------------------------------------------ CPU (oracle) baseline
+def cpu_full(v, f, R, target):
+    """One complete, measured CPU remesh of the workload by the oracle port of the reference
+    algorithm on every host core: the full UDF (all triangles), the full DMC extraction and the
+    full QEM run to the target (every iteration, every undo round).  Nothing is sampled or
+    scaled.  Returns (ms, stage seconds, cores, faces_out, qem iterations)."""
     from oracle import pyoracle as O
     cores = os.cpu_count() or 1
     O.set_workers(cores)
-    # UDF: every 100th triangle (per-triangle work scales linearly) + the dense grid pass
-    step = 100
-    sub = np.ascontiguousarray(f[::step])
     t0 = time.perf_counter()
-    O.compute_udf_sdf(v, sub, R)
-    t_sub = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    O.compute_udf_sdf(v, f[:1], R)
-    t_grid = time.perf_counter() - t0
-    t_udf = max(t_sub - t_grid, 0.0) * (len(f) / len(sub)) + t_grid
-    # DMC: full extraction of the (bit-identical) SDF grid
-    t0 = time.perf_counter()
-    O.dmc_extract(sdf_host, R)
-    t_dmc = time.perf_counter() - t0
-    # QEM: per face-iteration cost measured on the C1 DMC mesh, scaled by this run's work
-    if "c1" not in _C1_CACHE:
-        from paper_2509_05595_b200 import fixtures as FX
-        v1, f1, R1, t1 = FX.make_config("c1")
-        _, sdf1 = O.compute_udf_sdf(v1, f1, R1)
-        d1 = O.dmc_extract(sdf1, R1)
-        _C1_CACHE["c1"] = (d1["vertices"], d1["faces"], t1)
-    dv, df, t1 = _C1_CACHE["c1"]
-    t0 = time.perf_counter()
-    _, _, st = O.simplify(dv, df, t1)
-    t_c1 = time.perf_counter() - t0
-    per_fi = t_c1 / max(st["face_iterations"], 1)
-    t_qem = per_fi * face_iterations_target
-    ms = 1e3 * (t_udf + t_dmc + t_qem)
-    sample = (f"UDF on every {step}th triangle ({len(sub)} tris, scaled x{len(f) / len(sub):.0f}) + dense grid "
-              f"pass; DMC full {R}^3; QEM cost/face-iteration from the C1 DMC mesh ({len(df)} faces, "
-              f"{st['face_iterations']} face-iterations, {t_c1:.2f} s) x {face_iterations_target} face-iterations; "
-              f"stages s: udf {t_udf:.2f} dmc {t_dmc:.2f} qem {t_qem:.2f}")
-    return ms, sample, cores
+    _, sdf = O.compute_udf_sdf(v, f, R)
+    t1 = time.perf_counter()
+    d = O.dmc_extract(sdf, R)
+    del sdf
+    t2 = time.perf_counter()
+    _, fo, st = O.simplify(d["vertices"], d["faces"], target)
+    t3 = time.perf_counter()
+    stages = {"udf": round(t1 - t0, 3), "dmc": round(t2 - t1, 3), "qem": round(t3 - t2, 3)}
+    return 1e3 * (t3 - t0), stages, cores, int(len(fo)), int(st["iterations"])
 
 
-# QEM work units (sum over iterations of the alive face count) of each config.  The GPU path and
-# the oracle run the identical iteration sequence (bit-exact, tests/), so this is a property of
-# the workload: C1/C2 from the oracle's own simplify, C3 from the GPU run and checked by
-# tests/test_gpu_full_size.py.
-FACE_ITERATIONS = {"c1": 3_164_164, "c2": 29_291_110, "c3": 93_079_828}
+def cpu_baseline_entry(v, f, R, target, name):
+    ms, stages, cores, nf_out, iters = cpu_full(v, f, R, target)
+    return {"value": round(ms, 1), "unit": "ms/mesh", "cores": cores, "kind": "port",
+            "sample": (f"one complete {name.upper()} remesh on the host (no sampling, no scaling): UDF of all "
+                       f"{len(f)} triangles at R={R}, full DMC, full QEM to {target} faces ({iters} iterations, "
+                       f"{nf_out} faces out, the same as the GPU run); measured stage seconds {stages}"),
+            "stage_seconds": stages}
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
-    """CPU-only: the oracle port of the reference algorithm on all host cores (no GPU code)."""
+    """CPU-only: the oracle port of the reference algorithm on all host cores (no GPU code).
+    One complete measured remesh per invocation: a C3 pass is ~1.5-3 min of host time, so the
+    driver's --steps/--warmup are not repeated (the line reports steps=1, warmup=0)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import pyoracle as O
     v, f, R, target = workload(args.config)
-    O.set_workers(os.cpu_count() or 1)
-    _, sdf = O.compute_udf_sdf(v, f, R)  # the DMC sample's input, computed once outside the steps
-    fi = FACE_ITERATIONS[args.config]
-    for _ in range(args.warmup):
-        cpu_estimate(v, f, R, target, sdf, fi)
-    times = []
-    sample, cores = "", 1
-    for _ in range(args.steps):
-        ms, sample, cores = cpu_estimate(v, f, R, target, sdf, fi)
-        times.append(ms)
-    val = float(np.mean(times))
-    line = {"metric": "end-to-end remesh ms per mesh (UDF+DMC+QEM)", "value": round(val, 3), "unit": "ms/mesh",
-            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(val, 3), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+    cpu = cpu_baseline_entry(v, f, R, target, args.config)
+    val = cpu["value"]
+    line = {"metric": "end-to-end remesh ms per mesh (UDF+DMC+QEM)", "value": val, "unit": "ms/mesh",
+            "impl": "reference", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+            "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": val, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config.upper(), "faces_in": int(len(f)), "R": R, "target_faces": target},
-            "cpu_baseline": {"value": round(val, 3), "unit": "ms/mesh", "cores": cores, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": round(val, 3), "unit": "ms/mesh", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": cpu,
+            "e2e": {"value": val, "unit": "ms/mesh", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -320,10 +290,7 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu:
             try:
-                g = api.compute_sdf(mesh, R)
-                sdf = g.download()
-                ms_cpu, sample, cores = cpu_estimate(v, f, R, target, sdf, st["face_iterations"])
-                cpu = {"value": round(ms_cpu, 2), "unit": "ms/mesh", "cores": cores, "kind": "port", "sample": sample}
+                cpu = cpu_baseline_entry(v, f, R, target, args.config)
             except Exception as e:  # the checker is optional on the bench line; never the measured path
                 cpu = {"value": None, "unit": "ms/mesh", "cores": os.cpu_count(), "kind": "port",
                        "sample": f"unavailable: {e}"}

@@ -25,6 +25,9 @@
 //   stop      alive faces <= target, or 10 consecutive iterations without a collapse
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -295,8 +298,27 @@ struct Stats {
   int error = 0;
 };
 
+// ORC_PROFILE=1: per-phase wall seconds on stderr (diagnostics of the CPU baseline only)
+struct PhaseTimer {
+  bool on = std::getenv("ORC_PROFILE") != nullptr;
+  double t[10] = {0};
+  std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  void mark(int i) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    t[i] += std::chrono::duration<double>(now - last).count();
+    last = now;
+  }
+  ~PhaseTimer() {
+    if (on)
+      std::fprintf(stderr, "orc simplify s: incidence %.2f edges %.2f cost %.2f mark %.2f link %.2f collapse %.2f "
+                   "detect %.2f revert %.2f flags %.2f\n", t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], t[8]);
+  }
+};
+
 static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
                 std::vector<int64_t>* per_iter_collapses) {
+  PhaseTimer T;
   // initial quadrics, gathered in ascending face id
   m.Q.assign(m.nv, Quadric{});
   for (auto& q : m.Q) std::fill(q.q, q.q + 10, 0.0);
@@ -314,7 +336,9 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
   while (m.alive_faces > target && zero_run < P.stall) {
     S.iterations++;
     S.face_iterations += m.alive_faces;
+    T.mark(8);
     const Incidence I = build_incidence(m);
+    T.mark(0);
     // edges in lexicographic order
     // (per vertex: sorted unique upper neighbours, counted then written at scanned offsets)
     auto upper = [&](int64_t v, std::vector<int32_t>& nb) {
@@ -346,6 +370,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
         for (size_t i = 0; i < nb.size(); ++i) edges[eoff[v] + i] = {static_cast<int32_t>(v), nb[i]};
       }
     }, 1);
+    T.mark(1);
     const int64_t ne = static_cast<int64_t>(edges.size());
     std::vector<uint64_t> key(ne, ~0ull);
     std::vector<V3> place(ne);
@@ -372,6 +397,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
       S.error = 1;
       return;
     }
+    T.mark(2);
     std::vector<uint64_t> vmin(m.nv, ~0ull), vfmin(m.nv, ~0ull);
     for (int64_t e = 0; e < ne; ++e) {
       if (!valid[e]) continue;
@@ -388,11 +414,13 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
     for (int64_t e = 0; e < ne; ++e)
       if (valid[e] && key[e] == vfmin[edges[e].first] && key[e] == vfmin[edges[e].second])
         marked.push_back(e);
+    T.mark(3);
     // link condition on the pre-batch mesh
     std::vector<uint8_t> pass(marked.size());
     parallel_for(static_cast<int64_t>(marked.size()), [&](int64_t i) {
       pass[i] = link_condition(m, I, edges[marked[i]].first, edges[marked[i]].second) ? 1 : 0;
     }, 64);
+    T.mark(4);
     std::set<std::pair<int, int>> new_invalid;
     std::vector<int64_t> sel;
     for (size_t i = 0; i < marked.size(); ++i) {
@@ -459,6 +487,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
       std::sort(C.owned.begin(), C.owned.end());
       for (int f : C.owned) owner[f] = static_cast<int32_t>(ci);
     }
+    T.mark(5);
     // undo loop
     int rounds = 0;
     while (true) {
@@ -472,6 +501,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
           }
       if (!any) break;
       const auto pairs = detect_pairs(m.X.data(), m.F.data(), m.nf, m.falive.data(), query.data());
+      T.mark(6);
       if (pairs.empty()) break;
       ++rounds;
       std::vector<uint8_t> revert(cols.size(), 0);
@@ -500,6 +530,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
         S.undone++;
       }
     }
+    T.mark(7);
     S.undo_hist[std::min(rounds, 7)]++;
     S.max_undo_rounds = std::max<int64_t>(S.max_undo_rounds, rounds);
     int64_t succ = 0;

@@ -250,6 +250,20 @@ def inject_defects(v, f, seed: int, dup=0.01, holes=0.005, flipped=0.005, pokes=
     return np.concatenate(vs), np.concatenate(fs).astype(np.int32)
 
 
+def nested_shells(subdiv: int, gap: float, k: int, seed: int):
+    """k concentric noisy icospheres 1 + i*gap apart (alternating orientation): a thin-wall
+    fixture on which collapses poke through the neighbouring wall, so undo loops
+    need 2-3 rounds."""
+    v, f = icosphere(subdiv)
+    rng = Rng(seed)
+    n = len(v)
+    vs, fs = [], []
+    for i in range(k):
+        vs.append(v * (1.0 + i * gap + 0.1 * gap * rng.normal(n))[:, None])
+        fs.append((f[:, ::-1] if i % 2 == 0 else f) + i * n)
+    return np.concatenate(vs), np.concatenate(fs).astype(np.int32)
+
+
 def normalize_unit_cube(v: np.ndarray, padding: float):
     """mesh_io.cpp:393-408: uniform scale into [padding, 1-padding]^3, centred."""
     if not (0 <= padding < 0.5):

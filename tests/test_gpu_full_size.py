@@ -1,8 +1,9 @@
 """Full BASELINE sizes (C3: 1M-triangle soup at R=512; C4: 5.24M triangles at R=1024).
 C3 UDF/SDF and DMC are compared with the oracle bit for bit (the oracle needs ~30 s of host
-cores here); QEM at full size is checked through size-independent properties: the output is
+cores here); QEM at full size is compared with the oracle's recorded run in
+tests/test_gpu_qem_parity.py, and checked here through size-independent properties: the output is
 manifold, watertight and self-intersection free, the link condition preserved the Euler
-characteristic of the DMC surface, the face budget is met, and reruns are identical.  C4 checks
+characteristic of the DMC surface, and reruns are identical.  C4 checks
 that the z-slab decomposition (SDF slabs and slab-local DMC) reproduces the whole-grid result."""
 import numpy as np
 import pytest
@@ -42,9 +43,14 @@ def test_c3_qem_properties(api, c3):
     assert t0["manifold"] and t0["watertight"]
     out, st, tm = api.remesh_device(m, R, target)
     ov, of = out.download()
-    assert target <= len(of) <= target + 200 and st["iterations"] < 1000
-    import bench
-    assert st["face_iterations"] == bench.FACE_ITERATIONS["c3"]  # the reference arm's work units
+    # face count and work units exactly as the oracle's run (tests/golden/ref_qem_c3.json): the
+    # stall rule ends both at the same count above the target
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_qem_c3.json")) as fh:
+        g = json.load(fh)
+    assert len(of) == g["nf_out"] and st["iterations"] == g["iterations"]
+    assert st["face_iterations"] == g["face_iterations"]
     t1 = api.analyze_topology(out)
     assert t1["manifold"] and t1["watertight"] and t1["euler"] == t0["euler"]
     assert len(api.detect_self_intersections(out)) == 0
