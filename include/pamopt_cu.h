@@ -38,7 +38,7 @@ extern "C" {
 #define PAMOPT_CU_ECUDA -2    /* CUDA runtime failure */
 #define PAMOPT_CU_ENOMEM -3   /* device allocation failure */
 #define PAMOPT_CU_ENUMERIC -4 /* NaN edge cost */
-#define PAMOPT_CU_ECAP -5     /* a fixed per-element capacity was exceeded (valence > 255) */
+#define PAMOPT_CU_ECAP -5     /* reserved (no fixed per-element capacity remains) */
 
 typedef struct pamopt_cu_ctx_s* pamopt_cu_ctx;
 typedef struct pamopt_cu_mesh_s* pamopt_cu_mesh;
@@ -168,11 +168,40 @@ int pamopt_cu_dmc_active_cells(pamopt_cu_grid sdf, int64_t* cells, uint8_t* case
 /* the 256-entry patch table: per case {n, mask0..3, doubly-covered faces} (int32[256*6]) */
 int pamopt_cu_dmc_table(int32_t* out);
 
+/* SPEC-granular dual_mc operations.  pamopt_cu_dmc_stages runs classify_voxels
+ * + build_patches + build_quads on a whole grid and keeps the views on the grid handle:
+ * counts = {n_active, n_patch_vertices, n_quads}. */
+int pamopt_cu_dmc_stages(pamopt_cu_grid sdf, double beta, int64_t counts[3]);
+/* build_patches view: patch vertices double[3 n_patch_vertices] in (active cell, patch) order and
+ * the first patch vertex of every active cell, int64[n_active]; either may be NULL */
+int pamopt_cu_dmc_build_patches(pamopt_cu_grid sdf, double* vertices, int64_t* patch_first);
+/* build_quads view, one quad per valid interior grid edge in output order: quads int32[4 n]
+ * (patch-vertex ids, oriented negative -> positive), edges int64[n] = lower lattice vertex
+ * linear index * 3 + axis, samples float[2 n] at the edge's lower / upper vertex, split uint8[n]
+ * = triangulate_quads' decision (1 diagonal 0-2, 2 diagonal 1-3, 3 four triangles) */
+int pamopt_cu_dmc_build_quads(pamopt_cu_grid sdf, int32_t* quads, int64_t* edges, float* samples, uint8_t* split);
+/* triangulate_quads on explicit quads: out mesh V = [patch vertices, the
+ * extra 4-split vertices in quad order], faces in quad order (== extract for build_quads' output) */
+int pamopt_cu_triangulate_quads(pamopt_cu_ctx ctx, int32_t R, const double* patch_vertices, int64_t n_vertices,
+                                const int32_t* quads, const int64_t* edges, const float* samples, int64_t n_quads,
+                                double beta, pamopt_cu_mesh* out);
+/* interpolate_patch_vertex for n edges: p0, p1 double[3n], f0, f1 float[n] ->
+ * out double[3n]; PAMOPT_CU_EINVAL if some f0, f1 do not change sign (those outputs are 0) */
+int pamopt_cu_interpolate_patch_vertex(pamopt_cu_ctx ctx, const double* p0, const double* p1, const float* f0,
+                                       const float* f1, int64_t n, double beta, double* out);
+
 /* ---- tri_isect ------------------------------------------------------------------------ */
 /* all intersecting face pairs (f1<f2), sorted; pairs = int32[2*n] or NULL */
 int pamopt_cu_self_intersections(pamopt_cu_mesh mesh, int32_t* pairs, int64_t cap, int64_t* n);
 /* narrow-phase verdict for explicit face pairs (host arrays) */
 int pamopt_cu_tri_tri_pairs(pamopt_cu_mesh mesh, const int32_t* pairs, int64_t n, int32_t* out);
+/* classify_pair: shared-vertex count by index (3 = duplicate face) and the
+ * exact coplanarity flag (a degenerate face counts as coplanar); either output may be NULL */
+int pamopt_cu_classify_pair(pamopt_cu_mesh mesh, const int32_t* pairs, int64_t n, int32_t* shared, int32_t* coplanar);
+/* intersect_3d / intersect_coplanar for pairs of that class:
+ * out int32[n] = 1/0; PAMOPT_CU_EINVAL if some pair violates the class precondition (out -1) */
+int pamopt_cu_intersect_3d(pamopt_cu_mesh mesh, const int32_t* pairs, int64_t n, int32_t* out);
+int pamopt_cu_intersect_coplanar(pamopt_cu_mesh mesh, const int32_t* pairs, int64_t n, int32_t* out);
 
 /* ---- stage 2: simplify ---------------------------------------------------------------- */
 /* in place; on success the mesh is compacted (mesh.cpp:278-292).  PAMOPT_CU_EINVAL for a
@@ -180,6 +209,52 @@ int pamopt_cu_tri_tri_pairs(pamopt_cu_mesh mesh, const int32_t* pairs, int64_t n
 int pamopt_cu_simplify(pamopt_cu_mesh mesh, int64_t target_faces,
                        const pamopt_cu_simplify_params* params, pamopt_cu_simplify_stats* stats,
                        int64_t* per_iter_collapses, int64_t per_iter_cap);
+
+/* ---- stage 2, SPEC-granular operations ------------------------------ */
+/* Quadric per vertex, area-weighted unit-plane quadrics gathered in ascending
+ * face id: out double[10 nv] = {xx, xy, xz, xw, yy, yz, yw, zz, zw, ww} */
+int pamopt_cu_quadrics(pamopt_cu_mesh mesh, double* out);
+/* edge_cost of n explicit edges (int32[2n]) under the mesh's quadrics:
+ * cost double[n], placement double[3n] (adjugate solve or the {mid, a, b} fallback, P8) */
+int pamopt_cu_edge_cost(pamopt_cu_mesh mesh, const int32_t* edges, int64_t n, double w_e, double w_s, double* cost,
+                        double* placement);
+/* pack_cost: key = f32 bits(max(cost, 0)) << 32 | id; PAMOPT_CU_ENUMERIC if any
+ * cost is NaN (the keys of the other entries are still written) */
+int pamopt_cu_pack_cost(pamopt_cu_ctx ctx, const double* cost, const uint32_t* edge_ids, int64_t n, uint64_t* keys);
+/* HalfEdgeAdjacency::link_condition_holds (mesh.cpp:301-358) for n edges: out int32[n] = 1/0;
+ * PAMOPT_CU_EINVAL (std::invalid_argument, mesh.cpp:302) if a pair is not an edge of the mesh,
+ * out[i] = -1 for it.  Unbounded valence. */
+int pamopt_cu_link_condition(pamopt_cu_mesh mesh, const int32_t* edges, int64_t n, int32_t* out);
+
+/* Algorithm 1 one step at a time on a device mesh (simplified in place; the mesh handle must
+ * outlive the state).  Per iteration, in order: prepare (edges + edge_cost + pack_cost),
+ * propagate_and_mark, collapse_batch, undo_loop, end_iteration; qem_finish compacts the mesh.
+ * pamopt_cu_simplify is exactly this loop.  Calls out of order -> PAMOPT_CU_EINVAL. */
+typedef struct pamopt_cu_qem_s* pamopt_cu_qem;
+int pamopt_cu_qem_create(pamopt_cu_mesh mesh, int64_t target_faces, const pamopt_cu_simplify_params* params,
+                         pamopt_cu_qem* out);
+/* 1 when simplify_to's loop would stop: alive faces <= target, or the stall rule */
+int pamopt_cu_qem_done(pamopt_cu_qem q, int32_t* done);
+int pamopt_cu_qem_prepare(pamopt_cu_qem q, int64_t* n_edges);
+/* this iteration's edges (lexicographic ids, P5): int32[2 ne]; keys uint64[ne] (~0 = invalid
+ * edge); placements double[3 ne]; valid uint8[ne]; any output may be NULL */
+int pamopt_cu_qem_edges(pamopt_cu_qem q, int32_t* edges, uint64_t* keys, double* placements, uint8_t* valid,
+                        int64_t cap);
+int pamopt_cu_qem_propagate_and_mark(pamopt_cu_qem q, int64_t* n_marked);
+/* marked (independent) edges in ascending key order; face_keys = per face slot min key (~0 for
+ * a dead face), uint64[nf] with nf from pamopt_cu_qem_mesh; either may be NULL */
+int pamopt_cu_qem_marked(pamopt_cu_qem q, uint32_t* edge_ids, int64_t cap, uint64_t* face_keys, int64_t cap_faces);
+/* link condition + overshoot trim + parallel collapse; link_ok uint8[n_marked] (key order) */
+int pamopt_cu_qem_collapse_batch(pamopt_cu_qem q, uint8_t* link_ok, int64_t cap);
+/* detect -> revert -> repeat; applied uint8[n_marked] = collapse still applied (key order) */
+int pamopt_cu_qem_undo_loop(pamopt_cu_qem q, int32_t* rounds, int64_t* n_applied, uint8_t* applied, int64_t cap);
+int pamopt_cu_qem_end_iteration(pamopt_cu_qem q, int64_t* alive_faces);
+/* the working mesh with tombstones (ids stable until compaction): vertices double[3 nv],
+ * faces int32[3 nf], face_alive uint8[nf]; NULL outputs = sizes only */
+int pamopt_cu_qem_mesh(pamopt_cu_qem q, double* vertices, int32_t* faces, uint8_t* face_alive, int64_t* nv,
+                       int64_t* nf);
+int pamopt_cu_qem_finish(pamopt_cu_qem q, pamopt_cu_simplify_stats* stats);
+int pamopt_cu_qem_destroy(pamopt_cu_qem q);
 
 /* ---- certification and quality metrics ---------------------------- */
 /* analyze_topology (mesh.cpp:113-150; TopologySummary mesh.hpp:44-51) */

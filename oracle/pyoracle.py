@@ -56,6 +56,7 @@ def lib():
         L.orc_dmc_patches.argtypes = [C.c_int, C.c_int, i32p]
         L.orc_dmc_extract.argtypes = [f32p, C.c_int, C.c_double, i64p]
         L.orc_dmc_fetch.argtypes = [C.c_void_p] * 5
+        L.orc_dmc_stages.argtypes = [C.c_void_p] * 6
         L.orc_dmc_extract_slab.argtypes = [f32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, i64p]
         L.orc_tri_tri_pairs.argtypes = [f64p, i32p, i32p, C.c_int64, i32p]
         L.orc_orient3d.restype = C.c_int
@@ -68,6 +69,12 @@ def lib():
         L.orc_simplify.argtypes = [f64p, C.c_int64, i32p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int, i64p]
         L.orc_simplify_fetch.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_link_condition.argtypes = [f64p, C.c_int64, i32p, C.c_int64, i32p, C.c_int64, i32p]
+        L.orc_simplify_trace.restype = C.c_int
+        L.orc_simplify_trace.argtypes = [f64p, C.c_int64, i32p, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int,
+                                         C.c_int64, i64p]
+        L.orc_trace_fetch.argtypes = [C.c_void_p] * 10
+        L.orc_quadrics.argtypes = [f64p, C.c_int64, i32p, C.c_int64, f64p]
+        L.orc_edge_cost.argtypes = [f64p, C.c_int64, i32p, C.c_int64, i32p, C.c_int64, C.c_double, C.c_double, f64p, f64p]
         L.orc_topology.argtypes = [i32p, C.c_int64, C.c_int64, i64p]
         L.orc_topology_lists.argtypes = [C.c_void_p, C.c_void_p]
         L.orc_nearest.argtypes = [f64p, i32p, C.c_int64, f64p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -186,8 +193,22 @@ def dmc_extract(sdf, R: int, beta: float = 5.0) -> dict:
     faces = np.empty((nf, 3), np.int32)
     lib().orc_dmc_fetch(cells.ctypes.data, cases.ctypes.data, flips.ctypes.data, verts.ctypes.data,
                         faces.ctypes.data)
-    return dict(cells=cells, cases=cases, flips=flips, vertices=verts, faces=faces,
-                n_quads=int(sizes[3]), n_split4=int(sizes[4]))
+    out = dict(cells=cells, cases=cases, flips=flips, vertices=verts, faces=faces,
+               n_quads=int(sizes[3]), n_split4=int(sizes[4]))
+    # build_patches / build_quads views of the same run
+    st = np.zeros(2, np.int64)
+    lib().orc_dmc_stages(st.ctypes.data, None, None, None, None, None)
+    nq = int(st[1])
+    vbase = np.empty(na, np.int64)
+    quads = np.empty((nq, 4), np.int32)
+    qedge = np.empty(nq, np.int64)
+    qf = np.empty((nq, 2), np.float32)
+    qsplit = np.empty(nq, np.uint8)
+    lib().orc_dmc_stages(st.ctypes.data, vbase.ctypes.data, quads.ctypes.data, qedge.ctypes.data, qf.ctypes.data,
+                         qsplit.ctypes.data)
+    out.update(patch_first=vbase, n_patch_vertices=int(st[0]), quads=quads, quad_edges=qedge, quad_samples=qf,
+               quad_split=qsplit)
+    return out
 
 
 def dmc_extract_slab(planes, R: int, pz0: int, own_z0: int, own_z1: int, beta: float = 5.0) -> dict:
@@ -254,6 +275,44 @@ def simplify(v, f, target: int, we: float = 1e-3, ws: float = 5e-3, tolerance: i
     lib().orc_simplify_fetch(vo.ctypes.data, fo.ctypes.data, per_iter.ctypes.data)
     stats["per_iter_collapses"] = per_iter
     return vo, fo, stats
+
+
+def simplify_trace(v, f, target: int, iteration: int, we: float = 1e-3, ws: float = 5e-3, tolerance: int = 4):
+    """Step-level record of one simplify_to iteration (1-based): edges, keys, placements, face
+    keys, marked edge ids, link results, applied edge ids, undo rounds and the mesh after it."""
+    v, f = _vf(v, f)
+    sz = np.zeros(6, np.int64)
+    rc = lib().orc_simplify_trace(v.ravel(), len(v), f.ravel(), len(f), int(target), we, ws, tolerance,
+                                  int(iteration), sz)
+    if rc < 0:
+        raise ValueError("oracle simplify: NaN edge cost")
+    if rc > 0:
+        raise ValueError("oracle simplify: the run ended before that iteration")
+    ne, nf, nm, na, rounds, nv = (int(x) for x in sz)
+    t = dict(edges=np.empty((ne, 2), np.int32), keys=np.empty(ne, np.uint64), place=np.empty((ne, 3)),
+             face_keys=np.empty(nf, np.uint64), marked=np.empty(nm, np.int64), link_ok=np.empty(nm, np.uint8),
+             applied=np.empty(na, np.int64), X=np.empty((nv, 3)), F=np.empty((nf, 3), np.int32),
+             falive=np.empty(nf, np.uint8))
+    order = ["edges", "keys", "place", "face_keys", "marked", "link_ok", "applied", "X", "F", "falive"]
+    lib().orc_trace_fetch(*[t[k].ctypes.data for k in order])
+    t["rounds"] = rounds
+    return t
+
+
+def quadrics(v, f) -> np.ndarray:
+    v, f = _vf(v, f)
+    out = np.empty((len(v), 10))
+    lib().orc_quadrics(v.ravel(), len(v), f.ravel(), len(f), out.ravel())
+    return out
+
+
+def edge_cost(v, f, edges, we: float = 1e-3, ws: float = 5e-3):
+    v, f = _vf(v, f)
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
+    cost = np.empty(len(e))
+    place = np.empty((len(e), 3))
+    lib().orc_edge_cost(v.ravel(), len(v), f.ravel(), len(f), e.ravel(), len(e), we, ws, cost, place.ravel())
+    return cost, place
 
 
 def link_condition(v, f, edges) -> np.ndarray:

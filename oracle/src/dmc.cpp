@@ -230,6 +230,11 @@ struct DmcOut {
   std::vector<int32_t> faces;
   int64_t nquads = 0;
   int64_t nsplit4 = 0;
+  // build_quads view: patch-vertex ids (4 per quad), lower vertex * 3 + axis, samples, split
+  std::vector<int32_t> quads;
+  std::vector<int64_t> qedge;
+  std::vector<float> qf;
+  std::vector<uint8_t> qsplit;
   int64_t nvp_own = 0;  // patch vertices of the own layers (slab mode)
   int64_t n_extra = 0;
 };
@@ -307,6 +312,9 @@ void run_dmc(const float* sdf, int R, double beta, DmcOut& out, int64_t pz0 = 0,
   // quads + triangulation, ordered by (cell, axis)
   struct QuadOut {
     int64_t q[4];
+    int64_t edge;
+    float f0, f1;
+    int code;  // 1: diagonal 0-2, 2: diagonal 1-3, 3: four triangles
     int ntri;  // 2 or 4
     V3 extra;
     int32_t tri[4][3];  // local: 0..3 quad corners, 4 = extra vertex
@@ -352,8 +360,12 @@ void run_dmc(const float* sdf, int R, double beta, DmcOut& out, int64_t pz0 = 0,
       const bool d02 = conc[0] || conc[2], d13 = conc[1] || conc[3];
       QuadOut Q;
       for (int k = 0; k < 4; ++k) Q.q[k] = q[k];
+      Q.edge = (xyz[0] + (R + 1) * (xyz[1] + static_cast<int64_t>(R + 1) * xyz[2])) * 3 + a;
+      Q.f0 = f0;
+      Q.f1 = f1;
       auto set2 = [&](bool diag02) {
         Q.ntri = 2;
+        Q.code = diag02 ? 1 : 2;
         if (diag02) {
           const int32_t t[2][3] = {{0, 1, 2}, {0, 2, 3}};
           std::memcpy(Q.tri, t, sizeof(t));
@@ -366,6 +378,7 @@ void run_dmc(const float* sdf, int R, double beta, DmcOut& out, int64_t pz0 = 0,
       else if (d13 && !d02) set2(false);
       else if (d02 && d13) {
         Q.ntri = 4;
+        Q.code = 3;
         Q.extra = crossing(plo, phi, f0, f1, beta);
         const int32_t t[4][3] = {{0, 1, 4}, {1, 2, 4}, {2, 3, 4}, {3, 0, 4}};
         std::memcpy(Q.tri, t, sizeof(t));
@@ -394,6 +407,11 @@ void run_dmc(const float* sdf, int R, double beta, DmcOut& out, int64_t pz0 = 0,
       if ((qmask[i] >> a) & 1) {
         const QuadOut& Q = qo[i][a];
         ++out.nquads;
+        for (int k = 0; k < 4; ++k) out.quads.push_back(static_cast<int32_t>(Q.q[k]));
+        out.qedge.push_back(Q.edge);
+        out.qf.push_back(Q.f0);
+        out.qf.push_back(Q.f1);
+        out.qsplit.push_back(static_cast<uint8_t>(Q.code));
         int64_t ids[5] = {Q.q[0], Q.q[1], Q.q[2], Q.q[3], -1};
         if (Q.ntri == 4) {
           ids[4] = nv_patch + extra++;
@@ -465,6 +483,18 @@ void orc_dmc_extract_slab(const float* planes, int R, int pz0, int pz1, int own_
   sizes[4] = g_last.nsplit4;
   sizes[5] = g_last.nvp_own;
   sizes[6] = g_last.n_extra;
+}
+
+// build_patches / build_quads views of the last whole-grid extract: sizes {n_patch_vertices,
+// n_quads}; vbase int64[n_active], quads int32[4n], qedge int64[n], qf float[2n], qsplit uint8[n]
+void orc_dmc_stages(int64_t* sizes, int64_t* vbase, int32_t* quads, int64_t* qedge, float* qf, uint8_t* qsplit) {
+  sizes[0] = g_last.nvp_own;
+  sizes[1] = g_last.nquads;
+  if (vbase) std::memcpy(vbase, g_last.vbase.data(), (g_last.vbase.size() - 1) * 8);
+  if (quads) std::memcpy(quads, g_last.quads.data(), g_last.quads.size() * 4);
+  if (qedge) std::memcpy(qedge, g_last.qedge.data(), g_last.qedge.size() * 8);
+  if (qf) std::memcpy(qf, g_last.qf.data(), g_last.qf.size() * 4);
+  if (qsplit) std::memcpy(qsplit, g_last.qsplit.data(), g_last.qsplit.size());
 }
 
 void orc_dmc_fetch(int64_t* cells, uint8_t* cases, uint8_t* flips, double* verts, int32_t* faces) {

@@ -17,6 +17,7 @@
 //                 (zero cross products resolved by dot signs);
 //                 s=2 apexes strictly on the same side of the shared edge.
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -281,32 +282,48 @@ bool box_overlap(const Box& a, const Box& b) {
 // scan.  Only the set matters (it is sorted and deduplicated), never the grid.
 std::vector<std::pair<int32_t, int32_t>> detect_pairs(const double* v, const int32_t* f, int64_t nf,
                                                       const uint8_t* alive, const uint8_t* query) {
-  constexpr int64_t kMaxCells = 64;
+  constexpr int64_t kMaxCells = 64, kChunk = 4096;
   struct Range {
     int64_t lo[3], hi[3];
     int64_t count() const { return (hi[0] - lo[0] + 1) * (hi[1] - lo[1] + 1) * (hi[2] - lo[2] + 1); }
   };
+  const int64_t nchunk = (nf + kChunk - 1) / kChunk;
+  auto live = [&](int64_t i) { return !alive || alive[i]; };
+  auto in_build = [&](int64_t i) { return live(i) && (!query || query[i]); };
   std::vector<Box> boxes(nf);
-  parallel_for(nf, [&](int64_t i) {
-    if (!alive || alive[i]) boxes[i] = face_box(f + 3 * i, v);
-  }, 4096);
-  std::vector<int32_t> build, probe;
-  std::vector<uint8_t> in_build(nf, 0);
-  for (int64_t i = 0; i < nf; ++i) {
-    if (alive && !alive[i]) continue;
-    probe.push_back(static_cast<int32_t>(i));
-    if (!query || query[i]) {
-      build.push_back(static_cast<int32_t>(i));
-      in_build[i] = 1;
+  // boxes, and the build set (ascending ids) by a chunked count / scan / fill
+  std::vector<int64_t> coff(nchunk + 1, 0);
+  parallel_for(nchunk, [&](int64_t c) {
+    int64_t n = 0;
+    for (int64_t i = c * kChunk; i < std::min(nf, (c + 1) * kChunk); ++i) {
+      if (!live(i)) continue;
+      boxes[i] = face_box(f + 3 * i, v);
+      n += in_build(i);
     }
-  }
+    coff[c + 1] = n;
+  }, 1);
+  for (int64_t c = 0; c < nchunk; ++c) coff[c + 1] += coff[c];
+  std::vector<int32_t> build(coff[nchunk]);
+  parallel_for(nchunk, [&](int64_t c) {
+    int64_t k = coff[c];
+    for (int64_t i = c * kChunk; i < std::min(nf, (c + 1) * kChunk); ++i)
+      if (in_build(i)) build[k++] = static_cast<int32_t>(i);
+  }, 1);
   if (build.empty()) return {};
+  const int64_t nb_ = static_cast<int64_t>(build.size());
+  const int64_t nbc = (nb_ + kChunk - 1) / kChunk;
+  std::vector<double> ext_part(nbc, 0.0);
+  parallel_for(nbc, [&](int64_t c) {
+    double e = 0.0;
+    for (int64_t k = c * kChunk; k < std::min(nb_, (c + 1) * kChunk); ++k) {
+      const Box& x = boxes[build[k]];
+      e += std::max(std::max(x.hi.x - x.lo.x, x.hi.y - x.lo.y), x.hi.z - x.lo.z);
+    }
+    ext_part[c] = e;
+  }, 1);
   double ext = 0.0;
-  for (int32_t b : build) {
-    const Box& x = boxes[b];
-    ext += std::max(std::max(x.hi.x - x.lo.x, x.hi.y - x.lo.y), x.hi.z - x.lo.z);
-  }
-  const double mean = ext / static_cast<double>(build.size());
+  for (double e : ext_part) ext += e;
+  const double mean = ext / static_cast<double>(nb_);
   const double inv_h = 1.0 / (1.5 * (mean > 0.0 ? mean : 1e-3));
   auto range_of = [&](const Box& b) {
     Range r;
@@ -325,73 +342,93 @@ std::vector<std::pair<int32_t, int32_t>> detect_pairs(const double* v, const int
     h ^= h >> 32;
     return h & mask;
   };
-  // counting sort of (cell, build face) entries into hash buckets
-  std::vector<Range> brange(build.size());
-  std::vector<int32_t> big;
+  // hashed uniform grid over the build set: counting sort of (cell, face) entries into buckets
+  // (parallel count with atomics, serial scan, parallel fill; the order inside a bucket does not
+  // matter: the emitted pair set is sorted and deduplicated at the end)
+  std::vector<Range> brange(nb_);
+  std::vector<int64_t> ncell_part(nbc, 0);
+  parallel_for(nbc, [&](int64_t c) {
+    int64_t n = 0;
+    for (int64_t k = c * kChunk; k < std::min(nb_, (c + 1) * kChunk); ++k) {
+      brange[k] = range_of(boxes[build[k]]);
+      const int64_t cc = brange[k].count();
+      if (cc <= kMaxCells) n += cc;
+    }
+    ncell_part[c] = n;
+  }, 1);
   int64_t nent = 0;
-  for (size_t k = 0; k < build.size(); ++k) {
-    brange[k] = range_of(boxes[build[k]]);
-    const int64_t c = brange[k].count();
-    if (c > kMaxCells) big.push_back(build[k]);
-    else nent += c;
-  }
-  uint64_t nb = 1024;
-  while (nb < static_cast<uint64_t>(2 * nent + 1)) nb <<= 1;
-  const uint64_t mask = nb - 1;
-  std::vector<uint32_t> boff(nb + 1, 0);
+  for (int64_t n : ncell_part) nent += n;
+  std::vector<int32_t> big;
+  for (int64_t k = 0; k < nb_; ++k)
+    if (brange[k].count() > kMaxCells) big.push_back(build[k]);
+  uint64_t nbk = 1024;
+  while (nbk < static_cast<uint64_t>(2 * nent + 1)) nbk <<= 1;
+  const uint64_t mask = nbk - 1;
   struct Entry {
     int32_t face;
     int64_t lo[3];
   };
+  std::vector<std::atomic<uint32_t>> bcnt(nbk);
+  for (auto& x : bcnt) x.store(0, std::memory_order_relaxed);
+  auto for_cells = [&](const Range& r, auto&& fn) {
+    for (int64_t z = r.lo[2]; z <= r.hi[2]; ++z)
+      for (int64_t y = r.lo[1]; y <= r.hi[1]; ++y)
+        for (int64_t x = r.lo[0]; x <= r.hi[0]; ++x) fn(x, y, z);
+  };
+  parallel_for(nbc, [&](int64_t c) {
+    for (int64_t k = c * kChunk; k < std::min(nb_, (c + 1) * kChunk); ++k) {
+      if (brange[k].count() > kMaxCells) continue;
+      for_cells(brange[k], [&](int64_t x, int64_t y, int64_t z) {
+        bcnt[hash(x, y, z, mask)].fetch_add(1, std::memory_order_relaxed);
+      });
+    }
+  }, 1);
+  std::vector<uint32_t> boff(nbk + 1, 0);
+  for (uint64_t h = 0; h < nbk; ++h) {
+    boff[h + 1] = boff[h] + bcnt[h].load(std::memory_order_relaxed);
+    bcnt[h].store(boff[h], std::memory_order_relaxed);  // reused as the fill cursor
+  }
   std::vector<Entry> ent(static_cast<size_t>(nent));
-  for (int pass = 0; pass < 2; ++pass) {
-    std::vector<uint32_t> cur;
-    if (pass == 1) cur.assign(boff.begin(), boff.end() - 1);
-    for (size_t k = 0; k < build.size(); ++k) {
+  parallel_for(nbc, [&](int64_t c) {
+    for (int64_t k = c * kChunk; k < std::min(nb_, (c + 1) * kChunk); ++k) {
       const Range& r = brange[k];
       if (r.count() > kMaxCells) continue;
-      for (int64_t z = r.lo[2]; z <= r.hi[2]; ++z)
-        for (int64_t y = r.lo[1]; y <= r.hi[1]; ++y)
-          for (int64_t x = r.lo[0]; x <= r.hi[0]; ++x) {
-            const uint64_t h = hash(x, y, z, mask);
-            if (pass == 0) boff[h + 1]++;
-            else ent[cur[h]++] = Entry{build[k], {r.lo[0], r.lo[1], r.lo[2]}};
-          }
+      for_cells(r, [&](int64_t x, int64_t y, int64_t z) {
+        ent[bcnt[hash(x, y, z, mask)].fetch_add(1, std::memory_order_relaxed)] =
+            Entry{build[k], {r.lo[0], r.lo[1], r.lo[2]}};
+      });
     }
-    if (pass == 0)
-      for (uint64_t h = 0; h < nb; ++h) boff[h + 1] += boff[h];
-  }
-  // probe: every alive face against the grid; (p, b) with both in the build set only from p < b
-  const int64_t np = static_cast<int64_t>(probe.size());
-  constexpr int64_t kChunk = 2048;
-  const int64_t nchunk = (np + kChunk - 1) / kChunk;
+  }, 1);
+  std::vector<uint8_t> is_build(nf, 0);
+  parallel_for(nb_, [&](int64_t k) { is_build[build[k]] = 1; }, kChunk);
+  // probe: every alive face walks its cells; a pair is examined in the first common cell of the
+  // two ranges; (p, b) with both in the build set only from p < b
   std::vector<std::vector<std::pair<int32_t, int32_t>>> found(nchunk);
   parallel_for(nchunk, [&](int64_t ch) {
     auto& out = found[ch];
-    for (int64_t k = ch * kChunk; k < std::min(np, (ch + 1) * kChunk); ++k) {
-      const int32_t p = probe[k];
+    for (int64_t pi = ch * kChunk; pi < std::min(nf, (ch + 1) * kChunk); ++pi) {
+      if (!live(pi)) continue;
+      const int32_t p = static_cast<int32_t>(pi);
       const Box& bp = boxes[p];
       auto consider = [&](int32_t b) {
-        if (b == p || (in_build[p] && b < p)) return;
+        if (b == p || (is_build[p] && b < p)) return;
         if (!box_overlap(bp, boxes[b])) return;
         if (tri_tri_verdict(f + 3 * p, f + 3 * b, v)) out.emplace_back(std::min(p, b), std::max(p, b));
       };
       const Range rp = range_of(bp);
       if (rp.count() > kMaxCells) {  // huge probe: scan the build set (big build faces below)
-        for (size_t j = 0; j < build.size(); ++j)
+        for (int64_t j = 0; j < nb_; ++j)
           if (brange[j].count() <= kMaxCells) consider(build[j]);
       } else {
-        for (int64_t z = rp.lo[2]; z <= rp.hi[2]; ++z)
-          for (int64_t y = rp.lo[1]; y <= rp.hi[1]; ++y)
-            for (int64_t x = rp.lo[0]; x <= rp.hi[0]; ++x) {
-              const uint64_t h = hash(x, y, z, mask);
-              for (uint32_t e = boff[h]; e < boff[h + 1]; ++e) {
-                const Entry& en = ent[e];
-                if (x == std::max(rp.lo[0], en.lo[0]) && y == std::max(rp.lo[1], en.lo[1]) &&
-                    z == std::max(rp.lo[2], en.lo[2]))
-                  consider(en.face);
-              }
-            }
+        for_cells(rp, [&](int64_t x, int64_t y, int64_t z) {
+          const uint64_t h = hash(x, y, z, mask);
+          for (uint32_t e = boff[h]; e < boff[h + 1]; ++e) {
+            const Entry& en = ent[e];
+            if (x == std::max(rp.lo[0], en.lo[0]) && y == std::max(rp.lo[1], en.lo[1]) &&
+                z == std::max(rp.lo[2], en.lo[2]))
+              consider(en.face);
+          }
+        });
       }
       for (int32_t b : big) consider(b);
     }

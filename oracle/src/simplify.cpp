@@ -298,6 +298,22 @@ struct Stats {
   int error = 0;
 };
 
+// Step-level record of one iteration (granular parity tests of the SPEC operations)
+struct Trace {
+  int64_t iter = 0;  // 1-based iteration to record; the run stops after it
+  std::vector<std::pair<int32_t, int32_t>> edges;
+  std::vector<uint64_t> keys;       // ~0 for an invalid edge
+  std::vector<double> place;        // 3 per edge
+  std::vector<uint64_t> face_keys;  // per face slot, ~0 for a dead face
+  std::vector<int64_t> marked;      // edge ids, ascending
+  std::vector<uint8_t> link_ok;     // per marked edge
+  std::vector<int64_t> applied;     // edge ids of the collapses that survived the undo loop
+  int64_t rounds = 0;
+  std::vector<double> X;
+  std::vector<int32_t> F;
+  std::vector<uint8_t> falive;
+};
+
 // ORC_PROFILE=1: per-phase wall seconds on stderr (diagnostics of the CPU baseline only)
 struct PhaseTimer {
   bool on = std::getenv("ORC_PROFILE") != nullptr;
@@ -317,7 +333,7 @@ struct PhaseTimer {
 };
 
 static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
-                std::vector<int64_t>* per_iter_collapses) {
+                std::vector<int64_t>* per_iter_collapses, Trace* tr = nullptr) {
   PhaseTimer T;
   // initial quadrics, gathered in ascending face id
   m.Q.assign(m.nv, Quadric{});
@@ -414,6 +430,24 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
     for (int64_t e = 0; e < ne; ++e)
       if (valid[e] && key[e] == vfmin[edges[e].first] && key[e] == vfmin[edges[e].second])
         marked.push_back(e);
+    const bool rec = tr && S.iterations == tr->iter;
+    if (rec) {
+      tr->edges = edges;
+      tr->keys = key;
+      tr->place.resize(3 * ne);
+      for (int64_t e = 0; e < ne; ++e) {
+        tr->place[3 * e] = place[e].x;
+        tr->place[3 * e + 1] = place[e].y;
+        tr->place[3 * e + 2] = place[e].z;
+      }
+      tr->face_keys.assign(m.nf, ~0ull);
+      for (int64_t f = 0; f < m.nf; ++f)
+        if (m.falive[f]) {
+          const int32_t* t = m.face(static_cast<int>(f));
+          tr->face_keys[f] = std::min(std::min(vmin[t[0]], vmin[t[1]]), vmin[t[2]]);
+        }
+      tr->marked = marked;
+    }
     T.mark(3);
     // link condition on the pre-batch mesh
     std::vector<uint8_t> pass(marked.size());
@@ -421,6 +455,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
       pass[i] = link_condition(m, I, edges[marked[i]].first, edges[marked[i]].second) ? 1 : 0;
     }, 64);
     T.mark(4);
+    if (rec) tr->link_ok = pass;
     std::set<std::pair<int, int>> new_invalid;
     std::vector<int64_t> sel;
     for (size_t i = 0; i < marked.size(); ++i) {
@@ -537,6 +572,14 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
     for (auto& C : cols) succ += C.applied;
     S.collapses += succ;
     if (per_iter_collapses) per_iter_collapses->push_back(succ);
+    if (rec) {
+      for (size_t ci = 0; ci < cols.size(); ++ci)
+        if (cols[ci].applied) tr->applied.push_back(sel[ci]);
+      tr->rounds = rounds;
+      tr->X = m.X;
+      tr->F = m.F;
+      tr->falive = m.falive;
+    }
     if (succ > 0) {
       invalid = new_invalid;
       retain = 0;
@@ -551,6 +594,7 @@ static void run(Mesh& m, int64_t target, const Params& P, Stats& S,
         invalid.insert(new_invalid.begin(), new_invalid.end());
       }
     }
+    if (rec) return;
   }
 }
 
@@ -618,6 +662,94 @@ void orc_simplify_fetch(double* v, int32_t* f, int64_t* per_iter) {
   if (v) std::memcpy(v, g_v.data(), g_v.size() * 8);
   if (f) std::memcpy(f, g_f.data(), g_f.size() * 4);
   if (per_iter) std::memcpy(per_iter, g_iters.data(), g_iters.size() * 8);
+}
+
+// Step-level record of iteration `iter` of simplify_to (granular parity of edge_cost, pack_cost,
+// propagate_and_mark, collapse_batch, undo_loop).  sizes_out (int64[6]): ne, nf, nmarked,
+// napplied, rounds, nv.  Fetch with orc_trace_fetch.
+namespace {
+Trace g_trace;
+}
+int orc_simplify_trace(const double* v, int64_t nv, const int32_t* f, int64_t nf, int64_t target, double we,
+                       double ws, int tolerance, int64_t iter, int64_t* sizes_out) {
+  Mesh m;
+  m.nv = nv;
+  m.nf = nf;
+  m.X.assign(v, v + 3 * nv);
+  m.F.assign(f, f + 3 * nf);
+  m.valive.assign(nv, 1);
+  m.falive.assign(nf, 1);
+  m.alive_faces = nf;
+  Params P{we, ws, tolerance, 10};
+  Stats S;
+  g_trace = Trace();
+  g_trace.iter = iter;
+  run(m, target, P, S, nullptr, &g_trace);
+  sizes_out[0] = static_cast<int64_t>(g_trace.edges.size());
+  sizes_out[1] = nf;
+  sizes_out[2] = static_cast<int64_t>(g_trace.marked.size());
+  sizes_out[3] = static_cast<int64_t>(g_trace.applied.size());
+  sizes_out[4] = g_trace.rounds;
+  sizes_out[5] = nv;
+  return S.error ? -1 : (g_trace.X.empty() ? 1 : 0);
+}
+
+void orc_trace_fetch(int32_t* edges, uint64_t* keys, double* place, uint64_t* face_keys, int64_t* marked,
+                     uint8_t* link_ok, int64_t* applied, double* X, int32_t* F, uint8_t* falive) {
+  const Trace& t = g_trace;
+  for (size_t e = 0; e < t.edges.size(); ++e) {
+    edges[2 * e] = t.edges[e].first;
+    edges[2 * e + 1] = t.edges[e].second;
+  }
+  std::memcpy(keys, t.keys.data(), t.keys.size() * 8);
+  std::memcpy(place, t.place.data(), t.place.size() * 8);
+  std::memcpy(face_keys, t.face_keys.data(), t.face_keys.size() * 8);
+  std::memcpy(marked, t.marked.data(), t.marked.size() * 8);
+  std::memcpy(link_ok, t.link_ok.data(), t.link_ok.size());
+  std::memcpy(applied, t.applied.data(), t.applied.size() * 8);
+  std::memcpy(X, t.X.data(), t.X.size() * 8);
+  std::memcpy(F, t.F.data(), t.F.size() * 4);
+  std::memcpy(falive, t.falive.data(), t.falive.size());
+}
+
+// Quadric per vertex, gathered in ascending face id: double[10 nv]
+void orc_quadrics(const double* v, int64_t nv, const int32_t* f, int64_t nf, double* out) {
+  Mesh m;
+  m.nv = nv;
+  m.nf = nf;
+  m.X.assign(v, v + 3 * nv);
+  m.F.assign(f, f + 3 * nf);
+  std::fill(out, out + 10 * nv, 0.0);
+  for (int64_t i = 0; i < nf; ++i) {
+    double fq[10];
+    face_quadric(m, static_cast<int>(i), fq);
+    for (int k = 0; k < 3; ++k) {
+      double* q = out + 10 * m.F[3 * i + k];
+      for (int j = 0; j < 10; ++j) q[j] = q[j] + fq[j];
+    }
+  }
+}
+
+// edge_cost of explicit edges under the mesh's initial quadrics
+void orc_edge_cost(const double* v, int64_t nv, const int32_t* f, int64_t nf, const int32_t* edges, int64_t ne,
+                   double we, double ws, double* cost, double* place) {
+  Mesh m;
+  m.nv = nv;
+  m.nf = nf;
+  m.X.assign(v, v + 3 * nv);
+  m.F.assign(f, f + 3 * nf);
+  m.falive.assign(nf, 1);
+  m.Q.assign(nv, Quadric{});
+  orc_quadrics(v, nv, f, nf, reinterpret_cast<double*>(m.Q.data()));
+  const Incidence I = build_incidence(m);
+  const Params P{we, ws, 4, 10};
+  for (int64_t i = 0; i < ne; ++i) {
+    const CostOut c = edge_cost(m, I, edges[2 * i], edges[2 * i + 1], P);
+    cost[i] = c.cost;
+    place[3 * i] = c.x.x;
+    place[3 * i + 1] = c.x.y;
+    place[3 * i + 2] = c.x.z;
+  }
 }
 
 // Link condition restatement over an arbitrary mesh (checked against the reference).

@@ -135,9 +135,33 @@ _SIGS = {
     "pamopt_cu_mesh_rebase": (C.c_int, [vp, i64, i64, i64]),
     "pamopt_cu_dmc_active_cells": (C.c_int, [vp, vp, vp, vp, i64, P(i64)]),
     "pamopt_cu_dmc_table": (C.c_int, [vp]),
+    "pamopt_cu_dmc_stages": (C.c_int, [vp, dbl, vp]),
+    "pamopt_cu_dmc_build_patches": (C.c_int, [vp, vp, vp]),
+    "pamopt_cu_dmc_build_quads": (C.c_int, [vp, vp, vp, vp, vp]),
+    "pamopt_cu_triangulate_quads": (C.c_int, [vp, i32, vp, i64, vp, vp, vp, i64, dbl, P(vp)]),
+    "pamopt_cu_interpolate_patch_vertex": (C.c_int, [vp, vp, vp, vp, vp, i64, dbl, vp]),
     "pamopt_cu_self_intersections": (C.c_int, [vp, vp, i64, P(i64)]),
     "pamopt_cu_tri_tri_pairs": (C.c_int, [vp, vp, i64, vp]),
+    "pamopt_cu_classify_pair": (C.c_int, [vp, vp, i64, vp, vp]),
+    "pamopt_cu_intersect_3d": (C.c_int, [vp, vp, i64, vp]),
+    "pamopt_cu_intersect_coplanar": (C.c_int, [vp, vp, i64, vp]),
     "pamopt_cu_simplify": (C.c_int, [vp, i64, P(SimplifyParams), P(SimplifyStats), vp, i64]),
+    "pamopt_cu_quadrics": (C.c_int, [vp, vp]),
+    "pamopt_cu_edge_cost": (C.c_int, [vp, vp, i64, dbl, dbl, vp, vp]),
+    "pamopt_cu_pack_cost": (C.c_int, [vp, vp, vp, i64, vp]),
+    "pamopt_cu_link_condition": (C.c_int, [vp, vp, i64, vp]),
+    "pamopt_cu_qem_create": (C.c_int, [vp, i64, P(SimplifyParams), P(vp)]),
+    "pamopt_cu_qem_done": (C.c_int, [vp, P(i32)]),
+    "pamopt_cu_qem_prepare": (C.c_int, [vp, P(i64)]),
+    "pamopt_cu_qem_edges": (C.c_int, [vp, vp, vp, vp, vp, i64]),
+    "pamopt_cu_qem_propagate_and_mark": (C.c_int, [vp, P(i64)]),
+    "pamopt_cu_qem_marked": (C.c_int, [vp, vp, i64, vp, i64]),
+    "pamopt_cu_qem_collapse_batch": (C.c_int, [vp, vp, i64]),
+    "pamopt_cu_qem_undo_loop": (C.c_int, [vp, P(i32), P(i64), vp, i64]),
+    "pamopt_cu_qem_end_iteration": (C.c_int, [vp, P(i64)]),
+    "pamopt_cu_qem_mesh": (C.c_int, [vp, vp, vp, vp, P(i64), P(i64)]),
+    "pamopt_cu_qem_finish": (C.c_int, [vp, P(SimplifyStats)]),
+    "pamopt_cu_qem_destroy": (C.c_int, [vp]),
     "pamopt_cu_analyze_topology": (C.c_int, [vp, P(Topology), vp, i64, vp, i64]),
     "pamopt_cu_nearest_primitive": (C.c_int, [vp, vp, i64, vp, vp, vp]),
     "pamopt_cu_sample_points": (C.c_int, [vp, i64, C.c_uint64, vp, vp, P(dbl)]),

@@ -287,6 +287,53 @@ def dmc_active_cells(grid: DeviceGrid):
     return cells, cases, flips
 
 
+def dmc_stages(grid: DeviceGrid, beta: float = DEFAULT_BETA) -> dict:
+    """classify_voxels + build_patches + build_quads as separate views: active
+    cells, patch vertices with each active cell's first patch vertex, and the quads (patch-vertex
+    ids, valid edge = lower lattice vertex * 3 + axis, its two samples, triangulate_quads' split)."""
+    counts = np.zeros(3, np.int64)
+    check(lib().pamopt_cu_dmc_stages(grid.h, float(beta), ptr(counts)))
+    na, nv, nq = (int(x) for x in counts)
+    pv = np.empty((nv, 3))
+    first = np.empty(na, np.int64)
+    check(lib().pamopt_cu_dmc_build_patches(grid.h, ptr(pv), ptr(first)))
+    quads = np.empty((nq, 4), np.int32)
+    edges = np.empty(nq, np.int64)
+    samples = np.empty((nq, 2), np.float32)
+    split = np.empty(nq, np.uint8)
+    check(lib().pamopt_cu_dmc_build_quads(grid.h, ptr(quads), ptr(edges), ptr(samples), ptr(split)))
+    cells, cases, flips = dmc_active_cells(grid)
+    return dict(cells=cells, cases=cases, flips=flips, patch_vertices=pv, patch_first=first, quads=quads,
+                quad_edges=edges, quad_samples=samples, quad_split=split)
+
+
+def triangulate_quads(R: int, patch_vertices, quads, quad_edges, quad_samples, beta: float = DEFAULT_BETA,
+                      ctx: Context | None = None) -> DeviceMesh:
+    """triangulate_quads on explicit quads -> DeviceMesh."""
+    ctx = ctx or default_context()
+    pv = np.ascontiguousarray(patch_vertices, np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(quads, np.int32).reshape(-1, 4)
+    e = np.ascontiguousarray(quad_edges, np.int64).ravel()
+    s_ = np.ascontiguousarray(quad_samples, np.float32).reshape(-1, 2)
+    h = C.c_void_p()
+    check(lib().pamopt_cu_triangulate_quads(ctx.h, int(R), ptr(pv), len(pv), ptr(q), ptr(e), ptr(s_), len(q),
+                                            float(beta), C.byref(h)))
+    return DeviceMesh(h, ctx)
+
+
+def interpolate_patch_vertex(p0, p1, f0, f1, beta: float = DEFAULT_BETA, ctx: Context | None = None) -> np.ndarray:
+    """interpolate_patch_vertex for arrays of edges; raises for equal signs."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(p0, np.float64).reshape(-1, 3)
+    b = np.ascontiguousarray(p1, np.float64).reshape(-1, 3)
+    x = np.ascontiguousarray(f0, np.float32).ravel()
+    y = np.ascontiguousarray(f1, np.float32).ravel()
+    out = np.empty((len(a), 3))
+    check(lib().pamopt_cu_interpolate_patch_vertex(ctx.h, ptr(a), ptr(b), ptr(x), ptr(y), len(a), float(beta),
+                                                   ptr(out)))
+    return out
+
+
 def dmc_table() -> np.ndarray:
     out = np.empty(256 * 6, np.int32)
     check(lib().pamopt_cu_dmc_table(ptr(out)))
@@ -312,6 +359,34 @@ def tri_tri_pairs(mesh, pairs, ctx: Context | None = None) -> np.ndarray:
     return out
 
 
+def classify_pair(mesh, pairs, ctx: Context | None = None):
+    """classify_pair: (shared-vertex count, coplanar flag) per pair."""
+    m = _mesh(mesh, ctx)
+    p = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    sh = np.empty(len(p), np.int32)
+    cp = np.empty(len(p), np.int32)
+    check(lib().pamopt_cu_classify_pair(m.h, ptr(p), len(p), ptr(sh), ptr(cp)))
+    return sh, cp
+
+
+def intersect_3d(mesh, pairs, ctx: Context | None = None) -> np.ndarray:
+    """intersect_3d for non-coplanar pairs; raises for a coplanar pair."""
+    m = _mesh(mesh, ctx)
+    p = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    out = np.empty(len(p), np.int32)
+    check(lib().pamopt_cu_intersect_3d(m.h, ptr(p), len(p), ptr(out)))
+    return out
+
+
+def intersect_coplanar(mesh, pairs, ctx: Context | None = None) -> np.ndarray:
+    """intersect_coplanar for coplanar pairs; raises for a non-coplanar pair."""
+    m = _mesh(mesh, ctx)
+    p = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    out = np.empty(len(p), np.int32)
+    check(lib().pamopt_cu_intersect_coplanar(m.h, ptr(p), len(p), ptr(out)))
+    return out
+
+
 # ------------------------------------------------------------------ simplify (stage 2)
 def _params(we, ws, tolerance, stall=10) -> _lib.SimplifyParams:
     return _lib.SimplifyParams(float(we), float(ws), int(tolerance), int(stall))
@@ -328,6 +403,143 @@ def simplify_to(mesh, target_faces: int, we: float = DEFAULT_WE, ws: float = DEF
     stats = st.as_dict()
     stats["per_iter_collapses"] = per[: stats["iterations"]].copy()
     return m, stats
+
+
+# ------------------------------------------------- stage 2, SPEC-granular operations
+def _edges_arr(edges) -> np.ndarray:
+    return np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
+
+
+def quadrics(mesh, ctx: Context | None = None) -> np.ndarray:
+    """Quadric per vertex: (nv, 10) = xx xy xz xw yy yz yw zz zw ww."""
+    m = _mesh(mesh, ctx)
+    nv, _ = m.size()
+    out = np.empty((nv, 10))
+    check(lib().pamopt_cu_quadrics(m.h, ptr(out)))
+    return out
+
+
+def edge_cost(mesh, edges, we: float = DEFAULT_WE, ws: float = DEFAULT_WS, ctx: Context | None = None):
+    """edge_cost of explicit edges: (cost[n], placement[n, 3])."""
+    m = _mesh(mesh, ctx)
+    e = _edges_arr(edges)
+    cost = np.empty(len(e))
+    place = np.empty((len(e), 3))
+    check(lib().pamopt_cu_edge_cost(m.h, ptr(e), len(e), float(we), float(ws), ptr(cost), ptr(place)))
+    return cost, place
+
+
+def pack_cost(cost, edge_ids, ctx: Context | None = None) -> np.ndarray:
+    """pack_cost on the GPU; PamoptError (ENUMERIC) for a NaN cost."""
+    ctx = ctx or default_context()
+    c = np.ascontiguousarray(cost, np.float64).ravel()
+    ids = np.ascontiguousarray(edge_ids, np.uint32).ravel()
+    keys = np.empty(len(c), np.uint64)
+    check(lib().pamopt_cu_pack_cost(ctx.h, ptr(c), ptr(ids), len(c), ptr(keys)))
+    return keys
+
+
+def link_condition(mesh, edges, ctx: Context | None = None) -> np.ndarray:
+    """HalfEdgeAdjacency::link_condition_holds (mesh.cpp:301-358) per edge (bool); raises
+    PamoptInvalidArgument for a pair that is not an edge (mesh.cpp:302)."""
+    m = _mesh(mesh, ctx)
+    e = _edges_arr(edges)
+    out = np.empty(len(e), np.int32)
+    check(lib().pamopt_cu_link_condition(m.h, ptr(e), len(e), ptr(out)))
+    return out.astype(bool)
+
+
+class QemRun:
+    """Algorithm 1 one SPEC operation at a time (pamopt_cu_qem_*): the same code simplify_to
+    runs.  Per iteration: prepare(), propagate_and_mark(), collapse_batch(), undo_loop(),
+    end_iteration(); finish() compacts the mesh."""
+
+    def __init__(self, mesh: DeviceMesh, target_faces: int, we: float = DEFAULT_WE, ws: float = DEFAULT_WS,
+                 tolerance: int = DEFAULT_TOL):
+        self.mesh = mesh
+        self.h = C.c_void_p()
+        p = _params(we, ws, tolerance)
+        check(lib().pamopt_cu_qem_create(mesh.h, int(target_faces), C.byref(p), C.byref(self.h)))
+        self.ne = self.nm = 0
+
+    def done(self) -> bool:
+        d = C.c_int32()
+        check(lib().pamopt_cu_qem_done(self.h, C.byref(d)))
+        return bool(d.value)
+
+    def prepare(self) -> int:
+        n = C.c_int64()
+        check(lib().pamopt_cu_qem_prepare(self.h, C.byref(n)))
+        self.ne = n.value
+        return self.ne
+
+    def edges(self) -> dict:
+        n = self.ne
+        e = np.empty((n, 2), np.int32)
+        k = np.empty(n, np.uint64)
+        p = np.empty((n, 3))
+        v = np.empty(n, np.uint8)
+        check(lib().pamopt_cu_qem_edges(self.h, ptr(e), ptr(k), ptr(p), ptr(v), n))
+        return dict(edges=e, keys=k, place=p, valid=v)
+
+    def propagate_and_mark(self) -> int:
+        n = C.c_int64()
+        check(lib().pamopt_cu_qem_propagate_and_mark(self.h, C.byref(n)))
+        self.nm = n.value
+        return self.nm
+
+    def marked(self):
+        ids = np.empty(self.nm, np.uint32)
+        _, nf = self.state_sizes()
+        fk = np.empty(nf, np.uint64)
+        check(lib().pamopt_cu_qem_marked(self.h, ptr(ids), self.nm, ptr(fk), nf))
+        return ids, fk
+
+    def collapse_batch(self) -> np.ndarray:
+        ok = np.empty(self.nm, np.uint8)
+        check(lib().pamopt_cu_qem_collapse_batch(self.h, ptr(ok), self.nm))
+        return ok
+
+    def undo_loop(self):
+        r, n = C.c_int32(), C.c_int64()
+        applied = np.empty(self.nm, np.uint8)
+        check(lib().pamopt_cu_qem_undo_loop(self.h, C.byref(r), C.byref(n), ptr(applied), self.nm))
+        return r.value, n.value, applied
+
+    def end_iteration(self) -> int:
+        a = C.c_int64()
+        check(lib().pamopt_cu_qem_end_iteration(self.h, C.byref(a)))
+        return a.value
+
+    def state_sizes(self):
+        nv, nf = C.c_int64(), C.c_int64()
+        check(lib().pamopt_cu_qem_mesh(self.h, None, None, None, C.byref(nv), C.byref(nf)))
+        return nv.value, nf.value
+
+    def state_mesh(self):
+        nv, nf = self.state_sizes()
+        v = np.empty((nv, 3))
+        f = np.empty((nf, 3), np.int32)
+        a = np.empty(nf, np.uint8)
+        n1, n2 = C.c_int64(), C.c_int64()
+        check(lib().pamopt_cu_qem_mesh(self.h, ptr(v), ptr(f), ptr(a), C.byref(n1), C.byref(n2)))
+        return v, f, a
+
+    def finish(self) -> dict:
+        st = _lib.SimplifyStats()
+        check(lib().pamopt_cu_qem_finish(self.h, C.byref(st)))
+        return st.as_dict()
+
+    def close(self):
+        if self.h:
+            lib().pamopt_cu_qem_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ pipeline (stages 1-2)

@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <limits>
 #include <cstdio>
@@ -226,6 +227,11 @@ void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit) {
 using pcu::guarded;
 
 static void check_ctx(pamopt_cu_ctx c) { PCU_REQUIRE(c != nullptr, PAMOPT_CU_EINVAL, "null context"); }
+
+template <class T>
+static void d2h(pcu::Ctx& ctx, T* dst, const T* src, int64_t n) {
+  if (dst && n > 0) PCU_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
+}
 
 extern "C" {
 
@@ -1060,6 +1066,112 @@ int pamopt_cu_dmc_table(int32_t* out) {
   });
 }
 
+// ----------------------------------------------------------- stage 1b, granular operations
+int pamopt_cu_dmc_stages(pamopt_cu_grid gr, double beta, int64_t counts[3]) {
+  return guarded([&] {
+    PCU_REQUIRE(gr && counts, PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(beta > 0.0, PAMOPT_CU_EINVAL, "beta must be positive");
+    PCU_REQUIRE(gr->z0 == 0 && gr->z1 == gr->R + 1, PAMOPT_CU_EINVAL, "dmc stages: the grid is a z-slab");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    gr->last = pcu::DmcResult();
+    gr->last.want_stages = true;
+    pcu::dmc_extract(ctx, gr->g.get(), gr->R, beta, gr->last);
+    counts[0] = gr->last.n_active;
+    counts[1] = static_cast<int64_t>(gr->last.nv_patch);
+    counts[2] = static_cast<int64_t>(gr->last.n_quads);
+  });
+}
+
+int pamopt_cu_dmc_build_patches(pamopt_cu_grid gr, double* vertices, int64_t* patch_first) {
+  return guarded([&] {
+    PCU_REQUIRE(gr != nullptr, PAMOPT_CU_EINVAL, "null grid");
+    PCU_REQUIRE(gr->last.want_stages, PAMOPT_CU_EINVAL, "build_patches: call pamopt_cu_dmc_stages first");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    const pcu::DmcResult& r = gr->last;
+    d2h(ctx, vertices, r.V.get(), 3 * static_cast<int64_t>(r.nv_patch));  // V starts with the patch vertices
+    std::vector<uint32_t> vb(patch_first ? r.n_active : 0);
+    if (patch_first) d2h(ctx, vb.data(), r.vbase.get(), r.n_active);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    for (size_t i = 0; i < vb.size(); ++i) patch_first[i] = vb[i];
+  });
+}
+
+int pamopt_cu_dmc_build_quads(pamopt_cu_grid gr, int32_t* quads, int64_t* edges, float* samples, uint8_t* split) {
+  return guarded([&] {
+    PCU_REQUIRE(gr != nullptr, PAMOPT_CU_EINVAL, "null grid");
+    PCU_REQUIRE(gr->last.want_stages, PAMOPT_CU_EINVAL, "build_quads: call pamopt_cu_dmc_stages first");
+    pcu::Ctx& ctx = gr->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    const pcu::DmcResult& r = gr->last;
+    const int64_t n = static_cast<int64_t>(r.n_quads);
+    d2h(ctx, quads, r.quads.get(), 4 * n);
+    d2h(ctx, edges, r.qedge.get(), n);
+    d2h(ctx, samples, r.qf.get(), 2 * n);
+    d2h(ctx, split, r.qsplit.get(), n);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+int pamopt_cu_triangulate_quads(pamopt_cu_ctx c, int32_t R, const double* pv, int64_t nv, const int32_t* quads,
+                                const int64_t* edges, const float* samples, int64_t nq, double beta, pamopt_cu_mesh* out) {
+  return guarded([&] {
+    check_ctx(c);
+    check_R(R);
+    PCU_REQUIRE(out && nv >= 0 && nq >= 0 && (nv == 0 || pv) && (nq == 0 || (quads && edges && samples)),
+                PAMOPT_CU_EINVAL, "bad arguments");
+    PCU_REQUIRE(beta > 0.0, PAMOPT_CU_EINVAL, "beta must be positive");
+    const int64_t n1 = static_cast<int64_t>(R) + 1;
+    for (int64_t i = 0; i < nq; ++i) {
+      for (int k = 0; k < 4; ++k)
+        PCU_REQUIRE(quads[4 * i + k] >= 0 && quads[4 * i + k] < nv, PAMOPT_CU_EINVAL, "quad vertex out of range");
+      const int64_t lv = edges[i] / 3, a = edges[i] % 3;
+      const int64_t xyz[3] = {lv % n1, (lv / n1) % n1, lv / (n1 * n1)};
+      PCU_REQUIRE(edges[i] >= 0 && xyz[2] < n1 && xyz[a] + 1 < n1, PAMOPT_CU_EINVAL, "quad edge outside the lattice");
+    }
+    pcu::Ctx& ctx = c->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    pcu::DevBuf<double> dv(3 * (nv ? nv : 1), ctx.stream);
+    pcu::DevBuf<int32_t> dq(4 * (nq ? nq : 1), ctx.stream);
+    pcu::DevBuf<int64_t> de(nq ? nq : 1, ctx.stream);
+    pcu::DevBuf<float> df(2 * (nq ? nq : 1), ctx.stream);
+    if (nv) PCU_CUDA(cudaMemcpyAsync(dv.get(), pv, 3 * nv * 8, cudaMemcpyHostToDevice, ctx.stream));
+    if (nq) {
+      PCU_CUDA(cudaMemcpyAsync(dq.get(), quads, 4 * nq * 4, cudaMemcpyHostToDevice, ctx.stream));
+      PCU_CUDA(cudaMemcpyAsync(de.get(), edges, nq * 8, cudaMemcpyHostToDevice, ctx.stream));
+      PCU_CUDA(cudaMemcpyAsync(df.get(), samples, 2 * nq * 4, cudaMemcpyHostToDevice, ctx.stream));
+    }
+    std::unique_ptr<pamopt_cu_mesh_s> m(new pamopt_cu_mesh_s());
+    pcu::triangulate_quads(ctx, dv.get(), nv, dq.get(), de.get(), df.get(), nq, R, beta, m->V, m->F, m->nv, m->nf);
+    m->owner = c;
+    ctx_ref(c);
+    *out = m.release();
+  });
+}
+
+int pamopt_cu_interpolate_patch_vertex(pamopt_cu_ctx c, const double* p0, const double* p1, const float* f0,
+                                       const float* f1, int64_t n, double beta, double* out) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(n >= 0 && (n == 0 || (p0 && p1 && f0 && f1 && out)), PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(beta > 0.0, PAMOPT_CU_EINVAL, "beta must be positive");
+    if (n == 0) return;
+    pcu::Ctx& ctx = c->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    pcu::DevBuf<double> a(3 * n, ctx.stream), b(3 * n, ctx.stream), o(3 * n, ctx.stream);
+    pcu::DevBuf<float> x(n, ctx.stream), y(n, ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(a.get(), p0, 3 * n * 8, cudaMemcpyHostToDevice, ctx.stream));
+    PCU_CUDA(cudaMemcpyAsync(b.get(), p1, 3 * n * 8, cudaMemcpyHostToDevice, ctx.stream));
+    PCU_CUDA(cudaMemcpyAsync(x.get(), f0, n * 4, cudaMemcpyHostToDevice, ctx.stream));
+    PCU_CUDA(cudaMemcpyAsync(y.get(), f1, n * 4, cudaMemcpyHostToDevice, ctx.stream));
+    const int64_t bad = pcu::interpolate_patch_vertex(ctx, a.get(), b.get(), x.get(), y.get(), n, beta, o.get());
+    d2h(ctx, out, o.get(), 3 * n);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    PCU_REQUIRE(bad == 0, PAMOPT_CU_EINVAL, "interpolate_patch_vertex: f0 and f1 must change sign");
+  });
+}
+
 // -------------------------------------------------------------------------- tri_isect
 int pamopt_cu_self_intersections(pamopt_cu_mesh m, int32_t* pairs, int64_t cap, int64_t* n) {
   return guarded([&] {
@@ -1088,6 +1200,57 @@ int pamopt_cu_tri_tri_pairs(pamopt_cu_mesh m, const int32_t* pairs, int64_t n, i
     PCU_CUDA(cudaMemcpyAsync(out, dout.get(), n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx.stream));
     PCU_CUDA(cudaStreamSynchronize(ctx.stream));
   });
+}
+
+static void pairs_call(pamopt_cu_mesh m, const int32_t* pairs, int64_t n,
+                       const std::function<void(pcu::Ctx&, const int32_t*)>& fn) {
+  PCU_REQUIRE(m && n >= 0 && (n == 0 || pairs), PAMOPT_CU_EINVAL, "null argument");
+  if (n == 0) return;
+  pcu::Ctx& ctx = m->owner->ctx;
+  pcu::DeviceGuard g(ctx.device);
+  for (int64_t i = 0; i < 2 * n; ++i)
+    PCU_REQUIRE(pairs[i] >= 0 && pairs[i] < m->nf, PAMOPT_CU_EINVAL, "face index out of range");
+  check_indices(ctx, m);
+  pcu::DevBuf<int32_t> dp(2 * n, ctx.stream);
+  PCU_CUDA(cudaMemcpyAsync(dp.get(), pairs, 2 * n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx.stream));
+  fn(ctx, dp.get());
+  PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+int pamopt_cu_classify_pair(pamopt_cu_mesh m, const int32_t* pairs, int64_t n, int32_t* shared, int32_t* coplanar) {
+  return guarded([&] {
+    pairs_call(m, pairs, n, [&](pcu::Ctx& ctx, const int32_t* dp) {
+      pcu::DevBuf<int32_t> s(n, ctx.stream), c(n, ctx.stream);
+      pcu::classify_pairs(ctx, m->V.get(), m->F.get(), dp, n, s.get(), c.get());
+      d2h(ctx, shared, s.get(), n);
+      d2h(ctx, coplanar, c.get(), n);
+      PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    });
+  });
+}
+
+static int by_class(pamopt_cu_mesh m, const int32_t* pairs, int64_t n, int mode, int32_t* out) {
+  return guarded([&] {
+    PCU_REQUIRE(n == 0 || out, PAMOPT_CU_EINVAL, "null argument");
+    pairs_call(m, pairs, n, [&](pcu::Ctx& ctx, const int32_t* dp) {
+      pcu::DevBuf<int32_t> o(n, ctx.stream);
+      pcu::verdict_by_class(ctx, m->V.get(), m->F.get(), dp, n, mode, o.get());
+      d2h(ctx, out, o.get(), n);
+      PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    });
+    for (int64_t i = 0; i < n; ++i)
+      PCU_REQUIRE(out[i] >= 0, PAMOPT_CU_EINVAL,
+                  mode == 1 ? "intersect_3d: coplanar pair (use intersect_coplanar)"
+                            : "intersect_coplanar: non-coplanar pair (use intersect_3d)");
+  });
+}
+
+int pamopt_cu_intersect_3d(pamopt_cu_mesh m, const int32_t* pairs, int64_t n, int32_t* out) {
+  return by_class(m, pairs, n, 1, out);
+}
+
+int pamopt_cu_intersect_coplanar(pamopt_cu_mesh m, const int32_t* pairs, int64_t n, int32_t* out) {
+  return by_class(m, pairs, n, 2, out);
 }
 
 // ---------------------------------------------------------------------------- stage 2
@@ -1130,6 +1293,249 @@ int pamopt_cu_simplify(pamopt_cu_mesh m, int64_t target, const pamopt_cu_simplif
     if (per_iter)
       for (int64_t i = 0; i < std::min<int64_t>(per_iter_cap, static_cast<int64_t>(S.per_iter.size())); ++i)
         per_iter[i] = S.per_iter[i];
+  });
+}
+
+// ----------------------------------------------------------- stage 2, granular operations
+
+int pamopt_cu_quadrics(pamopt_cu_mesh m, double* out) {
+  return guarded([&] {
+    PCU_REQUIRE(m && out, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    validate(ctx, m);
+    pcu::DevBuf<double> q(10 * (m->nv ? m->nv : 1), ctx.stream);
+    pcu::quadrics_of(ctx, m->V.get(), m->F.get(), m->nv, m->nf, q.get());
+    d2h(ctx, out, q.get(), 10 * m->nv);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+static void check_edges(const pamopt_cu_mesh_s* m, const int32_t* edges, int64_t n) {
+  for (int64_t i = 0; i < 2 * n; ++i)
+    PCU_REQUIRE(edges[i] >= 0 && edges[i] < m->nv, PAMOPT_CU_EINVAL, "edge vertex out of range");
+}
+
+int pamopt_cu_edge_cost(pamopt_cu_mesh m, const int32_t* edges, int64_t n, double we, double ws, double* cost,
+                        double* place) {
+  return guarded([&] {
+    PCU_REQUIRE(m && n >= 0 && (n == 0 || (edges && cost)), PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(we >= 0 && ws >= 0, PAMOPT_CU_EINVAL, "edge_cost: weights must be >= 0");
+    check_edges(m, edges, n);
+    if (n == 0) return;
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    validate(ctx, m);
+    pcu::DevBuf<int32_t> de(2 * n, ctx.stream);
+    pcu::DevBuf<double> dc(n, ctx.stream), dp(3 * n, ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(de.get(), edges, 2 * n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx.stream));
+    pcu::edge_cost_of(ctx, m->V.get(), m->F.get(), m->nv, m->nf, de.get(), n, we, ws, dc.get(), dp.get());
+    d2h(ctx, cost, dc.get(), n);
+    d2h(ctx, place, dp.get(), 3 * n);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+int pamopt_cu_pack_cost(pamopt_cu_ctx c, const double* cost, const uint32_t* ids, int64_t n, uint64_t* keys) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(n >= 0 && (n == 0 || (cost && ids && keys)), PAMOPT_CU_EINVAL, "null argument");
+    if (n == 0) return;
+    pcu::Ctx& ctx = c->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    pcu::DevBuf<double> dc(n, ctx.stream);
+    pcu::DevBuf<uint32_t> di(n, ctx.stream);
+    pcu::DevBuf<uint64_t> dk(n, ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(dc.get(), cost, n * 8, cudaMemcpyHostToDevice, ctx.stream));
+    PCU_CUDA(cudaMemcpyAsync(di.get(), ids, n * 4, cudaMemcpyHostToDevice, ctx.stream));
+    const int64_t nan = pcu::pack_cost_of(ctx, dc.get(), di.get(), n, dk.get());
+    d2h(ctx, keys, dk.get(), n);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    PCU_REQUIRE(nan == 0, PAMOPT_CU_ENUMERIC, "pack_cost: NaN cost");
+  });
+}
+
+int pamopt_cu_link_condition(pamopt_cu_mesh m, const int32_t* edges, int64_t n, int32_t* out) {
+  return guarded([&] {
+    PCU_REQUIRE(m && n >= 0 && (n == 0 || (edges && out)), PAMOPT_CU_EINVAL, "null argument");
+    check_edges(m, edges, n);
+    if (n == 0) return;
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    validate(ctx, m);
+    pcu::DevBuf<int32_t> de(2 * n, ctx.stream), dout(n, ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(de.get(), edges, 2 * n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx.stream));
+    pcu::link_condition_of(ctx, m->F.get(), m->nv, m->nf, de.get(), n, dout.get());
+    d2h(ctx, out, dout.get(), n);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    for (int64_t i = 0; i < n; ++i)
+      PCU_REQUIRE(out[i] >= 0, PAMOPT_CU_EINVAL, "link_condition_holds: unknown edge");
+  });
+}
+
+struct pamopt_cu_qem_s {
+  pamopt_cu_mesh mesh = nullptr;
+  pcu::SimplifyStats S;
+  pcu::QemState* q = nullptr;
+  ~pamopt_cu_qem_s() {
+    if (q) pcu::qem_destroy(q);
+  }
+};
+
+extern "C++" {
+template <class Fn>
+static int with_qem(pamopt_cu_qem q, Fn&& fn) {
+  return guarded([&] {
+    PCU_REQUIRE(q && q->q, PAMOPT_CU_EINVAL, "null qem state");
+    pcu::Ctx& ctx = q->mesh->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    fn(ctx);
+  });
+}
+}
+
+int pamopt_cu_qem_create(pamopt_cu_mesh m, int64_t target, const pamopt_cu_simplify_params* params, pamopt_cu_qem* out) {
+  return guarded([&] {
+    PCU_REQUIRE(m && out, PAMOPT_CU_EINVAL, "null argument");
+    const pcu::SimplifyParams P = to_params(params);
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    validate(ctx, m);
+    std::unique_ptr<pamopt_cu_qem_s> s(new pamopt_cu_qem_s());
+    s->mesh = m;
+    s->q = pcu::qem_create(ctx, m->V, m->F, m->nv, m->nf, target, P, s->S);
+    *out = s.release();
+  });
+}
+
+int pamopt_cu_qem_done(pamopt_cu_qem q, int32_t* done) {
+  return with_qem(q, [&](pcu::Ctx&) {
+    PCU_REQUIRE(done, PAMOPT_CU_EINVAL, "null argument");
+    *done = pcu::qem_done(q->q) ? 1 : 0;
+  });
+}
+
+int pamopt_cu_qem_prepare(pamopt_cu_qem q, int64_t* n_edges) {
+  return with_qem(q, [&](pcu::Ctx&) {
+    PCU_REQUIRE(!pcu::qem_done(q->q), PAMOPT_CU_EINVAL, "qem: the run is finished");
+    pcu::qem_prepare(q->q);
+    if (n_edges) *n_edges = pcu::qem_view(q->q).ne;
+  });
+}
+
+int pamopt_cu_qem_edges(pamopt_cu_qem q, int32_t* edges, uint64_t* keys, double* place, uint8_t* valid, int64_t cap) {
+  return with_qem(q, [&](pcu::Ctx& ctx) {
+    PCU_REQUIRE(pcu::qem_phase(q->q) >= 1, PAMOPT_CU_EINVAL, "qem: edges exist after prepare()");
+    const pcu::QemView v = pcu::qem_view(q->q);
+    const int64_t n = std::min(cap, v.ne);
+    if (n <= 0) return;
+    std::vector<int32_t> a(edges ? n : 0), b(edges ? n : 0);
+    if (edges) {
+      d2h(ctx, a.data(), v.ea, n);
+      d2h(ctx, b.data(), v.eb, n);
+    }
+    d2h(ctx, keys, v.key, n);
+    d2h(ctx, place, v.place, 3 * n);
+    d2h(ctx, valid, v.valid, n);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (edges)
+      for (int64_t i = 0; i < n; ++i) {
+        edges[2 * i] = a[i];
+        edges[2 * i + 1] = b[i];
+      }
+    if (keys && place) {  // invalid edges carry no placement
+      for (int64_t i = 0; i < n; ++i)
+        if (keys[i] == ~0ull) place[3 * i] = place[3 * i + 1] = place[3 * i + 2] = 0.0;
+    }
+  });
+}
+
+int pamopt_cu_qem_propagate_and_mark(pamopt_cu_qem q, int64_t* n_marked) {
+  return with_qem(q, [&](pcu::Ctx&) {
+    pcu::qem_propagate_and_mark(q->q);
+    if (n_marked) *n_marked = pcu::qem_view(q->q).nm;
+  });
+}
+
+int pamopt_cu_qem_marked(pamopt_cu_qem q, uint32_t* ids, int64_t cap, uint64_t* face_keys, int64_t cap_faces) {
+  return with_qem(q, [&](pcu::Ctx& ctx) {
+    PCU_REQUIRE(pcu::qem_phase(q->q) >= 2, PAMOPT_CU_EINVAL, "qem: marked edges exist after propagate_and_mark()");
+    const pcu::QemView v = pcu::qem_view(q->q);
+    const int64_t n = std::min(cap, v.nm);
+    std::vector<uint64_t> k(ids && n > 0 ? n : 0);
+    if (ids && n > 0) d2h(ctx, k.data(), v.marked_sorted, n);
+    if (face_keys && cap_faces > 0 && v.nf > 0) {
+      pcu::DevBuf<uint64_t> fk(v.nf, ctx.stream);
+      pcu::qem_face_keys(q->q, fk.get());
+      d2h(ctx, face_keys, fk.get(), std::min(cap_faces, v.nf));
+      PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    for (int64_t i = 0; i < static_cast<int64_t>(k.size()); ++i) ids[i] = static_cast<uint32_t>(k[i]);
+  });
+}
+
+int pamopt_cu_qem_collapse_batch(pamopt_cu_qem q, uint8_t* link_ok, int64_t cap) {
+  return with_qem(q, [&](pcu::Ctx& ctx) {
+    pcu::qem_collapse_batch(q->q);
+    const pcu::QemView v = pcu::qem_view(q->q);
+    const int64_t n = std::min(cap, v.nm);
+    if (link_ok && n > 0) {
+      std::vector<uint32_t> r(n);
+      d2h(ctx, r.data(), v.rem, n);
+      PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+      for (int64_t i = 0; i < n; ++i) link_ok[i] = r[i] ? 1 : 0;
+    }
+  });
+}
+
+int pamopt_cu_qem_undo_loop(pamopt_cu_qem q, int32_t* rounds, int64_t* n_applied, uint8_t* applied, int64_t cap) {
+  return with_qem(q, [&](pcu::Ctx& ctx) {
+    pcu::qem_undo_loop(q->q);
+    const pcu::QemView v = pcu::qem_view(q->q);
+    if (rounds) *rounds = v.rounds;
+    if (n_applied) *n_applied = v.succ;
+    const int64_t n = std::min(cap, v.nm);
+    if (applied && n > 0) {
+      d2h(ctx, applied, v.applied, n);
+      PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+  });
+}
+
+int pamopt_cu_qem_end_iteration(pamopt_cu_qem q, int64_t* alive_faces) {
+  return with_qem(q, [&](pcu::Ctx&) {
+    pcu::qem_end_iteration(q->q);
+    if (alive_faces) *alive_faces = pcu::qem_view(q->q).alive_faces;
+  });
+}
+
+int pamopt_cu_qem_mesh(pamopt_cu_qem q, double* v, int32_t* f, uint8_t* falive, int64_t* nv, int64_t* nf) {
+  return with_qem(q, [&](pcu::Ctx& ctx) {
+    const pcu::QemView w = pcu::qem_view(q->q);
+    if (nv) *nv = w.nv;
+    if (nf) *nf = w.nf;
+    d2h(ctx, v, w.X, 3 * w.nv);
+    d2h(ctx, f, w.F, 3 * w.nf);
+    d2h(ctx, falive, w.falive, w.nf);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+int pamopt_cu_qem_finish(pamopt_cu_qem q, pamopt_cu_simplify_stats* stats) {
+  return with_qem(q, [&](pcu::Ctx& ctx) {
+    PCU_REQUIRE(pcu::qem_phase(q->q) == 0, PAMOPT_CU_EINVAL, "qem: finish() inside an iteration");
+    pcu::qem_finish(q->q);
+    PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+    to_stats(q->S, stats);
+  });
+}
+
+int pamopt_cu_qem_destroy(pamopt_cu_qem q) {
+  return guarded([&] {
+    if (!q) return;
+    pcu::DeviceGuard g(q->mesh->owner->ctx.device);
+    delete q;
   });
 }
 

@@ -432,6 +432,115 @@ __global__ void k_quad_write(GridView g, const uint32_t* __restrict__ cells, con
   }
 }
 
+// build_quads view: the quads in output order (cell, axis) with their valid
+// edge (lower lattice vertex linear index * 3 + axis), endpoint samples and split decision
+__global__ void k_quad_list(GridView g, const uint32_t* __restrict__ cells, const uint8_t* __restrict__ cases,
+                            const uint8_t* __restrict__ flips, const uint32_t* __restrict__ vbase,
+                            const uint32_t* __restrict__ cellmap, int64_t c0, int64_t na,
+                            const uint8_t* __restrict__ codes, const uint32_t* __restrict__ qoff,
+                            int32_t* __restrict__ quads, int64_t* __restrict__ qedge, float* __restrict__ qf,
+                            uint8_t* __restrict__ qsplit) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na || codes[i] == 0) return;
+  int64_t x, y, z;
+  cell_xyz(cells[i], g.R, x, y, z);
+  uint32_t o = qoff[i];
+  const int64_t n1 = g.R + 1;
+  for (int a = 0; a < 3; ++a) {
+    const int sc = (codes[i] >> (2 * a)) & 3;
+    if (!sc) continue;
+    QuadGeo Q;
+    make_quad(g, x, y, z, a, cellmap, cases, flips, vbase, c0, Q);
+    for (int k = 0; k < 4; ++k) quads[4 * o + k] = static_cast<int32_t>(Q.q[k]);
+    qedge[o] = (x + n1 * (y + n1 * z)) * 3 + a;
+    qf[2 * o] = Q.f0;
+    qf[2 * o + 1] = Q.f1;
+    qsplit[o] = static_cast<uint8_t>(sc);
+    ++o;
+  }
+}
+
+__global__ void k_quad_ncount(const uint8_t* __restrict__ codes, int64_t na, uint32_t* __restrict__ nq) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= na) return;
+  const uint8_t c = codes[i];
+  nq[i] = ((c & 3) != 0) + (((c >> 2) & 3) != 0) + (((c >> 4) & 3) != 0);
+}
+
+// triangulate_quads on explicit quads: edge = lower vertex * 3 + axis
+__device__ __forceinline__ QuadGeo quad_from(const int32_t* quads, const int64_t* qedge, const float* qf, int64_t i,
+                                             int R) {
+  QuadGeo Q;
+  for (int k = 0; k < 4; ++k) Q.q[k] = static_cast<uint32_t>(quads[4 * i + k]);
+  const int64_t n1 = R + 1, lv = qedge[i] / 3;
+  const int a = static_cast<int>(qedge[i] % 3);
+  const int64_t x = lv % n1, y = (lv / n1) % n1, z = lv / (n1 * n1);
+  int64_t up[3] = {x, y, z};
+  up[a] += 1;
+  Q.plo = gpoint(x, y, z, R);
+  Q.phi = gpoint(up[0], up[1], up[2], R);
+  Q.f0 = qf[2 * i];
+  Q.f1 = qf[2 * i + 1];
+  return Q;
+}
+
+__global__ void k_triq_count(const int32_t* __restrict__ quads, const int64_t* __restrict__ qedge,
+                             const float* __restrict__ qf, int64_t nq, int R, const double* __restrict__ V,
+                             uint8_t* __restrict__ code, uint64_t* __restrict__ counts) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nq) return;
+  const QuadGeo Q = quad_from(quads, qedge, qf, i, R);
+  const int sc = split_code(Q, V);
+  code[i] = static_cast<uint8_t>(sc);
+  counts[i] = (static_cast<uint64_t>(sc == 3 ? 4 : 2) << 32) | (sc == 3 ? 1u : 0u);
+}
+
+__global__ void k_triq_write(const int32_t* __restrict__ quads, const int64_t* __restrict__ qedge,
+                             const float* __restrict__ qf, int64_t nq, int R, const uint8_t* __restrict__ code,
+                             const uint64_t* __restrict__ offs, uint64_t nv_patch, double beta, double* __restrict__ V,
+                             int32_t* __restrict__ Fo) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nq) return;
+  const QuadGeo Q = quad_from(quads, qedge, qf, i, R);
+  const int32_t* q = quads + 4 * i;
+  int32_t* o = Fo + 3 * (offs[i] >> 32);
+  const int sc = code[i];
+  if (sc == 1) {
+    const int32_t t[6] = {q[0], q[1], q[2], q[0], q[2], q[3]};
+    for (int k = 0; k < 6; ++k) o[k] = t[k];
+  } else if (sc == 2) {
+    const int32_t t[6] = {q[0], q[1], q[3], q[1], q[2], q[3]};
+    for (int k = 0; k < 6; ++k) o[k] = t[k];
+  } else {
+    const uint64_t ve = nv_patch + (offs[i] & 0xffffffffu);
+    const D3 p = crossing(Q.plo, Q.phi, Q.f0, Q.f1, beta);
+    V[3 * ve] = p.x;
+    V[3 * ve + 1] = p.y;
+    V[3 * ve + 2] = p.z;
+    const int32_t e = static_cast<int32_t>(ve);
+    const int32_t t[12] = {q[0], q[1], e, q[1], q[2], e, q[2], q[3], e, q[3], q[0], e};
+    for (int k = 0; k < 12; ++k) o[k] = t[k];
+  }
+}
+
+// interpolate_patch_vertex for explicit edges; bad[i] = equal signs
+__global__ void k_interp(const double* __restrict__ p0, const double* __restrict__ p1, const float* __restrict__ f0,
+                         const float* __restrict__ f1, int64_t n, double beta, double* __restrict__ out,
+                         unsigned long long* __restrict__ bad) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  if ((f0[i] < 0.0f) == (f1[i] < 0.0f) || !isfinite(f0[i]) || !isfinite(f1[i])) {
+    atomicAdd(bad, 1ull);
+    out[3 * i] = out[3 * i + 1] = out[3 * i + 2] = 0.0;
+    return;
+  }
+  const D3 q = crossing(D3{p0[3 * i], p0[3 * i + 1], p0[3 * i + 2]}, D3{p1[3 * i], p1[3 * i + 1], p1[3 * i + 2]}, f0[i],
+                        f1[i], beta);
+  out[3 * i] = q.x;
+  out[3 * i + 1] = q.y;
+  out[3 * i + 2] = q.z;
+}
+
 }  // namespace
 
 void dmc_table_host(int32_t* out) {
@@ -522,6 +631,58 @@ void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, 
   PCU_LAUNCH(ctx, k_quad_write, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
              vbase.get(), cellmap.get(), c0, na, codes.get(), offs.get(), nv_patch, static_cast<int64_t>(shift), beta,
              res.V.get(), res.F.get());
+  if (res.want_stages && shift == 0) {  // build_patches / build_quads views (whole grid)
+    res.vbase = std::move(vbase);
+    res.nv_patch = nv_patch;
+    DevBuf<uint32_t> nq(na, ctx.stream), qoff(na, ctx.stream);
+    PCU_LAUNCH(ctx, k_quad_ncount, grid_for(na, 256), 256, 0, codes.get(), na, nq.get());
+    exclusive_scan_u32(ctx, nq.get(), qoff.get(), na);
+    res.n_quads = static_cast<uint64_t>(read_scalar(ctx, qoff.get() + na - 1)) + read_scalar(ctx, nq.get() + na - 1);
+    const uint64_t m = res.n_quads ? res.n_quads : 1;
+    res.quads.alloc(4 * m, ctx.stream);
+    res.qedge.alloc(m, ctx.stream);
+    res.qf.alloc(2 * m, ctx.stream);
+    res.qsplit.alloc(m, ctx.stream);
+    PCU_LAUNCH(ctx, k_quad_list, grid_for(na, 128), 128, 0, g, res.cells.get(), res.cases.get(), res.flips.get(),
+               res.vbase.get(), cellmap.get(), c0, na, codes.get(), qoff.get(), res.quads.get(), res.qedge.get(),
+               res.qf.get(), res.qsplit.get());
+  }
+}
+
+void triangulate_quads(Ctx& ctx, const double* d_patch_v, int64_t nv_patch, const int32_t* d_quads,
+                       const int64_t* d_qedge, const float* d_qf, int64_t nq, int R, double beta, DevBuf<double>& V,
+                       DevBuf<int32_t>& F, int64_t& nv, int64_t& nf) {
+  upload_table(ctx.device);
+  if (nq == 0) {
+    nv = nv_patch;
+    nf = 0;
+    V.alloc(3 * (nv ? nv : 1), ctx.stream);
+    if (nv) PCU_CUDA(cudaMemcpyAsync(V.get(), d_patch_v, 3 * nv * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+    F.alloc(1, ctx.stream);
+    return;
+  }
+  DevBuf<uint8_t> code(nq, ctx.stream);
+  DevBuf<uint64_t> counts(nq, ctx.stream), offs(nq, ctx.stream);
+  PCU_LAUNCH(ctx, k_triq_count, grid_for(nq, 128), 128, 0, d_quads, d_qedge, d_qf, nq, R, d_patch_v, code.get(),
+             counts.get());
+  exclusive_scan_u64(ctx, counts.get(), offs.get(), nq);
+  const uint64_t last = read_scalar(ctx, offs.get() + nq - 1) + read_scalar(ctx, counts.get() + nq - 1);
+  nf = static_cast<int64_t>(last >> 32);
+  nv = nv_patch + static_cast<int64_t>(last & 0xffffffffu);
+  V.alloc(3 * (nv ? nv : 1), ctx.stream);
+  F.alloc(3 * (nf ? nf : 1), ctx.stream);
+  if (nv_patch) PCU_CUDA(cudaMemcpyAsync(V.get(), d_patch_v, 3 * nv_patch * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+  PCU_LAUNCH(ctx, k_triq_write, grid_for(nq, 128), 128, 0, d_quads, d_qedge, d_qf, nq, R, code.get(), offs.get(),
+             static_cast<uint64_t>(nv_patch), beta, V.get(), F.get());
+}
+
+int64_t interpolate_patch_vertex(Ctx& ctx, const double* d_p0, const double* d_p1, const float* d_f0, const float* d_f1,
+                                 int64_t n, double beta, double* d_out) {
+  if (n == 0) return 0;
+  DevBuf<unsigned long long> bad(1, ctx.stream);
+  bad.memset(0, ctx.stream);
+  PCU_LAUNCH(ctx, k_interp, grid_for(n, 256), 256, 0, d_p0, d_p1, d_f0, d_f1, n, beta, d_out, bad.get());
+  return static_cast<int64_t>(read_scalar(ctx, bad.get()));
 }
 
 namespace {

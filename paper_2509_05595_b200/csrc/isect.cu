@@ -802,6 +802,46 @@ __global__ void __launch_bounds__(128, PCU_NARROW_MINB) k_narrow(const double* _
   }
 }
 
+// classify_pair: shared count by index; coplanar <=> every unshared vertex of
+// T2 has exact orientation 0 w.r.t. T1's plane (a degenerate face counts as coplanar: all its
+// orientations vanish).  3 shared = a duplicate face (excluded upstream by the SPEC).
+__device__ int pair_coplanar(const double* __restrict__ V, const int32_t* t1, const int32_t* t2, const PairInfo& I) {
+  const D3 T1[3] = {vtx(V, t1[0]), vtx(V, t1[1]), vtx(V, t1[2])};
+  if (degenerate(T1[0], T1[1], T1[2]) || degenerate(vtx(V, t2[0]), vtx(V, t2[1]), vtx(V, t2[2]))) return 1;
+  for (int j = 0; j < 3; ++j)
+    if (I.s2[j] < 0 && o3(vtx(V, t2[j]), T1[0], T1[1], T1[2]) != 0) return 0;
+  return 1;
+}
+
+__global__ void k_pair_class(const double* __restrict__ V, const int32_t* __restrict__ F,
+                             const int32_t* __restrict__ pairs, int64_t n, int32_t* __restrict__ shared,
+                             int32_t* __restrict__ coplanar) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int32_t* t1 = F + 3 * pairs[2 * i];
+  const int32_t* t2 = F + 3 * pairs[2 * i + 1];
+  const PairInfo I = pair_info(t1, t2);
+  shared[i] = I.shared;
+  coplanar[i] = I.shared == 3 ? 1 : pair_coplanar(V, t1, t2, I);
+}
+
+// intersect_3d (mode 1) / intersect_coplanar (mode 2) restricted to their class: out = -1 when
+// the pair violates the precondition (coplanar for 3D, non-coplanar for coplanar)
+__global__ void k_verdict_class(const double* __restrict__ V, const int32_t* __restrict__ F,
+                                const int32_t* __restrict__ pairs, int64_t n, int mode, int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int32_t* t1 = F + 3 * pairs[2 * i];
+  const int32_t* t2 = F + 3 * pairs[2 * i + 1];
+  const PairInfo I = pair_info(t1, t2);
+  const int cop = I.shared == 3 ? 1 : pair_coplanar(V, t1, t2, I);
+  if ((mode == 1) == (cop == 1)) {
+    out[i] = -1;
+    return;
+  }
+  out[i] = verdict(V, t1, t2) ? 1 : 0;  // the class-dispatching verdict takes exactly this branch
+}
+
 __global__ void k_verdict_pairs(const double* __restrict__ V, const int32_t* __restrict__ F,
                                 const int32_t* __restrict__ pairs, int64_t n, int32_t* __restrict__ out) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -954,6 +994,18 @@ std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, 
 void tri_tri_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int32_t* d_out) {
   if (n == 0) return;
   PCU_LAUNCH(ctx, k_verdict_pairs, grid_for(n, 128), 128, 0, dV, dF, d_pairs, n, d_out);
+}
+
+void classify_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int32_t* d_shared,
+                    int32_t* d_coplanar) {
+  if (n == 0) return;
+  PCU_LAUNCH(ctx, k_pair_class, grid_for(n, 128), 128, 0, dV, dF, d_pairs, n, d_shared, d_coplanar);
+}
+
+void verdict_by_class(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int mode,
+                      int32_t* d_out) {
+  if (n == 0) return;
+  PCU_LAUNCH(ctx, k_verdict_class, grid_for(n, 128), 128, 0, dV, dF, d_pairs, n, mode, d_out);
 }
 
 void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,

@@ -25,6 +25,14 @@ struct DmcResult {
   DevBuf<int32_t> F;
   uint64_t nv = 0, nf = 0, n_quads = 0;
   uint64_t nvp_own = 0, n_extra = 0;  // V = [own patch vertices, extra (4-split) vertices]
+  // stage views (whole-grid extract with want_stages): build_patches / build_quads
+  bool want_stages = false;
+  DevBuf<uint32_t> vbase;  // first patch vertex per active cell
+  uint64_t nv_patch = 0;
+  DevBuf<int32_t> quads;   // 4 patch-vertex ids per quad (oriented - -> +)
+  DevBuf<int64_t> qedge;   // lower lattice vertex * 3 + axis
+  DevBuf<float> qf;        // samples at the edge's lower / upper vertex
+  DevBuf<uint8_t> qsplit;  // 1: diagonal 0-2, 2: diagonal 1-3, 3: four triangles
 };
 void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res);
 // z-slab extraction: d_planes holds lattice planes [pz0, pz1); cells of layers
@@ -35,6 +43,14 @@ void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, 
 // F[i] -> patch_base + F[i] if F[i] < nvp_own, else extra_base + (F[i] - nvp_own)
 void mesh_rebase(Ctx& ctx, int32_t* dF, int64_t nidx, int64_t patch_base, int64_t nvp_own, int64_t extra_base);
 void dmc_table_host(int32_t* out);
+// triangulate_quads on explicit quads (patch vertices + quads + valid-edge data): V = [patch
+// vertices, extra vertices in quad order], faces in quad order
+void triangulate_quads(Ctx& ctx, const double* d_patch_v, int64_t nv_patch, const int32_t* d_quads,
+                       const int64_t* d_qedge, const float* d_qf, int64_t nq, int R, double beta, DevBuf<double>& V,
+                       DevBuf<int32_t>& F, int64_t& nv, int64_t& nf);
+// returns the number of entries whose samples do not change sign (SPEC.md:270 error)
+int64_t interpolate_patch_vertex(Ctx& ctx, const double* d_p0, const double* d_p1, const float* d_f0, const float* d_f1,
+                                 int64_t n, double beta, double* d_out);
 
 // ---- certification / quality metrics (metrics.cu)
 struct TopologyResult {
@@ -100,6 +116,12 @@ void normalize_unit_cube(Ctx& ctx, double* dV, int64_t nv, double padding, doubl
 std::vector<int32_t> self_intersections(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf,
                                         const uint8_t* d_alive, const uint8_t* d_query);
 void tri_tri_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int32_t* d_out);
+// classify_pair (shared count, coplanar flag) and the class-restricted verdicts (mode 1:
+// intersect_3d, mode 2: intersect_coplanar; -1 = precondition violated)
+void classify_pairs(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int32_t* d_shared,
+                    int32_t* d_coplanar);
+void verdict_by_class(Ctx& ctx, const double* dV, const int32_t* dF, const int32_t* d_pairs, int64_t n, int mode,
+                      int32_t* d_out);
 
 // Broad phase + narrow phase of the QEM undo loop, asynchronous: results (found pairs, buffer
 // overflow) are left in device scalars; detect_scalars_ptr/size let the caller fetch them in
@@ -134,6 +156,45 @@ struct SimplifyStats {
   int64_t face_iterations = 0, alg_bytes = 0;
   std::vector<int64_t> per_iter;
 };
+// Stepwise QEM run (one object per simplify_to).  The mesh buffers are
+// simplified in place; qem_finish compacts them.  Steps must be called in order per iteration.
+struct QemState;
+QemState* qem_create(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& F, int64_t& nv, int64_t& nf, int64_t target,
+                     const SimplifyParams& P, SimplifyStats& S);
+void qem_destroy(QemState* q);
+bool qem_done(const QemState* q);
+void qem_prepare(QemState* q);
+void qem_propagate_and_mark(QemState* q);
+void qem_collapse_batch(QemState* q);
+void qem_undo_loop(QemState* q);
+void qem_end_iteration(QemState* q);
+void qem_finish(QemState* q);
+int qem_phase(const QemState* q);
+// device views of the current iteration (valid until the next step)
+struct QemView {
+  int64_t nv = 0, nf = 0, ne = 0, nm = 0, alive_faces = 0, succ = 0;
+  int rounds = 0;
+  const double* X = nullptr;
+  const int32_t* F = nullptr;
+  const uint8_t *falive = nullptr, *valive = nullptr;
+  const double* Q = nullptr;
+  const int32_t *ea = nullptr, *eb = nullptr;
+  const uint64_t* key = nullptr;
+  const double* place = nullptr;
+  const uint8_t* valid = nullptr;
+  const uint64_t* marked_sorted = nullptr;
+  const uint32_t* rem = nullptr;
+  const uint8_t* applied = nullptr;
+};
+QemView qem_view(QemState* q);
+void qem_face_keys(QemState* q, uint64_t* d_out);  // per face: min key of its vertices' valid edges
+// standalone SPEC operations on a whole mesh (every face alive); device arrays
+void quadrics_of(Ctx& ctx, const double* X, const int32_t* F, int64_t nv, int64_t nf, double* dQ);
+void edge_cost_of(Ctx& ctx, const double* X, const int32_t* F, int64_t nv, int64_t nf, const int32_t* d_edges,
+                  int64_t n, double we, double ws, double* d_cost, double* d_place);
+int64_t pack_cost_of(Ctx& ctx, const double* d_cost, const uint32_t* d_ids, int64_t n, uint64_t* d_keys);  // #NaN
+void link_condition_of(Ctx& ctx, const int32_t* F, int64_t nv, int64_t nf, const int32_t* d_edges, int64_t n,
+                       int32_t* d_out);  // 1 / 0, -1 = not an edge
 // Simplifies in place.  On return dV/dF hold the compacted mesh (sizes updated).
 void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& F, int64_t& nv, int64_t& nf, int64_t target,
                   const SimplifyParams& P, SimplifyStats& S);

@@ -30,7 +30,11 @@
 namespace pcu {
 namespace {
 
-constexpr int kMaxDeg = 255;      // per-vertex incident-face capacity of the local buffers
+// Vertices with at most kLocalDeg incident faces keep their per-thread sets in registers/local
+// memory; larger valences (unbounded, as the reference's std::set-based code) work in global
+// scratch regions aligned with the CSR incidence (2 slots per incidence entry + 1 per vertex), which
+// no other thread touches: marked edges have disjoint 1-rings, so their endpoints are distinct.
+constexpr int kLocalDeg = 32;
 constexpr double k4Sqrt3 = 6.928203230275509;
 
 struct Counters {
@@ -110,13 +114,12 @@ __global__ void k_quadrics(const double* __restrict__ X, const int32_t* __restri
 }
 
 // ----------------------------------------------------------------------------- edges
-// neighbours b > a of vertex a, sorted unique; returns count (or -1 on capacity overflow).
+// neighbours b > a of vertex a, sorted unique; returns the count.  nb/mult hold >= 2 deg(a) slots.
 // mult[i] = number of alive faces holding edge (a, nb[i]).
+template <class I, class M>
 __device__ int upper_neighbours(int a, const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
-                                const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int32_t* nb,
-                                uint8_t* mult) {
+                                const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, I* nb, M* mult) {
   const int d = static_cast<int>(deg[a]);
-  if (d > kMaxDeg) return -1;
   int n = 0;
   for (int i = 0; i < d; ++i) {
     const int32_t* t = F + 3 * inc[off[a] + i];
@@ -152,20 +155,22 @@ __global__ void k_edge_count(const int32_t* __restrict__ F, const uint32_t* __re
                              Counters* cnt) {
   const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (a >= nv) return;
-  int32_t nb[2 * kMaxDeg];
-  uint8_t mult[2 * kMaxDeg];
-  const int u = deg[a] ? upper_neighbours(static_cast<int>(a), F, off, deg, inc, nb, mult) : 0;
-  if (u < 0) {
-    atomicAdd(&cnt->cap, 1ull);
-    ecount[a] = 0;
-    return;
-  }
-  int bad = 0;
   const int64_t s0 = 2 * static_cast<int64_t>(off[a]);
-  for (int i = 0; i < u; ++i) {
-    bad |= (mult[i] != 1 && mult[i] != 2);
-    snb[s0 + i] = nb[i];
-    smult[s0 + i] = mult[i];
+  const int d = static_cast<int>(deg[a]);
+  int u = 0;
+  int bad = 0;
+  if (d <= kLocalDeg) {
+    int32_t nb[2 * kLocalDeg];
+    uint8_t mult[2 * kLocalDeg];
+    u = d ? upper_neighbours(static_cast<int>(a), F, off, deg, inc, nb, mult) : 0;
+    for (int i = 0; i < u; ++i) {
+      bad |= (mult[i] != 1 && mult[i] != 2);
+      snb[s0 + i] = nb[i];
+      smult[s0 + i] = mult[i];
+    }
+  } else {  // high valence: sort and deduplicate in the vertex's own CSR-aligned scratch slots
+    u = upper_neighbours(static_cast<int>(a), F, off, deg, inc, snb + s0, smult + s0);
+    for (int i = 0; i < u; ++i) bad |= (smult[s0 + i] != 1 && smult[s0 + i] != 2);
   }
   if (bad) atomicAdd(&cnt->err, 1ull);  // non-manifold edge: input must come from stage 1
   ecount[a] = static_cast<uint32_t>(u);
@@ -270,22 +275,12 @@ __device__ double ring_skinny(const double* X, const int32_t* F, const int32_t* 
   return cs;
 }
 
-#ifndef PCU_COST_MINB
-#define PCU_COST_MINB 8
-#endif
-__global__ void __launch_bounds__(128, PCU_COST_MINB) k_cost(const double* __restrict__ X, const int32_t* __restrict__ F, const double* __restrict__ Q,
-                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
-                       const int32_t* __restrict__ inc, const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
-                       const uint8_t* __restrict__ valid, const unsigned long long* __restrict__ d_ne, double we,
-                       double ws, uint64_t* __restrict__ key, double* __restrict__ place, Counters* cnt) {
-  const int64_t ne = static_cast<int64_t>(*d_ne);
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-  if (!valid[e]) {
-    key[e] = ~0ull;
-    continue;
-  }
-  const int a = ea[e], b = eb[e];
+// Eq. 1 for edge (a, b) under the merged quadric K_a + K_b: placement x (adjugate solve, or the
+// cheapest of {mid, a, b} when det == 0 or the 1-norm condition exceeds 1e8, P8) and its cost
+__device__ __forceinline__ double edge_cost_eval(const double* __restrict__ X, const int32_t* __restrict__ F,
+                                                 const double* __restrict__ Q, const uint32_t* __restrict__ off,
+                                                 const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc,
+                                                 int a, int b, double we, double ws, D3& x) {
   double q[10];
   for (int k = 0; k < 10; ++k) q[k] = Q[10 * a + k] + Q[10 * b + k];
   const D3 pa = P3(X, a), pb = P3(X, b);
@@ -294,7 +289,7 @@ __global__ void __launch_bounds__(128, PCU_COST_MINB) k_cost(const double* __res
                m22 = q[7];
   const double det = m00 * (m11 * m22 - m12 * m21) - m01 * (m10 * m22 - m12 * m20) + m02 * (m10 * m21 - m11 * m20);
   bool ok = det != 0.0;
-  D3 x{0.0, 0.0, 0.0};
+  x = D3{0.0, 0.0, 0.0};
   if (ok) {
     const double rdet = 1.0 / det;  // adjugate * (1/det)
     const double i00 = (m11 * m22 - m12 * m21) * rdet, i01 = (m02 * m21 - m01 * m22) * rdet,
@@ -336,17 +331,69 @@ __global__ void __launch_bounds__(128, PCU_COST_MINB) k_cost(const double* __res
       x = pb;
     }
   }
-  if (cost != cost) {
-    atomicAdd(&cnt->nan, 1ull);
-    key[e] = ~0ull;
-    continue;
-  }
+  return cost;
+}
+
+// pack_cost: f32 bits of max(cost, 0) << 32 | id
+__device__ __forceinline__ uint64_t pack_key(double cost, uint64_t id) {
   const float cf = __double2float_rn(cost < 0.0 ? 0.0 : cost);
-  key[e] = (static_cast<uint64_t>(__float_as_uint(cf)) << 32) | static_cast<uint64_t>(e);
-  place[3 * e] = x.x;
-  place[3 * e + 1] = x.y;
-  place[3 * e + 2] = x.z;
+  return (static_cast<uint64_t>(__float_as_uint(cf)) << 32) | id;
+}
+
+#ifndef PCU_COST_MINB
+#define PCU_COST_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PCU_COST_MINB) k_cost(const double* __restrict__ X, const int32_t* __restrict__ F, const double* __restrict__ Q,
+                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
+                       const int32_t* __restrict__ inc, const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                       const uint8_t* __restrict__ valid, const unsigned long long* __restrict__ d_ne, double we,
+                       double ws, uint64_t* __restrict__ key, double* __restrict__ place, Counters* cnt) {
+  const int64_t ne = static_cast<int64_t>(*d_ne);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!valid[e]) {
+      key[e] = ~0ull;
+      continue;
+    }
+    D3 x;
+    const double cost = edge_cost_eval(X, F, Q, off, deg, inc, ea[e], eb[e], we, ws, x);
+    if (cost != cost) {
+      atomicAdd(&cnt->nan, 1ull);
+      key[e] = ~0ull;
+      continue;
+    }
+    key[e] = pack_key(cost, static_cast<uint64_t>(e));
+    place[3 * e] = x.x;
+    place[3 * e + 1] = x.y;
+    place[3 * e + 2] = x.z;
   }
+}
+
+// standalone edge_cost for explicit edges (granular C-ABI)
+__global__ void k_edge_cost_raw(const double* __restrict__ X, const int32_t* __restrict__ F, const double* __restrict__ Q,
+                                const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
+                                const int32_t* __restrict__ inc, const int32_t* __restrict__ edges, int64_t n, double we,
+                                double ws, double* __restrict__ cost, double* __restrict__ place) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  D3 x;
+  cost[i] = edge_cost_eval(X, F, Q, off, deg, inc, edges[2 * i], edges[2 * i + 1], we, ws, x);
+  place[3 * i] = x.x;
+  place[3 * i + 1] = x.y;
+  place[3 * i + 2] = x.z;
+}
+
+__global__ void k_pack_cost(const double* __restrict__ cost, const uint32_t* __restrict__ ids, int64_t n,
+                            uint64_t* __restrict__ keys, unsigned long long* __restrict__ nan) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double c = cost[i];
+  if (c != c) {
+    atomicAdd(nan, 1ull);
+    keys[i] = ~0ull;
+    return;
+  }
+  keys[i] = pack_key(c, ids[i]);
 }
 
 // --------------------------------------------------------------------- propagation
@@ -405,10 +452,10 @@ __device__ int faces_of_edge(int a, int b, const int32_t* F, const uint32_t* off
 // incident faces builds the multiset of their other vertices (a vertex counted once per face);
 // after sorting, v is a boundary vertex (mesh.cpp:298-356: some ring vertex lies in exactly one
 // incident face) iff some value occurs once — the same verdict without the O(deg^2) rescans.
-__device__ int link_set(int v, const int32_t* F, const uint32_t* off, const uint32_t* deg, const int32_t* inc,
-                        int32_t* out) {
+template <class I>
+__device__ int link_set(int v, const int32_t* F, const uint32_t* off, const uint32_t* deg, const int32_t* inc, I* out) {
   int n = 0;
-  const int d = min(static_cast<int>(deg[v]), kMaxDeg);
+  const int d = static_cast<int>(deg[v]);
   const int32_t* L = inc + off[v];
   for (int i = 0; i < d; ++i) {
     const int32_t* t = F + 3 * L[i];
@@ -443,13 +490,14 @@ __device__ int link_set(int v, const int32_t* F, const uint32_t* off, const uint
   return u;
 }
 
+// la / lb: >= 2 deg + 1 slots each (link sets of a and b); common = la ∩ lb is written in place
+// over la (its write position never passes the read position)
+template <class I>
 __device__ bool link_condition(int a, int b, const int32_t* F, const uint32_t* off, const uint32_t* deg,
-                               const int32_t* inc) {
-  int32_t la[2 * kMaxDeg + 1], lb[2 * kMaxDeg + 1];
+                               const int32_t* inc, I* la, I* lb) {
   const int na = link_set(a, F, off, deg, inc, la);
   const int nb = link_set(b, F, off, deg, inc, lb);
-  // common = la ∩ lb (sorted)
-  int32_t common[2 * kMaxDeg + 1];
+  I* common = la;
   int nc = 0;
   for (int i = 0, j = 0; i < na && j < nb;) {
     if (la[i] < lb[j]) ++i;
@@ -460,7 +508,9 @@ __device__ bool link_condition(int a, int b, const int32_t* F, const uint32_t* o
       ++j;
     }
   }
-  // link(ab): opposite vertices of faces(a,b) (+ -2 if boundary edge)
+  // link(ab): opposite vertices of faces(a,b) (+ -2 if boundary edge).  A manifold edge has at
+  // most two faces (k_edge_count rejects anything else before the first batch); more than 6
+  // opposite vertices cannot equal a link set here, so the edge fails the condition.
   int32_t lab[8];
   int nl = 0, nfe = 0;
   for (uint32_t i = 0; i < deg[a]; ++i) {
@@ -468,7 +518,10 @@ __device__ bool link_condition(int a, int b, const int32_t* F, const uint32_t* o
     if (!has(t, b)) continue;
     ++nfe;
     for (int k = 0; k < 3; ++k)
-      if (t[k] != a && t[k] != b && nl < 7) lab[nl++] = t[k];
+      if (t[k] != a && t[k] != b) {
+        if (nl == 7) return false;
+        lab[nl++] = t[k];
+      }
   }
   if (nfe == 1) lab[nl++] = -2;
   for (int i = 1; i < nl; ++i) {
@@ -513,12 +566,20 @@ __global__ void k_link(const uint64_t* __restrict__ marked, int64_t nm, const in
                        const int32_t* __restrict__ eb, const uint8_t* __restrict__ enf, const int32_t* __restrict__ F,
                        const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
                        const int32_t* __restrict__ inc, uint32_t* __restrict__ rem, uint64_t* __restrict__ newinv,
-                       Counters* cnt) {
+                       Counters* cnt, int32_t* __restrict__ lscr) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= nm) return;
   const uint32_t e = static_cast<uint32_t>(marked[i]);
   const int a = ea[e], b = eb[e];
-  if (link_condition(a, b, F, off, deg, inc)) {
+  bool ok;
+  if (deg[a] <= kLocalDeg && deg[b] <= kLocalDeg) {
+    int32_t la[2 * kLocalDeg + 1], lb[2 * kLocalDeg + 1];
+    ok = link_condition(a, b, F, off, deg, inc, la, lb);
+  } else {  // high valence: per-vertex global scratch (2 slots per incidence entry + 1)
+    ok = link_condition(a, b, F, off, deg, inc, lscr + 2 * static_cast<int64_t>(off[a]) + a,
+                        lscr + 2 * static_cast<int64_t>(off[b]) + b);
+  }
+  if (ok) {
     rem[i] = enf[e];
   } else {
     rem[i] = 0;
@@ -689,77 +750,239 @@ __global__ void k_inv_remap(uint64_t* __restrict__ inv, int64_t n, const uint32_
 
 }  // namespace
 
-void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv, int64_t& nf, int64_t target,
-                  const SimplifyParams& P, SimplifyStats& S) {
-  cudaStream_t st = ctx.stream;
-  PCU_REQUIRE(target >= 0, PAMOPT_CU_EINVAL, "simplify_to: negative target");
-  if (nf <= target || nf == 0) return;
-  double* X = V.get();
-  int32_t* F = Fb.get();
-  DevBuf<uint8_t> falive(nf, st), valive(nv, st);
-  PCU_CUDA(cudaMemsetAsync(falive.get(), 1, nf, st));
-  PCU_CUDA(cudaMemsetAsync(valive.get(), 1, nv, st));
-  DevBuf<double> Q(10 * nv, st);
-  DevBuf<uint32_t> deg(nv, st), off(nv, st), cur(nv, st), ecount(nv, st), eoff(nv, st);
-  const int64_t ecap = 3 * nf + 16;
-  DevBuf<int32_t> rlist(3 * nf + 16, st);
-  DevBuf<int32_t> inc(3 * nf, st), ea(ecap, st), eb(ecap, st), owner(nf, st), qf(3 * nf + 16, st),
-      qf2(3 * nf + 16, st), Fprev(3 * nf, st);
-  DevBuf<uint8_t> enf(ecap, st), valid(ecap, st), revert(ecap, st);
-  DevBuf<int32_t> snb(6 * nf + 16, st);  // upper-neighbour scratch, 2 slots per incidence entry
-  DevBuf<uint8_t> smult(6 * nf + 16, st);
-  DevBuf<uint64_t> key(ecap, st), marked(ecap, st), marked_sorted(ecap, st);
-  DevBuf<double> place(3 * ecap, st);
-  DevBuf<unsigned long long> vmin(nv, st), vfmin(nv, st);
-  DevBuf<uint32_t> rem(ecap, st), remoff(ecap, st);
-  DevBuf<Counters> cnt(1, st);
-  DevBuf<uint64_t> inv(16, st), newinv(ecap, st), invtmp(16, st);
+// --------------------------------------------------------- standalone SPEC operations (C-ABI)
+namespace {
+// link_condition_holds per query edge (mesh.cpp:301-358); -1 = not an edge of the mesh (the
+// reference throws std::invalid_argument, mesh.cpp:302).  High-valence queries get private
+// global scratch at lofs[i] (query edges may share vertices, unlike a marked batch).
+__global__ void k_link_sizes(const int32_t* __restrict__ edges, int64_t n, const uint32_t* __restrict__ deg,
+                             uint32_t* __restrict__ sz) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t da = deg[edges[2 * i]], db = deg[edges[2 * i + 1]];
+  sz[i] = (da <= kLocalDeg && db <= kLocalDeg) ? 0u : 2 * da + 2 * db + 2;
+}
+__global__ void k_link_pairs(const int32_t* __restrict__ edges, int64_t n, const int32_t* __restrict__ F,
+                             const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
+                             const int32_t* __restrict__ inc, const uint32_t* __restrict__ lofs,
+                             int32_t* __restrict__ lscr, int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const int a = min(edges[2 * i], edges[2 * i + 1]), b = max(edges[2 * i], edges[2 * i + 1]);
+  if (a == b || faces_of_edge(a, b, F, off, deg, inc) == 0) {
+    out[i] = -1;
+    return;
+  }
+  bool ok;
+  if (deg[a] <= kLocalDeg && deg[b] <= kLocalDeg) {
+    int32_t la[2 * kLocalDeg + 1], lb[2 * kLocalDeg + 1];
+    ok = link_condition(a, b, F, off, deg, inc, la, lb);
+  } else {
+    int32_t* base = lscr + lofs[i];
+    ok = link_condition(a, b, F, off, deg, inc, base, base + 2 * deg[a] + 1);
+  }
+  out[i] = ok ? 1 : 0;
+}
+
+struct StaticAdj {  // vertex -> face CSR of a whole mesh (every face alive), lists ascending
+  DevBuf<uint8_t> alive;
+  DevBuf<uint32_t> deg, off, cur;
+  DevBuf<int32_t> inc;
+  StaticAdj(Ctx& ctx, const int32_t* F, int64_t nv, int64_t nf) {
+    cudaStream_t st = ctx.stream;
+    alive.alloc(nf ? nf : 1, st);
+    deg.alloc(nv ? nv : 1, st);
+    off.alloc(nv ? nv : 1, st);
+    cur.alloc(nv ? nv : 1, st);
+    inc.alloc(3 * nf + 1, st);
+    if (nf) PCU_CUDA(cudaMemsetAsync(alive.get(), 1, nf, st));
+    PCU_CUDA(cudaMemsetAsync(deg.get(), 0, nv * sizeof(uint32_t), st));
+    PCU_CUDA(cudaMemsetAsync(cur.get(), 0, nv * sizeof(uint32_t), st));
+    if (nf) PCU_LAUNCH(ctx, k_deg, grid_for(nf, 256), 256, 0, F, alive.get(), nf, deg.get());
+    exclusive_scan_u32(ctx, deg.get(), off.get(), nv);
+    if (nf) PCU_LAUNCH(ctx, k_fill, grid_for(nf, 256), 256, 0, F, alive.get(), nf, off.get(), cur.get(), inc.get());
+    PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
+  }
+};
+}  // namespace
+
+void quadrics_of(Ctx& ctx, const double* X, const int32_t* F, int64_t nv, int64_t nf, double* dQ) {
+  if (nv == 0) return;
+  StaticAdj A(ctx, F, nv, nf);
+  PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, A.off.get(), A.deg.get(), A.inc.get(), nv, dQ);
+}
+
+void edge_cost_of(Ctx& ctx, const double* X, const int32_t* F, int64_t nv, int64_t nf, const int32_t* d_edges,
+                  int64_t n, double we, double ws, double* d_cost, double* d_place) {
+  if (n == 0) return;
+  StaticAdj A(ctx, F, nv, nf);
+  DevBuf<double> Q(10 * (nv ? nv : 1), ctx.stream);
+  PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, A.off.get(), A.deg.get(), A.inc.get(), nv, Q.get());
+  PCU_LAUNCH(ctx, k_edge_cost_raw, grid_for(n, 128), 128, 0, X, F, Q.get(), A.off.get(), A.deg.get(), A.inc.get(),
+             d_edges, n, we, ws, d_cost, d_place);
+}
+
+int64_t pack_cost_of(Ctx& ctx, const double* d_cost, const uint32_t* d_ids, int64_t n, uint64_t* d_keys) {
+  if (n == 0) return 0;
+  DevBuf<unsigned long long> nan(1, ctx.stream);
+  nan.memset(0, ctx.stream);
+  PCU_LAUNCH(ctx, k_pack_cost, grid_for(n, 256), 256, 0, d_cost, d_ids, n, d_keys, nan.get());
+  return static_cast<int64_t>(read_scalar(ctx, nan.get()));
+}
+
+void link_condition_of(Ctx& ctx, const int32_t* F, int64_t nv, int64_t nf, const int32_t* d_edges, int64_t n,
+                       int32_t* d_out) {
+  if (n == 0) return;
+  StaticAdj A(ctx, F, nv, nf);
+  DevBuf<uint32_t> sz(n, ctx.stream), lofs(n, ctx.stream);
+  PCU_LAUNCH(ctx, k_link_sizes, grid_for(n, 256), 256, 0, d_edges, n, A.deg.get(), sz.get());
+  exclusive_scan_u32(ctx, sz.get(), lofs.get(), n);
+  const int64_t tot = static_cast<int64_t>(read_scalar(ctx, lofs.get() + n - 1)) + read_scalar(ctx, sz.get() + n - 1);
+  DevBuf<int32_t> lscr(tot ? tot : 1, ctx.stream);
+  PCU_LAUNCH(ctx, k_link_pairs, grid_for(n, 64), 64, 0, d_edges, n, F, A.off.get(), A.deg.get(), A.inc.get(),
+             lofs.get(), lscr.get(), d_out);
+}
+
+// ---------------------------------------------------------------- stepwise driver (Algorithm 1)
+// One QEM run as a state object whose methods are the SPEC operations of one iteration, in order:
+//   prepare()             quadrics are kept; CSR incidence, lexicographic edges, invalid flags,
+//                         edge_cost + pack_cost for every valid edge
+//   propagate_and_mark()  per-face min keys, independent edges
+//   collapse_batch()      link condition, overshoot trim, parallel collapse
+//   undo_loop()           detect on batch-modified faces, revert owners, repeat
+//   end_iteration()       invalid-flag retention and the stall counter
+// simplify_run() drives it to the target (simplify_to); the C-ABI exposes the
+// same steps one by one (pamopt_cu_qem_*), so the granular operations ARE the pipeline code.
+struct QemState {
+  Ctx& ctx;
+  cudaStream_t st;
+  DevBuf<double>& V;
+  DevBuf<int32_t>& Fb;
+  int64_t& nv;
+  int64_t& nf;
+  int64_t target;
+  SimplifyParams P;
+  SimplifyStats& S;
+  double* X = nullptr;
+  int32_t* F = nullptr;
+  DevBuf<uint8_t> falive, valive;
+  DevBuf<double> Q;
+  DevBuf<uint32_t> deg, off, cur, ecount, eoff;
+  int64_t ecap;
+  DevBuf<int32_t> rlist, inc, ea, eb, owner, qf, qf2, Fprev, snb, lscr;
+  DevBuf<uint8_t> enf, valid, revert, smult;
+  DevBuf<uint64_t> key, marked, marked_sorted;
+  DevBuf<double> place;
+  DevBuf<unsigned long long> vmin, vfmin;
+  DevBuf<uint32_t> rem, remoff;
+  DevBuf<Counters> cnt;
+  DevBuf<uint64_t> inv, newinv;
   int64_t ninv = 0;
-  DevBuf<int32_t> bca(ecap, st), bcb(ecap, st);
-  DevBuf<uint8_t> bapplied(ecap, st);
-  DevBuf<double> boldx(3 * ecap, st), boldq(10 * ecap, st);
-  DevBuf<uint32_t> bnrem(ecap, st);
-  Batch B{bca.get(), bcb.get(), bapplied.get(), boldx.get(), boldq.get(), bnrem.get()};
-  IsectScratch* isc = isect_scratch_create();
-  struct ScratchGuard {
-    IsectScratch* s;
-    ~ScratchGuard() { isect_scratch_destroy(s); }
-  } guard{isc};
+  DevBuf<int32_t> bca, bcb;
+  DevBuf<uint8_t> bapplied;
+  DevBuf<double> boldx, boldq;
+  DevBuf<uint32_t> bnrem;
+  Batch B;
+  IsectScratch* isc = nullptr;
   size_t sort_tmp_bytes = 0;
   DevBuf<uint8_t> sort_tmp;
+  int64_t alive_faces = 0, alive_verts = 0;
+  int retain = 0, zero_run = 0;
+  int64_t ne_hint = 0;
+  std::vector<uint8_t> ds_host;
+  unsigned gs_grid = 0;
+  // per-iteration results
+  int64_t ne = 0, nm = 0, succ = 0, nnew = 0, nq = 0;
+  int rounds = 0;
+  Counters hc{};  // counters read at the collapse-batch synchronisation
+  int phase = 0;  // 0 idle, 1 prepared, 2 marked, 3 collapsed, 4 undone
 
-  auto build_incidence = [&]() {
+  QemState(Ctx& c, DevBuf<double>& V_, DevBuf<int32_t>& F_, int64_t& nv_, int64_t& nf_, int64_t target_,
+           const SimplifyParams& P_, SimplifyStats& S_)
+      : ctx(c), st(c.stream), V(V_), Fb(F_), nv(nv_), nf(nf_), target(target_), P(P_), S(S_) {
+    X = V.get();
+    F = Fb.get();
+    falive.alloc(nf ? nf : 1, st);
+    valive.alloc(nv ? nv : 1, st);
+    if (nf) PCU_CUDA(cudaMemsetAsync(falive.get(), 1, nf, st));
+    if (nv) PCU_CUDA(cudaMemsetAsync(valive.get(), 1, nv, st));
+    Q.alloc(10 * (nv ? nv : 1), st);
+    for (DevBuf<uint32_t>* b : {&deg, &off, &cur, &ecount, &eoff}) b->alloc(nv ? nv : 1, st);
+    ecap = 3 * nf + 16;
+    rlist.alloc(3 * nf + 16, st);
+    inc.alloc(3 * nf + 16, st);
+    ea.alloc(ecap, st);
+    eb.alloc(ecap, st);
+    owner.alloc(nf + 16, st);
+    qf.alloc(3 * nf + 16, st);
+    qf2.alloc(3 * nf + 16, st);
+    Fprev.alloc(3 * nf + 16, st);
+    snb.alloc(6 * nf + 16, st);  // upper-neighbour scratch, 2 slots per incidence entry
+    lscr.alloc(6 * nf + nv + 16, st);  // high-valence link-set scratch (2 per incidence + 1 per vertex)
+    enf.alloc(ecap, st);
+    valid.alloc(ecap, st);
+    revert.alloc(ecap, st);
+    smult.alloc(6 * nf + 16, st);
+    key.alloc(ecap, st);
+    marked.alloc(ecap, st);
+    marked_sorted.alloc(ecap, st);
+    place.alloc(3 * ecap, st);
+    vmin.alloc(nv ? nv : 1, st);
+    vfmin.alloc(nv ? nv : 1, st);
+    rem.alloc(ecap, st);
+    remoff.alloc(ecap, st);
+    cnt.alloc(1, st);
+    inv.alloc(16, st);
+    newinv.alloc(ecap, st);
+    bca.alloc(ecap, st);
+    bcb.alloc(ecap, st);
+    bapplied.alloc(ecap, st);
+    boldx.alloc(3 * ecap, st);
+    boldq.alloc(10 * ecap, st);
+    bnrem.alloc(ecap, st);
+    B = Batch{bca.get(), bcb.get(), bapplied.get(), boldx.get(), boldq.get(), bnrem.get()};
+    isc = isect_scratch_create();
+    alive_faces = nf;
+    alive_verts = nv;
+    ne_hint = 3 * nf / 2 + 16;
+    ds_host.resize(detect_scalars_size());
+    gs_grid = static_cast<unsigned>(ctx.num_sms * 16);
+    ctx.prof.reset(st);
+    if (nf == 0 || nv == 0) return;
+    build_incidence();
+    boxes_init(ctx, *isc, X, F, nf, falive.get());
+    PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, off.get(), deg.get(), inc.get(), nv, Q.get());
+  }
+  ~QemState() { isect_scratch_destroy(isc); }
+  QemState(const QemState&) = delete;
+  QemState& operator=(const QemState&) = delete;
+
+  bool done() const { return nf == 0 || !(alive_faces > target && zero_run < P.stall); }
+
+  void build_incidence() {
     PCU_CUDA(cudaMemsetAsync(deg.get(), 0, nv * sizeof(uint32_t), st));
     PCU_LAUNCH(ctx, k_deg, grid_for(nf, 256), 256, 0, F, falive.get(), nf, deg.get());
     exclusive_scan_u32(ctx, deg.get(), off.get(), nv);
     PCU_CUDA(cudaMemsetAsync(cur.get(), 0, nv * sizeof(uint32_t), st));
     PCU_LAUNCH(ctx, k_fill, grid_for(nf, 256), 256, 0, F, falive.get(), nf, off.get(), cur.get(), inc.get());
     PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
-  };
+  }
 
-  ctx.prof.reset(st);
-  build_incidence();
-  boxes_init(ctx, *isc, X, F, nf, falive.get());
-  PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, off.get(), deg.get(), inc.get(), nv, Q.get());
-
-  int64_t alive_faces = nf, alive_verts = nv;
-  int retain = 0, zero_run = 0;
-  int64_t ne_hint = 3 * nf / 2 + 16;
-  unsigned long long* d_ne = &cnt.get()->edges;
-  std::vector<uint8_t> ds_host(detect_scalars_size());
   // Host synchronisations per iteration: one after marking, one after the collapse batch, one
   // per undo round (counters + detection scalars fetched together).
-  auto sync_counters = [&](bool with_detect) {
+  Counters sync_counters(bool with_detect) {
     Counters h;
     PCU_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(Counters), cudaMemcpyDeviceToHost, st));
     if (with_detect)
       PCU_CUDA(cudaMemcpyAsync(ds_host.data(), detect_scalars_ptr(*isc), ds_host.size(), cudaMemcpyDeviceToHost, st));
     PCU_CUDA(cudaStreamSynchronize(st));
     return h;
-  };
-  const unsigned gs_grid = static_cast<unsigned>(ctx.num_sms * 16);
-  // shrink the working set once a sizeable fraction of it is dead (one host sync per compaction)
-  auto compact_state = [&]() {
+  }
+
+  // shrink the working set once a sizeable fraction of it is dead (one host sync per compaction).
+  // Edge ids (lexicographic ranks over alive edges), incidence order, collapse direction (a < b)
+  // and the invalid-pair order are all invariant under a monotone renumbering.
+  void compact_state() {
     DevBuf<uint32_t> vk(nv, st), vmap(nv, st), fk(nf, st), fmap(nf, st);
     PCU_LAUNCH(ctx, k_u8_to_u32, grid_for(nv, 256), 256, 0, valive.get(), nv, vk.get());
     PCU_LAUNCH(ctx, k_u8_to_u32, grid_for(nf, 256), 256, 0, falive.get(), nf, fk.get());
@@ -785,8 +1008,11 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     PCU_CUDA(cudaMemsetAsync(falive.get(), 1, nf, st));
     PCU_CUDA(cudaMemsetAsync(valive.get(), 1, nv, st));
     boxes_init(ctx, *isc, X, F, nf, falive.get());
-  };
-  while (alive_faces > target && zero_run < P.stall) {
+  }
+
+  // edges, invalid flags, edge_cost + pack_cost
+  void prepare() {
+    PCU_REQUIRE(phase == 0, PAMOPT_CU_EINVAL, "qem: prepare() out of order");
     S.iterations++;
     ctx.prof.mark(st, "misc");
     if (alive_faces * 5 < nf * 3 && nf > 4096) compact_state();
@@ -794,6 +1020,7 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     if (S.iterations > 1) build_incidence();
     ctx.prof.mark(st, "incidence");
     cnt.memset(0, st);
+    unsigned long long* d_ne = &cnt.get()->edges;
     // edges (device-side count; kernels below stride over it)
     PCU_LAUNCH(ctx, k_edge_count, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, ecount.get(),
                snb.get(), smult.get(), cnt.get());
@@ -807,6 +1034,14 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     PCU_LAUNCH(ctx, k_cost, eg, 128, 0, X, F, Q.get(), off.get(), deg.get(), inc.get(), ea.get(), eb.get(), valid.get(),
                d_ne, P.we, P.ws, key.get(), place.get(), cnt.get());
     ctx.prof.mark(st, "cost");
+    phase = 1;
+  }
+
+  // per-face min keys and the independent set; one host sync
+  void propagate_and_mark() {
+    PCU_REQUIRE(phase == 1, PAMOPT_CU_EINVAL, "qem: propagate_and_mark() out of order");
+    unsigned long long* d_ne = &cnt.get()->edges;
+    const unsigned eg = std::min<unsigned>(grid_for(ne_hint, 128), gs_grid);
     PCU_CUDA(cudaMemsetAsync(vmin.get(), 0xFF, nv * 8, st));
     PCU_CUDA(cudaMemsetAsync(vfmin.get(), 0xFF, nv * 8, st));
     PCU_LAUNCH(ctx, k_prop_edges, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vmin.get());
@@ -814,21 +1049,20 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     PCU_LAUNCH(ctx, k_mark, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vfmin.get(), marked.get(),
                cnt.get());
     Counters h = sync_counters(false);  // ---- sync 1
-    const int64_t ne = static_cast<int64_t>(h.edges);
+    ne = static_cast<int64_t>(h.edges);
     ne_hint = ne;
     S.face_iterations += alive_faces;
     S.alg_bytes += 28 * alive_faces + 92 * alive_verts + 8 * ne;
-    PCU_REQUIRE(h.cap == 0, PAMOPT_CU_ECAP, "simplify_to: vertex valence exceeds 255 incident faces");
     if (S.iterations == 1)
       PCU_REQUIRE(h.err == 0, PAMOPT_CU_EINVAL, "simplify_to: non-manifold input (an edge has >2 faces); run stage 1");
     PCU_REQUIRE(h.nan == 0, PAMOPT_CU_ENUMERIC, "simplify_to: NaN edge cost");
     ctx.prof.mark(st, "propagate+mark");
-    const int64_t nm = static_cast<int64_t>(h.marked);
-    int64_t succ = 0;
-    int rounds = 0;
-    int64_t nnew = 0;
-    if (nm > 0) {
-      // marked keys in ascending order (deterministic collapse ids + the trim order)
+    nm = static_cast<int64_t>(h.marked);
+    succ = 0;
+    rounds = 0;
+    nnew = 0;
+    nq = 0;
+    if (nm > 0) {  // marked keys in ascending order (deterministic collapse ids + the trim order)
       if (!small_sort_u64(ctx, marked.get(), marked_sorted.get(), nm)) {
         size_t need = 0;
         cub::DeviceRadixSort::SortKeys(nullptr, need, marked.get(), marked_sorted.get(), static_cast<int>(nm), 0, 64,
@@ -842,67 +1076,88 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
                                        static_cast<int>(nm), 0, 64, st);
         if (sev) ctx.prof.kend("cub_sort_marked", sev, st);
       }
-      PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, marked_sorted.get(), nm, ea.get(), eb.get(), enf.get(), F,
-                 off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get());
-      exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
-      ctx.prof.mark(st, "sort+link");
-      PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-      PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), st));
-      PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, marked_sorted.get(), nm, rem.get(), remoff.get(),
-                 alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
-                 falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
-      h = sync_counters(false);  // ---- sync 2
-      ctx.prof.mark(st, "collapse");
-      int64_t nq = static_cast<int64_t>(h.query);
-      boxes_update(ctx, *isc, X, F, qf.get(), nq, falive.get());  // moved / renamed faces
-      int32_t* qa = qf.get();
-      int32_t* qb = qf2.get();
-      bool first_round = true;
-      int64_t nrest = 0;
-      while (nq > 0) {
-        PCU_CUDA(cudaMemsetAsync(revert.get(), 0, nm, st));
-        PCU_CUDA(cudaMemsetAsync(&cnt.get()->restored, 0, 8, st));
-        if (first_round)
-          undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nq, owner.get(), revert.get());
-        else
-          undo_detect_restored_async(ctx, *isc, X, F, nf, falive.get(), rlist.get(), nrest, qa, nq, owner.get(),
-                                     revert.get());
-        PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
-                   Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get(),
-                   rlist.get());
-        // rebuild the query list from still-applied collapses
-        PCU_CUDA(cudaMemsetAsync(&cnt.get()->query, 0, 8, st));
-        PCU_LAUNCH(ctx, k_requery, grid_for(nq, 256), 256, 0, qa, nq, owner.get(), B.applied, qb, cnt.get());
-        h = sync_counters(true);  // ---- sync per round
-        boxes_update(ctx, *isc, X, F, rlist.get(), static_cast<int64_t>(h.restored), falive.get());  // restored faces
-        unsigned long long found = 0, ncand = 0;
-        int redo = 0;
-        detect_read(ds_host.data(), &found, &redo, &ncand);
-        ctx.prof.mark(st, "undo_round");
-        if (redo) {  // candidate buffer overflow: nothing was flagged or reverted; grow and repeat
-          detect_grow(*isc, ncand);
-          continue;
-        }
-        if (found == 0) break;
-        ++rounds;
-        first_round = false;
-        nq = static_cast<int64_t>(h.query);
-        nrest = static_cast<int64_t>(h.restored);
-        std::swap(qa, qb);
-      }
-      succ = static_cast<int64_t>(h.applied);
-      alive_faces -= static_cast<int64_t>(h.removed);
-      nnew = static_cast<int64_t>(h.newinv);
-      S.link_failures += static_cast<int64_t>(h.link_fail);
-      S.undone += static_cast<int64_t>(h.undone);
     }
+    phase = 2;
+  }
+
+  // link condition on the pre-batch mesh, overshoot trim, parallel collapse
+  void collapse_batch() {
+    PCU_REQUIRE(phase == 2, PAMOPT_CU_EINVAL, "qem: collapse_batch() out of order");
+    phase = 3;
+    if (nm == 0) return;
+    PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, marked_sorted.get(), nm, ea.get(), eb.get(), enf.get(), F,
+               off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
+    exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
+    ctx.prof.mark(st, "sort+link");
+    PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), st));
+    PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, marked_sorted.get(), nm, rem.get(), remoff.get(),
+               alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
+               falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
+    hc = sync_counters(false);  // ---- sync 2
+    ctx.prof.mark(st, "collapse");
+    nq = static_cast<int64_t>(hc.query);
+    boxes_update(ctx, *isc, X, F, qf.get(), nq, falive.get());  // moved / renamed faces
+  }
+
+  // detect -> revert owners -> repeat until clean
+  void undo_loop() {
+    PCU_REQUIRE(phase == 3, PAMOPT_CU_EINVAL, "qem: undo_loop() out of order");
+    phase = 4;
+    if (nm == 0) return;
+    int32_t* qa = qf.get();
+    int32_t* qb = qf2.get();
+    bool first_round = true;
+    int64_t nrest = 0;
+    int64_t nqr = nq;
+    Counters h = hc;
+    while (nqr > 0) {
+      PCU_CUDA(cudaMemsetAsync(revert.get(), 0, nm, st));
+      PCU_CUDA(cudaMemsetAsync(&cnt.get()->restored, 0, 8, st));
+      if (first_round)
+        undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nqr, owner.get(), revert.get());
+      else
+        undo_detect_restored_async(ctx, *isc, X, F, nf, falive.get(), rlist.get(), nrest, qa, nqr, owner.get(),
+                                   revert.get());
+      PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
+                 Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get(),
+                 rlist.get());
+      // rebuild the query list from still-applied collapses
+      PCU_CUDA(cudaMemsetAsync(&cnt.get()->query, 0, 8, st));
+      PCU_LAUNCH(ctx, k_requery, grid_for(nqr, 256), 256, 0, qa, nqr, owner.get(), B.applied, qb, cnt.get());
+      h = sync_counters(true);  // ---- sync per round
+      boxes_update(ctx, *isc, X, F, rlist.get(), static_cast<int64_t>(h.restored), falive.get());  // restored faces
+      unsigned long long found = 0, ncand = 0;
+      int redo = 0;
+      detect_read(ds_host.data(), &found, &redo, &ncand);
+      ctx.prof.mark(st, "undo_round");
+      if (redo) {  // candidate buffer overflow: nothing was flagged or reverted; grow and repeat
+        detect_grow(*isc, ncand);
+        continue;
+      }
+      if (found == 0) break;
+      ++rounds;
+      first_round = false;
+      nqr = static_cast<int64_t>(h.query);
+      nrest = static_cast<int64_t>(h.restored);
+      std::swap(qa, qb);
+    }
+    succ = static_cast<int64_t>(h.applied);
+    alive_faces -= static_cast<int64_t>(h.removed);
+    nnew = static_cast<int64_t>(h.newinv);
+    S.link_failures += static_cast<int64_t>(h.link_fail);
+    S.undone += static_cast<int64_t>(h.undone);
+  }
+
+  // statistics and the invalid-flag update (SPEC.md:559 stall counter)
+  void end_iteration() {
+    PCU_REQUIRE(phase == 4, PAMOPT_CU_EINVAL, "qem: end_iteration() out of order");
     S.undo_hist[std::min(rounds, 7)]++;
     S.max_undo_rounds = std::max<int64_t>(S.max_undo_rounds, rounds);
     S.collapses += succ;
     alive_verts -= succ;
     S.per_iter.push_back(succ);
-    // invalid-flag update (duplicates are harmless for the binary search)
-    bool keep_old;
+    bool keep_old;  // (duplicates are harmless for the binary search)
     if (succ > 0) {
       keep_old = false;
       retain = 0;
@@ -923,27 +1178,112 @@ void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv,
     inv = std::move(merged);
     ninv = nall;
     ctx.prof.mark(st, "invalid_update");
+    phase = 0;
   }
+
+  void iterate() {
+    prepare();
+    propagate_and_mark();
+    collapse_batch();
+    undo_loop();
+    end_iteration();
+  }
+
   // compaction (mesh.cpp:278-292): alive vertices used by alive faces, order preserving
-  DevBuf<uint32_t> vk(nv, st), vmap(nv, st), fk(nf, st), fmap(nf, st);
-  vk.memset(0, st);
-  PCU_LAUNCH(ctx, k_used, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vk.get());
-  PCU_LAUNCH(ctx, k_vkeep, grid_for(nv, 256), 256, 0, valive.get(), nv, vk.get());
-  PCU_LAUNCH(ctx, k_fkeep, grid_for(nf, 256), 256, 0, falive.get(), nf, fk.get());
-  exclusive_scan_u32(ctx, vk.get(), vmap.get(), nv);
-  exclusive_scan_u32(ctx, fk.get(), fmap.get(), nf);
-  const int64_t nv2 = static_cast<int64_t>(read_scalar(ctx, vmap.get() + nv - 1)) + read_scalar(ctx, vk.get() + nv - 1);
-  const int64_t nf2 = static_cast<int64_t>(read_scalar(ctx, fmap.get() + nf - 1)) + read_scalar(ctx, fk.get() + nf - 1);
-  DevBuf<double> Vo(3 * (nv2 ? nv2 : 1), st);
-  DevBuf<int32_t> Fo(3 * (nf2 ? nf2 : 1), st);
-  PCU_LAUNCH(ctx, k_compact, grid_for(std::max(nv, nf), 256), 256, 0, X, F, nv, nf, vk.get(), vmap.get(), fk.get(),
-             fmap.get(), Vo.get(), Fo.get());
-  V = std::move(Vo);
-  Fb = std::move(Fo);
-  nv = nv2;
-  nf = nf2;
-  ctx.prof.mark(st, "compact");
-  ctx.prof.dump("simplify");
+  void finish() {
+    if (nf == 0 || nv == 0) return;
+    DevBuf<uint32_t> vk(nv, st), vmap(nv, st), fk(nf, st), fmap(nf, st);
+    vk.memset(0, st);
+    PCU_LAUNCH(ctx, k_used, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vk.get());
+    PCU_LAUNCH(ctx, k_vkeep, grid_for(nv, 256), 256, 0, valive.get(), nv, vk.get());
+    PCU_LAUNCH(ctx, k_fkeep, grid_for(nf, 256), 256, 0, falive.get(), nf, fk.get());
+    exclusive_scan_u32(ctx, vk.get(), vmap.get(), nv);
+    exclusive_scan_u32(ctx, fk.get(), fmap.get(), nf);
+    const int64_t nv2 = static_cast<int64_t>(read_scalar(ctx, vmap.get() + nv - 1)) + read_scalar(ctx, vk.get() + nv - 1);
+    const int64_t nf2 = static_cast<int64_t>(read_scalar(ctx, fmap.get() + nf - 1)) + read_scalar(ctx, fk.get() + nf - 1);
+    DevBuf<double> Vo(3 * (nv2 ? nv2 : 1), st);
+    DevBuf<int32_t> Fo(3 * (nf2 ? nf2 : 1), st);
+    PCU_LAUNCH(ctx, k_compact, grid_for(std::max(nv, nf), 256), 256, 0, X, F, nv, nf, vk.get(), vmap.get(), fk.get(),
+               fmap.get(), Vo.get(), Fo.get());
+    V = std::move(Vo);
+    Fb = std::move(Fo);
+    nv = nv2;
+    nf = nf2;
+    X = V.get();
+    F = Fb.get();
+    ctx.prof.mark(st, "compact");
+    ctx.prof.dump("simplify");
+  }
+};
+
+namespace {
+__global__ void k_face_keys(const int32_t* __restrict__ F, const uint8_t* __restrict__ falive, int64_t nf,
+                            const unsigned long long* __restrict__ vmin, uint64_t* __restrict__ out) {
+  const int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (f >= nf) return;
+  if (!falive[f]) {
+    out[f] = ~0ull;
+    return;
+  }
+  unsigned long long k = vmin[F[3 * f]];
+  k = vmin[F[3 * f + 1]] < k ? vmin[F[3 * f + 1]] : k;
+  k = vmin[F[3 * f + 2]] < k ? vmin[F[3 * f + 2]] : k;
+  out[f] = k;
+}
+}  // namespace
+
+QemState* qem_create(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& F, int64_t& nv, int64_t& nf, int64_t target,
+                     const SimplifyParams& P, SimplifyStats& S) {
+  PCU_REQUIRE(target >= 0, PAMOPT_CU_EINVAL, "simplify_to: negative target");
+  return new QemState(ctx, V, F, nv, nf, target, P, S);
+}
+void qem_destroy(QemState* q) { delete q; }
+bool qem_done(const QemState* q) { return q->done(); }
+void qem_prepare(QemState* q) { q->prepare(); }
+void qem_propagate_and_mark(QemState* q) { q->propagate_and_mark(); }
+void qem_collapse_batch(QemState* q) { q->collapse_batch(); }
+void qem_undo_loop(QemState* q) { q->undo_loop(); }
+void qem_end_iteration(QemState* q) { q->end_iteration(); }
+void qem_finish(QemState* q) { q->finish(); }
+int qem_phase(const QemState* q) { return q->phase; }
+
+QemView qem_view(QemState* q) {
+  QemView v;
+  v.nv = q->nv;
+  v.nf = q->nf;
+  v.ne = q->phase >= 2 ? q->ne : static_cast<int64_t>(read_scalar(q->ctx, &q->cnt.get()->edges));
+  v.nm = q->nm;
+  v.alive_faces = q->alive_faces;
+  v.X = q->X;
+  v.F = q->F;
+  v.falive = q->falive.get();
+  v.valive = q->valive.get();
+  v.Q = q->Q.get();
+  v.ea = q->ea.get();
+  v.eb = q->eb.get();
+  v.key = q->key.get();
+  v.place = q->place.get();
+  v.valid = q->valid.get();
+  v.marked_sorted = q->marked_sorted.get();
+  v.rem = q->rem.get();
+  v.applied = q->B.applied;
+  v.rounds = q->rounds;
+  v.succ = q->succ;
+  return v;
+}
+
+void qem_face_keys(QemState* q, uint64_t* d_out) {
+  PCU_REQUIRE(q->phase >= 2, PAMOPT_CU_EINVAL, "qem: face keys exist after propagate_and_mark()");
+  PCU_LAUNCH(q->ctx, k_face_keys, grid_for(q->nf, 256), 256, 0, q->F, q->falive.get(), q->nf, q->vmin.get(), d_out);
+}
+
+void simplify_run(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& Fb, int64_t& nv, int64_t& nf, int64_t target,
+                  const SimplifyParams& P, SimplifyStats& S) {
+  PCU_REQUIRE(target >= 0, PAMOPT_CU_EINVAL, "simplify_to: negative target");
+  if (nf <= target || nf == 0) return;
+  QemState q(ctx, V, Fb, nv, nf, target, P, S);
+  while (!q.done()) q.iterate();
+  q.finish();
 }
 
 }  // namespace pcu

@@ -113,3 +113,23 @@ def verdict_pairs(v, f, pairs):
         s2 = [next((k for k in range(3) if t1[k] == t2[j]), -1) for j in range(3)]
         out.append(1 if intersect([v[i] for i in t1], [v[i] for i in t2], s1, s2) else 0)
     return out
+
+
+def classify_pairs(v, f, pairs):
+    """classify_pair in exact rationals: (shared count by index, coplanar), a
+    degenerate face counting as coplanar."""
+    sh, cp = [], []
+    for a, b in pairs:
+        t1, t2 = f[a], f[b]
+        ns = sum(1 for k in range(3) if t1[k] in t2)
+        T1 = [tuple(Fraction(c) for c in v[i]) for i in t1]
+        T2 = [tuple(Fraction(c) for c in v[i]) for i in t2]
+        n1 = _cross(_sub(T1[1], T1[0]), _sub(T1[2], T1[0]))
+        n2 = _cross(_sub(T2[1], T2[0]), _sub(T2[2], T2[0]))
+        if ns == 3 or n1 == (0, 0, 0) or n2 == (0, 0, 0):
+            c = 1
+        else:
+            c = int(all(_dot(n1, _sub(p, T1[0])) == 0 for p in T2))
+        sh.append(ns)
+        cp.append(c)
+    return sh, cp

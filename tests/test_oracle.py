@@ -233,3 +233,12 @@ def test_simplify_deterministic_across_workers(oracle):
     oracle.set_workers(os.cpu_count() or 4)
     b = oracle.simplify(v, f, 200)
     assert np.array_equal(a[1], b[1]) and np.array_equal(bits(a[0]), bits(b[0]))
+
+
+def test_oracle_link_condition_high_valence_matches_reference(oracle):
+    """Valence 600-1000 (tests/golden/make_golden_valence.py, the reference's own
+    link_condition_holds): the oracle restatement has no capacity limit either."""
+    g = np.load(os.path.join(GOLD, "ref_link_valence.npz"))
+    for n in sorted({k.rsplit("_", 1)[0] for k in g.files}):
+        got = oracle.link_condition(g[f"{n}_v"], g[f"{n}_f"], g[f"{n}_e"])
+        assert np.array_equal(got.astype(np.int8), g[f"{n}_r"]), n

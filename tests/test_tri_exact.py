@@ -30,3 +30,17 @@ def test_narrow_phase_rigid_invariance(oracle):
     a = oracle.tri_tri_pairs(v, f, pairs)
     b = oracle.tri_tri_pairs(v * 4.0 + 0.5, f, pairs)
     assert np.array_equal(a, b)
+
+
+def test_acceptance3_corpus_10100(oracle):
+    """SPEC.md:809 acceptance #3 at its stated size: 10,100 pairs, 0 false negatives (and here 0
+    false positives) against the exact rational oracle; the committed record
+    (tests/golden/make_golden_tri.py) is re-derived live on a sample of every case family."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "tri_corpus_10100.npz"))
+    v, f, pairs = corpus(10100, seed=11)
+    got = oracle.tri_tri_pairs(v, f, pairs)
+    ref = g["verdict"]
+    assert int(((ref == 1) & (got == 0)).sum()) == 0 and int(((ref == 0) & (got == 1)).sum()) == 0
+    sub = np.arange(0, 10100, 7)
+    assert np.array_equal(np.array(verdict_pairs(v.tolist(), f.tolist(), pairs[sub].tolist())), ref[sub])
