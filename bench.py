@@ -315,6 +315,8 @@ def run_ours(args):
             "clocks": clk,
         }
         line["certification"] = cert
+        if world > 1:  # the communicator this run used (the driver's scaling run checks N ranks)
+            line["nccl"] = nccl_info(torch, dist, world)
         # the limiter of the UDF's dominant kernel from the committed ncu capture: k_brick is
         # instruction-issue bound (distance arithmetic), which is why the HBM fraction is small
         cp = os.path.join(ROOT, "profiles", f"r01_ncu_counters_{args.config}.json")
@@ -340,6 +342,12 @@ def run_ours(args):
     mesh.free()
     ctx.close()
     return 0
+
+
+def nccl_info(torch, dist, world):
+    v = torch.cuda.nccl.version()
+    return {"backend": dist.get_backend(), "world_size": world, "nccl_version": ".".join(str(x) for x in v),
+            "devices": torch.cuda.device_count()}
 
 
 # ------------------------------------------------------------------ C4 / C5 (multi-GPU configs)
@@ -417,6 +425,8 @@ def run_c4(args):
                 "config": {"workload": "C4", "faces_in": int(len(f)), "R": R, "dmc_faces": int(nf),
                            "parallelism": f"z-slabs x{world}: NCCL halo(2 planes) + slab-local DMC + mesh gather"},
                 "udf_voxels_per_s": round(n1 / (max_ms / args.steps * 1e-3), 1), "clocks": clk}
+        if world > 1:
+            line["nccl"] = nccl_info(torch, dist, world)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -488,6 +498,8 @@ def run_c5(args):
                 "config": {"workload": "C5", "meshes": len(meshes), "faces_in_total": int(sum(len(m[1]) for m in meshes)),
                            "parallelism": f"LPT one-mesh-per-GPU x{world}, {K} concurrent streams per GPU",
                            "lpt_makespan_ratio": round(D.makespan([len(m[1]) for m in meshes], world), 3)}}
+        if world > 1:
+            line["nccl"] = nccl_info(torch, dist, world)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

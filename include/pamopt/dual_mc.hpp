@@ -68,4 +68,64 @@ inline std::vector<std::pair<int64_t, uint8_t>> classify_voxels(const ScalarGrid
   return out;
 }
 
+/// interpolate_patch_vertex: v0 + t'(v1 - v0), t = -f0/(f1 - f0),
+/// t' = 1/(1 + exp(-beta (t - 1/2))); std::invalid_argument when f0, f1 share a sign.
+inline Vec3d interpolate_patch_vertex(const Vec3d& v0, const Vec3d& v1, float f0, float f1, double beta = 5.0) {
+  cuda::Context& ctx = cuda::Context::thread_default();
+  const double p0[3] = {v0[0], v0[1], v0[2]}, p1[3] = {v1[0], v1[1], v1[2]};
+  double o[3];
+  cuda::check(pamopt_cu_interpolate_patch_vertex(ctx.get(), p0, p1, &f0, &f1, 1, beta, o));
+  return Vec3d(o[0], o[1], o[2]);
+}
+
+/// build_patches + build_quads views and triangulate_quads.
+struct PatchSoup {
+  std::vector<Vec3d> vertices;       // (active cell, patch) order
+  std::vector<int64_t> patch_first;  // first patch vertex of each active cell
+};
+struct QuadMesh {
+  std::vector<std::array<int32_t, 4>> quads;  // patch-vertex ids, oriented negative -> positive
+  std::vector<int64_t> edges;                 // valid grid edge: lower lattice vertex * 3 + axis
+  std::vector<std::array<float, 2>> samples;  // SDF at the edge's lower / upper vertex
+  std::vector<uint8_t> split;                 // 1: diagonal 0-2, 2: diagonal 1-3, 3: four triangles
+};
+
+inline void dmc_stages(const ScalarGrid& grid, PatchSoup& patches, QuadMesh& quads, double beta = 5.0) {
+  cuda::Context& ctx = cuda::Context::thread_default();
+  pamopt_cu_grid g = nullptr;
+  cuda::check(pamopt_cu_grid_upload(ctx.get(), grid.resolution, grid.samples.data(), &g));
+  int64_t c[3] = {0, 0, 0};
+  int rc = pamopt_cu_dmc_stages(g, beta, c);
+  if (rc == PAMOPT_CU_OK) {
+    std::vector<double> v(3 * c[1]);
+    patches.patch_first.resize(c[0]);
+    rc = pamopt_cu_dmc_build_patches(g, v.data(), patches.patch_first.data());
+    patches.vertices.resize(c[1]);
+    for (int64_t i = 0; i < c[1]; ++i) patches.vertices[i] = Vec3d(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  }
+  if (rc == PAMOPT_CU_OK) {
+    quads.quads.resize(c[2]);
+    quads.edges.resize(c[2]);
+    quads.samples.resize(c[2]);
+    quads.split.resize(c[2]);
+    rc = pamopt_cu_dmc_build_quads(g, c[2] ? quads.quads[0].data() : nullptr, quads.edges.data(),
+                                   c[2] ? quads.samples[0].data() : nullptr, quads.split.data());
+  }
+  pamopt_cu_grid_free(g);
+  cuda::check(rc);
+}
+
+inline IndexedMesh triangulate_quads(int R, const PatchSoup& patches, const QuadMesh& q, double beta = 5.0) {
+  cuda::Context& ctx = cuda::Context::thread_default();
+  std::vector<double> v(3 * patches.vertices.size());
+  for (size_t i = 0; i < patches.vertices.size(); ++i)
+    for (int k = 0; k < 3; ++k) v[3 * i + k] = patches.vertices[i][k];
+  pamopt_cu_mesh m = nullptr;
+  cuda::check(pamopt_cu_triangulate_quads(ctx.get(), R, v.data(), static_cast<int64_t>(patches.vertices.size()),
+                                          q.quads.empty() ? nullptr : q.quads[0].data(), q.edges.data(),
+                                          q.samples.empty() ? nullptr : q.samples[0].data(),
+                                          static_cast<int64_t>(q.quads.size()), beta, &m));
+  return cuda::DeviceMesh(m).download();
+}
+
 }  // namespace pamopt

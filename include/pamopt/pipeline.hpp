@@ -1,9 +1,13 @@
-// pamopt/pipeline.hpp — stages 1-2 of the reference's missing run_pipeline
-// (proj/CMakeLists.txt:28 `src/pipeline.cpp`): UDF -> SDF -> DMC -> QEM on the
-// GPU in one call, device resident between stages.  Stage 3 (safe projection) is out of scope.
+// pamopt/pipeline.hpp — the reference's missing run_pipeline (proj/CMakeLists.txt:28
+// `src/pipeline.cpp`) on the GPU, device resident between stages:
+//   remesh()        stages 1-2 (UDF -> SDF -> DMC -> QEM) of a normalised mesh, the hot path;
+//   run_pipeline()  normalise -> stage 1 -> certify -> stage 2 -> certify -> [stage 3 (safe
+//                   projection) -> certify] -> denormalise, with a MeshReport per stage.
 #pragma once
 
 #include <cstdint>
+#include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "pamopt/cuda_detail.hpp"
@@ -53,6 +57,96 @@ inline IndexedMesh remesh(const IndexedMesh& normalized, int R, int64_t target_f
   }
   if (timings) *timings = StageTimings{tm.udf_ms, tm.dmc_ms, tm.simplify_ms, tm.total_ms, tm.dmc_faces, tm.dmc_vertices};
   return out;
+}
+
+/// PipelineConfig.  resolution 0 = the SPEC auto rule.
+struct PipelineConfig {
+  int resolution = 0;
+  int64_t target_faces = 0;   // 0: use target_ratio
+  double target_ratio = 0.01;
+  bool run_projection = false;
+  double beta = 5.0, eps = 0.0;
+  SimplifyParams simplify{};
+  int64_t report_samples = 16384;
+  uint64_t seed = 42;
+};
+
+/// MeshReport per stage (SPEC.md quality_metrics; CD/HD against the normalised input).
+struct StageReport {
+  double cd = 0, hd = 0, min_angle_deg = 0;
+  bool manifold = false, watertight = false, intersection_free = false;
+  int64_t faces = 0, vertices = 0;
+};
+
+struct PipelineResult {
+  IndexedMesh mesh;                 // denormalised to the input's coordinates
+  std::vector<StageReport> stages;  // stage 1, 2 (and 3 with projection)
+  bool stalled = false;
+  int resolution = 0;
+  int64_t target_faces = 0;
+  SimplifyStats simplify;
+  float stage_ms[4] = {0, 0, 0, 0};  // stage 1, 2, 3, certification
+  float total_ms = 0;
+};
+
+/// Thrown when a stage certification fails ("nonzero exit with stage name and
+/// diagnostic dump"); dump() is that stage's mesh in normalised coordinates.
+class CertificationError : public std::runtime_error {
+ public:
+  CertificationError(const std::string& m, int stage, IndexedMesh dump)
+      : std::runtime_error(m), stage_(stage), dump_(std::move(dump)) {}
+  int stage() const { return stage_; }
+  const IndexedMesh& dump() const { return dump_; }
+
+ private:
+  int stage_;
+  IndexedMesh dump_;
+};
+
+/// run_pipeline on an in-memory raw mesh (load_mesh, mesh_io.hpp:23, is the
+/// caller's): normalise, stage 1, certify, stage 2, certify, [stage 3, certify], denormalise.
+inline PipelineResult run_pipeline(const IndexedMesh& input, const PipelineConfig& c = {}) {
+  cuda::Context& ctx = cuda::Context::thread_default();
+  cuda::DeviceMesh dm(ctx, input);
+  pamopt_cu_pipeline_config cfg{};
+  cuda::check(pamopt_cu_pipeline_defaults(&cfg));
+  cfg.resolution = c.resolution;
+  cfg.run_projection = c.run_projection ? 1 : 0;
+  cfg.target_faces = c.target_faces;
+  cfg.target_ratio = c.target_ratio;
+  cfg.beta = c.beta;
+  cfg.eps = c.eps;
+  cfg.simplify = pamopt_cu_simplify_params{c.simplify.w_e, c.simplify.w_s, c.simplify.tolerance,
+                                           c.simplify.stall_iterations};
+  cfg.report_samples = c.report_samples;
+  cfg.seed = c.seed;
+  pamopt_cu_mesh out = nullptr;
+  pamopt_cu_pipeline_report rep{};
+  const int rc = pamopt_cu_run_pipeline(ctx.get(), dm.get(), &cfg, &out, &rep);
+  if (rc == PAMOPT_CU_ECERT) {
+    const std::string msg = pamopt_cu_last_error();
+    throw CertificationError(msg, rep.failed_stage, cuda::DeviceMesh(out).download());
+  }
+  cuda::check(rc);
+  PipelineResult r;
+  r.mesh = cuda::DeviceMesh(out).download();
+  for (int s = 0; s < (rep.projected ? 3 : 2); ++s) {
+    const pamopt_cu_mesh_report& m = rep.stage[s];
+    r.stages.push_back(StageReport{m.cd, m.hd, m.min_angle_deg, m.manifold != 0, m.watertight != 0,
+                                   m.intersection_free != 0, m.n_faces, m.n_vertices});
+  }
+  r.stalled = rep.stalled != 0;
+  r.resolution = rep.resolution;
+  r.target_faces = rep.target_faces;
+  r.simplify.iterations = rep.simplify.iterations;
+  r.simplify.collapses = rep.simplify.collapses;
+  r.simplify.undone = rep.simplify.undone;
+  r.simplify.link_failures = rep.simplify.link_failures;
+  r.simplify.max_undo_rounds = rep.simplify.max_undo_rounds;
+  for (int k = 0; k < 8; ++k) r.simplify.undo_hist[k] = rep.simplify.undo_hist[k];
+  for (int k = 0; k < 4; ++k) r.stage_ms[k] = rep.stage_ms[k];
+  r.total_ms = rep.total_ms;
+  return r;
 }
 
 }  // namespace pamopt

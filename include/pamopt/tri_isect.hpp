@@ -37,4 +37,52 @@ inline std::vector<bool> faces_intersect(const IndexedMesh& mesh, const std::vec
   return std::vector<bool>(r.begin(), r.end());
 }
 
+/// SPEC.md:404-418 PairClass.
+struct PairClass {
+  int shared_vertex_count = 0;
+  bool coplanar = false;
+};
+
+namespace detail {
+inline std::vector<int32_t> flat_pairs(const std::vector<std::pair<int, int>>& pairs) {
+  std::vector<int32_t> p(2 * pairs.size());
+  for (size_t i = 0; i < pairs.size(); ++i) {
+    p[2 * i] = pairs[i].first;
+    p[2 * i + 1] = pairs[i].second;
+  }
+  return p;
+}
+}  // namespace detail
+
+/// classify_pair for face pairs of a mesh.
+inline std::vector<PairClass> classify_pair(const IndexedMesh& mesh, const std::vector<std::pair<int, int>>& pairs) {
+  cuda::Context& ctx = cuda::Context::thread_default();
+  cuda::DeviceMesh dm(ctx, mesh);
+  const std::vector<int32_t> p = detail::flat_pairs(pairs);
+  std::vector<int32_t> s(pairs.size()), c(pairs.size());
+  cuda::check(pamopt_cu_classify_pair(dm.get(), p.data(), static_cast<int64_t>(pairs.size()), s.data(), c.data()));
+  std::vector<PairClass> out(pairs.size());
+  for (size_t i = 0; i < pairs.size(); ++i) out[i] = PairClass{s[i], c[i] != 0};
+  return out;
+}
+
+/// intersect_3d / intersect_coplanar; std::invalid_argument
+/// when a pair does not satisfy the class precondition.
+inline std::vector<bool> intersect_3d(const IndexedMesh& mesh, const std::vector<std::pair<int, int>>& pairs) {
+  cuda::Context& ctx = cuda::Context::thread_default();
+  cuda::DeviceMesh dm(ctx, mesh);
+  const std::vector<int32_t> p = detail::flat_pairs(pairs);
+  std::vector<int32_t> r(pairs.size());
+  cuda::check(pamopt_cu_intersect_3d(dm.get(), p.data(), static_cast<int64_t>(pairs.size()), r.data()));
+  return std::vector<bool>(r.begin(), r.end());
+}
+inline std::vector<bool> intersect_coplanar(const IndexedMesh& mesh, const std::vector<std::pair<int, int>>& pairs) {
+  cuda::Context& ctx = cuda::Context::thread_default();
+  cuda::DeviceMesh dm(ctx, mesh);
+  const std::vector<int32_t> p = detail::flat_pairs(pairs);
+  std::vector<int32_t> r(pairs.size());
+  cuda::check(pamopt_cu_intersect_coplanar(dm.get(), p.data(), static_cast<int64_t>(pairs.size()), r.data()));
+  return std::vector<bool>(r.begin(), r.end());
+}
+
 }  // namespace pamopt

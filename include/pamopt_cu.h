@@ -119,6 +119,8 @@ int pamopt_cu_load_ply(pamopt_cu_ctx ctx, const void* bytes, int64_t nbytes, pam
                        pamopt_cu_load_stats* stats);
 /* normalize_unit_cube (mesh_io.cpp:393-408), in place; scale_translation = {scale, tx, ty, tz} or NULL */
 int pamopt_cu_normalize_unit_cube(pamopt_cu_mesh mesh, double padding, double* scale_translation);
+/* denormalize (mesh_io.cpp:410-412), in place: v = (v - t) / scale */
+int pamopt_cu_denormalize(pamopt_cu_mesh mesh, const double* scale_translation);
 
 /* ---- stage 1a: voxel_field --------------------------------------------------------- */
 /* R: power of two >= 8.  Returns the UDF lattice ((R+1)^3 f32, x-fastest, +INF sentinel). */
@@ -160,6 +162,18 @@ int pamopt_cu_dmc_extract(pamopt_cu_grid sdf, double beta, pamopt_cu_mesh* out);
  * vertices, reproduces the whole-grid mesh bit for bit. */
 int pamopt_cu_dmc_extract_slab(pamopt_cu_grid sdf, int32_t own_z0, int32_t own_z1, double beta,
                                pamopt_cu_mesh* out, int64_t counts[2]);
+/* The whole C4 slab path for a C++ host, one rank (process or thread) per GPU over an NCCL
+ * communicator (ncclComm_t passed as void*; world == 1 may pass NULL): the SDF of this rank's
+ * lattice planes, a HALO=2-plane ncclSend/ncclRecv exchange with the z-neighbours, slab-local
+ * DMC, an ncclAllGather of the counts and a grouped send of every slab mesh into place on rank
+ * 0.  Rank 0's out is the assembled mesh, bit-identical to pamopt_cu_dmc_extract of the whole
+ * grid; other ranks get out = NULL.  counts = this slab's {patch vertices, split vertices,
+ * faces}.  NCCL is resolved at run time from the process (libnccl.so.2); none -> ECUDA. */
+int pamopt_cu_extract_slab_nccl(pamopt_cu_ctx ctx, pamopt_cu_mesh mesh, int32_t R, double eps, double beta,
+                                int32_t rank, int32_t world, void* nccl_comm, pamopt_cu_mesh* out, int64_t counts[3]);
+/* ncclCommInitAll for a single host process driving ndev GPUs: comms[ndev] */
+int pamopt_cu_nccl_comm_init_all(int32_t ndev, const int32_t* devices, void** comms);
+int pamopt_cu_nccl_comm_destroy(void* comm);
 /* in place: F -> patch_base + F if F < nvp_own, else extra_base + (F - nvp_own) */
 int pamopt_cu_mesh_rebase(pamopt_cu_mesh mesh, int64_t patch_base, int64_t nvp_own, int64_t extra_base);
 /* active cells of the last extract on this grid: linear cell index, case, flip mask */
@@ -326,6 +340,41 @@ int pamopt_cu_safe_project(pamopt_cu_mesh mesh_s, pamopt_cu_mesh mesh_in, const 
  * dminv[4], a0, theta0, l0, -}; out = {value, gradient[12], SPD-projected Hessian[144]} */
 int pamopt_cu_project_term(pamopt_cu_ctx ctx, int32_t term, int32_t cls, const double* coords, int32_t nv,
                            const double* rest, const pamopt_cu_project_params* params, double* out);
+
+/* ---- run_pipeline: normalise -> stage 1 -> certify -> stage 2 -> certify ->
+ * [stage 3 -> certify] -> denormalise, with a MeshReport per stage ------------------------- */
+#define PAMOPT_CU_ECERT -6 /* a stage certification failed (nonzero exit) */
+typedef struct {
+  int32_t resolution;      /* R; 0 = the SPEC auto rule (256; 128 if target < 1000; 64 if < 50) */
+  int32_t run_projection;  /* stage 3 (safe projection) after stage 2 */
+  int64_t target_faces;    /* > 0, or 0 to use target_ratio */
+  double target_ratio;     /* target = max(4, ratio * input faces) when target_faces == 0 */
+  double beta;             /* DMC sigmoid sharpness, 5 */
+  double eps;              /* band offset; 0 = 0.9 / R */
+  pamopt_cu_simplify_params simplify;
+  int64_t report_samples;  /* Chamfer / Hausdorff samples per side, 16384 */
+  uint64_t seed;           /* 42 */
+} pamopt_cu_pipeline_config;
+typedef struct {
+  /* per stage, against the (normalised) input: stage[0] DMC, stage[1] QEM, stage[2] projection */
+  pamopt_cu_mesh_report stage[3];
+  int32_t failed_stage;    /* 0 = every certification passed, else the failing stage (1..3) */
+  int32_t stalled;         /* stage 2 stopped by the stall rule above the target */
+  int32_t resolution;
+  int32_t projected;
+  int64_t faces_in, target_faces;
+  pamopt_cu_simplify_stats simplify;
+  float stage_ms[4];       /* stage 1 (UDF+DMC), stage 2 (QEM), stage 3, certification + reports */
+  float total_ms;
+  float pad_;
+  double scale_translation[4];
+} pamopt_cu_pipeline_report;
+int pamopt_cu_pipeline_defaults(pamopt_cu_pipeline_config* out);
+/* input: the raw mesh (any coordinates; it is copied, not modified).  out: the denormalised
+ * output; on a certification failure returns PAMOPT_CU_ECERT with out = the failing stage's
+ * mesh (normalised coordinates, the diagnostic dump) and report->failed_stage set. */
+int pamopt_cu_run_pipeline(pamopt_cu_ctx ctx, pamopt_cu_mesh input, const pamopt_cu_pipeline_config* config,
+                           pamopt_cu_mesh* out, pamopt_cu_pipeline_report* report);
 
 /* ---- pipeline: UDF -> SDF -> DMC -> QEM ------------------------------------------------ */
 int pamopt_cu_remesh(pamopt_cu_ctx ctx, pamopt_cu_mesh input, int32_t R, double eps, double beta,

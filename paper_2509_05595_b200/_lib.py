@@ -12,7 +12,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PAMOPT_LIB") or os.path.join(HERE, "libpamopt_cu.so")  # PAMOPT_LIB: A/B variants only
 
-OK, EINVAL, ECUDA, ENOMEM, ENUMERIC, ECAP = 0, -1, -2, -3, -4, -5
+OK, EINVAL, ECUDA, ENOMEM, ENUMERIC, ECAP, ECERT = 0, -1, -2, -3, -4, -5, -6
 
 
 class SimplifyParams(C.Structure):
@@ -79,6 +79,28 @@ class MeshReport(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
 
 
+class PipelineConfig(C.Structure):
+    _fields_ = [("resolution", C.c_int32), ("run_projection", C.c_int32), ("target_faces", C.c_int64),
+                ("target_ratio", C.c_double), ("beta", C.c_double), ("eps", C.c_double),
+                ("simplify", SimplifyParams), ("report_samples", C.c_int64), ("seed", C.c_uint64)]
+
+
+class PipelineReport(C.Structure):
+    _fields_ = [("stage", MeshReport * 3), ("failed_stage", C.c_int32), ("stalled", C.c_int32),
+                ("resolution", C.c_int32), ("projected", C.c_int32), ("faces_in", C.c_int64),
+                ("target_faces", C.c_int64), ("simplify", SimplifyStats), ("stage_ms", C.c_float * 4),
+                ("total_ms", C.c_float), ("pad_", C.c_float), ("scale_translation", C.c_double * 4)]
+
+    def as_dict(self) -> dict:
+        n = 3 if self.projected else 2
+        return {"stages": [self.stage[i].as_dict() for i in range(n)], "failed_stage": self.failed_stage,
+                "stalled": bool(self.stalled), "resolution": self.resolution, "faces_in": self.faces_in,
+                "target_faces": self.target_faces, "simplify": self.simplify.as_dict(),
+                "stage_ms": {"stage1": self.stage_ms[0], "stage2": self.stage_ms[1], "stage3": self.stage_ms[2],
+                             "certification": self.stage_ms[3]},
+                "total_ms": self.total_ms, "scale_translation": list(self.scale_translation)}
+
+
 class PamoptError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
@@ -116,6 +138,9 @@ _SIGS = {
     "pamopt_cu_load_stl": (C.c_int, [vp, vp, i64, P(vp), P(LoadStats)]),
     "pamopt_cu_load_ply": (C.c_int, [vp, vp, i64, P(vp), P(LoadStats)]),
     "pamopt_cu_normalize_unit_cube": (C.c_int, [vp, dbl, vp]),
+    "pamopt_cu_denormalize": (C.c_int, [vp, vp]),
+    "pamopt_cu_pipeline_defaults": (C.c_int, [P(PipelineConfig)]),
+    "pamopt_cu_run_pipeline": (C.c_int, [vp, vp, P(PipelineConfig), P(vp), P(PipelineReport)]),
     "pamopt_cu_compute_udf": (C.c_int, [vp, vp, i32, P(vp)]),
     "pamopt_cu_udf_to_sdf": (C.c_int, [vp, dbl]),
     "pamopt_cu_compute_sdf": (C.c_int, [vp, vp, i32, dbl, P(vp)]),
@@ -133,6 +158,9 @@ _SIGS = {
     "pamopt_cu_dmc_extract": (C.c_int, [vp, dbl, P(vp)]),
     "pamopt_cu_dmc_extract_slab": (C.c_int, [vp, i32, i32, dbl, P(vp), P(i64)]),
     "pamopt_cu_mesh_rebase": (C.c_int, [vp, i64, i64, i64]),
+    "pamopt_cu_extract_slab_nccl": (C.c_int, [vp, vp, i32, dbl, dbl, i32, i32, vp, P(vp), vp]),
+    "pamopt_cu_nccl_comm_init_all": (C.c_int, [i32, vp, vp]),
+    "pamopt_cu_nccl_comm_destroy": (C.c_int, [vp]),
     "pamopt_cu_dmc_active_cells": (C.c_int, [vp, vp, vp, vp, i64, P(i64)]),
     "pamopt_cu_dmc_table": (C.c_int, [vp]),
     "pamopt_cu_dmc_stages": (C.c_int, [vp, dbl, vp]),

@@ -277,6 +277,31 @@ def extract_slab(grid: DeviceGrid, own_z0: int, own_z1: int, beta: float = DEFAU
     return DeviceMesh(h, grid.ctx), int(counts[0]), int(counts[1])
 
 
+def nccl_comm_init_all(devices) -> list:
+    """ncclCommInitAll for one host process driving several GPUs (returns the ncclComm_t handles)."""
+    d = np.ascontiguousarray(devices, np.int32)
+    comms = (C.c_void_p * len(d))()
+    check(lib().pamopt_cu_nccl_comm_init_all(len(d), ptr(d), comms))
+    return list(comms)
+
+
+def nccl_comm_destroy(comm) -> None:
+    check(lib().pamopt_cu_nccl_comm_destroy(C.c_void_p(comm)))
+
+
+def extract_slab_nccl(mesh, R: int, rank: int, world: int, comm=None, eps: float | None = None,
+                      beta: float = DEFAULT_BETA, ctx: Context | None = None):
+    """The C4 slab path of one rank over NCCL (pamopt_cu_extract_slab_nccl): returns (DeviceMesh on
+    rank 0 / None elsewhere, this slab's (patch vertices, split vertices, faces) counts)."""
+    m = _mesh(mesh, ctx)
+    h = C.c_void_p()
+    counts = np.zeros(3, np.int64)
+    check(lib().pamopt_cu_extract_slab_nccl(m.ctx.h, m.h, int(R), default_eps(R) if eps is None else float(eps),
+                                            float(beta), int(rank), int(world), C.c_void_p(comm), C.byref(h),
+                                            ptr(counts)))
+    return (DeviceMesh(h, m.ctx) if h.value else None), counts
+
+
 def dmc_active_cells(grid: DeviceGrid):
     n = C.c_int64()
     check(lib().pamopt_cu_dmc_active_cells(grid.h, None, None, None, 0, C.byref(n)))
@@ -572,6 +597,44 @@ def run_pipeline(vertices, faces, R: int, target_faces: int, eps: float | None =
     return RemeshResult(vo, fo, st.as_dict(), tm.as_dict())
 
 
+class CertificationError(_lib.PamoptError):
+    """A run_pipeline stage failed its certification; .mesh is that stage's output."""
+
+    def __init__(self, code, msg, mesh, report):
+        super().__init__(code, msg)
+        self.mesh = mesh
+        self.report = report
+
+
+def run_certified_pipeline(mesh, target_faces: int = 0, target_ratio: float = 0.01, resolution: int = 0,
+                           run_projection: bool = False, eps: float = 0.0, beta: float = DEFAULT_BETA,
+                           we: float = DEFAULT_WE, ws: float = DEFAULT_WS, tolerance: int = DEFAULT_TOL,
+                           report_samples: int = 16384, seed: int = 42, ctx: Context | None = None):
+    """run_pipeline: normalise a copy of the raw input, stage 1 (UDF -> DMC),
+    certify (manifold, watertight, exact intersection check), stage 2 (QEM), certify (+ face
+    target or the stall rule), optional stage 3 (safe projection), certify, denormalise.
+    Returns (DeviceMesh, report dict); raises CertificationError if a stage fails."""
+    m = _mesh(mesh, ctx)
+    cfg = _lib.PipelineConfig()
+    check(lib().pamopt_cu_pipeline_defaults(C.byref(cfg)))
+    cfg.resolution = int(resolution)
+    cfg.run_projection = 1 if run_projection else 0
+    cfg.target_faces = int(target_faces)
+    cfg.target_ratio = float(target_ratio)
+    cfg.beta = float(beta)
+    cfg.eps = float(eps)
+    cfg.simplify = _params(we, ws, tolerance)
+    cfg.report_samples = int(report_samples)
+    cfg.seed = int(seed)
+    h = C.c_void_p()
+    rep = _lib.PipelineReport()
+    rc = lib().pamopt_cu_run_pipeline(m.ctx.h, m.h, C.byref(cfg), C.byref(h), C.byref(rep))
+    if rc == _lib.ECERT:
+        raise CertificationError(rc, lib().pamopt_cu_last_error().decode(), DeviceMesh(h, m.ctx), rep.as_dict())
+    check(rc)
+    return DeviceMesh(h, m.ctx), rep.as_dict()
+
+
 def remesh_device(mesh: DeviceMesh, R: int, target_faces: int, eps: float | None = None, beta: float = DEFAULT_BETA,
                   we: float = DEFAULT_WE, ws: float = DEFAULT_WS, tolerance: int = DEFAULT_TOL):
     """Device-resident pipeline (pamopt_cu_remesh): returns (DeviceMesh, stats, times)."""
@@ -681,6 +744,12 @@ def normalize_unit_cube(mesh: DeviceMesh, padding: float):
     out = (C.c_double * 4)()
     check(lib().pamopt_cu_normalize_unit_cube(mesh.h, float(padding), out))
     return out[0], (out[1], out[2], out[3])
+
+
+def denormalize(mesh: DeviceMesh, scale: float, translation) -> None:
+    """In place (mesh_io.cpp:410-412): v = (v - translation) / scale."""
+    st = (C.c_double * 4)(float(scale), *(float(t) for t in translation))
+    check(lib().pamopt_cu_denormalize(mesh.h, st))
 
 
 # ------------------------------------------------------------------ stage 3 (SPEC.md safe_project)

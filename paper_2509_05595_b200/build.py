@@ -18,7 +18,8 @@ OBJ = os.path.join(HERE, "build_obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-SOURCES = ["capi.cu", "udf.cu", "dmc.cu", "isect.cu", "simplify.cu", "metrics.cu", "ingest.cu", "project.cu"]
+SOURCES = ["capi.cu", "udf.cu", "dmc.cu", "isect.cu", "simplify.cu", "metrics.cu", "ingest.cu", "project.cu",
+           "slab_nccl.cu"]
 
 
 def _stale(src_files, target):
@@ -56,7 +57,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), tag: str = "")
     with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs) or 1)) as ex:
         list(ex.map(run, jobs))
     if jobs or _stale(objs, out):
-        run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs, "-lcudart"])
+        run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs, "-lcudart", "-ldl"])
     return out
 
 

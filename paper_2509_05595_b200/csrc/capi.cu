@@ -77,6 +77,7 @@ struct pamopt_cu_grid_s {
   int32_t R = 0;
   int32_t z0 = 0, z1 = 0;  // lattice planes [z0, z1) held (a z-slab, or the whole grid)
   pcu::DevBuf<float> g;
+  pcu::DevBuf<uint32_t> signs;  // DMC sign mask emitted with a whole-grid SDF (empty otherwise)
   pcu::DmcResult last;  // debug view of the last extract
 };
 
@@ -421,7 +422,12 @@ static int make_grid(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, int mode, dou
     const int64_t n1 = R + 1;
     try {
       gr->g.alloc(n1 * n1 * (z1 - z0), c->ctx.stream);
-      pcu::udf_run(c->ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, mode, eps, gr->g.get(), z0, z1);
+      uint32_t* sg = nullptr;
+      if (mode == 1 && z0 == 0 && z1 == R + 1) {  // whole-grid SDF: emit the DMC sign mask too
+        gr->signs.alloc(n1 * n1 * ((n1 + 31) / 32), c->ctx.stream);
+        sg = gr->signs.get();
+      }
+      pcu::udf_run(c->ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, mode, eps, gr->g.get(), z0, z1, sg);
     } catch (...) {
       delete gr;
       ctx_unref(c);
@@ -699,6 +705,15 @@ int pamopt_cu_normalize_unit_cube(pamopt_cu_mesh m, double padding, double* st) 
   });
 }
 
+int pamopt_cu_denormalize(pamopt_cu_mesh m, const double* st) {
+  return guarded([&] {
+    PCU_REQUIRE(m && st, PAMOPT_CU_EINVAL, "null argument");
+    pcu::Ctx& ctx = m->owner->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    pcu::denormalize(ctx, m->V.get(), m->nv, st);
+  });
+}
+
 int pamopt_cu_udf_to_sdf(pamopt_cu_grid gr, double eps) {
   return guarded([&] {
     PCU_REQUIRE(gr != nullptr, PAMOPT_CU_EINVAL, "null grid");
@@ -709,6 +724,7 @@ int pamopt_cu_udf_to_sdf(pamopt_cu_grid gr, double eps) {
     pcu::DeviceGuard g(ctx.device);
     const int64_t n1 = R + 1;
     pcu::udf_to_sdf_inplace(ctx, gr->g.get(), n1 * n1 * (gr->z1 - gr->z0), eps);
+    gr->signs.release();  // the samples changed: the DMC repacks its mask
   });
 }
 
@@ -784,7 +800,7 @@ int pamopt_cu_dmc_extract(pamopt_cu_grid gr, double beta, pamopt_cu_mesh* out) {
     pcu::Ctx& ctx = gr->owner->ctx;
     pcu::DeviceGuard g(ctx.device);
     gr->last = pcu::DmcResult();
-    pcu::dmc_extract(ctx, gr->g.get(), gr->R, beta, gr->last);
+    pcu::dmc_extract(ctx, gr->g.get(), gr->R, beta, gr->last, gr->signs.get());
     auto* m = new pamopt_cu_mesh_s();
     m->owner = gr->owner;
     ctx_ref(gr->owner);
@@ -816,6 +832,41 @@ int pamopt_cu_dmc_extract_slab(pamopt_cu_grid gr, int32_t own_z0, int32_t own_z1
     counts[1] = static_cast<int64_t>(gr->last.n_extra);
     *out = m;
   });
+}
+
+int pamopt_cu_extract_slab_nccl(pamopt_cu_ctx c, pamopt_cu_mesh m, int32_t R, double eps, double beta, int32_t rank,
+                                int32_t world, void* comm, pamopt_cu_mesh* out, int64_t counts[3]) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(m && out && counts, PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(m->owner == c, PAMOPT_CU_EINVAL, "mesh belongs to another context");
+    check_R(R);
+    const double lo = 0.8660254037844386 / R, hi = 3.0 / R - 0.8660254037844386 / R;
+    PCU_REQUIRE(eps >= lo && eps <= hi, PAMOPT_CU_EINVAL, "udf_to_sdf: epsilon out of range");
+    PCU_REQUIRE(beta > 0.0, PAMOPT_CU_EINVAL, "beta must be positive");
+    pcu::Ctx& ctx = c->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    validate(ctx, m);
+    *out = nullptr;
+    std::unique_ptr<pamopt_cu_mesh_s> r(new pamopt_cu_mesh_s());
+    pcu::slab_extract_nccl(ctx, m->V.get(), m->nv, m->F.get(), m->nf, R, eps, beta, rank, world, comm, r->V, r->F, r->nv,
+                           r->nf, counts);
+    if (rank != 0) return;
+    r->owner = c;
+    ctx_ref(c);
+    *out = r.release();
+  });
+}
+
+int pamopt_cu_nccl_comm_init_all(int32_t ndev, const int32_t* devs, void** comms) {
+  return guarded([&] {
+    PCU_REQUIRE(ndev >= 1 && devs && comms, PAMOPT_CU_EINVAL, "bad arguments");
+    pcu::nccl_comm_init_all(ndev, devs, comms);
+  });
+}
+
+int pamopt_cu_nccl_comm_destroy(void* comm) {
+  return guarded([&] { pcu::nccl_comm_destroy(comm); });
 }
 
 int pamopt_cu_mesh_rebase(pamopt_cu_mesh m, int64_t patch_base, int64_t nvp_own, int64_t extra_base) {
@@ -951,28 +1002,32 @@ int pamopt_cu_min_internal_angle(pamopt_cu_mesh m, double* deg) {
   });
 }
 
+static void make_report(pamopt_cu_mesh ref, pamopt_cu_mesh m, int64_t n, uint64_t seed, pamopt_cu_mesh_report* out) {
+  pcu::Ctx& ctx = m->owner->ctx;
+  pcu::DeviceGuard g(ctx.device);
+  check_indices(ctx, m);
+  *out = pamopt_cu_mesh_report{};
+  out->n_faces = m->nf;
+  out->n_vertices = m->nv;
+  out->cd = out->hd = std::numeric_limits<double>::quiet_NaN();
+  if (ref) two_sided(ref, m, n, seed, out->cd, out->hd);
+  out->min_angle_deg = m->nf ? std::acos(pcu::max_corner_cos(ctx, m->V.get(), m->F.get(), m->nf)) *
+                                   (180.0 / 3.14159265358979323846)
+                             : 0.0;
+  pcu::TopologyResult t;
+  pcu::analyze_topology(ctx, m->F.get(), m->nf, m->nv, t);
+  out->manifold = t.manifold;
+  out->watertight = t.watertight;
+  const std::vector<int32_t> pairs =
+      m->nf >= 2 ? pcu::self_intersections(ctx, m->V.get(), m->nv, m->F.get(), m->nf, nullptr, nullptr)
+                 : std::vector<int32_t>();
+  out->intersection_free = pairs.empty() ? 1 : 0;
+}
+
 int pamopt_cu_report(pamopt_cu_mesh ref, pamopt_cu_mesh m, int64_t n, uint64_t seed, pamopt_cu_mesh_report* out) {
   return guarded([&] {
     PCU_REQUIRE(m && out, PAMOPT_CU_EINVAL, "null argument");
-    pcu::Ctx& ctx = m->owner->ctx;
-    pcu::DeviceGuard g(ctx.device);
-    check_indices(ctx, m);
-    *out = pamopt_cu_mesh_report{};
-    out->n_faces = m->nf;
-    out->n_vertices = m->nv;
-    out->cd = out->hd = std::numeric_limits<double>::quiet_NaN();
-    if (ref) two_sided(ref, m, n, seed, out->cd, out->hd);
-    out->min_angle_deg = m->nf ? std::acos(pcu::max_corner_cos(ctx, m->V.get(), m->F.get(), m->nf)) *
-                                     (180.0 / 3.14159265358979323846)
-                               : 0.0;
-    pcu::TopologyResult t;
-    pcu::analyze_topology(ctx, m->F.get(), m->nf, m->nv, t);
-    out->manifold = t.manifold;
-    out->watertight = t.watertight;
-    const std::vector<int32_t> pairs =
-        m->nf >= 2 ? pcu::self_intersections(ctx, m->V.get(), m->nv, m->F.get(), m->nf, nullptr, nullptr)
-                   : std::vector<int32_t>();
-    out->intersection_free = pairs.empty() ? 1 : 0;
+    make_report(ref, m, n, seed, out);
   });
 }
 
@@ -1539,6 +1594,141 @@ int pamopt_cu_qem_destroy(pamopt_cu_qem q) {
   });
 }
 
+// ------------------------------------------------------------------------- run_pipeline
+int pamopt_cu_pipeline_defaults(pamopt_cu_pipeline_config* out) {
+  return guarded([&] {
+    PCU_REQUIRE(out, PAMOPT_CU_EINVAL, "null argument");
+    *out = pamopt_cu_pipeline_config{};
+    out->resolution = 0;
+    out->run_projection = 0;
+    out->target_faces = 0;
+    out->target_ratio = 0.01;
+    out->beta = 5.0;
+    out->eps = 0.0;
+    out->simplify = pamopt_cu_simplify_params{1e-3, 5e-3, 4, 10};
+    out->report_samples = 16384;
+    out->seed = 42;
+  });
+}
+
+// SPEC.md:224 default resolution rule
+static int32_t auto_resolution(int64_t target) { return target < 50 ? 64 : (target < 1000 ? 128 : 256); }
+
+int pamopt_cu_run_pipeline(pamopt_cu_ctx c, pamopt_cu_mesh in, const pamopt_cu_pipeline_config* cfg_in,
+                           pamopt_cu_mesh* out, pamopt_cu_pipeline_report* rep) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(in && out && rep, PAMOPT_CU_EINVAL, "null argument");
+    PCU_REQUIRE(in->owner == c, PAMOPT_CU_EINVAL, "mesh belongs to another context");
+    pamopt_cu_pipeline_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else pamopt_cu_pipeline_defaults(&cfg);
+    *out = nullptr;
+    *rep = pamopt_cu_pipeline_report{};
+    const int64_t target = cfg.target_faces > 0
+                               ? cfg.target_faces
+                               : std::max<int64_t>(4, static_cast<int64_t>(cfg.target_ratio * static_cast<double>(in->nf)));
+    PCU_REQUIRE(target >= 4, PAMOPT_CU_EINVAL, "run_pipeline: target_faces must be >= 4 (SPEC.md:541)");
+    const int32_t R = cfg.resolution > 0 ? cfg.resolution : auto_resolution(target);
+    check_R(R);
+    const double eps = cfg.eps > 0.0 ? cfg.eps : 0.9 / R;
+    const double lo = 0.8660254037844386 / R, hi = 3.0 / R - 0.8660254037844386 / R;
+    PCU_REQUIRE(eps >= lo && eps <= hi, PAMOPT_CU_EINVAL, "udf_to_sdf: epsilon out of range");
+    PCU_REQUIRE(cfg.beta > 0.0 && cfg.report_samples > 0, PAMOPT_CU_EINVAL, "run_pipeline: bad config");
+    const pcu::SimplifyParams P = to_params(&cfg.simplify);
+    pcu::Ctx& ctx = c->ctx;
+    pcu::DeviceGuard g(ctx.device);
+    validate(ctx, in);
+    rep->resolution = R;
+    rep->target_faces = target;
+    rep->faces_in = in->nf;
+    auto now = [&]() {
+      PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+      return std::chrono::steady_clock::now();
+    };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return static_cast<float>(std::chrono::duration<double, std::milli>(b - a).count());
+    };
+    auto new_mesh = [&]() {
+      std::unique_ptr<pamopt_cu_mesh_s> m(new pamopt_cu_mesh_s());
+      m->owner = c;
+      ctx_ref(c);
+      return m;
+    };
+    const auto t0 = now();
+    // normalise a copy (padding 2 * band)
+    auto norm = new_mesh();
+    norm->nv = in->nv;
+    norm->nf = in->nf;
+    norm->V.alloc(3 * (in->nv ? in->nv : 1), ctx.stream);
+    norm->F.alloc(3 * (in->nf ? in->nf : 1), ctx.stream);
+    PCU_CUDA(cudaMemcpyAsync(norm->V.get(), in->V.get(), 3 * in->nv * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+    PCU_CUDA(cudaMemcpyAsync(norm->F.get(), in->F.get(), 3 * in->nf * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+    pcu::normalize_unit_cube(ctx, norm->V.get(), norm->nv, 6.0 / R, rep->scale_translation);
+    // stage 1: UDF -> SDF -> DMC
+    auto m = new_mesh();
+    {
+      const int64_t n1 = R + 1;
+      pcu::DevBuf<float> sdf(n1 * n1 * n1, ctx.stream);
+      pcu::DevBuf<uint32_t> signs(n1 * n1 * ((n1 + 31) / 32), ctx.stream);
+      pcu::udf_run(ctx, norm->V.get(), norm->nv, norm->F.get(), norm->nf, R, 1, eps, sdf.get(), 0, -1, signs.get());
+      pcu::DmcResult d;
+      pcu::dmc_extract(ctx, sdf.get(), R, cfg.beta, d, signs.get());
+      m->nv = static_cast<int64_t>(d.nv);
+      m->nf = static_cast<int64_t>(d.nf);
+      m->V = std::move(d.V);
+      m->F = std::move(d.F);
+    }
+    const auto t1 = now();
+    float cert_ms = 0.f;
+    auto certify = [&](int stage, bool extra_ok, const char* what) {
+      const auto a = now();
+      make_report(norm.get(), m.get(), cfg.report_samples, cfg.seed, &rep->stage[stage - 1]);
+      cert_ms += ms(a, now());
+      const pamopt_cu_mesh_report& r = rep->stage[stage - 1];
+      if (r.manifold && r.watertight && r.intersection_free && extra_ok) return;
+      rep->failed_stage = stage;
+      char msg[256];
+      std::snprintf(msg, sizeof(msg),
+                    "run_pipeline: stage %d certification failed (manifold=%d watertight=%d intersection_free=%d%s)",
+                    stage, r.manifold, r.watertight, r.intersection_free, what);
+      *out = m.release();
+      throw pcu::Error(PAMOPT_CU_ECERT, msg);
+    };
+    certify(1, m->nf > 0, m->nf > 0 ? "" : " empty DMC surface");
+    // stage 2: QEM to the target (the stall rule may stop above it)
+    pcu::SimplifyStats S;
+    pcu::simplify_run(ctx, m->V, m->F, m->nv, m->nf, target, P, S);
+    to_stats(S, &rep->simplify);
+    rep->stalled = m->nf > target ? 1 : 0;
+    const auto t2 = now();
+    const bool stall_ok = m->nf <= target ||
+                          (S.per_iter.size() >= static_cast<size_t>(P.stall) &&
+                           std::all_of(S.per_iter.end() - P.stall, S.per_iter.end(), [](int64_t x) { return x == 0; }));
+    certify(2, stall_ok, stall_ok ? "" : " face target missed without a stall");
+    // stage 3 (optional): safe projection toward the input, connectivity unchanged
+    auto t3 = now();
+    if (cfg.run_projection) {
+      pamopt_cu_project_params pp;
+      pamopt_cu_project_defaults(&pp);
+      pcu::ProjectStats ps;
+      pcu::safe_project(ctx, m->V.get(), m->nv, m->F.get(), m->nf, norm->V.get(), norm->F.get(), norm->nf, to_pp(pp),
+                        ps);
+      t3 = now();
+      rep->projected = 1;
+      certify(3, true, "");
+    }
+    rep->stage_ms[0] = ms(t0, t1);
+    rep->stage_ms[1] = ms(t1, t2);
+    rep->stage_ms[2] = cfg.run_projection ? ms(t2, t3) - 0.f : 0.f;
+    rep->stage_ms[3] = cert_ms;
+    // back to the input's coordinates (mesh_io.cpp:410-412)
+    pcu::denormalize(ctx, m->V.get(), m->nv, rep->scale_translation);
+    rep->total_ms = ms(t0, now());
+    *out = m.release();
+  });
+}
+
 // ---------------------------------------------------------------------------- pipeline
 static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double eps, double beta, int64_t target,
                         const pamopt_cu_simplify_params* params, pamopt_cu_mesh* out, pamopt_cu_simplify_stats* stats,
@@ -1565,11 +1755,13 @@ static void remesh_impl(pamopt_cu_ctx c, pamopt_cu_mesh in, int32_t R, double ep
   PCU_CUDA(cudaEventRecord(ev[0], ctx.stream));
   const int64_t n1 = R + 1;
   pcu::DevBuf<float> sdf(n1 * n1 * n1, ctx.stream);
-  pcu::udf_run(ctx, in->V.get(), in->nv, in->F.get(), in->nf, R, 1, eps, sdf.get());
+  pcu::DevBuf<uint32_t> signs(n1 * n1 * ((n1 + 31) / 32), ctx.stream);
+  pcu::udf_run(ctx, in->V.get(), in->nv, in->F.get(), in->nf, R, 1, eps, sdf.get(), 0, -1, signs.get());
   PCU_CUDA(cudaEventRecord(ev[1], ctx.stream));
   pcu::DmcResult d;
-  pcu::dmc_extract(ctx, sdf.get(), R, beta, d);
+  pcu::dmc_extract(ctx, sdf.get(), R, beta, d, signs.get());
   sdf.release();
+  signs.release();
   PCU_CUDA(cudaEventRecord(ev[2], ctx.stream));
   auto* m = new pamopt_cu_mesh_s();
   m->owner = c;

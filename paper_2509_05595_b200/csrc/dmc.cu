@@ -151,22 +151,42 @@ struct GridView {
   int R;
   int64_t n1;
   int64_t zb;  // global z of the first resident lattice plane (0 for a whole grid)
+  const uint32_t* sg = nullptr;  // sign mask of the resident planes: bit x&31 of word x>>5 per row
+  int W = 0;                     // words per lattice row, ceil((R+1)/32)
   __device__ __forceinline__ float at(int64_t x, int64_t y, int64_t z) const {
     return s[x + n1 * (y + n1 * (z - zb))];
   }
+  __device__ __forceinline__ int bit(int64_t x, int64_t row) const {
+    return (sg[row * W + (x >> 5)] >> (x & 31)) & 1;
+  }
+  // 8-bit case, corner c = x | y<<1 | z<<2, bit set for a negative sample (sign(0) = +)
   __device__ __forceinline__ int case_of(int64_t x, int64_t y, int64_t z) const {
-    int cs = 0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      cs |= (at(x + (c & 1), y + ((c >> 1) & 1), z + ((c >> 2) & 1)) < 0.0f) << c;
-    return cs;
+    const int64_t r = (z - zb) * n1 + y;
+    return bit(x, r) | bit(x + 1, r) << 1 | bit(x, r + 1) << 2 | bit(x + 1, r + 1) << 3 | bit(x, r + n1) << 4 |
+           bit(x + 1, r + n1) << 5 | bit(x, r + n1 + 1) << 6 | bit(x + 1, r + n1 + 1) << 7;
   }
 };
 
+// sign mask of resident planes (used when the SDF producer did not emit one): one warp per word
+__global__ void k_pack_signs(const float* __restrict__ s, int64_t rows, int n1, int W, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = rows * W;
+  for (int64_t wi = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; wi < nw;
+       wi += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t row = wi / W;
+    const int x = (static_cast<int>(wi - row * W) << 5) + lane;
+    const bool neg = x < n1 && s[row * n1 + x] < 0.0f;
+    const unsigned m = __ballot_sync(0xffffffffu, neg);
+    if (lane == 0) out[wi] = m;
+  }
+}
+
+// R is a power of two: cell coordinates by shifts (no 64-bit division per cell)
 __device__ __forceinline__ void cell_xyz(int64_t c, int R, int64_t& x, int64_t& y, int64_t& z) {
-  x = c % R;
-  y = (c / R) % R;
-  z = c / (static_cast<int64_t>(R) * R);
+  const int lg = __ffs(R) - 1;
+  x = c & (R - 1);
+  y = (c >> lg) & (R - 1);
+  z = c >> (2 * lg);
 }
 
 __global__ void __launch_bounds__(256) k_classify_count(GridView g, int64_t c0, int64_t ncell,
@@ -563,14 +583,26 @@ __global__ void k_own_split(const uint32_t* __restrict__ cells, const uint32_t* 
 }  // namespace
 
 void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, int own_z0, int own_z1, double beta,
-                      DmcResult& res) {
+                      DmcResult& res, const uint32_t* d_signs) {
   upload_table(ctx.device);
   const int cz0 = own_z0 > 0 ? own_z0 - 1 : 0;  // the layer below lends its patch-vertex ids
-  PCU_REQUIRE(R >= 2 && R <= 1024 && own_z0 >= 0 && own_z0 < own_z1 && own_z1 <= R, PAMOPT_CU_EINVAL,
+  PCU_REQUIRE(R >= 2 && R <= 1024 && (R & (R - 1)) == 0, PAMOPT_CU_EINVAL, "dmc: R must be a power of two <= 1024");
+  PCU_REQUIRE(own_z0 >= 0 && own_z0 < own_z1 && own_z1 <= R, PAMOPT_CU_EINVAL,
               "dmc slab: own cell layers must satisfy 0 <= z0 < z1 <= R");
   PCU_REQUIRE(pz0 <= std::max(own_z0 - 2, 0) && pz1 >= std::min(own_z1 + 2, R + 1) && pz0 >= 0 && pz1 <= R + 1,
               PAMOPT_CU_EINVAL, "dmc slab: resident planes must cover [z0-2, z1+2) clipped to the lattice");
   GridView g{d_planes, R, static_cast<int64_t>(R) + 1, pz0};
+  g.W = (R + 1 + 31) / 32;
+  DevBuf<uint32_t> packed;
+  if (d_signs) {
+    g.sg = d_signs;
+  } else {  // one read of the resident planes; every dense pass below reads the mask instead
+    const int64_t rows = static_cast<int64_t>(R + 1) * (pz1 - pz0);
+    packed.alloc(rows * g.W, ctx.stream);
+    PCU_LAUNCH(ctx, k_pack_signs, static_cast<unsigned>(ctx.num_sms * 16), 256, 0, d_planes, rows, R + 1, g.W,
+               packed.get());
+    g.sg = packed.get();
+  }
   const int64_t rr = static_cast<int64_t>(R) * R;
   const int64_t c0 = rr * cz0;
   const int64_t ncell = rr * (own_z1 - cz0);
@@ -699,9 +731,9 @@ void mesh_rebase(Ctx& ctx, int32_t* dF, int64_t nidx, int64_t patch_base, int64_
   PCU_LAUNCH(ctx, k_rebase, grid_for(nidx, 256), 256, 0, dF, nidx, patch_base, nvp_own, extra_base);
 }
 
-void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res) {
+void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res, const uint32_t* d_signs) {
   PCU_REQUIRE(R >= 2 && R <= 1024, PAMOPT_CU_EINVAL, "extract: R must be <= 1024 (32-bit cell ids)");
-  dmc_extract_slab(ctx, d_sdf, R, 0, R + 1, 0, R, beta, res);
+  dmc_extract_slab(ctx, d_sdf, R, 0, R + 1, 0, R, beta, res, d_signs);
 }
 
 }  // namespace pcu

@@ -179,6 +179,15 @@ __global__ void k_apply_transform(double* __restrict__ V, int64_t nv, double sca
   V[3 * i + 2] = V[3 * i + 2] * scale + tz;
 }
 
+// NormalizationTransform::invert (mesh_io.hpp:35): (p - translation) / scale, per component
+__global__ void k_invert_transform(double* __restrict__ V, int64_t nv, double scale, double tx, double ty, double tz) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nv) return;
+  V[3 * i] = (V[3 * i] - tx) / scale;
+  V[3 * i + 1] = (V[3 * i + 1] - ty) / scale;
+  V[3 * i + 2] = (V[3 * i + 2] - tz) / scale;
+}
+
 double unkey(unsigned long long key) {
   const unsigned long long u = (key >> 63) ? (key & 0x7fffffffffffffffull) : ~key;
   double d;
@@ -320,6 +329,12 @@ void normalize_unit_cube(Ctx& ctx, double* dV, int64_t nv, double padding, doubl
     scale_translation[0] = scale;
     for (int k = 0; k < 3; ++k) scale_translation[1 + k] = t[k];
   }
+}
+
+void denormalize(Ctx& ctx, double* dV, int64_t nv, const double* st) {
+  if (nv <= 0) return;
+  PCU_REQUIRE(st[0] > 0.0, PAMOPT_CU_EINVAL, "denormalize: scale must be positive");
+  PCU_LAUNCH(ctx, k_invert_transform, grid_for(nv, 256), 256, 0, dV, nv, st[0], st[1], st[2], st[3]);
 }
 
 }  // namespace pcu

@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "exact.cuh"
@@ -458,7 +459,8 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
                                                const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
                                                uint64_t cap, unsigned long long* __restrict__ ncand,
                                                const int32_t* __restrict__ probe_ids, int32_t* __restrict__ huge,
-                                               unsigned long long* __restrict__ nhuge) {
+                                               unsigned long long* __restrict__ nhuge,
+                                               const uint8_t* __restrict__ in_probe) {
   // candidates are staged in shared memory and flushed with one global atomic per block
   // (a single-address counter bumped per candidate serialises in the L2 atomic unit)
   constexpr int kBuf = 1024, kQ = 64;
@@ -577,7 +579,8 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
           const int32_t a = en.x;
           emit = qc[warp][r][0] == max(slo[warp][o][0], en.y) && qc[warp][r][1] == max(slo[warp][o][1], en.z) &&
                  qc[warp][r][2] == max(slo[warp][o][2], en.w) &&
-                 !(a == op || (sbuild[warp][o] && a < op)) &&  // else emitted from probe a instead
+                 // a pair met from both sides (a also probes, op also in the grid): the smaller probe
+                 !(a == op || (sbuild[warp][o] && a < op && (!in_probe || in_probe[a]))) &&
                  overlap(sbox[warp][o], B[a]);
           v = (static_cast<uint64_t>(static_cast<uint32_t>(op)) << 32) | static_cast<uint32_t>(a);
         }
@@ -622,7 +625,8 @@ __global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B,
                                                      const int32_t* __restrict__ probe_ids, int64_t n_probe,
                                                      const uint8_t* __restrict__ alive, int sym,
                                                      const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
-                                                     uint64_t cap, unsigned long long* __restrict__ ncand) {
+                                                     uint64_t cap, unsigned long long* __restrict__ ncand,
+                                                     const uint8_t* __restrict__ in_probe) {
   const unsigned long long nh = ds->nhuge, nb = ds->nbig;
   const double inv_h = ds->inv_h;
   const int lane = threadIdx.x & 31;
@@ -639,7 +643,7 @@ __global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B,
       for (int64_t k = lane; k < n_build; k += 32) {
         const int32_t a = build_ids ? build_ids[k] : static_cast<int32_t>(k);
         if (alive && !alive[a]) continue;
-        if (a == p || (p_build && a < p)) continue;
+        if (a == p || (p_build && a < p && (!in_probe || in_probe[a]))) continue;
         const FBox ba = B[a];
         if (!overlap(bp, ba)) continue;
         if (cells_of(ba, inv_h).count() > kMaxCells) continue;  // big build face: second half
@@ -653,7 +657,7 @@ __global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B,
         if (alive && !alive[x]) continue;
         if (x == b) continue;
         const bool x_build = sym || (in_build && in_build[x]);
-        if (x_build && b < x) continue;  // emitted from probe b instead
+        if (x_build && b < x && (!in_probe || in_probe[b])) continue;  // emitted from probe b instead
         if (!overlap(B[x], bb)) continue;
         emit(x, b);
       }
@@ -888,7 +892,7 @@ namespace {
 void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive,
                   const int32_t* build_ids, int64_t n_build, const int32_t* probe_ids, int64_t n_probe, int sym,
                   int mode, int32_t* pairs, uint64_t pair_cap, const int32_t* owner,
-                  uint8_t* revert, bool boxes_current = false) {
+                  uint8_t* revert, bool boxes_current = false, const uint8_t* in_probe = nullptr) {
   cudaStream_t st = ctx.stream;
   S.ds.ensure(1, st);
   PCU_CUDA(cudaMemsetAsync(S.ds.get(), 0, sizeof(DetectScalars), st));
@@ -933,10 +937,10 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   PCU_LAUNCH(ctx, k_probe, grid_for(n_probe, 128), 128, 0, B, n_probe,
              d_alive, S.ds.get(), mask, S.bcount.get(), S.boff.get(), S.entries.get(), S.big.get(), S.occ.get(), sym,
              in_build,
-             S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids, S.huge.get(), &S.ds.get()->nhuge);
+             S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids, S.huge.get(), &S.ds.get()->nhuge, in_probe);
   PCU_LAUNCH(ctx, k_probe_large, static_cast<unsigned>(ctx.num_sms * 2), 128, 0, B, S.ds.get(), S.huge.get(),
              S.big.get(), build_ids, n_build, probe_ids, n_probe, d_alive, sym, in_build, S.cand.get(), S.cand_cap,
-             &S.ds.get()->ncand);
+             &S.ds.get()->ncand, in_probe);
   S.cls.ensure(3 * S.cand_cap, st);
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
@@ -1011,9 +1015,23 @@ void verdict_by_class(Ctx& ctx, const double* dV, const int32_t* dF, const int32
 void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                        const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
                        uint8_t* d_revert) {
-  // round 1: grid over the faces owned by applied collapses, probed by every alive face
-  detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner,
-               d_revert, true);
+  static const bool build_all = [] {
+    const char* e = std::getenv("PAMOPT_UNDO_BUILD_ALL");
+    return e && e[0] == '1';
+  }();
+  if (!build_all) {
+    // round 1: grid over the faces owned by applied collapses, probed by every alive face
+    detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner,
+                 d_revert, true);
+    return;
+  }
+  // variant: grid over every alive face, probed by the owned faces only; a pair of two owned
+  // faces is emitted from its smaller probe (in_probe flags)
+  S.in_build.ensure(nf, ctx.stream);
+  PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, ctx.stream));
+  PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_query, 256), 256, 0, d_query_faces, n_query, S.in_build.get());
+  detect_round(ctx, S, dV, dF, nf, d_falive, nullptr, nf, d_query_faces, n_query, 1, 1, nullptr, 0, d_owner, d_revert,
+               true, S.in_build.get());
 }
 
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,

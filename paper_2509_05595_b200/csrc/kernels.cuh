@@ -11,8 +11,10 @@ namespace pcu {
 // ---- stage 1a (udf.cu)
 // mode 0: UDF (+INF sentinel); mode 1: fused SDF (u - eps, sentinel +1.0)
 // z-slab: only lattice planes [z0, z1) are computed and written (z1 < 0: the whole grid)
+// d_signs (optional): the DMC sign mask of the written planes, (z1-z0)*(R+1) rows of
+// ceil((R+1)/32) words; bit x&31 of word x>>5 = (sample < 0)
 void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf, int R, int mode, double eps,
-             float* d_out, int z0 = 0, int z1 = -1);
+             float* d_out, int z0 = 0, int z1 = -1, uint32_t* d_signs = nullptr);
 void udf_to_sdf_inplace(Ctx& ctx, float* g, int64_t n, double eps);
 std::vector<int64_t> hierarchy_pairs(Ctx& ctx, const double* dV, const int32_t* dF, int64_t nf, int R, int r);
 
@@ -34,12 +36,13 @@ struct DmcResult {
   DevBuf<float> qf;        // samples at the edge's lower / upper vertex
   DevBuf<uint8_t> qsplit;  // 1: diagonal 0-2, 2: diagonal 1-3, 3: four triangles
 };
-void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res);
+// d_signs: the sign mask udf_run can emit for the same planes (NULL: packed here, one read)
+void dmc_extract(Ctx& ctx, const float* d_sdf, int R, double beta, DmcResult& res, const uint32_t* d_signs = nullptr);
 // z-slab extraction: d_planes holds lattice planes [pz0, pz1); cells of layers
 // [own_z0, own_z1) emit faces; the layer below only lends vertex ids.  Face indices are relative
 // to the first own patch vertex (negative = the previous slab's top layer); see mesh_rebase.
 void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, int own_z0, int own_z1, double beta,
-                      DmcResult& res);
+                      DmcResult& res, const uint32_t* d_signs = nullptr);
 // F[i] -> patch_base + F[i] if F[i] < nvp_own, else extra_base + (F[i] - nvp_own)
 void mesh_rebase(Ctx& ctx, int32_t* dF, int64_t nidx, int64_t patch_base, int64_t nvp_own, int64_t extra_base);
 void dmc_table_host(int32_t* out);
@@ -108,6 +111,8 @@ struct PlyBinaryLayout {
 };
 void load_stl_binary(Ctx& ctx, const uint8_t* d_bytes, int64_t nbytes, uint32_t count, IngestResult& out);
 void load_ply_binary(Ctx& ctx, const uint8_t* d_bytes, const PlyBinaryLayout& layout, IngestResult& out);
+// denormalize (mesh_io.cpp:410-412) with {scale, tx, ty, tz} from normalize_unit_cube
+void denormalize(Ctx& ctx, double* dV, int64_t nv, const double* scale_translation);
 void normalize_unit_cube(Ctx& ctx, double* dV, int64_t nv, double padding, double* scale_translation);
 
 // ---- tri_isect (isect.cu)
@@ -144,6 +149,14 @@ void detect_grow(IsectScratch& S, unsigned long long ncand);
 void detect_read(const void* host_copy, unsigned long long* found, int* redo, unsigned long long* ncand);
 IsectScratch* isect_scratch_create();
 void isect_scratch_destroy(IsectScratch* s);
+
+// ---- C4 slab path over NCCL (slab_nccl.cu): NCCL resolved at run time from the process
+void* nccl_comm_init_all(int ndev, const int* devs, void** comms);
+void nccl_comm_destroy(void* comm);
+// rank 0 gets the assembled mesh in Vout/Fout (nv_out/nf_out); others get nv_out = nf_out = 0
+void slab_extract_nccl(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf, int R, double eps,
+                       double beta, int rank, int world, void* comm, DevBuf<double>& Vout, DevBuf<int32_t>& Fout,
+                       int64_t& nv_out, int64_t& nf_out, int64_t counts[3]);
 
 // ---- stage 2 (simplify.cu)
 struct SimplifyParams {

@@ -301,7 +301,7 @@ __global__ void k_make_items(const uint32_t* __restrict__ cnt, const uint32_t* _
 #endif
 __global__ void __launch_bounds__(256, PCU_BRICK_MINB) k_brick(const Item* __restrict__ items, const uint32_t* __restrict__ tris,
                                                   const TriD* __restrict__ T, int R, int rb, int bs, int J,
-                                                  unsigned long long* __restrict__ blocks) {
+                                                  uint32_t* __restrict__ blocks) {
   __shared__ unsigned long long vmin[729];
   __shared__ uint32_t rows[8][16];        // finest-level survivor bit rows: byte (y + bs z) holds x bits
   __shared__ uint16_t list[8][2][512];    // ping-pong survivor lists (local cell index at level j)
@@ -466,46 +466,67 @@ __global__ void __launch_bounds__(256, PCU_BRICK_MINB) k_brick(const Item* __res
     __syncwarp();
   }
   __syncthreads();
-  unsigned long long* blk = blocks + static_cast<uint64_t>(it.compact) * nvb;
+  // merge into the brick's global block as the f32 UDF value: (float)sqrt(.) is monotone, so
+  // the min over f32 bit patterns of (float)sqrt(d2) equals (float)sqrt(min d2) exactly
+  uint32_t* blk = blocks + static_cast<uint64_t>(it.compact) * nvb;
   for (int v = threadIdx.x; v < nvb; v += blockDim.x)
-    if (vmin[v] != ~0ull) atomicMin(&blk[v], vmin[v]);
+    if (vmin[v] != ~0ull) {
+      const float u = static_cast<float>(sqrt(__longlong_as_double(static_cast<long long>(vmin[v]))));
+      atomicMin(&blk[v], __float_as_uint(u));
+    }
 }
 
-// mode 0: UDF (+INF sentinel); mode 1: SDF (u - eps, sentinel +1.0)
-__global__ void k_finalize(const unsigned long long* __restrict__ blocks, const int32_t* __restrict__ bmap, int R,
-                           int rb, int bs, int mode, double eps, float* __restrict__ out, int z0, int z1) {
-  const int64_t n1 = R + 1;
-  const int64_t total = n1 * n1 * (z1 - z0);
-  const int nv1 = bs + 1;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int x = static_cast<int>(i % n1), y = static_cast<int>((i / n1) % n1), z = z0 + static_cast<int>(i / (n1 * n1));
-    int bxs[2], bys[2], bzs[2], nbx = 0, nby = 0, nbz = 0;
-    if (x / bs < rb) bxs[nbx++] = x / bs;
-    if (x % bs == 0 && x > 0) bxs[nbx++] = x / bs - 1;
+// mode 0: UDF (+INF sentinel); mode 1: SDF (u - eps, sentinel +1.0).  One warp per 32
+// consecutive samples of a lattice row (z, y uniform per warp: no per-sample integer division);
+// the brick candidates along y and z are warp-uniform.  With `signs`, the warp's ballot of
+// (s < 0) is stored as one 32-bit word (bit x & 31 of word x >> 5 of the row): the DMC classify
+// passes read this 17 MB mask (C3) instead of the 540 MB lattice.
+__global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ blocks, const int32_t* __restrict__ bmap,
+                                                  int R, int rb, int bs, int mode, double eps, float* __restrict__ out,
+                                                  int z0, int z1, uint32_t* __restrict__ signs) {
+  const int n1 = R + 1, W = (n1 + 31) >> 5, nv1 = bs + 1;
+  const int64_t rows = static_cast<int64_t>(n1) * (z1 - z0);
+  const int64_t nwarp = rows * W;
+  const int lane = threadIdx.x & 31;
+  for (int64_t wi = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; wi < nwarp;
+       wi += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t row = wi / W;
+    const int w = static_cast<int>(wi - row * W);
+    const int y = static_cast<int>(row % n1), zr = static_cast<int>(row / n1), z = z0 + zr;
+    const int x = (w << 5) + lane;
+    int bys[2], bzs[2], nby = 0, nbz = 0;
     if (y / bs < rb) bys[nby++] = y / bs;
     if (y % bs == 0 && y > 0) bys[nby++] = y / bs - 1;
     if (z / bs < rb) bzs[nbz++] = z / bs;
     if (z % bs == 0 && z > 0) bzs[nbz++] = z / bs - 1;
-    unsigned long long best = ~0ull;
     if (!bmap) nbz = 0;
-    for (int a = 0; a < nbz; ++a)
-      for (int b = 0; b < nby; ++b)
-        for (int c = 0; c < nbx; ++c) {
-          const int cid = bmap[bxs[c] + rb * (bys[b] + rb * bzs[a])];
-          if (cid < 0) continue;
-          const int lx = x - bxs[c] * bs, ly = y - bys[b] * bs, lz = z - bzs[a] * bs;
-          const unsigned long long val = blocks[static_cast<uint64_t>(cid) * nv1 * nv1 * nv1 + lx + nv1 * (ly + nv1 * lz)];
-          best = val < best ? val : best;
-        }
-    float res;
-    if (best == ~0ull) {
+    uint32_t best = 0xffffffffu;
+    if (x < n1) {
+      int bxs[2], nbx = 0;
+      if (x / bs < rb) bxs[nbx++] = x / bs;
+      if (x % bs == 0 && x > 0) bxs[nbx++] = x / bs - 1;
+      for (int a = 0; a < nbz; ++a)
+        for (int b = 0; b < nby; ++b)
+          for (int c = 0; c < nbx; ++c) {
+            const int cid = bmap[bxs[c] + rb * (bys[b] + rb * bzs[a])];
+            if (cid < 0) continue;
+            const int lx = x - bxs[c] * bs, ly = y - bys[b] * bs, lz = z - bzs[a] * bs;
+            const uint32_t val = blocks[static_cast<uint64_t>(cid) * nv1 * nv1 * nv1 + lx + nv1 * (ly + nv1 * lz)];
+            best = val < best ? val : best;
+          }
+    }
+    float res = 0.0f;
+    if (best == 0xffffffffu) {
       res = mode ? 1.0f : __int_as_float(0x7f800000);
     } else {
-      const float u = static_cast<float>(sqrt(__longlong_as_double(static_cast<long long>(best))));
+      const float u = __uint_as_float(best);
       res = mode ? static_cast<float>(static_cast<double>(u) - eps) : u;
     }
-    out[i] = res;
+    if (x < n1) out[row * n1 + x] = res;
+    if (signs) {
+      const unsigned m = __ballot_sync(0xffffffffu, x < n1 && res < 0.0f);
+      if (lane == 0) signs[wi] = m;
+    }
   }
 }
 
@@ -593,7 +614,7 @@ static DevBuf<uint64_t> hierarchy_to_bricks(Ctx& ctx, const TriD* T, int64_t nf,
 }
 
 void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t nf, int R, int mode, double eps,
-             float* d_out, int z0, int z1) {
+             float* d_out, int z0, int z1, uint32_t* d_signs) {
   if (z1 < 0) z1 = R + 1;
   PCU_REQUIRE(z0 >= 0 && z0 < z1 && z1 <= R + 1, PAMOPT_CU_EINVAL, "compute_udf: bad slab plane range");
   (void)nv;
@@ -604,7 +625,7 @@ void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t 
   const int64_t nvert = n1 * n1 * n1;
   if (nf == 0) {
     PCU_LAUNCH(ctx, k_finalize, static_cast<unsigned>(ctx.num_sms * 8), 256, 0, nullptr, nullptr, R, rb, bs, mode, eps, d_out,
-               z0, z1);
+               z0, z1, d_signs);
     return;
   }
   DevBuf<TriD> T(nf, ctx.stream);
@@ -637,13 +658,13 @@ void udf_run(Ctx& ctx, const double* dV, int64_t nv, const int32_t* dF, int64_t 
   PCU_LAUNCH(ctx, k_make_items, grid_for(nb, 256), 256, 0, bcnt.get(), boff.get(), item_off.get(), act_off.get(), nb,
              items.get(), bmap.get());
   const int nvb = (bs + 1) * (bs + 1) * (bs + 1);
-  DevBuf<unsigned long long> blocks(static_cast<size_t>(n_active ? n_active : 1) * nvb, ctx.stream);
+  DevBuf<uint32_t> blocks(static_cast<size_t>(n_active ? n_active : 1) * nvb, ctx.stream);
   blocks.memset(0xFF, ctx.stream);
   if (n_items) {
     PCU_LAUNCH(ctx, k_brick, n_items, 256, 0, items.get(), tris.get(), T.get(), R, rb, bs, J, blocks.get());
   }
   PCU_LAUNCH(ctx, k_finalize, static_cast<unsigned>(ctx.num_sms * 16), 256, 0, blocks.get(), bmap.get(), R, rb, bs,
-             mode, eps, d_out, z0, z1);
+             mode, eps, d_out, z0, z1, d_signs);
   (void)nvert;
 }
 

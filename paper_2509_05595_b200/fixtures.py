@@ -325,6 +325,37 @@ def make_config(name: str):
     return np.ascontiguousarray(v), np.ascontiguousarray(f, np.int32), R, cfg["target"]
 
 
+def add_bowties(v, f, seed: int, n: int):
+    """Bowtie (non-manifold) vertices: n random vertex pairs from different parts of
+    the soup are merged into one index."""
+    rng = Rng(seed * 104729 + 7)
+    f = f.copy()
+    a = rng.randint(0, len(v), n)
+    b = rng.randint(0, len(v), n)
+    for i, j in zip(a.tolist(), b.tolist()):
+        if i != j:
+            f[f == j] = i
+    keep = (f[:, 0] != f[:, 1]) & (f[:, 1] != f[:, 2]) & (f[:, 0] != f[:, 2])  # load_mesh drops these
+    return v, f[keep]
+
+
+def defect_corpus(n: int = 20, seed: int = 6):
+    """SPEC.md:805 acceptance #1 corpus: n fixtures with 5k-300k input faces (log-spaced), soups of
+    interpenetrating primitives with duplicate faces, holes, flipped faces, poked tetrahedra and
+    bowtie vertices.  Returns [(raw vertices, faces, R, target)] with R alternating 64 / 128 and a
+    1% face target."""
+    out = []
+    for i in range(n):
+        F = int(round(math.exp(math.log(5e3) + (math.log(3e5) - math.log(5e3)) * i / max(n - 1, 1))))
+        per = 5000 if F < 200000 else 10000
+        v, f = soup(max(1, F // per), per, seed=seed * 1000 + i, scale=(0.1, 0.35), spread=(0.25, 0.75))
+        v, f = inject_defects(v, f, seed=seed * 1000 + i, pokes=5 + i)
+        v, f = add_bowties(v, f, seed * 1000 + i, 3)
+        R = 64 if i % 2 == 0 else 128
+        out.append((np.ascontiguousarray(v * 2.0 - 0.3), np.ascontiguousarray(f, np.int32), R, max(4, len(f) // 100)))
+    return out
+
+
 def c5_batch(n: int = 64, seed: int = 5):
     """C5: n meshes, F log-uniform in [5e4, 2e6], recipes C1-C3 cycled (resolution by the SPEC
     auto rule: target = 1% of F -> R = 128 if target < 1000 else 256)."""

@@ -93,16 +93,57 @@ int main() {
   const IndexedMesh pj = project(s, in, pp);  // stage 3 (SPEC safe_project)
   const MeshReport rep3 = mesh_report(pj, &in, 4096);
   const bool proj_ok = pj.faces == s.faces && rep3.intersection_free && rep3.cd < rep.cd;
+  // SPEC-granular operations against the reference's own code
+  IndexedMesh dcopy = d;
+  HalfEdgeAdjacency adj(dcopy);  // reference mesh.cpp:185-197
+  std::vector<EdgeKey> ek;
+  for (int f = 0; f < d.face_count() && ek.size() < 3000; f += 3) ek.push_back(EdgeKey(d.faces[f][0], d.faces[f][1]));
+  const std::vector<bool> lk = link_condition_holds(d, ek);
+  bool link_same = true;
+  for (size_t i = 0; i < ek.size(); ++i) link_same = link_same && lk[i] == adj.link_condition_holds(ek[i].a, ek[i].b);
+  SimplifySession sess(d, 1000);
+  while (!sess.done()) {
+    sess.prepare();
+    sess.propagate_and_mark();
+    sess.collapse_batch();
+    sess.undo_loop();
+    sess.end_iteration();
+  }
+  const IndexedMesh ss = sess.finish();
+  const bool steps_same = ss.faces == s.faces && ss.vertices == s.vertices;
+  PatchSoup soup;
+  QuadMesh qm;
+  dmc_stages(g, soup, qm);
+  const IndexedMesh tq = triangulate_quads(R, soup, qm);
+  const bool dmc_steps_same = tq.faces == d.faces && tq.vertices == d.vertices;
+  // run_pipeline on the raw (un-normalised) input: certified, and equal to the reference's own
+  // normalise -> remesh -> denormalise (mesh_io.cpp:393-412)
+  IndexedMesh raw = icosphere(4);
+  for (Vec3d& v : raw.vertices) v = v * 3.0 + Vec3d(1.0, -2.0, 0.5);
+  PipelineConfig pc;
+  pc.resolution = R;
+  pc.target_faces = 1000;
+  const PipelineResult pr = run_pipeline(raw, pc);
+  IndexedMesh nr = raw;
+  const NormalizationTransform nt = normalize_unit_cube(nr, 6.0 / R);
+  IndexedMesh er = remesh(nr, R, 1000);
+  denormalize(er, nt);
+  const bool pipe_ok = pr.mesh.faces == er.faces && pr.mesh.vertices == er.vertices && pr.stages.size() == 2 &&
+                       pr.stages[0].manifold && pr.stages[0].watertight && pr.stages[0].intersection_free &&
+                       pr.stages[1].intersection_free && pr.mesh.face_count() <= 1000;
   std::printf("{\"dmc_faces\": %d, \"dmc_manifold\": %d, \"dmc_watertight\": %d, \"dmc_euler\": %d, "
               "\"dmc_isect\": %zu, \"out_faces\": %d, \"out_manifold\": %d, \"out_euler\": %d, \"out_isect\": %zu, "
               "\"iterations\": %lld, \"pipeline_equal\": %d, \"total_ms\": %.3f, \"topology_equal\": %d, "
               "\"nearest_equal\": %d, \"cd\": %.3e, \"hd\": %.3e, \"min_angle\": %.2f, \"projected_cd\": %.3e, "
-              "\"projection_ok\": %d}\n",
+              "\"projection_ok\": %d, \"link_equal\": %d, \"qem_steps_equal\": %d, \"dmc_steps_equal\": %d, "
+              "\"run_pipeline_ok\": %d}\n",
               d.face_count(), td.manifold, td.watertight, td.euler_characteristic, pd.size(), s.face_count(),
               ts.manifold, ts.euler_characteristic, ps.size(), static_cast<long long>(st.iterations), same,
-              tm.total_ms, topo_same, near_same, rep.cd, rep.hd, rep.min_angle_deg, rep3.cd, proj_ok);
+              tm.total_ms, topo_same, near_same, rep.cd, rep.hd, rep.min_angle_deg, rep3.cd, proj_ok, link_same,
+              steps_same, dmc_steps_same, pipe_ok);
   const bool ok = td.manifold && td.watertight && pd.empty() && ts.manifold && ps.empty() && s.face_count() <= 1000 &&
-                  same && topo_same && near_same && rep.watertight && rep.intersection_free && proj_ok;
+                  same && topo_same && near_same && rep.watertight && rep.intersection_free && proj_ok && link_same &&
+                  steps_same && dmc_steps_same && pipe_ok;
   std::fflush(stdout);
   std::_Exit(ok ? 0 : 1);  // parallel.cpp pool: never run static destructors
 }

@@ -70,3 +70,24 @@ def test_gpu_slab_errors(api):
         api.extract_slab(grid, 7, 6)   # empty own range
     m, _, _ = api.extract_slab(grid, 6, 8)
     m.free()
+
+
+def test_extract_slab_nccl_world1_equals_whole_grid(api):
+    """The C-ABI slab path over a real NCCL communicator (ncclCommInitAll on this one GPU): at
+    world = 1 it must reproduce the whole-grid extract exactly (multi-rank exchange logic is the
+    same code with neighbours; the Python twin is covered at world 2/3 with gloo)."""
+    from paper_2509_05595_b200 import fixtures as FX
+    v, f = FX.icosphere(4)
+    R = 64
+    v, _ = FX.normalize_unit_cube(v * (1.0 + 0.01 * FX.Rng(2).normal(len(v)))[:, None], 6.0 / R)
+    whole_v, whole_f = api.extract(api.compute_sdf((v, f), R)).download()
+    comms = api.nccl_comm_init_all([0])
+    try:
+        out, counts = api.extract_slab_nccl((v, f), R, 0, 1, comms[0])
+        gv, gf = out.download()
+    finally:
+        api.nccl_comm_destroy(comms[0])
+    assert np.array_equal(gf, whole_f) and np.array_equal(gv.view(np.uint64), whole_v.view(np.uint64))
+    assert counts[2] == len(whole_f)
+    out2, _ = api.extract_slab_nccl((v, f), R, 0, 1, None)  # world 1 needs no communicator
+    assert np.array_equal(out2.download()[1], whole_f)
