@@ -217,6 +217,8 @@ def lib():
             raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
+            if os.environ.get("PAMOPT_LIB") and not hasattr(L, name):
+                continue  # A/B variant library built from another revision
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -41,7 +41,7 @@ static void ctx_release(pamopt_cu_ctx c) {
 
 static void ctx_ref(pamopt_cu_ctx c) {
   std::lock_guard<std::mutex> l(c->mu);
-  ctx_ref(c);
+  ++c->refs;
 }
 
 static void ctx_unref(pamopt_cu_ctx c) {
