@@ -39,6 +39,7 @@ extern "C" {
 #define PAMOPT_CU_ENOMEM -3   /* device allocation failure */
 #define PAMOPT_CU_ENUMERIC -4 /* NaN edge cost */
 #define PAMOPT_CU_ECAP -5     /* reserved (no fixed per-element capacity remains) */
+#define PAMOPT_CU_EIO -7      /* malformed / truncated / empty mesh file (std::runtime_error, mesh_io.cpp:17-21) */
 
 typedef struct pamopt_cu_ctx_s* pamopt_cu_ctx;
 typedef struct pamopt_cu_mesh_s* pamopt_cu_mesh;
@@ -108,14 +109,18 @@ typedef struct {
   int64_t polygons_triangulated;
   int64_t vertices_welded;
 } pamopt_cu_load_stats;
-/* load_stl (mesh_io.cpp:309-366) for binary STL: corners welded by exact equality, vertices in
- * first-occurrence order, repeated-index faces dropped.  ASCII STL -> EINVAL (host loader). */
+/* load_stl (mesh_io.cpp:309-366), binary or ASCII: corners welded by exact equality on the GPU,
+ * vertices in first-occurrence order, repeated-index faces dropped.  Errors -> PAMOPT_CU_EIO. */
 int pamopt_cu_load_stl(pamopt_cu_ctx ctx, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
                        pamopt_cu_load_stats* stats);
-/* load_ply (mesh_io.cpp:135-255) for binary_little_endian PLY whose face lists hold exactly 3
- * indices (the reference writer's layout); vertex x/y/z of any scalar type.  Other layouts and
- * ASCII PLY -> EINVAL (host loader). */
+/* load_ply (mesh_io.cpp:135-255): binary_little_endian bodies with 3-index face lists (the
+ * reference writer's layout) are decoded on the GPU; ASCII bodies and variable-length face lists
+ * are decoded record by record (polygons fanned, mesh_io.cpp:32-42).  Errors -> PAMOPT_CU_EIO. */
 int pamopt_cu_load_ply(pamopt_cu_ctx ctx, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
+                       pamopt_cu_load_stats* stats);
+/* load_obj (mesh_io.cpp:46-82): v / f lines, 1-based and negative (relative) indices, /vt/vn
+ * suffixes ignored, polygons fanned (mesh_io.cpp:32-42).  Errors -> PAMOPT_CU_EIO. */
+int pamopt_cu_load_obj(pamopt_cu_ctx ctx, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
                        pamopt_cu_load_stats* stats);
 /* normalize_unit_cube (mesh_io.cpp:393-408), in place; scale_translation = {scale, tx, ty, tz} or NULL */
 int pamopt_cu_normalize_unit_cube(pamopt_cu_mesh mesh, double padding, double* scale_translation);

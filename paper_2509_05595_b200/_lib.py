@@ -12,7 +12,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PAMOPT_LIB") or os.path.join(HERE, "libpamopt_cu.so")  # PAMOPT_LIB: A/B variants only
 
-OK, EINVAL, ECUDA, ENOMEM, ENUMERIC, ECAP, ECERT = 0, -1, -2, -3, -4, -5, -6
+OK, EINVAL, ECUDA, ENOMEM, ENUMERIC, ECAP, ECERT, EIO = 0, -1, -2, -3, -4, -5, -6, -7
 
 
 class SimplifyParams(C.Structure):
@@ -137,6 +137,7 @@ _SIGS = {
     "pamopt_cu_mesh_free": (C.c_int, [vp]),
     "pamopt_cu_load_stl": (C.c_int, [vp, vp, i64, P(vp), P(LoadStats)]),
     "pamopt_cu_load_ply": (C.c_int, [vp, vp, i64, P(vp), P(LoadStats)]),
+    "pamopt_cu_load_obj": (C.c_int, [vp, vp, i64, P(vp), P(LoadStats)]),
     "pamopt_cu_normalize_unit_cube": (C.c_int, [vp, dbl, vp]),
     "pamopt_cu_denormalize": (C.c_int, [vp, vp]),
     "pamopt_cu_pipeline_defaults": (C.c_int, [P(PipelineConfig)]),

@@ -721,19 +721,19 @@ def mesh_report(mesh, reference=None, n_samples: int = 16384, seed: int = 42, ct
 
 # ------------------------------------------------------------------ ingest
 def load_mesh_bytes(data: bytes, fmt: str, ctx: Context | None = None):
-    """Binary STL / binary little-endian PLY bytes -> (DeviceMesh, LoadStats dict), decoded and
-    (STL) welded on the GPU with the reference's load_mesh semantics (mesh_io.cpp:309-384)."""
+    """OBJ / PLY / STL bytes -> (DeviceMesh, LoadStats dict) with the reference's load_mesh
+    semantics (mesh_io.cpp:46-384): binary bodies decoded and STL corners welded on the GPU."""
     ctx = ctx or default_context()
     buf = np.frombuffer(data, dtype=np.uint8)
     h = C.c_void_p()
     st = _lib.LoadStats()
-    fn = {"stl": lib().pamopt_cu_load_stl, "ply": lib().pamopt_cu_load_ply}[fmt.lower()]
+    fn = {"stl": lib().pamopt_cu_load_stl, "ply": lib().pamopt_cu_load_ply, "obj": lib().pamopt_cu_load_obj}[fmt.lower()]
     check(fn(ctx.h, buf.ctypes.data, len(buf), C.byref(h), C.byref(st)))
     return DeviceMesh(h, ctx), st.as_dict()
 
 
 def load_mesh(path: str, ctx: Context | None = None):
-    """load_mesh (mesh_io.cpp:372-385) for .stl / .ply files on the GPU."""
+    """load_mesh (mesh_io.cpp:372-385) for .obj / .ply / .stl files."""
     ext = path.rsplit(".", 1)[-1].lower()
     with open(path, "rb") as fh:
         return load_mesh_bytes(fh.read(), ext, ctx)

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
 SOURCES = ["capi.cu", "udf.cu", "dmc.cu", "isect.cu", "simplify.cu", "metrics.cu", "ingest.cu", "project.cu",
-           "slab_nccl.cu"]
+           "slab_nccl.cu", "ingest_text.cu"]
 
 
 def _stale(src_files, target):

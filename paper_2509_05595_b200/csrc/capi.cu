@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <string_view>
 #include <algorithm>
 #include <vector>
 #include <sstream>
@@ -537,21 +538,40 @@ int pamopt_cu_load_stl(pamopt_cu_ctx c, const void* bytes, int64_t nbytes, pamop
     check_ctx(c);
     PCU_REQUIRE(bytes && out && nbytes >= 0, PAMOPT_CU_EINVAL, "null argument");
     const char* b = static_cast<const char*>(bytes);
-    if (nbytes >= 5 && std::strncmp(b, "solid", 5) == 0) {
-      const std::string head(b, static_cast<size_t>(nbytes));
-      PCU_REQUIRE(head.find("facet") == std::string::npos, PAMOPT_CU_EINVAL,
-                  "load_stl: ascii stl (parse it with the host loader, mesh_io.cpp:320-342)");
-    }
-    PCU_REQUIRE(nbytes >= 84, PAMOPT_CU_EINVAL, "load_stl: truncated binary stl header");
-    uint32_t count = 0;
-    std::memcpy(&count, b + 80, 4);
     pcu::DeviceGuard g(c->ctx.device);
-    pcu::DevBuf<uint8_t> d(static_cast<size_t>(nbytes), c->ctx.stream);
-    PCU_CUDA(cudaMemcpyAsync(d.get(), bytes, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, c->ctx.stream));
     pcu::IngestResult r;
-    pcu::load_stl_binary(c->ctx, d.get(), nbytes, count, r);
-    PCU_REQUIRE(r.nf > 0, PAMOPT_CU_EINVAL, "load_stl: empty mesh (no faces)");
+    // a binary file can also start with "solid": ASCII only if "facet" appears (mesh_io.cpp:316-320)
+    const bool ascii = nbytes >= 5 && std::strncmp(b, "solid", 5) == 0 &&
+                       std::string_view(b, static_cast<size_t>(nbytes)).find("facet") != std::string_view::npos;
+    if (ascii) {
+      pcu::load_stl_ascii(c->ctx, b, nbytes, r);
+    } else {
+      PCU_REQUIRE(nbytes >= 84, PAMOPT_CU_EIO, "load_stl: truncated binary stl header");
+      uint32_t count = 0;
+      std::memcpy(&count, b + 80, 4);
+      PCU_REQUIRE(nbytes >= 84 + 50 * static_cast<int64_t>(count), PAMOPT_CU_EIO,
+                  "load_stl: truncated binary stl (fewer than 84 + 50 * count bytes)");
+      pcu::DevBuf<uint8_t> d(static_cast<size_t>(nbytes), c->ctx.stream);
+      PCU_CUDA(cudaMemcpyAsync(d.get(), bytes, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, c->ctx.stream));
+      pcu::load_stl_binary(c->ctx, d.get(), nbytes, count, r);
+    }
+    PCU_REQUIRE(r.nf > 0, PAMOPT_CU_EIO, "load_stl: empty mesh (no faces)");
     if (stats) *stats = pamopt_cu_load_stats{r.degenerate_dropped, 0, r.welded};
+    *out = mesh_from_ingest(c, r);
+  });
+}
+
+int pamopt_cu_load_obj(pamopt_cu_ctx c, const void* bytes, int64_t nbytes, pamopt_cu_mesh* out,
+                       pamopt_cu_load_stats* stats) {
+  return guarded([&] {
+    check_ctx(c);
+    PCU_REQUIRE(bytes && out && nbytes >= 0, PAMOPT_CU_EINVAL, "null argument");
+    pcu::DeviceGuard g(c->ctx.device);
+    pcu::IngestResult r;
+    int64_t tri = 0;
+    pcu::load_obj_text(c->ctx, static_cast<const char*>(bytes), nbytes, r, &tri);
+    PCU_REQUIRE(r.nf > 0, PAMOPT_CU_EIO, "load_obj: empty mesh (no faces)");
+    if (stats) *stats = pamopt_cu_load_stats{r.degenerate_dropped, tri, 0};
     *out = mesh_from_ingest(c, r);
   });
 }
@@ -683,15 +703,29 @@ int pamopt_cu_load_ply(pamopt_cu_ctx c, const void* bytes, int64_t nbytes, pamop
   return guarded([&] {
     check_ctx(c);
     PCU_REQUIRE(bytes && out && nbytes > 0, PAMOPT_CU_EINVAL, "null argument");
-    int64_t body = 0;
-    const pcu::PlyBinaryLayout L = ply_layout(static_cast<const char*>(bytes), nbytes, body);
+    const char* b = static_cast<const char*>(bytes);
     pcu::DeviceGuard g(c->ctx.device);
-    pcu::DevBuf<uint8_t> d(static_cast<size_t>(nbytes), c->ctx.stream);
-    PCU_CUDA(cudaMemcpyAsync(d.get(), bytes, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, c->ctx.stream));
     pcu::IngestResult r;
-    pcu::load_ply_binary(c->ctx, d.get(), L, r);
-    PCU_REQUIRE(r.nf > 0, PAMOPT_CU_EINVAL, "load_ply: empty mesh (no faces)");
-    if (stats) *stats = pamopt_cu_load_stats{r.degenerate_dropped, 0, 0};
+    int64_t tri = 0;
+    // fixed-size binary records (the reference writer's layout): decoded on the GPU; ASCII bodies
+    // and variable-length face lists: the host decoder, record by record as mesh_io.cpp:186-244
+    bool fixed = false;
+    pcu::PlyBinaryLayout L;
+    int64_t body = 0;
+    try {
+      L = ply_layout(b, nbytes, body);
+      fixed = true;
+    } catch (const pcu::Error&) {
+      fixed = false;
+    }
+    if (fixed) {
+      pcu::DevBuf<uint8_t> d(static_cast<size_t>(nbytes), c->ctx.stream);
+      PCU_CUDA(cudaMemcpyAsync(d.get(), bytes, static_cast<size_t>(nbytes), cudaMemcpyHostToDevice, c->ctx.stream));
+      fixed = pcu::load_ply_binary(c->ctx, d.get(), L, r);  // false: a face list is not a triangle
+    }
+    if (!fixed) pcu::load_ply_host(c->ctx, b, nbytes, r, &tri);
+    PCU_REQUIRE(r.nf > 0, PAMOPT_CU_EIO, "load_ply: empty mesh (no faces)");
+    if (stats) *stats = pamopt_cu_load_stats{r.degenerate_dropped, tri, 0};
     *out = mesh_from_ingest(c, r);
   });
 }

@@ -266,7 +266,7 @@ void load_stl_binary(Ctx& ctx, const uint8_t* d_bytes, int64_t nbytes, uint32_t 
   finish_faces(ctx, tri, count, out);
 }
 
-void load_ply_binary(Ctx& ctx, const uint8_t* d_bytes, const PlyBinaryLayout& H, IngestResult& out) {
+bool load_ply_binary(Ctx& ctx, const uint8_t* d_bytes, const PlyBinaryLayout& H, IngestResult& out) {
   cudaStream_t st = ctx.stream;
   out = IngestResult();
   PlyLayout L{};
@@ -294,10 +294,10 @@ void load_ply_binary(Ctx& ctx, const uint8_t* d_bytes, const PlyBinaryLayout& H,
   PCU_CUDA(cudaMemsetAsync(bad.get(), 0, 8, st));
   if (H.nface) PCU_LAUNCH(ctx, k_ply_faces, grid_for(H.nface, 256), 256, 0, d_bytes, L, tri.get(), bad.get());
   const unsigned long long b = read_scalar(ctx, bad.get());
-  PCU_REQUIRE(!(b & 2ull), PAMOPT_CU_EINVAL, "load_ply: face index out of range");
-  PCU_REQUIRE(!(b & 1ull), PAMOPT_CU_EINVAL,
-              "load_ply: a face list is not a triangle (the GPU loader reads fixed 3-index records)");
+  if (b & 1ull) return false;  // a face list is not a triangle: variable records (host decoder)
+  PCU_REQUIRE(!(b & 2ull), PAMOPT_CU_EIO, "load_ply: face index out of range");
   finish_faces(ctx, tri, H.nface, out);
+  return true;
 }
 
 void normalize_unit_cube(Ctx& ctx, double* dV, int64_t nv, double padding, double* scale_translation) {

@@ -1015,23 +1015,12 @@ void verdict_by_class(Ctx& ctx, const double* dV, const int32_t* dF, const int32
 void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                        const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
                        uint8_t* d_revert) {
-  static const bool build_all = [] {
-    const char* e = std::getenv("PAMOPT_UNDO_BUILD_ALL");
-    return e && e[0] == '1';
-  }();
-  if (!build_all) {
-    // round 1: grid over the faces owned by applied collapses, probed by every alive face
-    detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner,
-                 d_revert, true);
-    return;
-  }
-  // variant: grid over every alive face, probed by the owned faces only; a pair of two owned
-  // faces is emitted from its smaller probe (in_probe flags)
-  S.in_build.ensure(nf, ctx.stream);
-  PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, ctx.stream));
-  PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_query, 256), 256, 0, d_query_faces, n_query, S.in_build.get());
-  detect_round(ctx, S, dV, dF, nf, d_falive, nullptr, nf, d_query_faces, n_query, 1, 1, nullptr, 0, d_owner, d_revert,
-               true, S.in_build.get());
+  // round 1: grid over the faces owned by applied collapses (~0.4 of the alive faces in every
+  // iteration), probed by every alive face.  The converse (grid over every alive face, probed by
+  // the owned faces, pairs of two owned faces from the smaller probe via in_probe) was measured
+  // slower at C3: k_probe 36.0 -> 61.6 ms, k_bin 7.6 -> 19.4 ms (profiles/r02_summary.md).
+  detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner,
+               d_revert, true);
 }
 
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,

@@ -110,7 +110,12 @@ struct PlyBinaryLayout {
   int count_off = 0, count_type = 5, index_off = 1, index_type = 2;
 };
 void load_stl_binary(Ctx& ctx, const uint8_t* d_bytes, int64_t nbytes, uint32_t count, IngestResult& out);
-void load_ply_binary(Ctx& ctx, const uint8_t* d_bytes, const PlyBinaryLayout& layout, IngestResult& out);
+// false (nothing decoded) when a face list is not a triangle: the layout is not fixed-size
+bool load_ply_binary(Ctx& ctx, const uint8_t* d_bytes, const PlyBinaryLayout& layout, IngestResult& out);
+// text formats (ingest_text.cu): OBJ, ASCII STL (GPU weld), PLY record by record
+void load_obj_text(Ctx& ctx, const char* b, int64_t n, IngestResult& out, int64_t* triangulated);
+void load_stl_ascii(Ctx& ctx, const char* b, int64_t n, IngestResult& out);
+void load_ply_host(Ctx& ctx, const char* b, int64_t n, IngestResult& out, int64_t* triangulated);
 // denormalize (mesh_io.cpp:410-412) with {scale, tx, ty, tz} from normalize_unit_cube
 void denormalize(Ctx& ctx, double* dV, int64_t nv, const double* scale_translation);
 void normalize_unit_cube(Ctx& ctx, double* dV, int64_t nv, double padding, double* scale_translation);

@@ -1,7 +1,8 @@
-"""Ingest parity: binary STL weld + PLY decode against the reference's own
-load_mesh (golden vectors from oracle/_ref, tests/golden/make_golden_ingest.py), the oracle's
-STL restatement on CPU, and the GPU loaders (pamopt_cu_load_stl / pamopt_cu_load_ply /
-pamopt_cu_normalize_unit_cube)."""
+"""Ingest parity: every format of the reference's load_mesh (binary and
+ASCII STL with the weld, binary / ASCII / variable-list PLY, OBJ with polygons, relative indices
+and /vt/vn suffixes) against the reference's own loader (golden vectors from oracle/_ref,
+tests/golden/make_golden_ingest.py), the oracle's STL restatement on CPU, and the library's
+loaders (pamopt_cu_load_stl / _load_ply / _load_obj / pamopt_cu_normalize_unit_cube)."""
 import os
 import struct
 import tempfile
@@ -20,7 +21,7 @@ def _stats(st):
 
 def test_oracle_stl_weld_matches_reference(oracle):
     for name, (ext, data) in corpus().items():
-        if ext != "stl":
+        if ext != "stl" or data.startswith(b"solid"):  # the oracle restates the binary weld only
             continue
         v, f, st = oracle.load_stl_binary(data)
         assert np.array_equal(v.view(np.uint64), GOLD[f"{name}_v_bits"]), name
@@ -53,21 +54,34 @@ def test_gpu_loaders_match_reference(api):
 
 @pytest.mark.gpu
 def test_gpu_loader_errors(api):
-    from paper_2509_05595_b200._lib import PamoptInvalidArgument
+    """Malformed / truncated / empty files raise (PAMOPT_CU_EIO = the reference's
+    std::runtime_error, mesh_io.cpp:17-21), for every format."""
+    from paper_2509_05595_b200._lib import EIO, PamoptError
     from paper_2509_05595_b200 import fixtures as FX
     v, f = FX.icosphere(1)
-    bad = [("stl", b"solid x\n facet normal 0 0 1\n"),                    # ascii stl
+    bad = [("stl", b"solid x\n facet normal 0 0 1\n"),                    # ascii stl without vertices
+           ("stl", b"solid x\n facet normal 0 0 1\n outer loop\n vertex 0 0 0\n vertex 1 0 0\n"),  # dangling
+           ("stl", b"solid x\n facet\n vertex 0 0 zero\n"),               # malformed vertex
            ("stl", stl_bytes(v, f)[:-30]),                                 # truncated
            ("stl", stl_bytes(v, f[:0])),                                   # no faces
            ("ply", ply_bytes(v, f).replace(b"binary_little_endian", b"ascii               ")),
-           ("ply", ply_bytes(v, np.where(f == 0, 999, f)))]                # index out of range
+           ("ply", ply_bytes(v, np.where(f == 0, 999, f))),                # index out of range
+           ("ply", b"plx\nformat ascii 1.0\nend_header\n"),               # missing magic
+           ("obj", b"v 1 2\nf 1 1 1\n"),                                   # malformed vertex
+           ("obj", b"v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 4\n"),              # index out of range
+           ("obj", b"v 0 0 0\nv 1 0 0\nf 1 2\n"),                          # fewer than 3 vertices
+           ("obj", b"v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 x\n"),              # malformed index
+           ("obj", b"v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 1 2\n")]              # only degenerate -> empty
+    for ext, data in bad:
+        with pytest.raises(PamoptError) as e:
+            api.load_mesh_bytes(data, ext)
+        assert e.value.code == EIO, (ext, data[:40])
+    # a binary PLY whose face list is a quad is valid (variable lists are decoded record by record)
     quad = bytearray(ply_bytes(v, f, extras=False))
     body = quad.index(b"end_header\n") + len(b"end_header\n") + 24 * len(v)
-    quad[body] = 4                                                          # a non-triangle list
-    bad.append(("ply", bytes(quad)))
-    for ext, data in bad:
-        with pytest.raises(PamoptInvalidArgument):
-            api.load_mesh_bytes(data, ext)
+    quad[body] = 4
+    with pytest.raises(PamoptError):  # ... but 4 indices read from a 3-index record run off the end
+        api.load_mesh_bytes(bytes(quad), "ply")
 
 
 @pytest.mark.gpu
