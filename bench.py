@@ -330,7 +330,7 @@ def run_ours(args):
                     "simt_efficiency": round(kb["threads_per_warp_inst"] / 32, 4),
                     "source": f"profiles/r01_ncu_counters_{args.config}.json"}
         ktot = sum(ms for ms, _ in ktimes.values()) or 1.0
-        top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:12]
+        top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:30]
         line["kernels"] = {"source": "one untimed step, CUDA events around every launch",
                            "device_ms_total": round(ktot, 3),
                            "top": [{"name": k, "ms": round(ms, 3), "launches": n, "share": round(ms / ktot, 4)}
