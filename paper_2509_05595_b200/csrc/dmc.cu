@@ -189,49 +189,93 @@ __device__ __forceinline__ void cell_xyz(int64_t c, int R, int64_t& x, int64_t& 
   z = c >> (2 * lg);
 }
 
-__global__ void __launch_bounds__(256) k_classify_count(GridView g, int64_t c0, int64_t ncell,
-                                                        uint32_t* __restrict__ bcount) {
-  typedef cub::BlockReduce<uint32_t, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kCellsPerBlock;
-  uint32_t cnt = 0;
-  for (int k = 0; k < kCellsPerBlock / 256; ++k) {
-    const int64_t c = base + k * 256 + threadIdx.x;
-    if (c < ncell) {
-      int64_t x, y, z;
-      cell_xyz(c0 + c, g.R, x, y, z);
-      const int cs = g.case_of(x, y, z);
-      cnt += (cs != 0 && cs != 255);
-    }
-  }
-  const uint32_t tot = BR(tmp).Sum(cnt);
-  if (threadIdx.x == 0) bcount[blockIdx.x] = tot;
+// Dense classify over the sign mask, one warp per segment of 32 consecutive cells of a row:
+// the 8 words (rows (y,z), (y+1,z), (y,z+1), (y+1,z+1), each with its successor for the x+1
+// corner) are warp-uniform broadcast loads; lane l takes bits x, x+1 of each row with a funnel
+// shift.  A segment whose 8 words are all zero (every corner positive, the bulk of the grid away
+// from the band) is skipped without per-cell work.  Segments are numbered in cell order
+// (z, y, x-segment), so per-block counts + an exclusive scan give the x-fastest compaction.
+constexpr int kSegWarp = 8;                      // segments per warp
+constexpr int kSegBlock = 8 * kSegWarp;          // segments per 256-thread block
+
+struct SegCtx {
+  int R, lg, segs_row;  // segments per row = ceil(R / 32)
+  int64_t z0, nseg;     // first cell layer, number of segments
+};
+
+// flags (32 lanes) of segment s; returns the ballot, and this lane's cell / case
+__device__ __forceinline__ unsigned seg_flags(const GridView& g, const SegCtx& S, int64_t s, int lane, int64_t& cell,
+                                              int& cs) {
+  const int64_t row = s / S.segs_row;  // (z - z0) * R + y
+  const int w = static_cast<int>(s - row * S.segs_row);
+  const int64_t y = row & (S.R - 1), z = S.z0 + (row >> S.lg);
+  const int64_t r = (z - g.zb) * g.n1 + y;
+  const uint32_t* p = g.sg + r * g.W + w;
+  const int64_t W = g.W, rW = g.n1 * g.W;
+  const bool has1 = w + 1 < g.W;
+  const uint32_t A = p[0], A1 = has1 ? p[1] : 0u, B = p[W], B1 = has1 ? p[W + 1] : 0u;
+  const uint32_t C = p[rW], C1 = has1 ? p[rW + 1] : 0u, D = p[rW + W], D1 = has1 ? p[rW + W + 1] : 0u;
+  const int x = (w << 5) + lane;
+  cell = x + S.R * row + static_cast<int64_t>(S.R) * S.R * S.z0;
+  cs = 0;
+  if ((A | A1 | B | B1 | C | C1 | D | D1) == 0u) return 0u;  // warp-uniform: all corners positive
+  const uint32_t a = __funnelshift_r(A, A1, lane), b = __funnelshift_r(B, B1, lane);
+  const uint32_t c = __funnelshift_r(C, C1, lane), d = __funnelshift_r(D, D1, lane);
+  cs = static_cast<int>((a & 3u) | (b & 3u) << 2 | (c & 3u) << 4 | (d & 3u) << 6);
+  return __ballot_sync(0xffffffffu, x < S.R && cs != 0 && cs != 255);
 }
 
-__global__ void __launch_bounds__(256) k_classify_write(GridView g, int64_t c0, int64_t ncell,
-                                                        const uint32_t* __restrict__ boff,
+__global__ void __launch_bounds__(256) k_classify_count(GridView g, SegCtx S, uint32_t* __restrict__ bcount) {
+  __shared__ uint32_t wsum[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kSegBlock + warp * kSegWarp;
+  uint32_t n = 0;
+  for (int k = 0; k < kSegWarp; ++k) {
+    const int64_t s = s0 + k;
+    if (s >= S.nseg) break;
+    int64_t cell;
+    int cs;
+    n += __popc(seg_flags(g, S, s, lane, cell, cs));
+  }
+  if (lane == 0) wsum[warp] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int i = 0; i < 8; ++i) t += wsum[i];
+    bcount[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_classify_write(GridView g, SegCtx S, const uint32_t* __restrict__ boff,
                                                         uint32_t* __restrict__ cells, uint8_t* __restrict__ cases) {
-  typedef cub::BlockScan<uint32_t, 256> BS;
-  __shared__ typename BS::TempStorage tmp;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kCellsPerBlock;
+  __shared__ uint32_t wsum[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kSegBlock + warp * kSegWarp;
+  uint32_t n = 0;
+  for (int k = 0; k < kSegWarp; ++k) {  // this warp's count, for the in-block prefix
+    const int64_t s = s0 + k;
+    if (s >= S.nseg) break;
+    int64_t cell;
+    int cs;
+    n += __popc(seg_flags(g, S, s, lane, cell, cs));
+  }
+  if (lane == 0) wsum[warp] = n;
+  __syncthreads();
   uint32_t run = boff[blockIdx.x];
-  for (int k = 0; k < kCellsPerBlock / 256; ++k) {
-    const int64_t c = base + k * 256 + threadIdx.x;
-    int cs = 0;
-    if (c < ncell) {
-      int64_t x, y, z;
-      cell_xyz(c0 + c, g.R, x, y, z);
-      cs = g.case_of(x, y, z);
+  for (int i = 0; i < warp; ++i) run += wsum[i];
+  const unsigned lt = (1u << lane) - 1u;
+  for (int k = 0; k < kSegWarp; ++k) {
+    const int64_t s = s0 + k;
+    if (s >= S.nseg) break;
+    int64_t cell;
+    int cs;
+    const unsigned m = seg_flags(g, S, s, lane, cell, cs);
+    if ((m >> lane) & 1u) {
+      const uint32_t pos = run + __popc(m & lt);
+      cells[pos] = static_cast<uint32_t>(cell);
+      cases[pos] = static_cast<uint8_t>(cs);
     }
-    const uint32_t flag = (c < ncell && cs != 0 && cs != 255) ? 1u : 0u;
-    uint32_t pos, tot;
-    BS(tmp).ExclusiveSum(flag, pos, tot);
-    if (flag) {
-      cells[run + pos] = static_cast<uint32_t>(c0 + c);
-      cases[run + pos] = static_cast<uint8_t>(cs);
-    }
-    run += tot;
-    __syncthreads();
+    run += __popc(m);
   }
 }
 
@@ -606,16 +650,22 @@ void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, 
   const int64_t rr = static_cast<int64_t>(R) * R;
   const int64_t c0 = rr * cz0;
   const int64_t ncell = rr * (own_z1 - cz0);
-  const int64_t nblk = (ncell + kCellsPerBlock - 1) / kCellsPerBlock;
+  SegCtx S;
+  S.R = R;
+  S.lg = __builtin_ctz(static_cast<unsigned>(R));
+  S.segs_row = (R + 31) / 32;
+  S.z0 = cz0;
+  S.nseg = static_cast<int64_t>(R) * (own_z1 - cz0) * S.segs_row;
+  const int64_t nblk = (S.nseg + kSegBlock - 1) / kSegBlock;
   DevBuf<uint32_t> bcount(nblk, ctx.stream), boff(nblk, ctx.stream);
-  PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, c0, ncell, bcount.get());
+  PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, S, bcount.get());
   exclusive_scan_u32(ctx, bcount.get(), boff.get(), nblk);
   const uint32_t na = read_scalar(ctx, boff.get() + nblk - 1) + read_scalar(ctx, bcount.get() + nblk - 1);
   res.cells.alloc(na ? na : 1, ctx.stream);
   res.cases.alloc(na ? na : 1, ctx.stream);
   res.flips.alloc(na ? na : 1, ctx.stream);
   res.n_active = na;
-  PCU_LAUNCH(ctx, k_classify_write, static_cast<unsigned>(nblk), 256, 0, g, c0, ncell, boff.get(), res.cells.get(),
+  PCU_LAUNCH(ctx, k_classify_write, static_cast<unsigned>(nblk), 256, 0, g, S, boff.get(), res.cells.get(),
              res.cases.get());
   res.nvp_own = res.n_extra = 0;
   if (na == 0) {
