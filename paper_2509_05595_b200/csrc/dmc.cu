@@ -189,90 +189,87 @@ __device__ __forceinline__ void cell_xyz(int64_t c, int R, int64_t& x, int64_t& 
   z = c >> (2 * lg);
 }
 
-// Dense classify over the sign mask, one warp per segment of 32 consecutive cells of a row:
-// the 8 words (rows (y,z), (y+1,z), (y,z+1), (y+1,z+1), each with its successor for the x+1
-// corner) are warp-uniform broadcast loads; lane l takes bits x, x+1 of each row with a funnel
-// shift.  A segment whose 8 words are all zero (every corner positive, the bulk of the grid away
-// from the band) is skipped without per-cell work.  Segments are numbered in cell order
-// (z, y, x-segment), so per-block counts + an exclusive scan give the x-fastest compaction.
-constexpr int kSegWarp = 8;                      // segments per warp
-constexpr int kSegBlock = 8 * kSegWarp;          // segments per 256-thread block
+// Dense classify over the sign mask: one warp per row of cells (y, z), 32 consecutive cells per
+// step.  The 8 words of a step (rows (y,z), (y+1,z), (y,z+1), (y+1,z+1), each with its successor
+// for the x+1 corner) are warp-uniform broadcast loads; lane l takes bits x, x+1 of each row with
+// a funnel shift.  A step whose 8 words are all zero (every corner positive: the bulk of the grid
+// away from the band) does no per-cell work.  Blocks take 8 consecutive rows, so per-block counts
+// + an exclusive scan give the x-fastest compaction; all index math is 32-bit shifts.
+constexpr int kRowsBlock = 8;  // rows (warps) per 256-thread block
 
 struct SegCtx {
-  int R, lg, segs_row;  // segments per row = ceil(R / 32)
-  int64_t z0, nseg;     // first cell layer, number of segments
+  int R, lg;     // cells per row, log2 R
+  int nrows;     // rows of the classified layers: R * layers
+  int z0;        // first cell layer
 };
 
-// flags (32 lanes) of segment s; returns the ballot, and this lane's cell / case
-__device__ __forceinline__ unsigned seg_flags(const GridView& g, const SegCtx& S, int64_t s, int lane, int64_t& cell,
-                                              int& cs) {
-  const int64_t row = s / S.segs_row;  // (z - z0) * R + y
-  const int w = static_cast<int>(s - row * S.segs_row);
-  const int64_t y = row & (S.R - 1), z = S.z0 + (row >> S.lg);
-  const int64_t r = (z - g.zb) * g.n1 + y;
-  const uint32_t* p = g.sg + r * g.W + w;
+// ballot of active cells of the step (row, w); this lane's case in cs
+__device__ __forceinline__ unsigned step_flags(const GridView& g, const uint32_t* __restrict__ p, int has1, int valid,
+                                               int lane, int& cs) {
   const int64_t W = g.W, rW = g.n1 * g.W;
-  const bool has1 = w + 1 < g.W;
-  const uint32_t A = p[0], A1 = has1 ? p[1] : 0u, B = p[W], B1 = has1 ? p[W + 1] : 0u;
-  const uint32_t C = p[rW], C1 = has1 ? p[rW + 1] : 0u, D = p[rW + W], D1 = has1 ? p[rW + W + 1] : 0u;
-  const int x = (w << 5) + lane;
-  cell = x + S.R * row + static_cast<int64_t>(S.R) * S.R * S.z0;
+  const uint32_t A = p[0], B = p[W], C = p[rW], D = p[rW + W];
+  const uint32_t A1 = has1 ? p[1] : 0u, B1 = has1 ? p[W + 1] : 0u, C1 = has1 ? p[rW + 1] : 0u,
+                 D1 = has1 ? p[rW + W + 1] : 0u;
   cs = 0;
   if ((A | A1 | B | B1 | C | C1 | D | D1) == 0u) return 0u;  // warp-uniform: all corners positive
   const uint32_t a = __funnelshift_r(A, A1, lane), b = __funnelshift_r(B, B1, lane);
   const uint32_t c = __funnelshift_r(C, C1, lane), d = __funnelshift_r(D, D1, lane);
   cs = static_cast<int>((a & 3u) | (b & 3u) << 2 | (c & 3u) << 4 | (d & 3u) << 6);
-  return __ballot_sync(0xffffffffu, x < S.R && cs != 0 && cs != 255);
+  return __ballot_sync(0xffffffffu, lane < valid && cs != 0 && cs != 255);
+}
+
+// the mask words of cell row `row` (= (z - z0) * R + y), word 0
+__device__ __forceinline__ const uint32_t* row_words(const GridView& g, const SegCtx& S, int row) {
+  const int y = row & (S.R - 1), z = S.z0 + (row >> S.lg);
+  return g.sg + ((static_cast<int64_t>(z) - g.zb) * g.n1 + y) * g.W;
 }
 
 __global__ void __launch_bounds__(256) k_classify_count(GridView g, SegCtx S, uint32_t* __restrict__ bcount) {
-  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t wsum[kRowsBlock];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kSegBlock + warp * kSegWarp;
+  const int row = blockIdx.x * kRowsBlock + warp;
   uint32_t n = 0;
-  for (int k = 0; k < kSegWarp; ++k) {
-    const int64_t s = s0 + k;
-    if (s >= S.nseg) break;
-    int64_t cell;
-    int cs;
-    n += __popc(seg_flags(g, S, s, lane, cell, cs));
+  if (row < S.nrows) {
+    const uint32_t* p = row_words(g, S, row);
+    for (int w = 0, x0 = 0; x0 < S.R; ++w, x0 += 32) {
+      int cs;
+      n += __popc(step_flags(g, p + w, w + 1 < g.W, S.R - x0, lane, cs));
+    }
   }
   if (lane == 0) wsum[warp] = n;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t t = 0;
-    for (int i = 0; i < 8; ++i) t += wsum[i];
+    for (int i = 0; i < kRowsBlock; ++i) t += wsum[i];
     bcount[blockIdx.x] = t;
   }
 }
 
 __global__ void __launch_bounds__(256) k_classify_write(GridView g, SegCtx S, const uint32_t* __restrict__ boff,
                                                         uint32_t* __restrict__ cells, uint8_t* __restrict__ cases) {
-  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t wsum[kRowsBlock];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kSegBlock + warp * kSegWarp;
+  const int row = blockIdx.x * kRowsBlock + warp;
+  const uint32_t* p = row < S.nrows ? row_words(g, S, row) : nullptr;
   uint32_t n = 0;
-  for (int k = 0; k < kSegWarp; ++k) {  // this warp's count, for the in-block prefix
-    const int64_t s = s0 + k;
-    if (s >= S.nseg) break;
-    int64_t cell;
-    int cs;
-    n += __popc(seg_flags(g, S, s, lane, cell, cs));
-  }
+  if (p)
+    for (int w = 0, x0 = 0; x0 < S.R; ++w, x0 += 32) {  // this warp's count, for the in-block prefix
+      int cs;
+      n += __popc(step_flags(g, p + w, w + 1 < g.W, S.R - x0, lane, cs));
+    }
   if (lane == 0) wsum[warp] = n;
   __syncthreads();
+  if (!p) return;
   uint32_t run = boff[blockIdx.x];
   for (int i = 0; i < warp; ++i) run += wsum[i];
   const unsigned lt = (1u << lane) - 1u;
-  for (int k = 0; k < kSegWarp; ++k) {
-    const int64_t s = s0 + k;
-    if (s >= S.nseg) break;
-    int64_t cell;
+  const uint32_t cbase = static_cast<uint32_t>(row + S.R * S.z0) << S.lg;  // (z * R + y) * R
+  for (int w = 0, x0 = 0; x0 < S.R; ++w, x0 += 32) {
     int cs;
-    const unsigned m = seg_flags(g, S, s, lane, cell, cs);
+    const unsigned m = step_flags(g, p + w, w + 1 < g.W, S.R - x0, lane, cs);
     if ((m >> lane) & 1u) {
       const uint32_t pos = run + __popc(m & lt);
-      cells[pos] = static_cast<uint32_t>(cell);
+      cells[pos] = cbase + x0 + lane;
       cases[pos] = static_cast<uint8_t>(cs);
     }
     run += __popc(m);
@@ -653,10 +650,9 @@ void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, 
   SegCtx S;
   S.R = R;
   S.lg = __builtin_ctz(static_cast<unsigned>(R));
-  S.segs_row = (R + 31) / 32;
   S.z0 = cz0;
-  S.nseg = static_cast<int64_t>(R) * (own_z1 - cz0) * S.segs_row;
-  const int64_t nblk = (S.nseg + kSegBlock - 1) / kSegBlock;
+  S.nrows = R * (own_z1 - cz0);
+  const int64_t nblk = (S.nrows + kRowsBlock - 1) / kRowsBlock;
   DevBuf<uint32_t> bcount(nblk, ctx.stream), boff(nblk, ctx.stream);
   PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, S, bcount.get());
   exclusive_scan_u32(ctx, bcount.get(), boff.get(), nblk);

@@ -476,56 +476,61 @@ __global__ void __launch_bounds__(256, PCU_BRICK_MINB) k_brick(const Item* __res
     }
 }
 
-// mode 0: UDF (+INF sentinel); mode 1: SDF (u - eps, sentinel +1.0).  One warp per 32
-// consecutive samples of a lattice row (z, y uniform per warp: no per-sample integer division);
-// the brick candidates along y and z are warp-uniform.  With `signs`, the warp's ballot of
-// (s < 0) is stored as one 32-bit word (bit x & 31 of word x >> 5 of the row): the DMC classify
-// passes read this 17 MB mask (C3) instead of the 540 MB lattice.
+// mode 0: UDF (+INF sentinel); mode 1: SDF (u - eps, sentinel +1.0).  One warp per lattice row
+// (y, z): the brick candidates along y and z are computed once per row, then the warp walks the
+// row 32 samples at a time (bs is a power of two: brick coordinates by shifts, no division per
+// sample).  With `signs`, each step's ballot of (s < 0) is stored as one 32-bit word (bit x & 31
+// of word x >> 5 of the row): the DMC classify passes read this 17 MB mask (C3) instead of the
+// 540 MB lattice.
 __global__ void __launch_bounds__(256) k_finalize(const uint32_t* __restrict__ blocks, const int32_t* __restrict__ bmap,
                                                   int R, int rb, int bs, int mode, double eps, float* __restrict__ out,
                                                   int z0, int z1, uint32_t* __restrict__ signs) {
-  const int n1 = R + 1, W = (n1 + 31) >> 5, nv1 = bs + 1;
-  const int64_t rows = static_cast<int64_t>(n1) * (z1 - z0);
-  const int64_t nwarp = rows * W;
+  const int n1 = R + 1, W = (n1 + 31) >> 5, nv1 = bs + 1, lgbs = __ffs(bs) - 1;
+  const int rows = n1 * (z1 - z0);
   const int lane = threadIdx.x & 31;
-  for (int64_t wi = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; wi < nwarp;
-       wi += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const int64_t row = wi / W;
-    const int w = static_cast<int>(wi - row * W);
-    const int y = static_cast<int>(row % n1), zr = static_cast<int>(row / n1), z = z0 + zr;
-    const int x = (w << 5) + lane;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int64_t bvol = static_cast<int64_t>(nv1) * nv1 * nv1;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nwarps) {
+    const int zr = row / n1, y = row - zr * n1, z = z0 + zr;
     int bys[2], bzs[2], nby = 0, nbz = 0;
-    if (y / bs < rb) bys[nby++] = y / bs;
-    if (y % bs == 0 && y > 0) bys[nby++] = y / bs - 1;
-    if (z / bs < rb) bzs[nbz++] = z / bs;
-    if (z % bs == 0 && z > 0) bzs[nbz++] = z / bs - 1;
+    if ((y >> lgbs) < rb) bys[nby++] = y >> lgbs;
+    if ((y & (bs - 1)) == 0 && y > 0) bys[nby++] = (y >> lgbs) - 1;
+    if ((z >> lgbs) < rb) bzs[nbz++] = z >> lgbs;
+    if ((z & (bs - 1)) == 0 && z > 0) bzs[nbz++] = (z >> lgbs) - 1;
     if (!bmap) nbz = 0;
-    uint32_t best = 0xffffffffu;
-    if (x < n1) {
-      int bxs[2], nbx = 0;
-      if (x / bs < rb) bxs[nbx++] = x / bs;
-      if (x % bs == 0 && x > 0) bxs[nbx++] = x / bs - 1;
-      for (int a = 0; a < nbz; ++a)
-        for (int b = 0; b < nby; ++b)
-          for (int c = 0; c < nbx; ++c) {
-            const int cid = bmap[bxs[c] + rb * (bys[b] + rb * bzs[a])];
-            if (cid < 0) continue;
-            const int lx = x - bxs[c] * bs, ly = y - bys[b] * bs, lz = z - bzs[a] * bs;
-            const uint32_t val = blocks[static_cast<uint64_t>(cid) * nv1 * nv1 * nv1 + lx + nv1 * (ly + nv1 * lz)];
-            best = val < best ? val : best;
+    float* orow = out + static_cast<int64_t>(row) * n1;
+    for (int w = 0; w < W; ++w) {
+      const int x = (w << 5) + lane;
+      uint32_t best = 0xffffffffu;
+      if (x < n1) {
+        int bxs[2], nbx = 0;
+        if ((x >> lgbs) < rb) bxs[nbx++] = x >> lgbs;
+        if ((x & (bs - 1)) == 0 && x > 0) bxs[nbx++] = (x >> lgbs) - 1;
+        for (int a = 0; a < nbz; ++a)
+          for (int b = 0; b < nby; ++b) {
+            const int* brow = bmap + rb * (bys[b] + rb * bzs[a]);
+            const int ly = y - (bys[b] << lgbs), lz = z - (bzs[a] << lgbs);
+            for (int c = 0; c < nbx; ++c) {
+              const int cid = brow[bxs[c]];
+              if (cid < 0) continue;
+              const int lx = x - (bxs[c] << lgbs);
+              const uint32_t val = blocks[cid * bvol + lx + nv1 * (ly + nv1 * lz)];
+              best = val < best ? val : best;
+            }
           }
-    }
-    float res = 0.0f;
-    if (best == 0xffffffffu) {
-      res = mode ? 1.0f : __int_as_float(0x7f800000);
-    } else {
-      const float u = __uint_as_float(best);
-      res = mode ? static_cast<float>(static_cast<double>(u) - eps) : u;
-    }
-    if (x < n1) out[row * n1 + x] = res;
-    if (signs) {
-      const unsigned m = __ballot_sync(0xffffffffu, x < n1 && res < 0.0f);
-      if (lane == 0) signs[wi] = m;
+      }
+      float res;
+      if (best == 0xffffffffu) {
+        res = mode ? 1.0f : __int_as_float(0x7f800000);
+      } else {
+        const float u = __uint_as_float(best);
+        res = mode ? static_cast<float>(static_cast<double>(u) - eps) : u;
+      }
+      if (x < n1) orow[x] = res;
+      if (signs) {
+        const unsigned m = __ballot_sync(0xffffffffu, x < n1 && res < 0.0f);
+        if (lane == 0) signs[static_cast<int64_t>(row) * W + w] = m;
+      }
     }
   }
 }
