@@ -189,90 +189,104 @@ __device__ __forceinline__ void cell_xyz(int64_t c, int R, int64_t& x, int64_t& 
   z = c >> (2 * lg);
 }
 
-// Dense classify over the sign mask: one warp per row of cells (y, z), 32 consecutive cells per
-// step.  The 8 words of a step (rows (y,z), (y+1,z), (y,z+1), (y+1,z+1), each with its successor
-// for the x+1 corner) are warp-uniform broadcast loads; lane l takes bits x, x+1 of each row with
-// a funnel shift.  A step whose 8 words are all zero (every corner positive: the bulk of the grid
-// away from the band) does no per-cell work.  Blocks take 8 consecutive rows, so per-block counts
-// + an exclusive scan give the x-fastest compaction; all index math is 32-bit shifts.
-constexpr int kRowsBlock = 8;  // rows (warps) per 256-thread block
-
+// Dense classify over the sign mask, 32 cells per lane: lane (row r, word w) loads the 4 rows'
+// words w and w+1 (rows (y,z), (y+1,z), (y,z+1), (y+1,z+1); consecutive lanes read consecutive
+// words of a row, so the loads coalesce) and forms the 8 corner masks of its 32 cells with funnel
+// shifts.  A cell is active iff some corner is negative and not all are: active = OR & ~AND of
+// the 8 masks — the whole dense pass is ~20 bit operations per 32 cells.  Lanes are ordered
+// (row, word), rows (z, y), so per-block counts + a scan give the x-fastest compaction; the
+// write pass assembles the 8-bit case only for the set bits.  All index math is 32-bit shifts.
 struct SegCtx {
   int R, lg;     // cells per row, log2 R
+  int lgw;       // log2 words per row (words of 32 cells; R < 32 -> 1 word)
   int nrows;     // rows of the classified layers: R * layers
   int z0;        // first cell layer
 };
 
-// ballot of active cells of the step (row, w); this lane's case in cs
-__device__ __forceinline__ unsigned step_flags(const GridView& g, const uint32_t* __restrict__ p, int has1, int valid,
-                                               int lane, int& cs) {
-  const int64_t W = g.W, rW = g.n1 * g.W;
-  const uint32_t A = p[0], B = p[W], C = p[rW], D = p[rW + W];
-  const uint32_t A1 = has1 ? p[1] : 0u, B1 = has1 ? p[W + 1] : 0u, C1 = has1 ? p[rW + 1] : 0u,
-                 D1 = has1 ? p[rW + W + 1] : 0u;
-  cs = 0;
-  if ((A | A1 | B | B1 | C | C1 | D | D1) == 0u) return 0u;  // warp-uniform: all corners positive
-  const uint32_t a = __funnelshift_r(A, A1, lane), b = __funnelshift_r(B, B1, lane);
-  const uint32_t c = __funnelshift_r(C, C1, lane), d = __funnelshift_r(D, D1, lane);
-  cs = static_cast<int>((a & 3u) | (b & 3u) << 2 | (c & 3u) << 4 | (d & 3u) << 6);
-  return __ballot_sync(0xffffffffu, lane < valid && cs != 0 && cs != 255);
-}
+struct Corners {
+  uint32_t m[8];  // m[c]: bit b = corner c of cell (32 w + b) is negative
+  uint32_t valid;
+};
 
-// the mask words of cell row `row` (= (z - z0) * R + y), word 0
-__device__ __forceinline__ const uint32_t* row_words(const GridView& g, const SegCtx& S, int row) {
+__device__ __forceinline__ Corners corners_of(const GridView& g, const SegCtx& S, int lanei) {
+  Corners K;
+  const int row = lanei >> S.lgw, w = lanei & ((1 << S.lgw) - 1);
   const int y = row & (S.R - 1), z = S.z0 + (row >> S.lg);
-  return g.sg + ((static_cast<int64_t>(z) - g.zb) * g.n1 + y) * g.W;
+  const uint32_t* p = g.sg + ((static_cast<int64_t>(z) - g.zb) * g.n1 + y) * g.W + w;
+  const int64_t W = g.W, rW = g.n1 * g.W;
+  const bool has1 = w + 1 < g.W;
+  const uint32_t* q[4] = {p, p + W, p + rW, p + rW + W};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t lo = q[k][0], hi = has1 ? q[k][1] : 0u;
+    K.m[2 * k] = lo;                             // corner (0, dy, dz): bit x
+    K.m[2 * k + 1] = __funnelshift_r(lo, hi, 1);  // corner (1, dy, dz): bit x + 1
+  }
+  const int nvalid = min(32, S.R - (w << 5));
+  K.valid = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+  return K;
 }
 
-__global__ void __launch_bounds__(256) k_classify_count(GridView g, SegCtx S, uint32_t* __restrict__ bcount) {
-  __shared__ uint32_t wsum[kRowsBlock];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * kRowsBlock + warp;
-  uint32_t n = 0;
-  if (row < S.nrows) {
-    const uint32_t* p = row_words(g, S, row);
-    for (int w = 0, x0 = 0; x0 < S.R; ++w, x0 += 32) {
-      int cs;
-      n += __popc(step_flags(g, p + w, w + 1 < g.W, S.R - x0, lane, cs));
-    }
+__device__ __forceinline__ uint32_t active_mask(const Corners& K) {
+  uint32_t o = 0u, a = 0xffffffffu;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    o |= K.m[c];
+    a &= K.m[c];
   }
-  if (lane == 0) wsum[warp] = n;
+  return o & ~a & K.valid;
+}
+
+__global__ void __launch_bounds__(256) k_classify_count(GridView g, SegCtx S, int64_t nlanes,
+                                                        uint32_t* __restrict__ bcount) {
+  __shared__ uint32_t wsum[8];
+  const int64_t li = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  uint32_t n = li < nlanes ? __popc(active_mask(corners_of(g, S, static_cast<int>(li)))) : 0u;
+  for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = n;
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t t = 0;
-    for (int i = 0; i < kRowsBlock; ++i) t += wsum[i];
+    for (int i = 0; i < 8; ++i) t += wsum[i];
     bcount[blockIdx.x] = t;
   }
 }
 
-__global__ void __launch_bounds__(256) k_classify_write(GridView g, SegCtx S, const uint32_t* __restrict__ boff,
+__global__ void __launch_bounds__(256) k_classify_write(GridView g, SegCtx S, int64_t nlanes,
+                                                        const uint32_t* __restrict__ boff,
                                                         uint32_t* __restrict__ cells, uint8_t* __restrict__ cases) {
-  __shared__ uint32_t wsum[kRowsBlock];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = blockIdx.x * kRowsBlock + warp;
-  const uint32_t* p = row < S.nrows ? row_words(g, S, row) : nullptr;
-  uint32_t n = 0;
-  if (p)
-    for (int w = 0, x0 = 0; x0 < S.R; ++w, x0 += 32) {  // this warp's count, for the in-block prefix
-      int cs;
-      n += __popc(step_flags(g, p + w, w + 1 < g.W, S.R - x0, lane, cs));
-    }
-  if (lane == 0) wsum[warp] = n;
+  __shared__ uint32_t wsum[8];
+  const int64_t li = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Corners K{};
+  uint32_t act = 0u;
+  if (li < nlanes) {
+    K = corners_of(g, S, static_cast<int>(li));
+    act = active_mask(K);
+  }
+  const uint32_t n = __popc(act);
+  uint32_t incl = n;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
   __syncthreads();
-  if (!p) return;
-  uint32_t run = boff[blockIdx.x];
+  uint32_t run = boff[blockIdx.x] + incl - n;
   for (int i = 0; i < warp; ++i) run += wsum[i];
-  const unsigned lt = (1u << lane) - 1u;
-  const uint32_t cbase = static_cast<uint32_t>(row + S.R * S.z0) << S.lg;  // (z * R + y) * R
-  for (int w = 0, x0 = 0; x0 < S.R; ++w, x0 += 32) {
-    int cs;
-    const unsigned m = step_flags(g, p + w, w + 1 < g.W, S.R - x0, lane, cs);
-    if ((m >> lane) & 1u) {
-      const uint32_t pos = run + __popc(m & lt);
-      cells[pos] = cbase + x0 + lane;
-      cases[pos] = static_cast<uint8_t>(cs);
-    }
-    run += __popc(m);
+  if (!act) return;
+  const int i = static_cast<int>(li);
+  const int row = i >> S.lgw, w = i & ((1 << S.lgw) - 1);
+  const uint32_t cbase = (static_cast<uint32_t>(row + S.R * S.z0) << S.lg) + (w << 5);  // (z*R + y)*R + 32w
+  while (act) {
+    const int b = __ffs(act) - 1;
+    act &= act - 1;
+    int cs = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cs |= ((K.m[c] >> b) & 1u) << c;
+    cells[run] = cbase + b;
+    cases[run] = static_cast<uint8_t>(cs);
+    ++run;
   }
 }
 
@@ -650,18 +664,20 @@ void dmc_extract_slab(Ctx& ctx, const float* d_planes, int R, int pz0, int pz1, 
   SegCtx S;
   S.R = R;
   S.lg = __builtin_ctz(static_cast<unsigned>(R));
+  S.lgw = R >= 32 ? S.lg - 5 : 0;
   S.z0 = cz0;
   S.nrows = R * (own_z1 - cz0);
-  const int64_t nblk = (S.nrows + kRowsBlock - 1) / kRowsBlock;
+  const int64_t nlanes = static_cast<int64_t>(S.nrows) << S.lgw;
+  const int64_t nblk = (nlanes + 255) / 256;
   DevBuf<uint32_t> bcount(nblk, ctx.stream), boff(nblk, ctx.stream);
-  PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, S, bcount.get());
+  PCU_LAUNCH(ctx, k_classify_count, static_cast<unsigned>(nblk), 256, 0, g, S, nlanes, bcount.get());
   exclusive_scan_u32(ctx, bcount.get(), boff.get(), nblk);
   const uint32_t na = read_scalar(ctx, boff.get() + nblk - 1) + read_scalar(ctx, bcount.get() + nblk - 1);
   res.cells.alloc(na ? na : 1, ctx.stream);
   res.cases.alloc(na ? na : 1, ctx.stream);
   res.flips.alloc(na ? na : 1, ctx.stream);
   res.n_active = na;
-  PCU_LAUNCH(ctx, k_classify_write, static_cast<unsigned>(nblk), 256, 0, g, S, boff.get(), res.cells.get(),
+  PCU_LAUNCH(ctx, k_classify_write, static_cast<unsigned>(nblk), 256, 0, g, S, nlanes, boff.get(), res.cells.get(),
              res.cases.get());
   res.nvp_own = res.n_extra = 0;
   if (na == 0) {
