@@ -280,12 +280,30 @@ def run_ours(args):
             return {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 5), "traffic": traffic, "alg_bytes": int(bytes_), "ms": round(ms, 3)}
 
-        # DRAM bytes of the UDF stage's kernels from the committed ncu capture of the same config
-        udf_traffic = None
-        tp = os.path.join(ROOT, "profiles", f"r01_udf_traffic_{args.config}.json")
+        # DRAM bytes of every stage's kernels from the committed ncu launch list of the same
+        # config (tools/agg_launches.py --json; per pipeline pass, serialised cold-cache launches)
+        traffic = {}
+        tp = os.path.join(ROOT, "profiles", f"r02_stage_traffic_{args.config}.json")
         if os.path.exists(tp):
             with open(tp) as fh:
-                udf_traffic = json.load(fh).get("dram_bytes")
+                traffic = {k: v.get("dram_bytes") for k, v in json.load(fh)["stages"].items()}
+        udf_traffic = traffic.get("udf")
+
+        # roofline of the dominant kernel of the metric's UDF stage, k_brick: the stage's
+        # algorithmic bytes per launch / its launch duration measured live (CUDA
+        # events on the library stream in the profiled untimed step); traffic = ncu DRAM bytes of
+        # that kernel in the committed capture
+        kb_ms, kb_n = ktimes.get("k_brick", (udf_ms, 1))
+        kernel_roof = roof(udf_bytes, kb_ms / max(kb_n, 1))
+        kernel_roof["kernel"] = "k_brick"
+        kernel_roof["alg_bytes_per_launch"] = kernel_roof.pop("alg_bytes")
+        kernel_roof["ms_per_launch"] = kernel_roof.pop("ms")
+        try:
+            with open(os.path.join(ROOT, "profiles", f"r02_ncu_counters_{args.config}.json")) as fh:
+                kk = json.load(fh)["kernels"]["k_brick"]
+            kernel_roof["traffic"] = int(kk["dram_read"] + kk["dram_write"])
+        except (OSError, KeyError):
+            pass
 
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -303,8 +321,9 @@ def run_ours(args):
                        "dmc_faces": int(tm["dmc_faces"]), "faces_out": int(nf), "qem_iterations": st["iterations"],
                        "parallelism": f"replicas x{world} (one mesh per GPU)",
                        "l2": "flushed (256 MB write) before every timed step"},
-            "roofline": roof(udf_bytes, udf_ms, udf_traffic),
-            "stages": {"udf": roof(udf_bytes, udf_ms, udf_traffic), "dmc": roof(dmc_bytes, dmc_ms), "qem": roof(qem_bytes, qem_ms),
+            "roofline": kernel_roof,
+            "stages": {"udf": roof(udf_bytes, udf_ms, udf_traffic), "dmc": roof(dmc_bytes, dmc_ms, traffic.get("dmc")),
+                       "qem": roof(qem_bytes, qem_ms, traffic.get("qem")),
                        "udf_voxels_per_s": round(n1 / (udf_ms * 1e-3), 1),
                        "undo_hist": st["undo_hist"][:4]},
             "peak_source": peak_kind,
@@ -317,18 +336,26 @@ def run_ours(args):
         line["certification"] = cert
         if world > 1:  # the communicator this run used (the driver's scaling run checks N ranks)
             line["nccl"] = nccl_info(torch, dist, world)
-        # the limiter of the UDF's dominant kernel from the committed ncu capture: k_brick is
-        # instruction-issue bound (distance arithmetic), which is why the HBM fraction is small
-        cp = os.path.join(ROOT, "profiles", f"r01_ncu_counters_{args.config}.json")
+        # the limiters of the dominant kernels from the committed ncu capture: k_brick (UDF) is
+        # instruction-issue bound on the distance arithmetic, k_cost (QEM) on FP64 gathers; their
+        # pipe fractions are quoted against the measured FFMA / DFMA peaks (tools/peak_fma.cu)
+        cp = os.path.join(ROOT, "profiles", f"r02_ncu_counters_{args.config}.json")
         if os.path.exists(cp):
             with open(cp) as fh:
-                kb = json.load(fh)["kernels"].get("k_brick")
-            if kb:
-                line["roofline"]["compute"] = {
-                    "kernel": "k_brick", "bound": "issue", "issue_active_frac": round(kb["issue_active_pct"] / 100, 4),
+                nc = json.load(fh)
+            pk = nc.get("peaks", {})
+            comp = {}
+            for kname, kb in nc["kernels"].items():
+                if kname not in ("k_brick", "k_cost"):
+                    continue
+                comp[kname] = {
+                    "bound": "issue", "issue_active_frac": round(kb.get("issue_active_pct", 0.0) / 100, 4),
                     "fp64_pipe_frac": round(kb["fp64_pipe_pct"] / 100, 4), "fma_pipe_frac": round(kb["fma_pipe_pct"] / 100, 4),
-                    "simt_efficiency": round(kb["threads_per_warp_inst"] / 32, 4),
-                    "source": f"profiles/r01_ncu_counters_{args.config}.json"}
+                    "fp64_tflops_est": round(kb["fp64_pipe_pct"] / 100 * pk.get("dfma_tflops", 0.0), 2),
+                    "fp32_tflops_est": round(kb["fma_pipe_pct"] / 100 * pk.get("ffma_tflops", 0.0), 2),
+                    "simt_efficiency": round(kb["threads_per_warp_inst"] / 32, 4)}
+            line["roofline"]["compute"] = {"kernels": comp, "peaks_measured": pk,
+                                           "source": f"profiles/r02_ncu_counters_{args.config}.json"}
         ktot = sum(ms for ms, _ in ktimes.values()) or 1.0
         top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:30]
         line["kernels"] = {"source": "one untimed step, CUDA events around every launch",
