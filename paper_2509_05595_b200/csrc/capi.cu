@@ -150,6 +150,48 @@ __global__ void __launch_bounds__(1024) k_small_scan(const uint32_t* in, int n, 
   }
 }
 
+// Up to 4 memsets in one launch (the QEM loop issues several per step; at small sizes each
+// separate cudaMemsetAsync costs a launch).  Ranges are filled as 32-bit words with the byte
+// value replicated, and a byte tail.
+__global__ void k_fill_multi(FillRanges fr) {
+  uint64_t total = 0;
+  for (int r = 0; r < fr.n; ++r) total += fr.r[r].bytes;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i * 4 < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t off = i * 4;
+    for (int r = 0; r < fr.n; ++r) {
+      const FillRange& R = fr.r[r];
+      const uint64_t words = (R.bytes + 3) / 4;
+      if (off < words * 4) {
+        uint8_t* p = static_cast<uint8_t*>(R.p) + off;
+        const uint32_t v = 0x01010101u * R.byte;
+        if (off + 4 <= R.bytes && (reinterpret_cast<uintptr_t>(p) & 3u) == 0) {
+          *reinterpret_cast<uint32_t*>(p) = v;
+        } else {
+          for (uint64_t b = off; b < R.bytes && b < off + 4; ++b) static_cast<uint8_t*>(R.p)[b] = R.byte;
+        }
+        break;
+      }
+      off -= words * 4;
+    }
+  }
+}
+
+void fill_multi(Ctx& ctx, std::initializer_list<FillRange> ranges) {
+  FillRanges fr{};
+  uint64_t total = 0;
+  for (const FillRange& r : ranges) {
+    if (!r.p || r.bytes == 0) continue;
+    PCU_REQUIRE(fr.n < 4, PAMOPT_CU_EINVAL, "fill_multi: at most 4 ranges");
+    PCU_REQUIRE((reinterpret_cast<uintptr_t>(r.p) & 3u) == 0, PAMOPT_CU_EINVAL, "fill_multi: unaligned range");
+    fr.r[fr.n++] = r;
+    total += (r.bytes + 3) / 4;
+  }
+  if (fr.n == 0) return;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, static_cast<uint64_t>(ctx.num_sms) * 16));
+  PCU_LAUNCH(ctx, k_fill_multi, g, 256, 0, fr);
+}
+
 void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n) {
   if (n <= 0) return;
   if (n <= kSmallScan) {

@@ -15,6 +15,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <initializer_list>
 #include <vector>
 
 #include "../../include/pamopt_cu.h"
@@ -206,6 +207,17 @@ inline unsigned grid_for(int64_t n, int block) {
 
 // ------------------------------------------------------------------- CUB-backed helpers
 // exclusive scan of n elements (in -> out), returns nothing; out may alias in.
+// several byte-value fills (memset semantics) in one launch; pointers 4-byte aligned
+struct FillRange {
+  void* p;
+  uint64_t bytes;
+  uint8_t byte;
+};
+struct FillRanges {
+  FillRange r[4];
+  int n;
+};
+void fill_multi(Ctx& ctx, std::initializer_list<FillRange> ranges);
 void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n);
 void exclusive_scan_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n);
 void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit = 64);

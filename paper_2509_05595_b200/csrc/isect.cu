@@ -362,7 +362,7 @@ struct DetectScalars {
   unsigned long long ncls[3];
   unsigned long long nhuge;  // probes covering > kMaxCells cells, handed to k_probe_huge
   int redo;  // candidate buffer overflowed: the round's outputs are void, the caller repeats it
-  int pad;
+  unsigned ext_blocks;  // k_ext_sum blocks finished (the last one sets inv_h)
 };
 
 __global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t n,
@@ -389,10 +389,16 @@ __global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict
   out[f] = fb;
 }
 
+// cell size = PCU_CELL_SCALE x the mean box extent of the build set; the block that finishes last
+// turns the sum into inv_h (one launch instead of a reduction + a one-thread kernel)
+#ifndef PCU_CELL_SCALE
+#define PCU_CELL_SCALE 1.5
+#endif
 __global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict__ ids, int64_t n,
                           const uint8_t* __restrict__ alive, DetectScalars* ds) {
   typedef cub::BlockReduce<double, 256> BR;
   __shared__ typename BR::TempStorage tmp;
+  __shared__ bool last;
   double s = 0.0;
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -402,17 +408,17 @@ __global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict_
     s += fmax(fmax(b.hi[0] - b.lo[0], b.hi[1] - b.lo[1]), b.hi[2] - b.lo[2]);
   }
   const double t = BR(tmp).Sum(s);
-  if (threadIdx.x == 0) atomicAdd(&ds->ext_sum, t);
-}
-
-// cell size = mean box extent of the build set
-#ifndef PCU_CELL_SCALE
-#define PCU_CELL_SCALE 1.5
-#endif
-// grid cell edge = PCU_CELL_SCALE x the mean box extent of the build set
-__global__ void k_set_invh(DetectScalars* ds, int64_t n) {
-  const double mean = n > 0 ? ds->ext_sum / static_cast<double>(n) : 1.0;
-  ds->inv_h = 1.0 / (PCU_CELL_SCALE * (mean > 0.0 ? mean : 1e-3));
+  if (threadIdx.x == 0) {
+    atomicAdd(&ds->ext_sum, t);
+    __threadfence();
+    last = atomicAdd(&ds->ext_blocks, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    const double sum = atomicAdd(&ds->ext_sum, 0.0);  // every block's contribution is visible
+    const double mean = n > 0 ? sum / static_cast<double>(n) : 1.0;
+    ds->inv_h = 1.0 / (PCU_CELL_SCALE * (mean > 0.0 ? mean : 1e-3));
+  }
 }
 
 // pass 0: count bucket entries (or big); pass 1: fill
@@ -895,7 +901,16 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
                   uint8_t* revert, bool boxes_current = false, const uint8_t* in_probe = nullptr) {
   cudaStream_t st = ctx.stream;
   S.ds.ensure(1, st);
-  PCU_CUDA(cudaMemsetAsync(S.ds.get(), 0, sizeof(DetectScalars), st));
+  const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_build) * 2 + 1);
+  const uint32_t mask = nb - 1;
+  S.bcount.ensure(nb, st);
+  S.boff.ensure(nb, st);
+  S.bcur.ensure(nb, st);
+  S.occ.ensure(nb / 32 + 1, st);
+  // the round's scalars and the grid's bucket counters / occupancy bitmap, zeroed in one launch
+  fill_multi(ctx, {{S.ds.get(), sizeof(DetectScalars), 0}, {S.bcount.get(), static_cast<uint64_t>(nb) * 4, 0},
+                   {S.bcur.get(), static_cast<uint64_t>(nb) * 4, 0},
+                   {S.occ.get(), (static_cast<uint64_t>(nb) / 32 + 1) * 4, 0}});
   const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
   if (!boxes_current) {
     S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), st);
@@ -906,16 +921,6 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   }
   PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n_build, 256), ctx.num_sms * 4)), 256, 0,
              B, build_ids, n_build, d_alive, S.ds.get());
-  PCU_LAUNCH(ctx, k_set_invh, 1, 1, 0, S.ds.get(), n_build);
-  const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_build) * 2 + 1);
-  const uint32_t mask = nb - 1;
-  S.bcount.ensure(nb, st);
-  S.boff.ensure(nb, st);
-  S.bcur.ensure(nb, st);
-  PCU_CUDA(cudaMemsetAsync(S.bcount.get(), 0, nb * 4, st));
-  PCU_CUDA(cudaMemsetAsync(S.bcur.get(), 0, nb * 4, st));
-  S.occ.ensure(nb / 32 + 1, st);
-  PCU_CUDA(cudaMemsetAsync(S.occ.get(), 0, (nb / 32 + 1) * 4, st));
   // hard capacity: a non-big face covers at most kMaxCells cells
   S.entries.ensure(static_cast<size_t>(n_build) * kMaxCells + 16, st);
   S.big.ensure(static_cast<size_t>(n_build) + 16, st);

@@ -960,10 +960,9 @@ struct QemState {
   bool done() const { return nf == 0 || !(alive_faces > target && zero_run < P.stall); }
 
   void build_incidence() {
-    PCU_CUDA(cudaMemsetAsync(deg.get(), 0, nv * sizeof(uint32_t), st));
+    fill_multi(ctx, {{deg.get(), nv * sizeof(uint32_t), 0}, {cur.get(), nv * sizeof(uint32_t), 0}});
     PCU_LAUNCH(ctx, k_deg, grid_for(nf, 256), 256, 0, F, falive.get(), nf, deg.get());
     exclusive_scan_u32(ctx, deg.get(), off.get(), nv);
-    PCU_CUDA(cudaMemsetAsync(cur.get(), 0, nv * sizeof(uint32_t), st));
     PCU_LAUNCH(ctx, k_fill, grid_for(nf, 256), 256, 0, F, falive.get(), nf, off.get(), cur.get(), inc.get());
     PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
   }
@@ -1042,8 +1041,7 @@ struct QemState {
     PCU_REQUIRE(phase == 1, PAMOPT_CU_EINVAL, "qem: propagate_and_mark() out of order");
     unsigned long long* d_ne = &cnt.get()->edges;
     const unsigned eg = std::min<unsigned>(grid_for(ne_hint, 128), gs_grid);
-    PCU_CUDA(cudaMemsetAsync(vmin.get(), 0xFF, nv * 8, st));
-    PCU_CUDA(cudaMemsetAsync(vfmin.get(), 0xFF, nv * 8, st));
+    fill_multi(ctx, {{vmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}, {vfmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}});
     PCU_LAUNCH(ctx, k_prop_edges, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vmin.get());
     PCU_LAUNCH(ctx, k_prop_faces, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vmin.get(), vfmin.get());
     PCU_LAUNCH(ctx, k_mark, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vfmin.get(), marked.get(),
@@ -1112,8 +1110,9 @@ struct QemState {
     int64_t nqr = nq;
     Counters h = hc;
     while (nqr > 0) {
-      PCU_CUDA(cudaMemsetAsync(revert.get(), 0, nm, st));
-      PCU_CUDA(cudaMemsetAsync(&cnt.get()->restored, 0, 8, st));
+      // (the query counter was read at the last synchronisation; k_revert does not use it)
+      fill_multi(ctx, {{revert.get(), static_cast<uint64_t>(nm), 0}, {&cnt.get()->restored, 8, 0},
+                       {&cnt.get()->query, 8, 0}});
       if (first_round)
         undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nqr, owner.get(), revert.get());
       else
@@ -1123,7 +1122,6 @@ struct QemState {
                  Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get(),
                  rlist.get());
       // rebuild the query list from still-applied collapses
-      PCU_CUDA(cudaMemsetAsync(&cnt.get()->query, 0, 8, st));
       PCU_LAUNCH(ctx, k_requery, grid_for(nqr, 256), 256, 0, qa, nqr, owner.get(), B.applied, qb, cnt.get());
       h = sync_counters(true);  // ---- sync per round
       boxes_update(ctx, *isc, X, F, rlist.get(), static_cast<int64_t>(h.restored), falive.get());  // restored faces
