@@ -150,9 +150,9 @@ __global__ void __launch_bounds__(1024) k_small_scan(const uint32_t* in, int n, 
   }
 }
 
-// Up to 4 memsets in one launch (the QEM loop issues several per step; at small sizes each
+// Up to 4 small memsets in one launch (the QEM loop issues several per step; at small sizes each
 // separate cudaMemsetAsync costs a launch).  Ranges are filled as 32-bit words with the byte
-// value replicated, and a byte tail.
+// value replicated, and a byte tail; ranges above 1 MB go to cudaMemsetAsync instead.
 __global__ void k_fill_multi(FillRanges fr) {
   uint64_t total = 0;
   for (int r = 0; r < fr.n; ++r) total += fr.r[r].bytes;
@@ -182,6 +182,10 @@ void fill_multi(Ctx& ctx, std::initializer_list<FillRange> ranges) {
   uint64_t total = 0;
   for (const FillRange& r : ranges) {
     if (!r.p || r.bytes == 0) continue;
+    if (r.bytes > (1u << 20)) {  // large: the copy engine's memset runs at HBM rate
+      PCU_CUDA(cudaMemsetAsync(r.p, r.byte, r.bytes, ctx.stream));
+      continue;
+    }
     PCU_REQUIRE(fr.n < 4, PAMOPT_CU_EINVAL, "fill_multi: at most 4 ranges");
     PCU_REQUIRE((reinterpret_cast<uintptr_t>(r.p) & 3u) == 0, PAMOPT_CU_EINVAL, "fill_multi: unaligned range");
     fr.r[fr.n++] = r;
