@@ -339,6 +339,23 @@ int pamopt_cu_project_defaults(pamopt_cu_project_params* out);
 int pamopt_cu_safe_project(pamopt_cu_mesh mesh_s, pamopt_cu_mesh mesh_in, const pamopt_cu_project_params* params,
                            pamopt_cu_project_stats* stats);
 
+/* the same solve with a per-iteration record (host buffers; any pointer may be null) so a CPU
+ * restatement can replay each Newton step: iterations [0, max_iters) are recorded.  m = samples.
+ * X/grad/dir/targets: max_iters x 3nv; m2s: max_iters x m x 4 (face vertices, frozen class);
+ * contacts: max_iters x contact_cap x 6 (term 4 PT / 5 EE, class, 4 vertices), n_contacts:
+ * max_iters; scalars: max_iters x 8 = {B0, |g|, CG iterations, ACCD t_max, alpha, B(x + alpha p),
+ * accepted, line-search tries}; samples: 3m */
+typedef struct {
+  int32_t max_iters;
+  int64_t contact_cap;
+  double *X, *grad, *dir, *targets;
+  int32_t *m2s, *contacts;
+  int64_t* n_contacts;
+  double *scalars, *samples;
+} pamopt_cu_project_trace;
+int pamopt_cu_safe_project_traced(pamopt_cu_mesh mesh_s, pamopt_cu_mesh mesh_in, const pamopt_cu_project_params* params,
+                                  pamopt_cu_project_stats* stats, const pamopt_cu_project_trace* trace);
+
 /* one stage-3 energy stencil on the GPU (unit checks of the terms).  term: 0 S2M, 1 M2S,
  * 2 elastic, 3 bending, 4 point-triangle barrier, 5 edge-edge barrier; cls: the frozen distance
  * class (M2S / barrier); coords: nv (1, 3 or 4) vertices; rest[16] = {s0, ytgt[3], ys[3], m2s_w,

@@ -64,6 +64,12 @@ class ProjectStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ProjectTrace(C.Structure):
+    _fields_ = [("max_iters", C.c_int32), ("contact_cap", C.c_int64), ("X", C.c_void_p), ("grad", C.c_void_p),
+                ("dir", C.c_void_p), ("targets", C.c_void_p), ("m2s", C.c_void_p), ("contacts", C.c_void_p),
+                ("n_contacts", C.c_void_p), ("scalars", C.c_void_p), ("samples", C.c_void_p)]
+
+
 class Topology(C.Structure):
     _fields_ = [("manifold", C.c_int32), ("watertight", C.c_int32), ("euler_characteristic", C.c_int64),
                 ("boundary_edge_count", C.c_int64), ("n_nonmanifold_edges", C.c_int64),
@@ -200,6 +206,7 @@ _SIGS = {
     "pamopt_cu_report": (C.c_int, [vp, vp, i64, C.c_uint64, P(MeshReport)]),
     "pamopt_cu_project_defaults": (C.c_int, [P(ProjectParams)]),
     "pamopt_cu_safe_project": (C.c_int, [vp, vp, P(ProjectParams), P(ProjectStats)]),
+    "pamopt_cu_safe_project_traced": (C.c_int, [vp, vp, P(ProjectParams), P(ProjectStats), P(ProjectTrace)]),
     "pamopt_cu_project_term": (C.c_int, [vp, i32, i32, vp, i32, vp, P(ProjectParams), vp]),
     "pamopt_cu_remesh": (C.c_int, [vp, vp, i32, dbl, dbl, i64, P(SimplifyParams), P(vp), P(SimplifyStats),
                                    P(StageTimes)]),

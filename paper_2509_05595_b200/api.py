@@ -772,6 +772,34 @@ def safe_project(mesh_s: DeviceMesh, mesh_in, **overrides):
     return st.as_dict()
 
 
+def safe_project_traced(mesh_s: DeviceMesh, mesh_in, record: int, contact_cap: int = 1 << 16, **overrides):
+    """safe_project with a per-iteration record of the first `record` Newton iterations (the
+    step oracle's input): X, grad, dir, targets (record x nv x 3), m2s (record x m x 4),
+    contacts (list of (n, 6) arrays), scalars (record x 8: B0, |g|, CG its, t_max, alpha, B1,
+    accepted, tries), samples (m x 3).  Returns (stats, trace dict)."""
+    p = _lib.ProjectParams()
+    check(lib().pamopt_cu_project_defaults(C.byref(p)))
+    for k, v in overrides.items():
+        setattr(p, k, v)
+    mi = _mesh(mesh_in, mesh_s.ctx)
+    nv, m, K = mesh_s.size()[0], int(p.samples), int(record)
+    buf = {"X": np.zeros((K, nv, 3)), "grad": np.zeros((K, nv, 3)), "dir": np.zeros((K, nv, 3)),
+           "targets": np.zeros((K, nv, 3)), "m2s": np.zeros((K, m, 4), np.int32),
+           "contacts": np.zeros((K, contact_cap, 6), np.int32), "n_contacts": np.zeros(K, np.int64),
+           "scalars": np.full((K, 8), np.nan), "samples": np.zeros((m, 3))}
+    tr = _lib.ProjectTrace(K, contact_cap, *(buf[k].ctypes.data for k in
+                                             ("X", "grad", "dir", "targets", "m2s", "contacts", "n_contacts",
+                                              "scalars", "samples")))
+    st = _lib.ProjectStats()
+    check(lib().pamopt_cu_safe_project_traced(mesh_s.h, mi.h, C.byref(p), C.byref(st), C.byref(tr)))
+    n_it = min(K, int(st.iterations))
+    buf["contacts"] = [buf["contacts"][i, :min(int(buf["n_contacts"][i]), contact_cap)].copy() for i in range(n_it)]
+    for k in ("X", "grad", "dir", "targets", "m2s", "scalars", "n_contacts"):
+        buf[k] = buf[k][:n_it]
+    buf["params"] = {k: getattr(p, k) for k, _ in p._fields_}
+    return st.as_dict(), buf
+
+
 TERMS = {"s2m": 0, "m2s": 1, "elastic": 2, "bending": 3, "pt": 4, "ee": 5}
 
 

@@ -1141,6 +1141,11 @@ int pamopt_cu_project_defaults(pamopt_cu_project_params* out) {
 
 int pamopt_cu_safe_project(pamopt_cu_mesh ms, pamopt_cu_mesh mi, const pamopt_cu_project_params* params,
                            pamopt_cu_project_stats* stats) {
+  return pamopt_cu_safe_project_traced(ms, mi, params, stats, nullptr);
+}
+
+int pamopt_cu_safe_project_traced(pamopt_cu_mesh ms, pamopt_cu_mesh mi, const pamopt_cu_project_params* params,
+                                  pamopt_cu_project_stats* stats, const pamopt_cu_project_trace* trace) {
   return guarded([&] {
     PCU_REQUIRE(ms && mi, PAMOPT_CU_EINVAL, "null mesh");
     PCU_REQUIRE(ms->owner == mi->owner, PAMOPT_CU_EINVAL, "safe_project: meshes belong to different contexts");
@@ -1154,7 +1159,15 @@ int pamopt_cu_safe_project(pamopt_cu_mesh ms, pamopt_cu_mesh mi, const pamopt_cu
     check_indices(ctx, ms);
     check_indices(ctx, mi);
     pcu::ProjectStats st;
-    pcu::safe_project(ctx, ms->V.get(), ms->nv, ms->F.get(), ms->nf, mi->V.get(), mi->F.get(), mi->nf, to_pp(p), st);
+    pcu::ProjectTrace tr;
+    if (trace) {
+      PCU_REQUIRE(trace->max_iters >= 0 && trace->contact_cap >= 0, PAMOPT_CU_EINVAL, "safe_project: bad trace sizes");
+      tr = pcu::ProjectTrace{trace->max_iters, trace->contact_cap, trace->X,        trace->grad,
+                             trace->dir,       trace->targets,     trace->m2s,      trace->contacts,
+                             trace->n_contacts, trace->scalars,    trace->samples};
+    }
+    pcu::safe_project(ctx, ms->V.get(), ms->nv, ms->F.get(), ms->nf, mi->V.get(), mi->F.get(), mi->nf, to_pp(p), st,
+                      trace ? &tr : nullptr);
     if (stats)
       *stats = pamopt_cu_project_stats{st.iterations, st.cg_iterations, st.refreshes, st.converged, st.energy0,
                                        st.energy, st.grad_norm, st.last_alpha};

@@ -87,9 +87,25 @@ struct ProjectStats {
   int64_t iterations = 0, cg_iterations = 0, refreshes = 0, converged = 0;
   double energy0 = 0, energy = 0, grad_norm = 0, last_alpha = 0;
 };
+// per-iteration record of the solve (host buffers, any may be null) for the step oracle in
+// tests/test_gpu_project_steps.py: iterations [0, max_iters) are recorded
+struct ProjectTrace {
+  int max_iters = 0;
+  int64_t contact_cap = 0;
+  double* X = nullptr;          // max_iters x 3nv: positions at the start of the iteration
+  double* grad = nullptr;       // max_iters x 3nv: assembled gradient
+  double* dir = nullptr;        // max_iters x 3nv: PCG solution p of H p = -g
+  double* targets = nullptr;    // max_iters x 3nv: S2M targets in use
+  int32_t* m2s = nullptr;       // max_iters x m x 4: M2S stencil (3 vertices, frozen class)
+  int32_t* contacts = nullptr;  // max_iters x contact_cap x 6: term, class, 4 vertices
+  int64_t* n_contacts = nullptr;
+  double* scalars = nullptr;    // max_iters x 8: B0, |g|, CG iterations, t_max, alpha, B1, accepted, tries
+  double* samples = nullptr;    // 3m: the M2S samples on M_in
+};
 // deforms dV (mesh_s vertices) in place; connectivity unchanged
 void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t nf, const double* dVin,
-                  const int32_t* dFin, int64_t nfin, const ProjectParams& params, ProjectStats& stats);
+                  const int32_t* dFin, int64_t nfin, const ProjectParams& params, ProjectStats& stats,
+                  ProjectTrace* trace = nullptr);
 
 // one term stencil evaluated on the GPU (unit checks): out = {value, grad[12], projected H[144]}
 void project_term_probe(Ctx& ctx, int term, int cls, const double* coords, int nv, const double* rest,

@@ -581,7 +581,10 @@ __global__ void k_sweep(const uint64_t* __restrict__ sorted, int64_t nf, const d
   for (int64_t j = i + 1; j < nf; ++j) {
     const int32_t b = static_cast<int32_t>(sorted[j] & 0xffffffffu);
     const double* Bx = box + 6 * b;
-    if (Bx[0] > A[3]) break;
+    // the sort key is lo.x rounded to f32: faces with equal keys may be out of order in double,
+    // so stop only once lo.x is past A's hi.x by more than that rounding, and test x exactly
+    if (Bx[0] - 1e-6 * fabs(Bx[0]) > A[3]) break;
+    if (Bx[0] > A[3] || Bx[3] < A[0]) continue;
     if (Bx[1] > A[4] || Bx[4] < A[1] || Bx[2] > A[5] || Bx[5] < A[2]) continue;
     const unsigned long long k = atomicAdd(np, 1ull);
     if (k < cap) pairs[k] = (static_cast<uint64_t>(min(a, b)) << 32) | static_cast<uint32_t>(max(a, b));
@@ -856,7 +859,8 @@ struct Assembly {
 }  // namespace
 
 void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t nf, const double* dVin,
-                  const int32_t* dFin, int64_t nfin, const ProjectParams& PP, ProjectStats& stats) {
+                  const int32_t* dFin, int64_t nfin, const ProjectParams& PP, ProjectStats& stats,
+                  ProjectTrace* tr) {
   cudaStream_t st = ctx.stream;
   PCU_REQUIRE(nv > 0 && nf > 0 && nfin > 0, PAMOPT_CU_EINVAL, "safe_project: empty mesh");
   const std::vector<int32_t> sip = self_intersections(ctx, dV, nv, dF, nf, nullptr, nullptr);
@@ -916,6 +920,7 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
   double ain = 0.0;
   PCU_REQUIRE(sample_points(ctx, dVin, dFin, nfin, m, PP.seed, ys.get(), nullptr, &ain), PAMOPT_CU_EINVAL,
               "safe_project: zero-area input mesh");
+  if (tr && tr->samples) PCU_CUDA(cudaMemcpyAsync(tr->samples, ys.get(), 3 * m * 8, cudaMemcpyDeviceToHost, st));
   TermData D{X0.get(), s0.get(), ytgt.get(), ys.get(), ain / static_cast<double>(m), dminv.get(), a0.get(),
              theta0.get(), l0.get()};
   // ---- static stencils: S2M, elastic, bending
@@ -1049,7 +1054,30 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
   };
 
   stats = ProjectStats();
+  std::vector<Stencil> hrec;
+  auto rec_vec = [&](double* base, int it, const double* dsrc) {  // one 3nv record
+    if (base) PCU_CUDA(cudaMemcpyAsync(base + static_cast<size_t>(it) * n3, dsrc, n3 * 8, cudaMemcpyDeviceToHost, st));
+  };
+  auto rec_stencils = [&](int32_t* base, int64_t stride, int width, const Stencil* dsrc, int64_t n) {
+    hrec.resize(n);
+    if (n) PCU_CUDA(cudaMemcpyAsync(hrec.data(), dsrc, n * sizeof(Stencil), cudaMemcpyDeviceToHost, st));
+    PCU_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < n && i < stride; ++i) {
+      int32_t* o = base + width * i;
+      if (width == 6) {
+        o[0] = hrec[i].term;
+        o[1] = hrec[i].cls;
+        for (int k = 0; k < 4; ++k) o[2 + k] = hrec[i].v[k];
+      } else {
+        for (int k = 0; k < 3; ++k) o[k] = hrec[i].v[k];
+        o[3] = hrec[i].cls;
+      }
+    }
+  };
   for (int it = 0; it < PP.iterations; ++it) {
+    const bool rec = tr && it < tr->max_iters;
+    double* rs = rec && tr->scalars ? tr->scalars + 8 * static_cast<size_t>(it) : nullptr;
+    if (rec) rec_vec(tr->X, it, dV);
     if (it % PP.refresh == 0) {
       // S2M targets: nearest points of M_in; M2S: nearest faces of S(X) with frozen classes
       nearest_primitive(ctx, dVin, dFin, nfin, dV, nv, sface.get(), scratch_d2.get(), ytgt.get());
@@ -1062,6 +1090,14 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     build_contacts(dV, ncont, touching);
     PCU_REQUIRE(!touching, PAMOPT_CU_ENUMERIC, "safe_project: a contact pair reached distance 0 (infeasible)");
     const int64_t ns = nstatic + m + ncont;
+    if (rec) {
+      rec_vec(tr->targets, it, ytgt.get());
+      if (tr->m2s) rec_stencils(tr->m2s + static_cast<size_t>(it) * 4 * m, m, 4, stc.get() + nstatic, m);
+      if (tr->contacts)
+        rec_stencils(tr->contacts + static_cast<size_t>(it) * 6 * tr->contact_cap, tr->contact_cap, 6,
+                     stc.get() + nstatic + m, ncont);
+      if (tr->n_contacts) tr->n_contacts[it] = ncont;
+    }
     // ---- assemble gradient + projected Hessian blocks
     A.val.ensure(ns, st);
     A.gslot.ensure(kMaxN * ns, st);
@@ -1077,6 +1113,7 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     sort_pairs_u64(ctx, A.keys2.get(), 4 * ns);
     PCU_LAUNCH(ctx, k_slot_csr, grid_for(4 * ns + 1, 256), 256, 0, A.keys2.get(), 4 * ns, nv, A.vstart.get());
     gather(A.gslot.get(), g.get());
+    if (rec) rec_vec(tr->grad, it, g.get());
     {  // global BSR matrix (3x3 blocks), deterministic summation in stencil order
       const int64_t np = 16 * ns;
       bk.ensure(np, st);
@@ -1166,6 +1203,7 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
       }
     }
     stats.cg_iterations += cg;
+    if (rec) rec_vec(tr->dir, it, pdir.get());
     // ---- ACCD step bound over the swept primitives
     primitives(dV, pdir.get(), P.dhat);
     DevBuf<unsigned long long> tb(1, st);
@@ -1182,7 +1220,9 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     double alpha = std::min(1.0, 0.9 * tmax);
     // ---- backtracking line search: B decreases and the exact check finds no intersection
     bool accepted = false;
+    int tries = 0;
     for (int ls = 0; ls < 64 && alpha > 0.0; ++ls, alpha *= 0.5) {
+      ++tries;
       PCU_LAUNCH(ctx, k_step, grid_for(n3, 256), 256, 0, n3, dV, alpha, pdir.get(), Xn.get());
       int64_t nc2 = 0;
       bool touch2 = false;
@@ -1198,6 +1238,11 @@ void safe_project(Ctx& ctx, double* dV, int64_t nv, const int32_t* dF, int64_t n
     }
     if (it == 0) stats.energy0 = B0;
     stats.iterations = it + 1;
+    if (rs) {
+      const double r8[8] = {B0, gnorm, static_cast<double>(cg), tmax, alpha, accepted ? stats.energy : B0,
+                            accepted ? 1.0 : 0.0, static_cast<double>(tries)};
+      std::memcpy(rs, r8, sizeof(r8));
+    }
     if (!accepted) {  // no decrease along a feasible step: converged
       stats.energy = B0;
       stats.converged = 1;

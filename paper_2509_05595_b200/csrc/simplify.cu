@@ -872,6 +872,8 @@ struct QemState {
   DevBuf<int32_t> rlist, inc, ea, eb, owner, qf, qf2, Fprev, snb, lscr;
   DevBuf<uint8_t> enf, valid, revert, smult;
   DevBuf<uint64_t> key, marked, marked_sorted;
+  const uint64_t* mlist = nullptr;  // this iteration's marked list (marked_sorted or marked)
+  bool key_order = false;           // stepwise API: always sort the marked list
   DevBuf<double> place;
   DevBuf<unsigned long long> vmin, vfmin;
   DevBuf<uint32_t> rem, remoff;
@@ -1060,7 +1062,14 @@ struct QemState {
     rounds = 0;
     nnew = 0;
     nq = 0;
-    if (nm > 0) {  // marked keys in ascending order (deterministic collapse ids + the trim order)
+    mlist = marked_sorted.get();
+    // Marked keys in ascending order fix the overshoot trim (P9), which applies the cheapest
+    // collapses first.  Marked edges have disjoint face neighbourhoods, so when no trim can fire
+    // (every collapse removes at most 2 faces) the batch's result does not depend on the order and
+    // the hot loop uses k_mark's list as is; the stepwise API keeps key order for its views.
+    const bool any_order = !key_order && alive_faces - 2 * nm > target;
+    if (nm > 0 && any_order) mlist = marked.get();
+    if (nm > 0 && !any_order) {
       if (!small_sort_u64(ctx, marked.get(), marked_sorted.get(), nm)) {
         size_t need = 0;
         cub::DeviceRadixSort::SortKeys(nullptr, need, marked.get(), marked_sorted.get(), static_cast<int>(nm), 0, 64,
@@ -1083,13 +1092,13 @@ struct QemState {
     PCU_REQUIRE(phase == 2, PAMOPT_CU_EINVAL, "qem: collapse_batch() out of order");
     phase = 3;
     if (nm == 0) return;
-    PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, marked_sorted.get(), nm, ea.get(), eb.get(), enf.get(), F,
+    PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, mlist, nm, ea.get(), eb.get(), enf.get(), F,
                off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
     exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
     ctx.prof.mark(st, "sort+link");
     PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
     PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), st));
-    PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, marked_sorted.get(), nm, rem.get(), remoff.get(),
+    PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, mlist, nm, rem.get(), remoff.get(),
                alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
                falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
     hc = sync_counters(false);  // ---- sync 2
@@ -1233,7 +1242,9 @@ __global__ void k_face_keys(const int32_t* __restrict__ F, const uint8_t* __rest
 QemState* qem_create(Ctx& ctx, DevBuf<double>& V, DevBuf<int32_t>& F, int64_t& nv, int64_t& nf, int64_t target,
                      const SimplifyParams& P, SimplifyStats& S) {
   PCU_REQUIRE(target >= 0, PAMOPT_CU_EINVAL, "simplify_to: negative target");
-  return new QemState(ctx, V, F, nv, nf, target, P, S);
+  auto* q = new QemState(ctx, V, F, nv, nf, target, P, S);
+  q->key_order = true;
+  return q;
 }
 void qem_destroy(QemState* q) { delete q; }
 bool qem_done(const QemState* q) { return q->done(); }
@@ -1262,7 +1273,7 @@ QemView qem_view(QemState* q) {
   v.key = q->key.get();
   v.place = q->place.get();
   v.valid = q->valid.get();
-  v.marked_sorted = q->marked_sorted.get();
+  v.marked_sorted = q->mlist;
   v.rem = q->rem.get();
   v.applied = q->B.applied;
   v.rounds = q->rounds;
