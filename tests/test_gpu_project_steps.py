@@ -13,9 +13,10 @@ CPU (oracle/project_ref.py) and each piece of the step is check
   line search alpha = min(1, 0.9 t_max) / 2^(tries-1); X' = X + alpha p bit for bit;
               B(X') recomputed with the contacts at X' < B(X); X' intersection-free (exact)
 
-Fixture: two concentric icospheres 8e-4 apart (inside the barrier distance d̂ = 1e-3, so the
-point-triangle and edge-edge barrier terms are active from the first iteration), projected onto
-a wavy pair of shells that pulls the walls together."""
+Fixtures: "pull", two concentric icospheres 8e-4 apart (inside the barrier distance d̂ = 1e-3,
+so the point-triangle and edge-edge barrier terms are active from the first iteration) projected
+onto a wavy pair of shells that pulls the walls together; "collide", two spheres 5e-4 apart
+projected onto an overlapping pair, so ACCD bounds the steps."""
 import numpy as np
 import pytest
 
@@ -26,7 +27,9 @@ pytestmark = pytest.mark.gpu
 ITERS = 11  # iterations 0..10: two refreshes (0 and 10) with the default period
 
 
-def _shells(gap, wave):
+def _shells(gap=8e-4, wave=0.01):
+    """"pull": inner shell r = 1, outer r = 1 + gap (inside d̂ everywhere); M_in = the pair at
+    radii (1, 1 + gap / 2) times a smooth wave, so the distance terms pull the walls together."""
     v, f = FX.icosphere(3)
     n = len(v)
     r_out = 1.0 + gap
@@ -37,9 +40,26 @@ def _shells(gap, wave):
     return vs, fs, vin, fs.copy()
 
 
-@pytest.fixture(scope="module")
-def run(api):
-    vs, fs, vin, fin = _shells(8e-4, 0.01)
+def _collide(gap=5e-4, shift=0.05):
+    """"collide": two unit spheres side by side, their facing extreme vertices gap apart; M_in =
+    the same spheres moved `shift` toward each other (overlapping), so the Newton direction drives
+    the walls through each other and ACCD bounds the step."""
+    v, f = FX.icosphere(3)
+    n = len(v)
+    a = v + [-1.0 - gap / 2, 0, 0]
+    b = v + [1.0 + gap / 2, 0, 0]
+    vs = np.concatenate([a, b])
+    fs = np.concatenate([f, f + n]).astype(np.int32)
+    vin = np.concatenate([a + [shift, 0, 0], b - [shift, 0, 0]])
+    return vs, fs, vin, fs.copy()
+
+
+CASES = {"pull": _shells, "collide": _collide}
+
+
+@pytest.fixture(scope="module", params=sorted(CASES))
+def run(api, request):
+    vs, fs, vin, fin = CASES[request.param]()
     m = api.DeviceMesh.upload(vs, fs)
     st, tr = api.safe_project_traced(m, (vin, fin), ITERS, iterations=ITERS)
     return vs, fs, vin, fin, st, tr
@@ -54,9 +74,14 @@ def test_trace_is_complete(run):
     vs, fs, vin, fin, st, tr = run
     assert st["iterations"] == ITERS and len(tr["X"]) == ITERS
     assert np.array_equal(tr["X"][0], vs)
-    assert all(len(c) > 0 for c in tr["contacts"])  # the barrier is active throughout
+    assert len(tr["contacts"][0]) > 0  # the barrier is active from the first iteration
     kinds = set(np.concatenate([c[:, 0] for c in tr["contacts"]]).tolist())
     assert kinds == {4, 5}
+    sc = tr["scalars"]
+    assert (sc[:, 6] == 1).all() and (sc[:, 5] < sc[:, 0]).all()
+    assert (sc[:, 2] < tr["params"]["cg_max"]).any()  # the CG residual check is exercised
+    if np.abs(vs[:, 0]).max() > 1.5:  # "collide": ACCD bounds the steps
+        assert (sc[:, 3] < 1.0).any()
 
 
 def test_refresh_targets_and_samples(run, oracle):
@@ -116,7 +141,8 @@ def test_energy_and_gradient(run, replay):
         gg = tr["grad"][it].ravel()
         assert np.abs(gg - g.ravel()).max() <= 1e-9 * np.abs(g).max(), it
         assert abs(np.linalg.norm(gg) - sc[1]) <= 1e-12 * sc[1]
-        assert parts.get("pt", 0.0) > 0.0 and parts.get("ee", 0.0) > 0.0
+        kinds = set(tr["contacts"][it][:, 0].tolist())
+        assert (parts.get("pt", 0.0) > 0.0) == (4 in kinds) and (parts.get("ee", 0.0) > 0.0) == (5 in kinds)
         if it > 0:
             assert parts["elastic"] > 0.0 and parts["bend"] > 0.0
     assert abs(out[0][0] - st["energy0"]) <= 1e-10 * out[0][0]
