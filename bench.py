@@ -593,7 +593,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--batch", type=int, default=64, help="C5 batch size")
-    ap.add_argument("--streams", type=int, default=8, help="C5: concurrent meshes (contexts) per GPU")
+    ap.add_argument("--streams", type=int, default=16, help="C5: concurrent meshes (contexts) per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     args = ap.parse_args()

@@ -1055,11 +1055,14 @@ void boxes_update(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
 const void* detect_scalars_ptr(IsectScratch& S) { return S.ds.get(); }
 size_t detect_scalars_size() { return sizeof(DetectScalars); }
 void detect_grow(IsectScratch& S, unsigned long long ncand) { S.cand_cap = ncand + ncand / 4 + 4096; }
-void detect_read(const void* host_copy, unsigned long long* found, int* redo, unsigned long long* ncand) {
+void detect_read(const void* host_copy, unsigned long long* found, int* redo, unsigned long long* ncand,
+                 unsigned long long* ncls) {
   const DetectScalars* d = static_cast<const DetectScalars*>(host_copy);
   *found = d->found;
   *redo = d->redo;
   *ncand = d->ncand;
+  if (ncls)
+    for (int k = 0; k < 3; ++k) ncls[k] = d->ncls[k];
 }
 
 }  // namespace pcu

@@ -167,7 +167,8 @@ void boxes_update(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
 const void* detect_scalars_ptr(IsectScratch& S);
 size_t detect_scalars_size();
 void detect_grow(IsectScratch& S, unsigned long long ncand);
-void detect_read(const void* host_copy, unsigned long long* found, int* redo, unsigned long long* ncand);
+void detect_read(const void* host_copy, unsigned long long* found, int* redo, unsigned long long* ncand,
+                 unsigned long long* ncls = nullptr);
 IsectScratch* isect_scratch_create();
 void isect_scratch_destroy(IsectScratch* s);
 

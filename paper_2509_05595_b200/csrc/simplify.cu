@@ -24,6 +24,9 @@
 
 #include <algorithm>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -192,20 +195,47 @@ __global__ void k_edge_fill(const uint32_t* __restrict__ off, const uint32_t* __
   }
 }
 
+// invalid (a, b) pairs live in an open-addressing hash set (linear probing,
+// empty = ~0): one insert pass per iteration instead of a sort, one probe per edge instead of a
+// binary search.  Membership is all that is read, so the result does not depend on the layout.
+__device__ __forceinline__ uint64_t inv_hash(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  return k ^ (k >> 33);
+}
+
+__global__ void k_inv_insert(const uint64_t* __restrict__ keys, int64_t n, unsigned long long* __restrict__ tab,
+                             uint64_t mask) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long k = keys[i];
+  if (k == ~0ull) return;  // a pair dropped by compact_state
+  for (uint64_t h = inv_hash(k) & mask;; h = (h + 1) & mask) {
+    const unsigned long long prev = atomicCAS(&tab[h], ~0ull, k);
+    if (prev == ~0ull || prev == k) return;
+  }
+}
+
 __global__ void k_mark_invalid(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
-                               const unsigned long long* __restrict__ d_ne, const uint64_t* __restrict__ inv,
-                               int64_t ninv, uint8_t* __restrict__ valid) {
+                               const unsigned long long* __restrict__ d_ne, const uint64_t* __restrict__ tab,
+                               uint64_t mask, int64_t ninv, uint8_t* __restrict__ valid) {
   const int64_t ne = static_cast<int64_t>(*d_ne);
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < ne;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-  const uint64_t key = (static_cast<uint64_t>(ea[e]) << 32) | static_cast<uint32_t>(eb[e]);
-  int64_t lo = 0, hi = ninv;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (inv[mid] < key) lo = mid + 1;
-    else hi = mid;
-  }
-  valid[e] = (lo < ninv && inv[lo] == key) ? 0 : 1;
+    const uint64_t key = (static_cast<uint64_t>(ea[e]) << 32) | static_cast<uint32_t>(eb[e]);
+    bool hit = false;
+    if (ninv > 0)
+      for (uint64_t h = inv_hash(key) & mask;; h = (h + 1) & mask) {
+        const uint64_t t = tab[h];
+        if (t == key) {
+          hit = true;
+          break;
+        }
+        if (t == ~0ull) break;
+      }
+    valid[e] = hit ? 0 : 1;
   }
 }
 
@@ -874,12 +904,26 @@ struct QemState {
   DevBuf<uint64_t> key, marked, marked_sorted;
   const uint64_t* mlist = nullptr;  // this iteration's marked list (marked_sorted or marked)
   bool key_order = false;           // stepwise API: always sort the marked list
+  const bool undo_stats = std::getenv("PAMOPT_UNDO_STATS") != nullptr;
   DevBuf<double> place;
   DevBuf<unsigned long long> vmin, vfmin;
   DevBuf<uint32_t> rem, remoff;
   DevBuf<Counters> cnt;
   DevBuf<uint64_t> inv, newinv;
   int64_t ninv = 0;
+  DevBuf<uint64_t> inv_tab;  // hash set of the ninv invalid pairs (k_inv_insert)
+  uint64_t inv_mask = 0;
+
+  void build_inv_table() {
+    if (ninv == 0) return;
+    uint64_t cap = 1024;
+    while (cap < 2 * static_cast<uint64_t>(ninv)) cap <<= 1;
+    inv_tab.ensure(cap, st);
+    inv_mask = cap - 1;
+    PCU_CUDA(cudaMemsetAsync(inv_tab.get(), 0xFF, cap * 8, st));
+    PCU_LAUNCH(ctx, k_inv_insert, grid_for(ninv, 256), 256, 0, inv.get(), ninv,
+               reinterpret_cast<unsigned long long*>(inv_tab.get()), inv_mask);
+  }
   DevBuf<int32_t> bca, bcb;
   DevBuf<uint8_t> bapplied;
   DevBuf<double> boldx, boldq;
@@ -997,7 +1041,7 @@ struct QemState {
                vmap.get(), fk.get(), fmap.get(), Xo.get(), Qo.get(), Fo.get());
     if (ninv) {
       PCU_LAUNCH(ctx, k_inv_remap, grid_for(ninv, 256), 256, 0, inv.get(), ninv, vk.get(), vmap.get());
-      sort_pairs_u64(ctx, inv.get(), ninv);  // dropped pairs (~0) sort last and never match
+      build_inv_table();  // dropped pairs (~0) are not inserted
     }
     V = std::move(Xo);
     Q = std::move(Qo);
@@ -1031,7 +1075,8 @@ struct QemState {
                smult.get(), ea.get(), eb.get(), enf.get());
     ctx.prof.mark(st, "edges");
     const unsigned eg = std::min<unsigned>(grid_for(ne_hint, 128), gs_grid);
-    PCU_LAUNCH(ctx, k_mark_invalid, eg, 128, 0, ea.get(), eb.get(), d_ne, inv.get(), ninv, valid.get());
+    PCU_LAUNCH(ctx, k_mark_invalid, eg, 128, 0, ea.get(), eb.get(), d_ne, inv_tab.get(), inv_mask, ninv,
+               valid.get());
     PCU_LAUNCH(ctx, k_cost, eg, 128, 0, X, F, Q.get(), off.get(), deg.get(), inc.get(), ea.get(), eb.get(), valid.get(),
                d_ne, P.we, P.ws, key.get(), place.get(), cnt.get());
     ctx.prof.mark(st, "cost");
@@ -1136,7 +1181,12 @@ struct QemState {
       boxes_update(ctx, *isc, X, F, rlist.get(), static_cast<int64_t>(h.restored), falive.get());  // restored faces
       unsigned long long found = 0, ncand = 0;
       int redo = 0;
-      detect_read(ds_host.data(), &found, &redo, &ncand);
+      unsigned long long ncls[3];
+      detect_read(ds_host.data(), &found, &redo, &ncand, ncls);
+      if (undo_stats)  // PAMOPT_UNDO_STATS=1: one line per detection round (diagnostics)
+        std::fprintf(stderr, "undo it=%lld round=%d alive=%lld queries=%lld restored=%lld cand=%llu cls=%llu/%llu/%llu found=%llu\n",
+                     static_cast<long long>(S.iterations), rounds, static_cast<long long>(alive_faces),
+                     static_cast<long long>(nqr), static_cast<long long>(nrest), ncand, ncls[0], ncls[1], ncls[2], found);
       ctx.prof.mark(st, "undo_round");
       if (redo) {  // candidate buffer overflow: nothing was flagged or reverted; grow and repeat
         detect_grow(*isc, ncand);
@@ -1181,9 +1231,9 @@ struct QemState {
       PCU_CUDA(cudaMemcpyAsync(merged.get(), inv.get(), ninv * 8, cudaMemcpyDeviceToDevice, st));
     if (nnew)
       PCU_CUDA(cudaMemcpyAsync(merged.get() + (keep_old ? ninv : 0), newinv.get(), nnew * 8, cudaMemcpyDeviceToDevice, st));
-    if (nall) sort_pairs_u64(ctx, merged.get(), nall);
     inv = std::move(merged);
     ninv = nall;
+    build_inv_table();
     ctx.prof.mark(st, "invalid_update");
     phase = 0;
   }
