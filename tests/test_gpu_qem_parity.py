@@ -87,3 +87,26 @@ def test_thin_wall_multi_round_undo(api, oracle, k, gap, target, min_rounds):
     assert np.array_equal(gs["per_iter_collapses"], st["per_iter_collapses"])
     assert np.array_equal(gf, fo) and np.array_equal(gv.view(np.uint64), vo.view(np.uint64))
     assert len(api.detect_self_intersections(out)) == 0
+
+
+@pytest.mark.parametrize("index", [28, 37, 48])
+def test_c5_long_tail_meshes_match_live_oracle(api, oracle, index):
+    """C5 batch meshes whose runs end in a long tail (hundreds of iterations of a few collapses,
+    most batches undone, the stall rule ending the run) — the regime where the hot loop takes
+    k_mark's marked list unsorted and keeps the invalid pairs in a hash set.  GPU = oracle bit
+    for bit, and the device-resident pipeline (the bench's path) returns the same mesh."""
+    v, f, R, target = FX.c5_batch(index + 1)[index]
+    m = api.DeviceMesh.upload(v, f)
+    dmc = api.extract(api.compute_sdf(m, R))
+    dv, df = dmc.download()
+    out, st = api.simplify_to(dmc, target)
+    ov, of = out.download()
+    vo, fo, so = oracle.simplify(dv, df, target)
+    assert st["iterations"] == so["iterations"] and st["iterations"] > 100
+    assert np.array_equal(st["per_iter_collapses"], so["per_iter_collapses"])
+    assert list(st["undo_hist"]) == so["undo_hist"]
+    assert np.array_equal(of, fo) and np.array_equal(ov.view(np.uint64), vo.view(np.uint64))
+    pm, pst, _ = api.remesh_device(api.DeviceMesh.upload(v, f), R, target)
+    pv, pf = pm.download()
+    assert pst["iterations"] == st["iterations"]
+    assert np.array_equal(pf, of) and np.array_equal(pv.view(np.uint64), ov.view(np.uint64))
