@@ -29,6 +29,11 @@ def test_invalid_arguments_raise(api, c1):
     from paper_2509_05595_b200._lib import PamoptInvalidArgument
     with pytest.raises(PamoptInvalidArgument):
         api.compute_udf((c1["v"], c1["f"]), 100)              # R not a power of two
+    for R in (2048, 4096):  # 32-bit cell ids: R is capped at 1024 before anything is allocated
+        with pytest.raises(PamoptInvalidArgument):
+            api.compute_sdf((c1["v"], c1["f"]), R)
+        with pytest.raises(PamoptInvalidArgument):
+            api.remesh_device(api.DeviceMesh.upload(c1["v"], c1["f"]), R, 100)
     g = api.compute_udf((c1["v"], c1["f"]), 32)
     with pytest.raises(PamoptInvalidArgument):
         api.udf_to_sdf(g, 0.5)                                # eps out of range
