@@ -36,6 +36,7 @@ static void ctx_release(pamopt_cu_ctx c) {
   pcu::DeviceGuard g(c->ctx.device);
   if (c->ctx.scratch) cudaFreeAsync(c->ctx.scratch, c->ctx.stream);
   cudaStreamSynchronize(c->ctx.stream);
+  c->ctx.release_aux();
   cudaStreamDestroy(c->ctx.stream);
   delete c;
 }

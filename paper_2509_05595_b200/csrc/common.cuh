@@ -133,6 +133,47 @@ struct Ctx {
   // last remesh_host result
   std::vector<double> host_v;
   std::vector<int32_t> host_f;
+  // a second stream for independent kernels of one step (fork / join through the two events),
+  // created on first use
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t aux_stream() {
+    if (!aux) {
+      PCU_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+      PCU_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      PCU_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    return aux;
+  }
+  void release_aux() {
+    if (!aux) return;
+    cudaStreamSynchronize(aux);
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
+    cudaStreamDestroy(aux);
+    aux = nullptr;
+  }
+};
+
+// launches between construction and destruction go to the context's aux stream, which first
+// waits for everything already queued on the main stream; the destructor makes the main stream
+// wait for the aux work (fork / join)
+struct AuxFork {
+  Ctx& ctx;
+  cudaStream_t main;
+  explicit AuxFork(Ctx& c) : ctx(c), main(c.stream) {
+    cudaStream_t a = ctx.aux_stream();
+    PCU_CUDA(cudaEventRecord(ctx.ev_fork, main));
+    PCU_CUDA(cudaStreamWaitEvent(a, ctx.ev_fork, 0));
+    ctx.stream = a;
+  }
+  // back to the main stream for launches that run concurrently with the aux ones
+  void to_main() { ctx.stream = main; }
+  ~AuxFork() {
+    ctx.stream = main;
+    cudaEventRecord(ctx.ev_join, ctx.aux);
+    cudaStreamWaitEvent(main, ctx.ev_join, 0);
+  }
 };
 
 struct DeviceGuard {

@@ -950,13 +950,20 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
              S.cls.get(), pairs, pair_cap, owner, revert);
-  PCU_LAUNCH(ctx, k_narrow1_fast, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap,
-             owner, revert);
-  // the undecided remainder is a small fraction of the bucket: one CTA per SM
-  PCU_LAUNCH(ctx, (k_narrow<1, 2>), static_cast<unsigned>(ctx.num_sms), 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap,
-             owner, revert);
-  PCU_LAUNCH(ctx, k_narrow<0>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
-             revert);
+  // the 1-shared chain (certified filter, then the exact pass over its few undecided pairs, a
+  // latency-bound launch) runs on the aux stream beside the 0-shared bucket: the buckets are
+  // independent, and both only add to the found / pair counters and set revert flags
+  {
+    AuxFork fork(ctx);
+    PCU_LAUNCH(ctx, k_narrow1_fast, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap,
+               owner, revert);
+    // the undecided remainder is a small fraction of the bucket: one CTA per SM
+    PCU_LAUNCH(ctx, (k_narrow<1, 2>), static_cast<unsigned>(ctx.num_sms), 128, 0, dV, dF, S.cls.get(), S.cand_cap,
+               S.ds.get(), mode, pairs, pair_cap, owner, revert);
+    fork.to_main();
+    PCU_LAUNCH(ctx, k_narrow<0>, g, 128, 0, dV, dF, S.cls.get(), S.cand_cap, S.ds.get(), mode, pairs, pair_cap, owner,
+               revert);
+  }
 }
 
 }  // namespace
