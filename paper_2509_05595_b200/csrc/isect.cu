@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <optional>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -919,6 +920,17 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
     PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()),
                S.degen.get(), nullptr);
   }
+  // build-set membership flags (round 1 of the undo loop) on the aux stream, beside the binning
+  const uint8_t* in_build = nullptr;
+  std::optional<AuxFork> fork;
+  if (!sym && mode == 1 && !probe_ids) {
+    S.in_build.ensure(nf, st);
+    fork.emplace(ctx);
+    PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, ctx.stream));
+    PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_build, 256), 256, 0, build_ids, n_build, S.in_build.get());
+    fork->to_main();
+    in_build = S.in_build.get();
+  }
   PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n_build, 256), ctx.num_sms * 4)), 256, 0,
              B, build_ids, n_build, d_alive, S.ds.get());
   // hard capacity: a non-big face covers at most kMaxCells cells
@@ -929,13 +941,7 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   exclusive_scan_u32(ctx, S.bcount.get(), S.boff.get(), nb);
   PCU_LAUNCH(ctx, k_bin, grid_for(n_build, 256), 256, 0, B, build_ids, n_build, d_alive, S.ds.get(), mask, 1,
              S.bcount.get(), S.boff.get(), S.bcur.get(), S.entries.get(), S.big.get(), S.occ.get());
-  const uint8_t* in_build = nullptr;
-  if (!sym && mode == 1 && !probe_ids) {
-    S.in_build.ensure(nf, st);
-    PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, st));
-    PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_build, 256), 256, 0, build_ids, n_build, S.in_build.get());
-    in_build = S.in_build.get();
-  }
+  fork.reset();  // join: k_probe reads in_build
   if (S.cand_cap == 0) S.cand_cap = static_cast<uint64_t>(nf) * 4 + 4096;
   S.cand.ensure(S.cand_cap, st);
   S.huge.ensure(static_cast<size_t>(n_probe) + 16, st);

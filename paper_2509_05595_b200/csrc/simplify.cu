@@ -1137,12 +1137,18 @@ struct QemState {
     PCU_REQUIRE(phase == 2, PAMOPT_CU_EINVAL, "qem: collapse_batch() out of order");
     phase = 3;
     if (nm == 0) return;
-    PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, mlist, nm, ea.get(), eb.get(), enf.get(), F,
-               off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
-    exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
+    {
+      // the pre-batch face copy (the undo loop's restore source) and the owner reset run on the
+      // aux stream while the link condition is evaluated (both only read F)
+      AuxFork fork(ctx);
+      PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx.stream));
+      PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), ctx.stream));
+      fork.to_main();
+      PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, mlist, nm, ea.get(), eb.get(), enf.get(), F,
+                 off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
+      exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
+    }
     ctx.prof.mark(st, "sort+link");
-    PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-    PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), st));
     PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, mlist, nm, rem.get(), remoff.get(),
                alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
                falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
