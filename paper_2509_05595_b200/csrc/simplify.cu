@@ -1112,7 +1112,8 @@ struct QemState {
     // collapses first.  Marked edges have disjoint face neighbourhoods, so when no trim can fire
     // (every collapse removes at most 2 faces) the batch's result does not depend on the order and
     // the hot loop uses k_mark's list as is; the stepwise API keeps key order for its views.
-    const bool any_order = !key_order && alive_faces - 2 * nm > target;
+    // (h.err counts edges with more than 2 faces; with none, every collapse removes <= 2 faces)
+    const bool any_order = !key_order && h.err == 0 && alive_faces - 2 * nm > target;
     if (nm > 0 && any_order) mlist = marked.get();
     if (nm > 0 && !any_order) {
       if (!small_sort_u64(ctx, marked.get(), marked_sorted.get(), nm)) {
