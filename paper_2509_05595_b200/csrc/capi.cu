@@ -155,8 +155,8 @@ __global__ void __launch_bounds__(1024) k_small_scan(const uint32_t* in, int n, 
 // separate cudaMemsetAsync costs a launch).  Ranges are filled as 32-bit words with the byte
 // value replicated, and a byte tail; ranges above 1 MB go to cudaMemsetAsync instead.
 __global__ void k_fill_multi(FillRanges fr) {
-  uint64_t total = 0;
-  for (int r = 0; r < fr.n; ++r) total += fr.r[r].bytes;
+  uint64_t total = 0;  // the flattened space: each range padded to whole words
+  for (int r = 0; r < fr.n; ++r) total += (fr.r[r].bytes + 3) / 4 * 4;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i * 4 < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint64_t off = i * 4;
@@ -178,16 +178,19 @@ __global__ void k_fill_multi(FillRanges fr) {
   }
 }
 
-void fill_multi(Ctx& ctx, std::initializer_list<FillRange> ranges) {
+void fill_multi(Ctx& ctx, std::initializer_list<FillRange> ranges) { fill_multi(ctx, ranges.begin(), ranges.size()); }
+
+void fill_multi(Ctx& ctx, const FillRange* ranges, size_t count) {
   FillRanges fr{};
   uint64_t total = 0;
-  for (const FillRange& r : ranges) {
+  for (size_t i = 0; i < count; ++i) {
+    const FillRange& r = ranges[i];
     if (!r.p || r.bytes == 0) continue;
     if (r.bytes > (1u << 20)) {  // large: the copy engine's memset runs at HBM rate
       PCU_CUDA(cudaMemsetAsync(r.p, r.byte, r.bytes, ctx.stream));
       continue;
     }
-    PCU_REQUIRE(fr.n < 4, PAMOPT_CU_EINVAL, "fill_multi: at most 4 ranges");
+    PCU_REQUIRE(fr.n < kMaxFillRanges, PAMOPT_CU_EINVAL, "fill_multi: too many ranges");
     PCU_REQUIRE((reinterpret_cast<uintptr_t>(r.p) & 3u) == 0, PAMOPT_CU_EINVAL, "fill_multi: unaligned range");
     fr.r[fr.n++] = r;
     total += (r.bytes + 3) / 4;

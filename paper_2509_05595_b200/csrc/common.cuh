@@ -254,11 +254,13 @@ struct FillRange {
   uint64_t bytes;
   uint8_t byte;
 };
+constexpr int kMaxFillRanges = 8;
 struct FillRanges {
-  FillRange r[4];
+  FillRange r[kMaxFillRanges];
   int n;
 };
 void fill_multi(Ctx& ctx, std::initializer_list<FillRange> ranges);
+void fill_multi(Ctx& ctx, const FillRange* ranges, size_t count);
 void exclusive_scan_u32(Ctx& ctx, const uint32_t* in, uint32_t* out, int64_t n);
 void exclusive_scan_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n);
 void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit = 64);

@@ -899,7 +899,8 @@ namespace {
 void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive,
                   const int32_t* build_ids, int64_t n_build, const int32_t* probe_ids, int64_t n_probe, int sym,
                   int mode, int32_t* pairs, uint64_t pair_cap, const int32_t* owner,
-                  uint8_t* revert, bool boxes_current = false, const uint8_t* in_probe = nullptr) {
+                  uint8_t* revert, bool boxes_current = false, const uint8_t* in_probe = nullptr,
+                  std::initializer_list<FillRange> extra_fills = {}) {
   cudaStream_t st = ctx.stream;
   S.ds.ensure(1, st);
   const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_build) * 2 + 1);
@@ -909,9 +910,17 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   S.bcur.ensure(nb, st);
   S.occ.ensure(nb / 32 + 1, st);
   // the round's scalars and the grid's bucket counters / occupancy bitmap, zeroed in one launch
-  fill_multi(ctx, {{S.ds.get(), sizeof(DetectScalars), 0}, {S.bcount.get(), static_cast<uint64_t>(nb) * 4, 0},
-                   {S.bcur.get(), static_cast<uint64_t>(nb) * 4, 0},
-                   {S.occ.get(), (static_cast<uint64_t>(nb) / 32 + 1) * 4, 0}});
+  // (plus the caller's resets for the round, in the same launch)
+  FillRange fills[kMaxFillRanges] = {{S.ds.get(), sizeof(DetectScalars), 0},
+                                     {S.bcount.get(), static_cast<uint64_t>(nb) * 4, 0},
+                                     {S.bcur.get(), static_cast<uint64_t>(nb) * 4, 0},
+                                     {S.occ.get(), (static_cast<uint64_t>(nb) / 32 + 1) * 4, 0}};
+  size_t nfill = 4;
+  for (const FillRange& r : extra_fills) {
+    PCU_REQUIRE(nfill < kMaxFillRanges, PAMOPT_CU_EINVAL, "detect_round: too many resets");
+    fills[nfill++] = r;
+  }
+  fill_multi(ctx, fills, nfill);
   const FBox* B = reinterpret_cast<const FBox*>(S.fbox.get());
   if (!boxes_current) {
     S.fbox.ensure(6 * static_cast<size_t>(nf > 0 ? nf : 1), st);
@@ -1032,22 +1041,22 @@ void verdict_by_class(Ctx& ctx, const double* dV, const int32_t* dF, const int32
 
 void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                        const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
-                       uint8_t* d_revert) {
+                       uint8_t* d_revert, std::initializer_list<FillRange> resets) {
   // round 1: grid over the faces owned by applied collapses (~0.4 of the alive faces in every
   // iteration), probed by every alive face.  The converse (grid over every alive face, probed by
   // the owned faces, pairs of two owned faces from the smaller probe via in_probe) was measured
   // slower at C3: k_probe 36.0 -> 61.6 ms, k_bin 7.6 -> 19.4 ms (profiles/r02_summary.md).
   detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner,
-               d_revert, true);
+               d_revert, true, nullptr, resets);
 }
 
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                                 const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
                                 const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
-                                uint8_t* d_revert) {
+                                uint8_t* d_revert, std::initializer_list<FillRange> resets) {
   // later rounds: only (restored face, applied-owned face) pairs can be new
   detect_round(ctx, S, dV, dF, nf, d_falive, d_restored, n_restored, d_owned, n_owned, 0, 1, nullptr, 0, d_owner,
-               d_revert, true);
+               d_revert, true, nullptr, resets);
 }
 
 // Persistent face boxes for the QEM loop: computed once, then refreshed only for the faces a

@@ -156,11 +156,11 @@ void verdict_by_class(Ctx& ctx, const double* dV, const int32_t* dF, const int32
 struct IsectScratch;
 void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                        const uint8_t* d_falive, const int32_t* d_query_faces, int64_t n_query, const int32_t* d_owner,
-                       uint8_t* d_revert);
+                       uint8_t* d_revert, std::initializer_list<FillRange> resets = {});
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
                                 const uint8_t* d_falive, const int32_t* d_restored, int64_t n_restored,
                                 const int32_t* d_owned, int64_t n_owned, const int32_t* d_owner,
-                                uint8_t* d_revert);
+                                uint8_t* d_revert, std::initializer_list<FillRange> resets = {});
 void boxes_init(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf, const uint8_t* d_alive);
 void boxes_update(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, const int32_t* ids, int64_t n,
                   const uint8_t* d_alive);

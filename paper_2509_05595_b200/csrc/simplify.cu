@@ -1171,14 +1171,16 @@ struct QemState {
     int64_t nqr = nq;
     Counters h = hc;
     while (nqr > 0) {
-      // (the query counter was read at the last synchronisation; k_revert does not use it)
-      fill_multi(ctx, {{revert.get(), static_cast<uint64_t>(nm), 0}, {&cnt.get()->restored, 8, 0},
-                       {&cnt.get()->query, 8, 0}});
+      // the round's resets ride in the detection's fill launch (the query counter was read at the
+      // last synchronisation; k_revert does not use it)
+      const std::initializer_list<FillRange> resets = {{revert.get(), static_cast<uint64_t>(nm), 0},
+                                                       {&cnt.get()->restored, 8, 0},
+                                                       {&cnt.get()->query, 8, 0}};
       if (first_round)
-        undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nqr, owner.get(), revert.get());
+        undo_detect_async(ctx, *isc, X, F, nf, falive.get(), qa, nqr, owner.get(), revert.get(), resets);
       else
         undo_detect_restored_async(ctx, *isc, X, F, nf, falive.get(), rlist.get(), nrest, qa, nqr, owner.get(),
-                                   revert.get());
+                                   revert.get(), resets);
       PCU_LAUNCH(ctx, k_revert, grid_for(nm, 128), 128, 0, nm, revert.get(), off.get(), deg.get(), inc.get(),
                  Fprev.get(), X, F, falive.get(), valive.get(), Q.get(), owner.get(), B, newinv.get(), cnt.get(),
                  rlist.get());
