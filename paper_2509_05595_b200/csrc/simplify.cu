@@ -995,6 +995,7 @@ struct QemState {
     gs_grid = static_cast<unsigned>(ctx.num_sms * 16);
     ctx.prof.reset(st);
     if (nf == 0 || nv == 0) return;
+    fill_multi(ctx, {{deg.get(), nv * sizeof(uint32_t), 0}, {cur.get(), nv * sizeof(uint32_t), 0}});
     build_incidence();
     boxes_init(ctx, *isc, X, F, nf, falive.get());
     PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, off.get(), deg.get(), inc.get(), nv, Q.get());
@@ -1005,8 +1006,8 @@ struct QemState {
 
   bool done() const { return nf == 0 || !(alive_faces > target && zero_run < P.stall); }
 
+  // (deg and cur must be zero on entry: the constructor and prepare() reset them)
   void build_incidence() {
-    fill_multi(ctx, {{deg.get(), nv * sizeof(uint32_t), 0}, {cur.get(), nv * sizeof(uint32_t), 0}});
     PCU_LAUNCH(ctx, k_deg, grid_for(nf, 256), 256, 0, F, falive.get(), nf, deg.get());
     exclusive_scan_u32(ctx, deg.get(), off.get(), nv);
     PCU_LAUNCH(ctx, k_fill, grid_for(nf, 256), 256, 0, F, falive.get(), nf, off.get(), cur.get(), inc.get());
@@ -1062,9 +1063,13 @@ struct QemState {
     ctx.prof.mark(st, "misc");
     if (alive_faces * 5 < nf * 3 && nf > 4096) compact_state();
     ctx.prof.mark(st, "compact_state");
+    // this iteration's resets in one launch: the incidence counters, the counters block, and the
+    // per-vertex minima propagate_and_mark() fills
+    const uint64_t nvb = S.iterations > 1 ? nv * sizeof(uint32_t) : 0;
+    fill_multi(ctx, {{deg.get(), nvb, 0}, {cur.get(), nvb, 0}, {cnt.get(), sizeof(Counters), 0},
+                     {vmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}, {vfmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}});
     if (S.iterations > 1) build_incidence();
     ctx.prof.mark(st, "incidence");
-    cnt.memset(0, st);
     unsigned long long* d_ne = &cnt.get()->edges;
     // edges (device-side count; kernels below stride over it)
     PCU_LAUNCH(ctx, k_edge_count, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, ecount.get(),
@@ -1088,7 +1093,7 @@ struct QemState {
     PCU_REQUIRE(phase == 1, PAMOPT_CU_EINVAL, "qem: propagate_and_mark() out of order");
     unsigned long long* d_ne = &cnt.get()->edges;
     const unsigned eg = std::min<unsigned>(grid_for(ne_hint, 128), gs_grid);
-    fill_multi(ctx, {{vmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}, {vfmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}});
+    // (vmin / vfmin were reset to ~0 by prepare())
     PCU_LAUNCH(ctx, k_prop_edges, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vmin.get());
     PCU_LAUNCH(ctx, k_prop_faces, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vmin.get(), vfmin.get());
     PCU_LAUNCH(ctx, k_mark, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vfmin.get(), marked.get(),
