@@ -366,12 +366,8 @@ struct DetectScalars {
   unsigned ext_blocks;  // k_ext_sum blocks finished (the last one sets inv_h)
 };
 
-__global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t n,
-                         const uint8_t* __restrict__ alive, FBox* __restrict__ out, uint8_t* __restrict__ degen,
-                         const int32_t* __restrict__ ids) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k >= n) return;
-  const int64_t f = ids ? ids[k] : k;
+__device__ __forceinline__ FBox fbox_of(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t f,
+                                        const uint8_t* __restrict__ alive, uint8_t* __restrict__ degen) {
   FBox fb;
   if (alive && !alive[f]) {
     for (int k = 0; k < 3; ++k) {
@@ -387,7 +383,16 @@ __global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict
     const int32_t* t = F + 3 * f;
     degen[f] = degenerate(vtx(V, t[0]), vtx(V, t[1]), vtx(V, t[2])) ? 1 : 0;
   }
-  out[f] = fb;
+  return fb;
+}
+
+__global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict__ F, int64_t n,
+                         const uint8_t* __restrict__ alive, FBox* __restrict__ out, uint8_t* __restrict__ degen,
+                         const int32_t* __restrict__ ids) {
+  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (k >= n) return;
+  const int64_t f = ids ? ids[k] : k;
+  out[f] = fbox_of(V, F, f, alive, degen);
 }
 
 // cell size = PCU_CELL_SCALE x the mean box extent of the build set; the block that finishes last
@@ -395,8 +400,11 @@ __global__ void k_fboxes(const double* __restrict__ V, const int32_t* __restrict
 #ifndef PCU_CELL_SCALE
 #define PCU_CELL_SCALE 1.5
 #endif
-__global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict__ ids, int64_t n,
-                          const uint8_t* __restrict__ alive, DetectScalars* ds) {
+// With `fresh` (the QEM undo loop: the build set is exactly the faces a collapse batch or a
+// revert just changed), the build faces' boxes and degenerate flags are recomputed here first.
+__global__ void k_ext_sum(FBox* __restrict__ B, const int32_t* __restrict__ ids, int64_t n,
+                          const uint8_t* __restrict__ alive, DetectScalars* ds, const double* __restrict__ V,
+                          const int32_t* __restrict__ F, uint8_t* __restrict__ degen, int fresh) {
   typedef cub::BlockReduce<double, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   __shared__ bool last;
@@ -404,8 +412,13 @@ __global__ void k_ext_sum(const FBox* __restrict__ B, const int32_t* __restrict_
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t f = ids ? ids[k] : k;
+    FBox b;
+    if (fresh) {
+      b = fbox_of(V, F, f, alive, degen);
+      B[f] = b;
+    }
     if (alive && !alive[f]) continue;
-    const FBox& b = B[f];
+    if (!fresh) b = B[f];
     s += fmax(fmax(b.hi[0] - b.lo[0], b.hi[1] - b.lo[1]), b.hi[2] - b.lo[2]);
   }
   const double t = BR(tmp).Sum(s);
@@ -900,7 +913,7 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
                   const int32_t* build_ids, int64_t n_build, const int32_t* probe_ids, int64_t n_probe, int sym,
                   int mode, int32_t* pairs, uint64_t pair_cap, const int32_t* owner,
                   uint8_t* revert, bool boxes_current = false, const uint8_t* in_probe = nullptr,
-                  std::initializer_list<FillRange> extra_fills = {}) {
+                  std::initializer_list<FillRange> extra_fills = {}, bool fresh_build_boxes = false) {
   cudaStream_t st = ctx.stream;
   S.ds.ensure(1, st);
   const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_build) * 2 + 1);
@@ -941,7 +954,8 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
     in_build = S.in_build.get();
   }
   PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n_build, 256), ctx.num_sms * 4)), 256, 0,
-             B, build_ids, n_build, d_alive, S.ds.get());
+             const_cast<FBox*>(B), build_ids, n_build, d_alive, S.ds.get(), dV, dF, S.degen.get(),
+             fresh_build_boxes ? 1 : 0);
   // hard capacity: a non-big face covers at most kMaxCells cells
   S.entries.ensure(static_cast<size_t>(n_build) * kMaxCells + 16, st);
   S.big.ensure(static_cast<size_t>(n_build) + 16, st);
@@ -1047,7 +1061,7 @@ void undo_detect_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_
   // the owned faces, pairs of two owned faces from the smaller probe via in_probe) was measured
   // slower at C3: k_probe 36.0 -> 61.6 ms, k_bin 7.6 -> 19.4 ms (profiles/r02_summary.md).
   detect_round(ctx, S, dV, dF, nf, d_falive, d_query_faces, n_query, nullptr, nf, 0, 1, nullptr, 0, d_owner,
-               d_revert, true, nullptr, resets);
+               d_revert, true, nullptr, resets, true);
 }
 
 void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF, int64_t nf,
@@ -1056,7 +1070,7 @@ void undo_detect_restored_async(Ctx& ctx, IsectScratch& S, const double* dV, con
                                 uint8_t* d_revert, std::initializer_list<FillRange> resets) {
   // later rounds: only (restored face, applied-owned face) pairs can be new
   detect_round(ctx, S, dV, dF, nf, d_falive, d_restored, n_restored, d_owned, n_owned, 0, 1, nullptr, 0, d_owner,
-               d_revert, true, nullptr, resets);
+               d_revert, true, nullptr, resets, true);
 }
 
 // Persistent face boxes for the QEM loop: computed once, then refreshed only for the faces a

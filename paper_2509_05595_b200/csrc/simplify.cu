@@ -182,10 +182,11 @@ __global__ void k_edge_count(const int32_t* __restrict__ F, const uint32_t* __re
 __global__ void k_edge_fill(const uint32_t* __restrict__ off, const uint32_t* __restrict__ ecount, int64_t nv,
                             const uint32_t* __restrict__ eoff, const int32_t* __restrict__ snb,
                             const uint8_t* __restrict__ smult, int32_t* __restrict__ ea, int32_t* __restrict__ eb,
-                            uint8_t* __restrict__ enf) {
+                            uint8_t* __restrict__ enf, unsigned long long* __restrict__ total) {
   const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (a >= nv) return;
   const int u = static_cast<int>(ecount[a]);
+  if (a == nv - 1) *total = static_cast<unsigned long long>(eoff[a]) + static_cast<unsigned>(u);  // edge count
   const int64_t s0 = 2 * static_cast<int64_t>(off[a]);
   const uint32_t e0 = eoff[a];
   for (int i = 0; i < u; ++i) {
@@ -462,11 +463,6 @@ __global__ void k_mark(const int32_t* __restrict__ ea, const int32_t* __restrict
     const uint64_t k = key[e];
     if (k == vfmin[ea[e]] && k == vfmin[eb[e]]) marked[agg_inc(&cnt->marked)] = k;
   }
-}
-
-__global__ void k_total(const uint32_t* __restrict__ off, const uint32_t* __restrict__ cnt, int64_t n,
-                        unsigned long long* __restrict__ out) {
-  *out = static_cast<unsigned long long>(off[n - 1]) + cnt[n - 1];
 }
 
 // ---------------------------------------------------------------------- link condition
@@ -1075,9 +1071,8 @@ struct QemState {
     PCU_LAUNCH(ctx, k_edge_count, grid_for(nv, 128), 128, 0, F, off.get(), deg.get(), inc.get(), nv, ecount.get(),
                snb.get(), smult.get(), cnt.get());
     exclusive_scan_u32(ctx, ecount.get(), eoff.get(), nv);
-    PCU_LAUNCH(ctx, k_total, 1, 1, 0, eoff.get(), ecount.get(), nv, d_ne);
     PCU_LAUNCH(ctx, k_edge_fill, grid_for(nv, 128), 128, 0, off.get(), ecount.get(), nv, eoff.get(), snb.get(),
-               smult.get(), ea.get(), eb.get(), enf.get());
+               smult.get(), ea.get(), eb.get(), enf.get(), d_ne);
     ctx.prof.mark(st, "edges");
     const unsigned eg = std::min<unsigned>(grid_for(ne_hint, 128), gs_grid);
     PCU_LAUNCH(ctx, k_mark_invalid, eg, 128, 0, ea.get(), eb.get(), d_ne, inv_tab.get(), inv_mask, ninv,
@@ -1161,7 +1156,7 @@ struct QemState {
     hc = sync_counters(false);  // ---- sync 2
     ctx.prof.mark(st, "collapse");
     nq = static_cast<int64_t>(hc.query);
-    boxes_update(ctx, *isc, X, F, qf.get(), nq, falive.get());  // moved / renamed faces
+    // (the moved / renamed faces get their boxes in the first undo round: they are its build set)
   }
 
   // detect -> revert owners -> repeat until clean
@@ -1192,7 +1187,6 @@ struct QemState {
       // rebuild the query list from still-applied collapses
       PCU_LAUNCH(ctx, k_requery, grid_for(nqr, 256), 256, 0, qa, nqr, owner.get(), B.applied, qb, cnt.get());
       h = sync_counters(true);  // ---- sync per round
-      boxes_update(ctx, *isc, X, F, rlist.get(), static_cast<int64_t>(h.restored), falive.get());  // restored faces
       unsigned long long found = 0, ncand = 0;
       int redo = 0;
       unsigned long long ncls[3];
@@ -1213,6 +1207,9 @@ struct QemState {
       nrest = static_cast<int64_t>(h.restored);
       std::swap(qa, qb);
     }
+    // restored faces get their boxes in the next round (its build set); after the last round the
+    // faces restored by it still need them
+    if (nqr == 0 && nrest > 0) boxes_update(ctx, *isc, X, F, rlist.get(), nrest, falive.get());
     succ = static_cast<int64_t>(h.applied);
     alive_faces -= static_cast<int64_t>(h.removed);
     nnew = static_cast<int64_t>(h.newinv);
