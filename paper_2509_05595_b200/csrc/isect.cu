@@ -18,7 +18,6 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
-#include <optional>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -476,7 +475,7 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
                                                const uint32_t* __restrict__ bcount, const uint32_t* __restrict__ boff,
                                                const int4* __restrict__ entries, const int32_t* __restrict__ big,
                                                const uint32_t* __restrict__ occ, int sym,
-                                               const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
+                                               const int32_t* __restrict__ in_build, uint64_t* __restrict__ cand,
                                                uint64_t cap, unsigned long long* __restrict__ ncand,
                                                const int32_t* __restrict__ probe_ids, int32_t* __restrict__ huge,
                                                unsigned long long* __restrict__ nhuge,
@@ -512,7 +511,7 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
   bool p_build = false;
   int64_t ncell = 0;
   if (p >= 0) {
-    p_build = sym || (in_build && in_build[p]);
+    p_build = sym || (in_build && in_build[p] >= 0);
     bp = B[p];
     cp = cells_of(bp, inv_h);
     ncell = cp.count();
@@ -644,7 +643,7 @@ __global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B,
                                                      const int32_t* __restrict__ build_ids, int64_t n_build,
                                                      const int32_t* __restrict__ probe_ids, int64_t n_probe,
                                                      const uint8_t* __restrict__ alive, int sym,
-                                                     const uint8_t* __restrict__ in_build, uint64_t* __restrict__ cand,
+                                                     const int32_t* __restrict__ in_build, uint64_t* __restrict__ cand,
                                                      uint64_t cap, unsigned long long* __restrict__ ncand,
                                                      const uint8_t* __restrict__ in_probe) {
   const unsigned long long nh = ds->nhuge, nb = ds->nbig;
@@ -658,7 +657,7 @@ __global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B,
   for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); w < nh + nb; w += nw) {
     if (w < nh) {
       const int32_t p = huge[w];
-      const bool p_build = sym || (in_build && in_build[p]);
+      const bool p_build = sym || (in_build && in_build[p] >= 0);
       const FBox bp = B[p];
       for (int64_t k = lane; k < n_build; k += 32) {
         const int32_t a = build_ids ? build_ids[k] : static_cast<int32_t>(k);
@@ -676,7 +675,7 @@ __global__ void __launch_bounds__(128) k_probe_large(const FBox* __restrict__ B,
         const int32_t x = probe_ids ? probe_ids[k] : static_cast<int32_t>(k);
         if (alive && !alive[x]) continue;
         if (x == b) continue;
-        const bool x_build = sym || (in_build && in_build[x]);
+        const bool x_build = sym || (in_build && in_build[x] >= 0);
         if (x_build && b < x && (!in_probe || in_probe[b])) continue;  // emitted from probe b instead
         if (!overlap(B[x], bb)) continue;
         emit(x, b);
@@ -873,11 +872,6 @@ __global__ void k_verdict_pairs(const double* __restrict__ V, const int32_t* __r
   out[i] = verdict(V, F + 3 * pairs[2 * i], F + 3 * pairs[2 * i + 1]) ? 1 : 0;
 }
 
-__global__ void k_flag_ids(const int32_t* __restrict__ ids, int64_t n, uint8_t* __restrict__ flag) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) flag[ids[i]] = 1;
-}
-
 uint32_t pow2_at_least(uint64_t x) {
   uint32_t p = 1024;
   while (p < x && p < (1u << 30)) p <<= 1;
@@ -892,7 +886,6 @@ struct IsectScratch {
   DevBuf<uint32_t> occ;      // non-empty bucket bitmap
   DevBuf<int32_t> big;
   DevBuf<int32_t> huge;      // huge probe ids
-  DevBuf<uint8_t> in_build;
   DevBuf<uint64_t> cand;
   DevBuf<float> fbox;        // 6 floats per face
   DevBuf<uint8_t> degen;     // degenerate-face flags
@@ -942,17 +935,9 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
     PCU_LAUNCH(ctx, k_fboxes, grid_for(nf, 256), 256, 0, dV, dF, nf, d_alive, reinterpret_cast<FBox*>(S.fbox.get()),
                S.degen.get(), nullptr);
   }
-  // build-set membership flags (round 1 of the undo loop) on the aux stream, beside the binning
-  const uint8_t* in_build = nullptr;
-  std::optional<AuxFork> fork;
-  if (!sym && mode == 1 && !probe_ids) {
-    S.in_build.ensure(nf, st);
-    fork.emplace(ctx);
-    PCU_CUDA(cudaMemsetAsync(S.in_build.get(), 0, nf, ctx.stream));
-    PCU_LAUNCH(ctx, k_flag_ids, grid_for(n_build, 256), 256, 0, build_ids, n_build, S.in_build.get());
-    fork->to_main();
-    in_build = S.in_build.get();
-  }
+  // build-set membership (round 1 of the undo loop): the build set is exactly the faces an applied
+  // collapse owns, so owner[f] >= 0 is the flag
+  const int32_t* in_build = (!sym && mode == 1 && !probe_ids) ? owner : nullptr;
   PCU_LAUNCH(ctx, k_ext_sum, static_cast<unsigned>(std::min<int64_t>(grid_for(n_build, 256), ctx.num_sms * 4)), 256, 0,
              const_cast<FBox*>(B), build_ids, n_build, d_alive, S.ds.get(), dV, dF, S.degen.get(),
              fresh_build_boxes ? 1 : 0);
@@ -964,7 +949,6 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   exclusive_scan_u32(ctx, S.bcount.get(), S.boff.get(), nb);
   PCU_LAUNCH(ctx, k_bin, grid_for(n_build, 256), 256, 0, B, build_ids, n_build, d_alive, S.ds.get(), mask, 1,
              S.bcount.get(), S.boff.get(), S.bcur.get(), S.entries.get(), S.big.get(), S.occ.get());
-  fork.reset();  // join: k_probe reads in_build
   if (S.cand_cap == 0) S.cand_cap = static_cast<uint64_t>(nf) * 4 + 4096;
   S.cand.ensure(S.cand_cap, st);
   S.huge.ensure(static_cast<size_t>(n_probe) + 16, st);

@@ -1059,11 +1059,12 @@ struct QemState {
     ctx.prof.mark(st, "misc");
     if (alive_faces * 5 < nf * 3 && nf > 4096) compact_state();
     ctx.prof.mark(st, "compact_state");
-    // this iteration's resets in one launch: the incidence counters, the counters block, and the
-    // per-vertex minima propagate_and_mark() fills
+    // this iteration's resets in one launch: the incidence counters, the counters block, the
+    // per-vertex minima propagate_and_mark() fills and the face owners collapse_batch() sets
     const uint64_t nvb = S.iterations > 1 ? nv * sizeof(uint32_t) : 0;
     fill_multi(ctx, {{deg.get(), nvb, 0}, {cur.get(), nvb, 0}, {cnt.get(), sizeof(Counters), 0},
-                     {vmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}, {vfmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}});
+                     {vmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}, {vfmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF},
+                     {owner.get(), static_cast<uint64_t>(nf) * 4, 0xFF}});
     if (S.iterations > 1) build_incidence();
     ctx.prof.mark(st, "incidence");
     unsigned long long* d_ne = &cnt.get()->edges;
@@ -1139,11 +1140,10 @@ struct QemState {
     phase = 3;
     if (nm == 0) return;
     {
-      // the pre-batch face copy (the undo loop's restore source) and the owner reset run on the
-      // aux stream while the link condition is evaluated (both only read F)
+      // the pre-batch face copy (the undo loop's restore source) runs on the aux stream while the
+      // link condition is evaluated (both only read F)
       AuxFork fork(ctx);
       PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx.stream));
-      PCU_CUDA(cudaMemsetAsync(owner.get(), 0xFF, nf * sizeof(int32_t), ctx.stream));
       fork.to_main();
       PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, mlist, nm, ea.get(), eb.get(), enf.get(), F,
                  off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
@@ -1236,15 +1236,26 @@ struct QemState {
       keep_old = retain < P.tolerance;
       if (!keep_old) retain = 0;
     }
-    const int64_t nall = (keep_old ? ninv : 0) + nnew;
-    DevBuf<uint64_t> merged(nall ? nall : 1, st);
-    if (keep_old && ninv)
-      PCU_CUDA(cudaMemcpyAsync(merged.get(), inv.get(), ninv * 8, cudaMemcpyDeviceToDevice, st));
-    if (nnew)
-      PCU_CUDA(cudaMemcpyAsync(merged.get() + (keep_old ? ninv : 0), newinv.get(), nnew * 8, cudaMemcpyDeviceToDevice, st));
-    inv = std::move(merged);
-    ninv = nall;
-    build_inv_table();
+    if (!keep_old) {  // the set restarts from this iteration's pairs: swap the buffers
+      std::swap(inv, newinv);
+      if (newinv.n < static_cast<size_t>(ecap)) newinv.alloc(ecap, st);
+      ninv = nnew;
+      build_inv_table();
+    } else if (nnew) {  // the set grows: append, and insert the new pairs into the table
+      if (inv.n < static_cast<size_t>(ninv + nnew)) {
+        DevBuf<uint64_t> grown(2 * static_cast<size_t>(ninv + nnew), st);
+        if (ninv) PCU_CUDA(cudaMemcpyAsync(grown.get(), inv.get(), ninv * 8, cudaMemcpyDeviceToDevice, st));
+        inv = std::move(grown);
+      }
+      PCU_CUDA(cudaMemcpyAsync(inv.get() + ninv, newinv.get(), nnew * 8, cudaMemcpyDeviceToDevice, st));
+      const bool fresh = ninv == 0;
+      ninv += nnew;
+      if (fresh || 2 * static_cast<uint64_t>(ninv) > inv_mask + 1)
+        build_inv_table();
+      else
+        PCU_LAUNCH(ctx, k_inv_insert, grid_for(nnew, 256), 256, 0, newinv.get(), nnew,
+                   reinterpret_cast<unsigned long long*>(inv_tab.get()), inv_mask);
+    }
     ctx.prof.mark(st, "invalid_update");
     phase = 0;
   }
