@@ -960,7 +960,13 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
              S.big.get(), build_ids, n_build, probe_ids, n_probe, d_alive, sym, in_build, S.cand.get(), S.cand_cap,
              &S.ds.get()->ncand, in_probe);
   S.cls.ensure(3 * S.cand_cap, st);
-  const unsigned g = static_cast<unsigned>(ctx.num_sms * 16);
+  // narrow-phase grids sized from the expected candidate count (about 10-30 per face of the
+  // smaller set): the small rounds of a long QEM tail do not schedule thousands of idle CTAs; the
+  // kernels stride over the device-side counts, so any grid is correct
+  const uint64_t est = 32 * static_cast<uint64_t>(std::max<int64_t>(std::min(n_build, n_probe), 1));
+  const unsigned g = static_cast<unsigned>(
+      std::min<uint64_t>(std::max<uint64_t>((est + 255) / 256, static_cast<uint64_t>(ctx.num_sms)),
+                         static_cast<uint64_t>(ctx.num_sms) * 16));
   PCU_LAUNCH(ctx, k_classify, g, 256, 0, dV, dF, B, S.degen.get(), S.cand.get(), S.cand_cap, S.ds.get(), mode,
              S.cls.get(), pairs, pair_cap, owner, revert);
   // the 1-shared chain (certified filter, then the exact pass over its few undecided pairs, a
