@@ -587,30 +587,122 @@ __device__ bool link_condition(int a, int b, const int32_t* F, const uint32_t* o
   return true;
 }
 
-// marked[i] (sorted keys) -> pass flag, removal count; failures appended to the invalid list
-__global__ void k_link(const uint64_t* __restrict__ marked, int64_t nm, const int32_t* __restrict__ ea,
-                       const int32_t* __restrict__ eb, const uint8_t* __restrict__ enf, const int32_t* __restrict__ F,
-                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
-                       const int32_t* __restrict__ inc, uint32_t* __restrict__ rem, uint64_t* __restrict__ newinv,
-                       Counters* cnt, int32_t* __restrict__ lscr) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= nm) return;
-  const uint32_t e = static_cast<uint32_t>(marked[i]);
+// The same verdict with one warp per edge, for vertices of at most 32 incident faces: lane i holds
+// the i-th incident face of a and of b, and the sets of link_condition are counted with shuffles
+// instead of sorted per thread.  With valid faces every incident face contributes exactly its two
+// other vertices, and the checks reduce to (link_condition, step by step):
+//   * boundary(v): some ring vertex of v lies in exactly one incident face;
+//   * link(ab) = the opposite vertices of the faces holding a and b (+ -2 if exactly one face);
+//     every opposite vertex is in link(a) ∩ link(b), so link(a) ∩ link(b) = link(ab) iff their
+//     sizes agree and -2 is in both or neither (8+ faces on ab: false, as link_condition);
+//   * then for each pair x < y of common vertices, no faces {x, y, a} and {x, y, b} both; and
+//     with -2 common, no x on exactly one face with a and exactly one face with b.
+__device__ bool link_condition_warp(int a, int b, const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
+                                    const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int lane) {
+  constexpr unsigned kAll = 0xffffffffu;
+  const int da = static_cast<int>(deg[a]), db = static_cast<int>(deg[b]);
+  int ua = -1, wa = -1, ub = -1, wb = -1, opp = -1;
+  bool hb = false;
+  if (lane < da) {
+    const int32_t* t = F + 3 * inc[off[a] + lane];
+    const int t0 = t[0], t1 = t[1], t2 = t[2];
+    ua = t0 == a ? t1 : t0;
+    wa = (t0 == a || t1 == a) ? t2 : t1;
+    hb = ua == b || wa == b;
+    if (hb) opp = ua == b ? wa : ua;
+  }
+  if (lane < db) {
+    const int32_t* t = F + 3 * inc[off[b] + lane];
+    const int t0 = t[0], t1 = t[1], t2 = t[2];
+    ub = t0 == b ? t1 : t0;
+    wb = (t0 == b || t1 == b) ? t2 : t1;
+  }
+  int cau = 0, caw = 0, cbu = 0, cbw = 0;  // multiplicities in the own link multiset
+  bool ibu = false, ibw = false;           // a's ring vertices found in b's ring
+  bool fu = true, fw = wa != ua;           // first occurrence among a's ring entries
+  bool fo = hb;                            // first occurrence among the opposite vertices
+  const int n = max(da, db);
+  for (int j = 0; j < n; ++j) {
+    const int xu = __shfl_sync(kAll, ua, j), xw = __shfl_sync(kAll, wa, j);
+    const int yu = __shfl_sync(kAll, ub, j), yw = __shfl_sync(kAll, wb, j);
+    const int xo = __shfl_sync(kAll, opp, j);
+    cau += (xu == ua) + (xw == ua);
+    caw += (xu == wa) + (xw == wa);
+    cbu += (yu == ub) + (yw == ub);
+    cbw += (yu == wb) + (yw == wb);
+    ibu |= yu == ua || yw == ua;
+    ibw |= yu == wa || yw == wa;
+    if (j < lane) {
+      fu &= xu != ua && xw != ua;
+      fw &= xu != wa && xw != wa;
+      fo &= xo != opp;
+    }
+  }
+  const bool va = lane < da, vb = lane < db;
+  const bool bnd_a = __any_sync(kAll, va && (cau == 1 || caw == 1));
+  const bool bnd_b = __any_sync(kAll, vb && (cbu == 1 || cbw == 1));
+  const int nfe = __popc(__ballot_sync(kAll, hb));
+  if (nfe >= 8) return false;
+  const int ncommon = __popc(__ballot_sync(kAll, va && fu && ibu)) + __popc(__ballot_sync(kAll, va && fw && ibw)) +
+                      ((bnd_a && bnd_b) ? 1 : 0);
+  const unsigned om = __ballot_sync(kAll, fo);  // lanes holding the distinct opposite vertices
+  const int nlab = __popc(om) + (nfe == 1 ? 1 : 0);
+  if (nfe == 1 && !(bnd_a && bnd_b)) return false;
+  if (nlab != ncommon) return false;
+  const bool has_vb = bnd_a && bnd_b;
+  for (unsigned m = om; m;) {
+    const int jx = __ffs(m) - 1;
+    m &= m - 1;
+    const int x = __shfl_sync(kAll, opp, jx);
+    for (unsigned m2 = om; m2;) {
+      const int jy = __ffs(m2) - 1;
+      m2 &= m2 - 1;
+      const int y = __shfl_sync(kAll, opp, jy);
+      if (y <= x) continue;
+      const bool in_la = __any_sync(kAll, va && ((ua == x && wa == y) || (ua == y && wa == x)));
+      const bool in_lb = __any_sync(kAll, vb && ((ub == x && wb == y) || (ub == y && wb == x)));
+      if (in_la && in_lb) return false;
+    }
+    if (has_vb) {
+      const int fa = __popc(__ballot_sync(kAll, va && (ua == x || wa == x)));
+      const int fb = __popc(__ballot_sync(kAll, vb && (ub == x || wb == x)));
+      if (fa == 1 && fb == 1) return false;
+    }
+  }
+  return true;
+}
+
+// marked[w] -> pass flag, removal count; failures appended to the invalid list.  One warp per
+// marked edge; a vertex with more than 32 incident faces takes the per-thread path (lane 0) with
+// its CSR-aligned global scratch (marked edges never share a vertex).
+__global__ void k_link_warp(const uint64_t* __restrict__ marked, int64_t nm, const int32_t* __restrict__ ea,
+                            const int32_t* __restrict__ eb, const uint8_t* __restrict__ enf,
+                            const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
+                            const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc,
+                            uint32_t* __restrict__ rem, uint64_t* __restrict__ newinv, Counters* cnt,
+                            int32_t* __restrict__ lscr) {
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nm) return;  // warp-uniform
+  const uint32_t e = static_cast<uint32_t>(marked[w]);
   const int a = ea[e], b = eb[e];
   bool ok;
-  if (deg[a] <= kLocalDeg && deg[b] <= kLocalDeg) {
-    int32_t la[2 * kLocalDeg + 1], lb[2 * kLocalDeg + 1];
-    ok = link_condition(a, b, F, off, deg, inc, la, lb);
-  } else {  // high valence: per-vertex global scratch (2 slots per incidence entry + 1)
-    ok = link_condition(a, b, F, off, deg, inc, lscr + 2 * static_cast<int64_t>(off[a]) + a,
-                        lscr + 2 * static_cast<int64_t>(off[b]) + b);
-  }
-  if (ok) {
-    rem[i] = enf[e];
+  if (deg[a] <= 32 && deg[b] <= 32) {
+    ok = link_condition_warp(a, b, F, off, deg, inc, lane);
   } else {
-    rem[i] = 0;
+    ok = false;
+    if (lane == 0)
+      ok = link_condition(a, b, F, off, deg, inc, lscr + 2 * static_cast<int64_t>(off[a]) + a,
+                          lscr + 2 * static_cast<int64_t>(off[b]) + b);
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+  }
+  if (lane != 0) return;
+  if (ok) {
+    rem[w] = enf[e];
+  } else {
+    rem[w] = 0;
     atomicAdd(&cnt->link_fail, 1ull);
-    newinv[agg_inc(&cnt->newinv)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+    newinv[atomicAdd(&cnt->newinv, 1ull)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
   }
 }
 
@@ -1145,7 +1237,7 @@ struct QemState {
       AuxFork fork(ctx);
       PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx.stream));
       fork.to_main();
-      PCU_LAUNCH(ctx, k_link, grid_for(nm, 64), 64, 0, mlist, nm, ea.get(), eb.get(), enf.get(), F,
+      PCU_LAUNCH(ctx, k_link_warp, grid_for(32 * nm, 256), 256, 0, mlist, nm, ea.get(), eb.get(), enf.get(), F,
                  off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
       exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
     }
