@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
                                                uint64_t cap, unsigned long long* __restrict__ ncand,
                                                const int32_t* __restrict__ probe_ids, int32_t* __restrict__ huge,
                                                unsigned long long* __restrict__ nhuge,
-                                               const uint8_t* __restrict__ in_probe) {
+                                               const uint8_t* __restrict__ in_probe, int ppw) {
   // candidates are staged in shared memory and flushed with one global atomic per block
   // (a single-address counter bumped per candidate serialises in the L2 atomic unit)
   constexpr int kBuf = 1024, kQ = 64;
@@ -499,9 +499,11 @@ __global__ void __launch_bounds__(128) k_probe(const FBox* __restrict__ B, int64
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  // ppw probes per warp (lanes >= ppw only help drain): fewer for small probe sets, so a short
+  // round spreads its (cell, entry) work over more warps
+  const int64_t k = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * ppw + lane;
   int32_t p = -1;
-  if (k < n) {
+  if (lane < ppw && k < n) {
     p = probe_ids ? probe_ids[k] : static_cast<int32_t>(k);
     if (alive && !alive[p]) p = -1;
   }
@@ -872,6 +874,10 @@ __global__ void k_verdict_pairs(const double* __restrict__ V, const int32_t* __r
   out[i] = verdict(V, F + 3 * pairs[2 * i], F + 3 * pairs[2 * i + 1]) ? 1 : 0;
 }
 
+// hash buckets per build face (a face covers ~8 cells: fewer buckets mix cells in one list)
+#ifndef PCU_BUCKETS_PER_FACE
+#define PCU_BUCKETS_PER_FACE 2
+#endif
 uint32_t pow2_at_least(uint64_t x) {
   uint32_t p = 1024;
   while (p < x && p < (1u << 30)) p <<= 1;
@@ -909,7 +915,7 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
                   std::initializer_list<FillRange> extra_fills = {}, bool fresh_build_boxes = false) {
   cudaStream_t st = ctx.stream;
   S.ds.ensure(1, st);
-  const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_build) * 2 + 1);
+  const uint32_t nb = pow2_at_least(static_cast<uint64_t>(n_build) * PCU_BUCKETS_PER_FACE + 1);
   const uint32_t mask = nb - 1;
   S.bcount.ensure(nb, st);
   S.boff.ensure(nb, st);
@@ -952,10 +958,11 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   if (S.cand_cap == 0) S.cand_cap = static_cast<uint64_t>(nf) * 4 + 4096;
   S.cand.ensure(S.cand_cap, st);
   S.huge.ensure(static_cast<size_t>(n_probe) + 16, st);
-  PCU_LAUNCH(ctx, k_probe, grid_for(n_probe, 128), 128, 0, B, n_probe,
+  const int ppw = n_probe >= (1 << 17) ? 32 : n_probe >= (1 << 16) ? 16 : n_probe >= (1 << 15) ? 8 : 4;
+  PCU_LAUNCH(ctx, k_probe, grid_for(n_probe * (32 / ppw), 128), 128, 0, B, n_probe,
              d_alive, S.ds.get(), mask, S.bcount.get(), S.boff.get(), S.entries.get(), S.big.get(), S.occ.get(), sym,
              in_build,
-             S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids, S.huge.get(), &S.ds.get()->nhuge, in_probe);
+             S.cand.get(), S.cand_cap, &S.ds.get()->ncand, probe_ids, S.huge.get(), &S.ds.get()->nhuge, in_probe, ppw);
   PCU_LAUNCH(ctx, k_probe_large, static_cast<unsigned>(ctx.num_sms * 2), 128, 0, B, S.ds.get(), S.huge.get(),
              S.big.get(), build_ids, n_build, probe_ids, n_probe, d_alive, sym, in_build, S.cand.get(), S.cand_cap,
              &S.ds.get()->ncand, in_probe);
