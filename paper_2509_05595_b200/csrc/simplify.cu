@@ -38,6 +38,7 @@ namespace {
 // scratch regions aligned with the CSR incidence (2 slots per incidence entry + 1 per vertex), which
 // no other thread touches: marked edges have disjoint 1-rings, so their endpoints are distinct.
 constexpr int kLocalDeg = 32;
+static_assert(kLocalDeg <= 32, "link_condition_warp holds one incident face per lane");
 constexpr double k4Sqrt3 = 6.928203230275509;
 
 struct Counters {
@@ -880,26 +881,28 @@ __global__ void k_link_sizes(const int32_t* __restrict__ edges, int64_t n, const
   const uint32_t da = deg[edges[2 * i]], db = deg[edges[2 * i + 1]];
   sz[i] = (da <= kLocalDeg && db <= kLocalDeg) ? 0u : 2 * da + 2 * db + 2;
 }
+// one warp per queried edge: vertices of at most 32 faces take link_condition_warp (the batch's
+// check), larger ones the per-thread link_condition in lane 0 with per-edge scratch
 __global__ void k_link_pairs(const int32_t* __restrict__ edges, int64_t n, const int32_t* __restrict__ F,
                              const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
                              const int32_t* __restrict__ inc, const uint32_t* __restrict__ lofs,
                              int32_t* __restrict__ lscr, int32_t* __restrict__ out) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
+  const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;  // warp-uniform
   const int a = min(edges[2 * i], edges[2 * i + 1]), b = max(edges[2 * i], edges[2 * i + 1]);
   if (a == b || faces_of_edge(a, b, F, off, deg, inc) == 0) {
-    out[i] = -1;
+    if (lane == 0) out[i] = -1;
     return;
   }
-  bool ok;
+  bool ok = false;
   if (deg[a] <= kLocalDeg && deg[b] <= kLocalDeg) {
-    int32_t la[2 * kLocalDeg + 1], lb[2 * kLocalDeg + 1];
-    ok = link_condition(a, b, F, off, deg, inc, la, lb);
-  } else {
+    ok = link_condition_warp(a, b, F, off, deg, inc, lane);
+  } else if (lane == 0) {
     int32_t* base = lscr + lofs[i];
     ok = link_condition(a, b, F, off, deg, inc, base, base + 2 * deg[a] + 1);
   }
-  out[i] = ok ? 1 : 0;
+  if (lane == 0) out[i] = ok ? 1 : 0;
 }
 
 struct StaticAdj {  // vertex -> face CSR of a whole mesh (every face alive), lists ascending
@@ -957,7 +960,7 @@ void link_condition_of(Ctx& ctx, const int32_t* F, int64_t nv, int64_t nf, const
   exclusive_scan_u32(ctx, sz.get(), lofs.get(), n);
   const int64_t tot = static_cast<int64_t>(read_scalar(ctx, lofs.get() + n - 1)) + read_scalar(ctx, sz.get() + n - 1);
   DevBuf<int32_t> lscr(tot ? tot : 1, ctx.stream);
-  PCU_LAUNCH(ctx, k_link_pairs, grid_for(n, 64), 64, 0, d_edges, n, F, A.off.get(), A.deg.get(), A.inc.get(),
+  PCU_LAUNCH(ctx, k_link_pairs, grid_for(32 * n, 256), 256, 0, d_edges, n, F, A.off.get(), A.deg.get(), A.inc.get(),
              lofs.get(), lscr.get(), d_out);
 }
 
