@@ -37,6 +37,7 @@ static void ctx_release(pamopt_cu_ctx c) {
   if (c->ctx.scratch) cudaFreeAsync(c->ctx.scratch, c->ctx.stream);
   cudaStreamSynchronize(c->ctx.stream);
   c->ctx.release_aux();
+  if (c->ctx.pin) cudaFreeHost(c->ctx.pin);
   cudaStreamDestroy(c->ctx.stream);
   delete c;
 }

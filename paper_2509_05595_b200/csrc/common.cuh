@@ -15,6 +15,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <cstring>
 #include <initializer_list>
 #include <vector>
 
@@ -137,6 +138,12 @@ struct Ctx {
   // created on first use
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // pinned landing zone for read_scalar (a pageable D2H copy stages through the driver)
+  void* pin = nullptr;
+  void* pinned_scratch() {
+    if (!pin) PCU_CUDA(cudaMallocHost(&pin, 256));
+    return pin;
+  }
   cudaStream_t aux_stream() {
     if (!aux) {
       PCU_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -268,9 +275,12 @@ void sort_pairs_u64(Ctx& ctx, uint64_t* keys, int64_t n, int end_bit = 64);
 bool small_sort_u64(Ctx& ctx, const uint64_t* in, uint64_t* out, int64_t n);
 template <class T>
 T read_scalar(Ctx& ctx, const T* dptr) {
+  static_assert(sizeof(T) <= 256, "read_scalar: value too large for the pinned scratch");
   T h;
-  PCU_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
+  void* p = ctx.pinned_scratch();
+  PCU_CUDA(cudaMemcpyAsync(p, dptr, sizeof(T), cudaMemcpyDeviceToHost, ctx.stream));
   PCU_CUDA(cudaStreamSynchronize(ctx.stream));
+  std::memcpy(&h, p, sizeof(T));
   return h;
 }
 

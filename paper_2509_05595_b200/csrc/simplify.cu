@@ -25,6 +25,7 @@
 #include <algorithm>
 
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1027,6 +1028,7 @@ struct QemState {
   int retain = 0, zero_run = 0;
   int64_t ne_hint = 0;
   std::vector<uint8_t> ds_host;
+  void* hpin = nullptr;  // pinned: Counters, then the detection scalars
   unsigned gs_grid = 0;
   // per-iteration results
   int64_t ne = 0, nm = 0, succ = 0, nnew = 0, nq = 0;
@@ -1083,6 +1085,9 @@ struct QemState {
     alive_verts = nv;
     ne_hint = 3 * nf / 2 + 16;
     ds_host.resize(detect_scalars_size());
+    // pinned landing zone for the per-sync counter reads (a pageable D2H copy stages through the
+    // driver and costs several us more per synchronisation)
+    PCU_CUDA(cudaMallocHost(&hpin, sizeof(Counters) + ds_host.size()));
     gs_grid = static_cast<unsigned>(ctx.num_sms * 16);
     ctx.prof.reset(st);
     if (nf == 0 || nv == 0) return;
@@ -1091,7 +1096,10 @@ struct QemState {
     boxes_init(ctx, *isc, X, F, nf, falive.get());
     PCU_LAUNCH(ctx, k_quadrics, grid_for(nv, 128), 128, 0, X, F, off.get(), deg.get(), inc.get(), nv, Q.get());
   }
-  ~QemState() { isect_scratch_destroy(isc); }
+  ~QemState() {
+    isect_scratch_destroy(isc);
+    if (hpin) cudaFreeHost(hpin);
+  }
   QemState(const QemState&) = delete;
   QemState& operator=(const QemState&) = delete;
 
@@ -1108,11 +1116,15 @@ struct QemState {
   // Host synchronisations per iteration: one after marking, one after the collapse batch, one
   // per undo round (counters + detection scalars fetched together).
   Counters sync_counters(bool with_detect) {
-    Counters h;
-    PCU_CUDA(cudaMemcpyAsync(&h, cnt.get(), sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    uint8_t* hc = static_cast<uint8_t*>(hpin);
+    PCU_CUDA(cudaMemcpyAsync(hc, cnt.get(), sizeof(Counters), cudaMemcpyDeviceToHost, st));
     if (with_detect)
-      PCU_CUDA(cudaMemcpyAsync(ds_host.data(), detect_scalars_ptr(*isc), ds_host.size(), cudaMemcpyDeviceToHost, st));
+      PCU_CUDA(cudaMemcpyAsync(hc + sizeof(Counters), detect_scalars_ptr(*isc), ds_host.size(),
+                               cudaMemcpyDeviceToHost, st));
     PCU_CUDA(cudaStreamSynchronize(st));
+    Counters h;
+    std::memcpy(&h, hc, sizeof(Counters));
+    if (with_detect) std::memcpy(ds_host.data(), hc + sizeof(Counters), ds_host.size());
     return h;
   }
 
