@@ -69,12 +69,8 @@ __global__ void k_fill(const int32_t* __restrict__ F, const uint8_t* __restrict_
   }
 }
 
-__global__ void k_sort_lists(const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg, int64_t nv,
-                             int32_t* __restrict__ inc) {
-  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (v >= nv) return;
-  int32_t* L = inc + off[v];
-  const int n = static_cast<int>(deg[v]);
+// one vertex's incident faces in ascending id (the pinned gather / traversal order)
+__device__ __forceinline__ void sort_list(int32_t* L, int n) {
   for (int i = 1; i < n; ++i) {
     const int32_t x = L[i];
     int j = i - 1;
@@ -84,6 +80,13 @@ __global__ void k_sort_lists(const uint32_t* __restrict__ off, const uint32_t* _
     }
     L[j + 1] = x;
   }
+}
+
+__global__ void k_sort_lists(const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg, int64_t nv,
+                             int32_t* __restrict__ inc) {
+  const int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (v >= nv) return;
+  sort_list(inc + off[v], static_cast<int>(deg[v]));
 }
 
 // quadrics gathered in ascending face id
@@ -154,12 +157,15 @@ __device__ int upper_neighbours(int a, const int32_t* __restrict__ F, const uint
 
 // per vertex a: its upper neighbours b > a (ascending) with the face count of edge ab; the
 // sorted list is parked in the CSR-aligned scratch (2 slots per incident face) for k_edge_fill
+// (each vertex's thread first sorts its own incidence list: k_fill appends in atomic order, and
+// every later kernel of the iteration reads the lists in ascending face id)
 __global__ void k_edge_count(const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
-                             const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, int64_t nv,
+                             const uint32_t* __restrict__ deg, int32_t* __restrict__ inc, int64_t nv,
                              uint32_t* __restrict__ ecount, int32_t* __restrict__ snb, uint8_t* __restrict__ smult,
                              Counters* cnt) {
   const int64_t a = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (a >= nv) return;
+  sort_list(inc + off[a], static_cast<int>(deg[a]));
   const int64_t s0 = 2 * static_cast<int64_t>(off[a]);
   const int d = static_cast<int>(deg[a]);
   int u = 0;
@@ -1105,12 +1111,13 @@ struct QemState {
 
   bool done() const { return nf == 0 || !(alive_faces > target && zero_run < P.stall); }
 
-  // (deg and cur must be zero on entry: the constructor and prepare() reset them)
-  void build_incidence() {
+  // (deg and cur must be zero on entry: the constructor and prepare() reset them).  prepare()
+  // leaves the per-vertex sort to k_edge_count, its next kernel.
+  void build_incidence(bool sort_lists = true) {
     PCU_LAUNCH(ctx, k_deg, grid_for(nf, 256), 256, 0, F, falive.get(), nf, deg.get());
     exclusive_scan_u32(ctx, deg.get(), off.get(), nv);
     PCU_LAUNCH(ctx, k_fill, grid_for(nf, 256), 256, 0, F, falive.get(), nf, off.get(), cur.get(), inc.get());
-    PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
+    if (sort_lists) PCU_LAUNCH(ctx, k_sort_lists, grid_for(nv, 256), 256, 0, off.get(), deg.get(), nv, inc.get());
   }
 
   // Host synchronisations per iteration: one after marking, one after the collapse batch, one
@@ -1172,7 +1179,7 @@ struct QemState {
     fill_multi(ctx, {{deg.get(), nvb, 0}, {cur.get(), nvb, 0}, {cnt.get(), sizeof(Counters), 0},
                      {vmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF}, {vfmin.get(), static_cast<uint64_t>(nv) * 8, 0xFF},
                      {owner.get(), static_cast<uint64_t>(nf) * 4, 0xFF}});
-    if (S.iterations > 1) build_incidence();
+    if (S.iterations > 1) build_incidence(false);
     ctx.prof.mark(st, "incidence");
     unsigned long long* d_ne = &cnt.get()->edges;
     // edges (device-side count; kernels below stride over it)
