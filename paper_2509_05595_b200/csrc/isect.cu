@@ -874,6 +874,9 @@ __global__ void k_verdict_pairs(const double* __restrict__ V, const int32_t* __r
   out[i] = verdict(V, F + 3 * pairs[2 * i], F + 3 * pairs[2 * i + 1]) ? 1 : 0;
 }
 
+#ifndef PCU_PROBE_FULL_WARP
+#define PCU_PROBE_FULL_WARP (1 << 17)
+#endif
 // hash buckets per build face (a face covers ~8 cells: fewer buckets mix cells in one list)
 #ifndef PCU_BUCKETS_PER_FACE
 #define PCU_BUCKETS_PER_FACE 2
@@ -958,7 +961,8 @@ void detect_round(Ctx& ctx, IsectScratch& S, const double* dV, const int32_t* dF
   if (S.cand_cap == 0) S.cand_cap = static_cast<uint64_t>(nf) * 4 + 4096;
   S.cand.ensure(S.cand_cap, st);
   S.huge.ensure(static_cast<size_t>(n_probe) + 16, st);
-  const int ppw = n_probe >= (1 << 17) ? 32 : n_probe >= (1 << 16) ? 16 : n_probe >= (1 << 15) ? 8 : 4;
+  const int64_t p32 = PCU_PROBE_FULL_WARP;  // probe-set size from which a warp takes 32 probes
+  const int ppw = n_probe >= p32 ? 32 : n_probe >= p32 / 2 ? 16 : n_probe >= p32 / 4 ? 8 : 4;
   PCU_LAUNCH(ctx, k_probe, grid_for(n_probe * (32 / ppw), 128), 128, 0, B, n_probe,
              d_alive, S.ds.get(), mask, S.bcount.get(), S.boff.get(), S.entries.get(), S.big.get(), S.occ.get(), sym,
              in_build,
