@@ -683,34 +683,37 @@ __device__ bool link_condition_warp(int a, int b, const int32_t* __restrict__ F,
 // marked[w] -> pass flag, removal count; failures appended to the invalid list.  One warp per
 // marked edge; a vertex with more than 32 incident faces takes the per-thread path (lane 0) with
 // its CSR-aligned global scratch (marked edges never share a vertex).
-__global__ void k_link_warp(const uint64_t* __restrict__ marked, int64_t nm, const int32_t* __restrict__ ea,
+__global__ void k_link_warp(const uint64_t* __restrict__ marked, int64_t nm_host,
+                            const unsigned long long* __restrict__ nm_dev, const int32_t* __restrict__ ea,
                             const int32_t* __restrict__ eb, const uint8_t* __restrict__ enf,
                             const int32_t* __restrict__ F, const uint32_t* __restrict__ off,
                             const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc,
                             uint32_t* __restrict__ rem, uint64_t* __restrict__ newinv, Counters* cnt,
                             int32_t* __restrict__ lscr) {
-  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= nm) return;  // warp-uniform
-  const uint32_t e = static_cast<uint32_t>(marked[w]);
-  const int a = ea[e], b = eb[e];
-  bool ok;
-  if (deg[a] <= 32 && deg[b] <= 32) {
-    ok = link_condition_warp(a, b, F, off, deg, inc, lane);
-  } else {
-    ok = false;
-    if (lane == 0)
-      ok = link_condition(a, b, F, off, deg, inc, lscr + 2 * static_cast<int64_t>(off[a]) + a,
-                          lscr + 2 * static_cast<int64_t>(off[b]) + b);
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-  }
-  if (lane != 0) return;
-  if (ok) {
-    rem[w] = enf[e];
-  } else {
-    rem[w] = 0;
-    atomicAdd(&cnt->link_fail, 1ull);
-    newinv[atomicAdd(&cnt->newinv, 1ull)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+  const int64_t nm = nm_dev ? static_cast<int64_t>(*nm_dev) : nm_host;  // (device count: no host read)
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < nm; w += nw) {
+    const uint32_t e = static_cast<uint32_t>(marked[w]);
+    const int a = ea[e], b = eb[e];
+    bool ok;
+    if (deg[a] <= 32 && deg[b] <= 32) {
+      ok = link_condition_warp(a, b, F, off, deg, inc, lane);
+    } else {
+      ok = false;
+      if (lane == 0)
+        ok = link_condition(a, b, F, off, deg, inc, lscr + 2 * static_cast<int64_t>(off[a]) + a,
+                            lscr + 2 * static_cast<int64_t>(off[b]) + b);
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+    }
+    if (lane != 0) continue;
+    if (ok) {
+      rem[w] = enf[e];
+    } else {
+      rem[w] = 0;
+      atomicAdd(&cnt->link_fail, 1ull);
+      newinv[atomicAdd(&cnt->newinv, 1ull)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+    }
   }
 }
 
@@ -724,19 +727,19 @@ struct Batch {
   uint32_t* nrem;   // faces removed
 };
 
-__global__ void k_collapse(const uint64_t* __restrict__ marked, int64_t nm, const uint32_t* __restrict__ rem,
-                           const uint32_t* __restrict__ remoff, int64_t alive_faces, int64_t target,
-                           const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
-                           const double* __restrict__ place, const uint32_t* __restrict__ off,
-                           const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, double* __restrict__ X,
-                           int32_t* __restrict__ F, uint8_t* __restrict__ falive, uint8_t* __restrict__ valive,
-                           double* __restrict__ Q, int32_t* __restrict__ owner, int32_t* __restrict__ qfaces,
-                           Batch B, Counters* cnt) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= nm) return;
+__device__ __forceinline__ void collapse_one(int64_t i, const uint64_t* __restrict__ marked,
+                                             const uint32_t* __restrict__ rem, const uint32_t* __restrict__ remoff,
+                                             int64_t alive_faces, int64_t target, const int32_t* __restrict__ ea,
+                                             const int32_t* __restrict__ eb, const double* __restrict__ place,
+                                             const uint32_t* __restrict__ off, const uint32_t* __restrict__ deg,
+                                             const int32_t* __restrict__ inc, double* __restrict__ X,
+                                             int32_t* __restrict__ F, uint8_t* __restrict__ falive,
+                                             uint8_t* __restrict__ valive, double* __restrict__ Q,
+                                             int32_t* __restrict__ owner, int32_t* __restrict__ qfaces, Batch B,
+                                             Counters* cnt) {
   B.applied[i] = 0;
-  if (rem[i] == 0) return;                                             // failed the link condition
-  if (!(alive_faces - static_cast<int64_t>(remoff[i]) > target)) return;  // overshoot trim (P9)
+  if (rem[i] == 0) return;                                                          // failed the link condition
+  if (remoff && !(alive_faces - static_cast<int64_t>(remoff[i]) > target)) return;  // overshoot trim (P9)
   const uint32_t e = static_cast<uint32_t>(marked[i]);
   const int a = ea[e], b = eb[e];
   B.ca[i] = a;
@@ -775,6 +778,23 @@ __global__ void k_collapse(const uint64_t* __restrict__ marked, int64_t nm, cons
       qfaces[agg_inc(&cnt->query)] = f;
     }
   }
+}
+
+__global__ void k_collapse(const uint64_t* __restrict__ marked, int64_t nm, const uint32_t* __restrict__ rem,
+                           const uint32_t* __restrict__ remoff, int64_t alive_faces, int64_t target,
+                           const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                           const double* __restrict__ place, const uint32_t* __restrict__ off,
+                           const uint32_t* __restrict__ deg, const int32_t* __restrict__ inc, double* __restrict__ X,
+                           int32_t* __restrict__ F, uint8_t* __restrict__ falive, uint8_t* __restrict__ valive,
+                           double* __restrict__ Q, int32_t* __restrict__ owner, int32_t* __restrict__ qfaces,
+                           Batch B, Counters* cnt, const unsigned long long* __restrict__ nm_dev) {
+  // remoff == nullptr: no overshoot trim can fire this iteration; nm_dev: the marked count stays
+  // on the device (grid-stride over it)
+  const int64_t n = nm_dev ? static_cast<int64_t>(*nm_dev) : nm;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    collapse_one(i, marked, rem, remoff, alive_faces, target, ea, eb, place, off, deg, inc, X, F, falive, valive, Q,
+                 owner, qfaces, B, cnt);
 }
 
 // keep query faces whose owner is still applied
@@ -1001,6 +1021,7 @@ struct QemState {
   DevBuf<uint8_t> enf, valid, revert, smult;
   DevBuf<uint64_t> key, marked, marked_sorted;
   const uint64_t* mlist = nullptr;  // this iteration's marked list (marked_sorted or marked)
+  bool deferred = false;            // marked count read after the batch (see propagate_and_mark)
   bool key_order = false;           // stepwise API: always sort the marked list
   const bool undo_stats = std::getenv("PAMOPT_UNDO_STATS") != nullptr;
   DevBuf<double> place;
@@ -1208,20 +1229,27 @@ struct QemState {
     PCU_LAUNCH(ctx, k_prop_faces, grid_for(nf, 256), 256, 0, F, falive.get(), nf, vmin.get(), vfmin.get());
     PCU_LAUNCH(ctx, k_mark, eg, 256, 0, ea.get(), eb.get(), key.get(), valid.get(), d_ne, vfmin.get(), marked.get(),
                cnt.get());
-    Counters h = sync_counters(false);  // ---- sync 1
-    ne = static_cast<int64_t>(h.edges);
-    ne_hint = ne;
-    S.face_iterations += alive_faces;
-    S.alg_bytes += 28 * alive_faces + 92 * alive_verts + 8 * ne;
-    if (S.iterations == 1)
-      PCU_REQUIRE(h.err == 0, PAMOPT_CU_EINVAL, "simplify_to: non-manifold input (an edge has >2 faces); run stage 1");
-    PCU_REQUIRE(h.nan == 0, PAMOPT_CU_ENUMERIC, "simplify_to: NaN edge cost");
-    ctx.prof.mark(st, "propagate+mark");
-    nm = static_cast<int64_t>(h.marked);
     succ = 0;
     rounds = 0;
     nnew = 0;
     nq = 0;
+    // Deferred mode (the hot loop after iteration 1): marked edges share no vertex, so at most
+    // alive_verts / 2 of them each remove at most 2 faces; when even that cannot reach the
+    // target, no overshoot trim can fire, the marked order does not matter, and the link check
+    // and the collapse run over the device-side count.  The counters are read once, after the
+    // batch (sync 2), instead of here.
+    deferred = !key_order && S.iterations > 1 && alive_faces - alive_verts > target;
+    if (deferred) {
+      mlist = marked.get();
+      ctx.prof.mark(st, "propagate+mark");
+      phase = 2;
+      return;
+    }
+    Counters h = sync_counters(false);  // ---- sync 1
+    account_marking(h);
+    if (S.iterations == 1)
+      PCU_REQUIRE(h.err == 0, PAMOPT_CU_EINVAL, "simplify_to: non-manifold input (an edge has >2 faces); run stage 1");
+    ctx.prof.mark(st, "propagate+mark");
     mlist = marked_sorted.get();
     // Marked keys in ascending order fix the overshoot trim (P9), which applies the cheapest
     // collapses first.  Marked edges have disjoint face neighbourhoods, so when no trim can fire
@@ -1248,26 +1276,43 @@ struct QemState {
     phase = 2;
   }
 
+  // counters of the marking step (read at sync 1, or at sync 2 in deferred mode)
+  void account_marking(const Counters& h) {
+    ne = static_cast<int64_t>(h.edges);
+    ne_hint = ne;
+    nm = static_cast<int64_t>(h.marked);
+    S.face_iterations += alive_faces;
+    S.alg_bytes += 28 * alive_faces + 92 * alive_verts + 8 * ne;
+    PCU_REQUIRE(h.nan == 0, PAMOPT_CU_ENUMERIC, "simplify_to: NaN edge cost");
+  }
+
   // link condition on the pre-batch mesh, overshoot trim, parallel collapse
   void collapse_batch() {
     PCU_REQUIRE(phase == 2, PAMOPT_CU_EINVAL, "qem: collapse_batch() out of order");
     phase = 3;
-    if (nm == 0) return;
+    if (!deferred && nm == 0) return;
+    const unsigned long long* nm_dev = deferred ? &cnt.get()->marked : nullptr;
     {
       // the pre-batch face copy (the undo loop's restore source) runs on the aux stream while the
       // link condition is evaluated (both only read F)
       AuxFork fork(ctx);
       PCU_CUDA(cudaMemcpyAsync(Fprev.get(), F, 3 * nf * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx.stream));
       fork.to_main();
-      PCU_LAUNCH(ctx, k_link_warp, grid_for(32 * nm, 256), 256, 0, mlist, nm, ea.get(), eb.get(), enf.get(), F,
-                 off.get(), deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
-      exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
+      const unsigned lg = deferred ? gs_grid : grid_for(32 * nm, 256);
+      PCU_LAUNCH(ctx, k_link_warp, lg, 256, 0, mlist, nm, nm_dev, ea.get(), eb.get(), enf.get(), F, off.get(),
+                 deg.get(), inc.get(), rem.get(), newinv.get(), cnt.get(), lscr.get());
+      if (!deferred) exclusive_scan_u32(ctx, rem.get(), remoff.get(), nm);
     }
     ctx.prof.mark(st, "sort+link");
-    PCU_LAUNCH(ctx, k_collapse, grid_for(nm, 128), 128, 0, mlist, nm, rem.get(), remoff.get(),
-               alive_faces, target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F,
-               falive.get(), valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get());
+    const unsigned cg = deferred ? gs_grid : grid_for(nm, 128);
+    PCU_LAUNCH(ctx, k_collapse, cg, 128, 0, mlist, nm, rem.get(), deferred ? nullptr : remoff.get(), alive_faces,
+               target, ea.get(), eb.get(), place.get(), off.get(), deg.get(), inc.get(), X, F, falive.get(),
+               valive.get(), Q.get(), owner.get(), qf.get(), B, cnt.get(), nm_dev);
     hc = sync_counters(false);  // ---- sync 2
+    if (deferred) {
+      account_marking(hc);
+      PCU_REQUIRE(hc.err == 0, PAMOPT_CU_EINVAL, "simplify_to: non-manifold edge during simplification");
+    }
     ctx.prof.mark(st, "collapse");
     nq = static_cast<int64_t>(hc.query);
     // (the moved / renamed faces get their boxes in the first undo round: they are its build set)
